@@ -1,0 +1,204 @@
+"""Pin the numpy oracle (oracle/gooms_port.py) against vectors the reference produced.
+
+The fixtures come from tests/golden/make_golden.py, which runs the unmodified
+reference (`/root/reference/pkg/src/gooms`). Where the oracle follows the
+reference's ufunc order exactly the check is bitwise.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import gooms_port as G
+from goom_testlib import load_golden
+
+NEG_INF = float("-inf")
+
+
+def eq(a, b):
+    np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("name", ["lmme_2x2", "lmme_64_f64", "lmme_64_f32", "lmme_batched_f32"])
+def test_lmme_bitwise(name):
+    z = load_golden(name)
+    ol, os_ = G.lmme(z["alog"], z["asign"], z["blog"], z["bsign"])
+    assert ol.dtype == z["olog"].dtype
+    eq(ol, z["olog"])
+    eq(os_, z["osign"])
+
+
+def test_lmme_2x2_value():
+    z = load_golden("lmme_2x2")
+    np.testing.assert_allclose(G.to_real(z["olog"], z["osign"]), [[19, 22], [43, 50]], rtol=1e-14)
+
+
+def test_lmme_rowscale():
+    z = load_golden("lmme_rowscale")
+    for key, src in (("0", z["a"]), ("1", z["s"])):
+        al, as_ = G.log_sign(src)
+        bl, bs = G.log_sign(z["b"])
+        ol, os_ = G.lmme(al, as_, bl, bs)
+        eq(ol, z["olog" + key])
+        eq(os_, z["osign" + key])
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_gadd_bitwise_and_commutative(tag):
+    z = load_golden(f"gadd_{tag}")
+    ol, os_ = G.gadd(z["alog"], z["asign"], z["blog"], z["bsign"])
+    eq(ol, z["olog"])
+    eq(os_, z["osign"])
+    ol2, os2 = G.gadd(z["blog"], z["bsign"], z["alog"], z["asign"])
+    eq(ol2, ol)
+    eq(os2, os_)
+    assert np.all(ol[:256] == NEG_INF) and np.all(os_[:256] == 1.0)
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_from_real(tag):
+    z = load_golden(f"from_real_{tag}")
+    ml, ms = G.log_sign(z["x"])
+    eq(ml, z["olog"])
+    eq(ms, z["osign"])
+
+
+def test_to_real_scaled_and_col_norms():
+    z = load_golden("to_real_scaled")
+    for i in range(z["log"].shape[0]):
+        o, c = G.to_real_scaled(z["log"][i], z["sign"][i])
+        eq(o, z["out"][i])
+        assert c == z["c"][i]
+    z = load_golden("col_log_norms")
+    eq(G.col_log_norms(z["log"]), z["out"])
+
+
+def _stack(z, prefix=""):
+    return G.Stack(z["alog"].copy(), z["asign"].copy(), z["blog"].copy(), z["bsign"].copy(),
+                   z["flags"].copy())
+
+
+def test_affine_scans():
+    z = load_golden("affine_T64_d4")
+    st = _stack(z)
+    seq = G.scan_sequential(st)
+    eq(np.array([seq.alog, seq.asign, seq.blog, seq.bsign]), z["seq"])
+    par = G.scan_affine_blocked(st, 8)
+    eq(np.array([par.alog, par.asign, par.blog, par.bsign]), z["par8"])
+
+
+@pytest.mark.parametrize("tag,dt", [("f64", np.float64), ("f32", np.float32)])
+def test_config1_chain(tag, dt):
+    z = load_golden("config1_chain")
+    al, as_ = G.log_sign(z["mats"].astype(dt))
+    T = len(al)
+    bl = np.full_like(al, NEG_INF)
+    st = G.Stack(al, as_, bl, np.ones_like(as_), np.zeros(T, dtype=bool))
+    seq = G.scan_sequential(st)
+    eq(np.array([seq.alog, seq.asign]), z[f"seq_{tag}"])
+    L, S = G.chain_blocked(al, as_, 32)
+    eq(np.array([L, S]), z[f"par32_{tag}"])
+
+
+def _chain_stack(al, as_):
+    T = len(al)
+    return G.Stack(al.copy(), as_.copy(), np.full_like(al, NEG_INF), np.ones_like(as_),
+                   np.zeros(T, dtype=bool))
+
+
+def test_selective_norm_threshold():
+    z = load_golden("sel_norm_T300_d4")
+    st = _chain_stack(z["alog"], z["asign"])
+    pol = G.norm_threshold_policy(12.0)
+    out, sites = G.scan_selective(st, pol, None)
+    assert sites == list(z["sites"])
+    eq(np.array([[out.state(i)[0] for i in range(len(out))],
+                 [out.state(i)[1] for i in range(len(out))]]), z["seq_state"])
+    eq(out.flags, z["seq_flags"])
+    out7, sites7 = G.scan_selective(st, pol, 7)
+    assert sites7 == list(z["sites"])
+    eq(np.array([[out7.state(i)[0] for i in range(len(out7))],
+                 [out7.state(i)[1] for i in range(len(out7))]]), z["par_state"])
+
+
+def test_selective_interval8():
+    z = load_golden("sel_norm_interval8")
+    st = _chain_stack(z["alog"], z["asign"])
+    out, sites = G.scan_selective(st, G.norm_threshold_policy(5.0, interval=8), None)
+    assert sites == list(z["sites"])
+    eq(np.array([[out.state(i)[0] for i in range(len(out))],
+                 [out.state(i)[1] for i in range(len(out))]]), z["seq_state"])
+
+
+def test_selective_with_biases_rounds():
+    z = load_golden("sel_norm_bias")
+    T = len(z["alog"])
+    st = G.Stack(z["alog"].copy(), z["asign"].copy(), z["blog"].copy(), z["bsign"].copy(),
+                 np.zeros(T, dtype=bool))
+    pol = G.norm_threshold_policy(12.0)
+    out, sites = G.scan_selective(st, pol, None)
+    assert sites == list(z["sites"])
+    eq(out.flags, z["seq_flags"])
+    out16, sites16 = G.scan_selective(st, pol, 16)
+    assert sites16 == list(z["sites"])
+    got = np.array([out16.state(i)[0] for i in range(T)])
+    assert G.rel_log_diff(got, z["seq_state"][0]) < 1e-10
+
+
+def test_colinearity_chain_lorenz():
+    z = load_golden("sel_colin_lorenz")
+    V, Vs, sites = G.selective_chain(z["alog"], z["asign"], G.colinearity_policy(0.99, 12), 256)
+    assert sites == list(z["sites"])
+    eq(V, z["Vlog"])
+    eq(Vs, z["Vsign"])
+    w = load_golden("sel_colin_lorenz_walk")
+    V1, Vs1, s1 = G.selective_chain(z["alog"][:600], z["asign"][:600], G.colinearity_policy(0.99, 1), 64)
+    assert s1 == list(w["sites"])
+    eq(V1, w["Vlog"])
+    eq(Vs1, w["Vsign"])
+
+
+def test_orthonormal_reset_kat():
+    z = load_golden("orthonormal_reset")
+    rl, rs = G.orthonormal_reset(z["qlog"], z["qsign"])
+    eq(rl, z["rlog"])
+    eq(rs, z["rsign"])
+    hl, hs = G.orthonormal_reset(z["hlog"], np.ones((2, 2)))
+    eq(hl, z["hrlog"])
+    eq(hs, z["hrsign"])
+
+
+def test_appendix_c_with_callable_policy():
+    z = load_golden("appendix_c")
+    target = z["a1"] @ z["x0"]
+
+    def select(l, s):
+        return np.allclose(G.to_real(l, s), target, rtol=1e-9)
+
+    def reset(l, s):
+        x = G.to_real(l, s)
+        return G.log_sign(x / (1.0 + np.linalg.norm(x)))
+
+    mats = [z["x0"], z["a1"], z["a2"], z["a3"]]
+    al, as_ = G.log_sign(np.array(mats))
+    st = _chain_stack(al, as_)
+    pol = G.Policy(select=select, reset=reset)
+    for block in (None, 1, 2, 3, 4):
+        out, sites = G.scan_selective(st, pol, block)
+        assert sites == [2]
+        for i, key in ((1, "want1"), (2, "want2"), (3, "want3")):
+            np.testing.assert_allclose(G.to_real(*out.state(i)), z[key], rtol=1e-12)
+        assert list(out.flags) == [False, False, True, True]
+
+
+def test_complex_adapters_round_trip():
+    rng = np.random.default_rng(0)
+    log = rng.uniform(-50, 50, (7, 9)).astype(np.float32)
+    sign = rng.choice([-1.0, 1.0], (7, 9)).astype(np.float32)
+    z = G.join_complex(log, sign)
+    assert z.dtype == np.complex64
+    l2, s2 = G.split_complex(z, np.float32)
+    eq(l2, log)
+    eq(s2, sign)
+    # non-canonical phases: 2*pi is positive, 3*pi negative
+    w = np.array([1 + 2j * np.pi, 1 + 3j * np.pi], dtype=np.complex64)
+    assert list(G.split_complex(w)[1]) == [1.0, -1.0]
