@@ -1,0 +1,160 @@
+/*
+ * goom.h — C ABI of the B200-native GOOM LMME prefix-scan library (libgoom.so).
+ *
+ * A GOOM ("generalized order of magnitude") stores a real x as the complex64
+ * natural log  z = log|x| + i*pi*[x<0]; zero is (-inf, 0). Inputs may carry any
+ * imaginary part: the sign is -1 iff cos(imag) < 0. Outputs are canonical
+ * (imag exactly 0.0f or (float)M_PI).
+ *
+ * Every entry point replaces one array-level routine of the reference CPU
+ * package `gooms` (/root/reference/pkg/src/gooms, cited file:line below). The
+ * reference has no FFI; its boundary is the Python call surface, which the
+ * Python package `paper_2510_03426_b200` re-exposes on top of this ABI (see
+ * INTEGRATION.md for the ctypes binding a `gooms` maintainer would add).
+ *
+ * Conventions
+ *   - Pointers are DEVICE pointers unless the name ends in `_host`.
+ *   - Matrices are dense row-major; a batch of matrices is addressed as
+ *     base + (b / div) * stride elements (stride 0 broadcasts one matrix).
+ *   - All calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) unless documented otherwise; outputs are caller-owned.
+ *   - Workspace: functions taking (ws, ws_bytes) first report their need via
+ *     the matching *_workspace_size() call; ws may be NULL iff that is 0.
+ *   - Results are deterministic: no value-affecting atomics, fixed reduction
+ *     orders; bitwise repeatable for a given argument set.
+ *   - Return value: 0 = GOOM_OK, else a goom_status; goom_last_error() gives
+ *     a thread-local message. Shape/argument errors map to the reference's
+ *     ValueError (core.py:280-283, scan.py:40-43,94-95,518-519,539-540).
+ */
+#ifndef GOOM_H_
+#define GOOM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct goom_c64 { float re, im; } goom_c64;
+
+typedef enum goom_status {
+  GOOM_OK = 0,
+  GOOM_EINVAL = 1,        /* bad argument (ValueError in the reference)       */
+  GOOM_ESHAPE = 2,        /* dimension mismatch (ValueError)                  */
+  GOOM_EDTYPE = 3,        /* unsupported element type                         */
+  GOOM_ECUDA = 4,         /* CUDA runtime / launch failure                    */
+  GOOM_EUNSUPPORTED = 5,  /* no sm_100a device / feature not built            */
+  GOOM_EWORKSPACE = 6,    /* workspace missing or too small                   */
+  GOOM_ERANK = 7          /* rank-deficient reset (lyapunov.py:191-192)       */
+} goom_status;
+
+/* ---- library ------------------------------------------------------------- */
+const char* goom_last_error(void);
+const char* goom_version(void);
+/* 1 if `device` is an sm_100 part this build can run on, else 0. */
+int goom_device_supported(int device);
+
+/* ---- conversions (core.py:93-113, 188-239, 313-323) ------------------------ */
+/* x -> (log|x|, sign); x == 0 -> (zero_log, +1).  _log_sign_arrays core.py:229-239.
+ * NaN/inf inputs are NOT checked here (the Python layer raises like core.py:194-197). */
+int goom_from_real_f32(const float* x, goom_c64* out, int64_t n, float zero_log, void* stream);
+int goom_from_real_f64(const double* x, goom_c64* out, int64_t n, double zero_log, void* stream);
+/* sign * exp(log), overflow -> +-inf.  GoomMatrix.to_real core.py:213-216. */
+int goom_to_real_f32(const goom_c64* z, float* out, int64_t n, void* stream);
+int goom_to_real_f64(const goom_c64* z, double* out, int64_t n, void* stream);
+/* Per matrix b of `batch` (each `n` elements): c_b = max log (0 if all zero),
+ * out = sign * exp(log - c_b + 2).  to_real_scaled core.py:313-323.
+ * c is a device array of `batch` floats. */
+int goom_to_real_scaled_f32(const goom_c64* z, float* out, float* c, int64_t batch, int64_t n,
+                            void* stream);
+/* Elementwise signed log-sum-exp, bitwise commutative.  _gadd_arrays core.py:264-275. */
+int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream);
+/* Per-column log Euclidean norms of batch x (rows x cols) -> batch x cols floats.
+ * _col_log_norms core.py:288-296. */
+int goom_col_log_norms_c64(const goom_c64* z, float* out, int64_t batch, int rows, int cols,
+                           void* stream);
+
+/* ---- LMME (core.py:242-285, Eq. 10-12) ------------------------------------- */
+/* C[b] = A[b] (x) B[b]  for b < batch;  A: n x k, B: k x m, C: n x m.
+ * a = max(rowmax Re A, 0), b = max(colmax Re B, 0); I = (sA e^{A-a}) @ (sB e^{B-b})
+ * (fp32-accurate: SIMT FP32 for small/odd shapes, 3xTF32 tcgen05 for tiles);
+ * C = (log|I| + a) + b, sign(I).  Operand b addresses base + (b/div)*stride.
+ * C must not alias A or B. */
+typedef struct goom_operand {
+  const goom_c64* ptr;
+  int64_t stride;  /* elements between consecutive matrices (0 = broadcast) */
+  int64_t div;     /* matrix index = b / div (>= 1)                          */
+} goom_operand;
+
+size_t goom_lmme_workspace_size(int64_t batch, int n, int k, int m);
+int goom_lmme_c64(goom_operand A, goom_operand B, goom_c64* C, int64_t strideC, int64_t batch,
+                  int n, int k, int m, void* ws, size_t ws_bytes, void* stream);
+/* Fused combine step: C[b] = (A[b] (x) B[b]) (+) D[b]   (_combine_arrays bias slot,
+ * scan.py:176-177).  D.ptr == NULL behaves like goom_lmme_c64. */
+int goom_lmme_gadd_c64(goom_operand A, goom_operand B, goom_operand D, goom_c64* C,
+                       int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
+                       size_t ws_bytes, void* stream);
+/* Force a kernel family for testing: 0 auto, 1 SIMT, 2 tcgen05 3xTF32. Returns the
+ * previous value. Process-wide. */
+int goom_set_lmme_backend(int backend);
+
+/* ---- prefix scans (scan.py:181-214, 317-353, 529-563) ---------------------- */
+/* Inclusive product chain out[t] = A[t] (x) ... (x) A[0] (x) carry_in, blocked exactly
+ * like _scan_affine_stack's A slot (scan.py:181-214) with block = `block`:
+ * products accumulate on the left. carry_in (d x d) may be NULL. */
+size_t goom_scan_chain_workspace_size(int64_t T, int d, int block);
+int goom_scan_chain_c64(const goom_c64* A, goom_c64* out, int64_t T, int d, int block,
+                        const goom_c64* carry_in, void* ws, size_t ws_bytes, void* stream);
+
+/* Inclusive affine scan of pairs (A_t: d x d, B_t: d x m, flag_t) under
+ * combine_affine (scan.py:92-103): (A,B) <- (A_t A, A_t B (+) B_t), flag OR.
+ * Same two-level tree as _scan_affine_stack. flags may be NULL (all false). */
+size_t goom_scan_affine_workspace_size(int64_t T, int d, int m, int block);
+int goom_scan_affine_c64(const goom_c64* A, const goom_c64* B, const uint8_t* flags_in,
+                         goom_c64* outA, goom_c64* outB, uint8_t* flags_out, int64_t T, int d,
+                         int m, int block, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- selective resetting (scan.py:342-484, lyapunov.py:146-278) ------------- */
+typedef enum goom_policy_kind {
+  GOOM_POLICY_NEVER = 0,        /* select == false                                    */
+  GOOM_POLICY_COLINEARITY = 1,  /* lyapunov.colinearity_policy: |cos| > threshold or
+                                   logdet(unit-column state) < log_volume_floor;
+                                   reset = CGS2 orthonormal basis (lyapunov.py:175-219) */
+  GOOM_POLICY_NORM_THRESHOLD = 2 /* max column log-norm > threshold; reset = Householder
+                                   Q (LAPACK sign convention) of the unit-column state
+                                   (the reference scan tests' policy, test_scan.py:60-75) */
+} goom_policy_kind;
+
+typedef struct goom_reset_policy {
+  int32_t kind;            /* goom_policy_kind                              */
+  int32_t check_interval;  /* >= 1; tested positions p: (p+1) % interval == 0 */
+  int32_t consume_leaf;    /* 1: reset value replaces the site's state        */
+  int32_t reserved;
+  double threshold;        /* cosine threshold or log-norm threshold          */
+  double log_volume_floor; /* log(volume_floor), colinearity only             */
+} goom_reset_policy;
+
+/* Selective scan over a pure product chain: V[t] = compound state at t with
+ * value-determined resets (_selective_chain_core scan.py:342-353; strided tile
+ * walk for interval > 1, per-position walk for interval == 1 with tile `block`).
+ * sites: device int64 array with room for T entries; n_sites: device int64.
+ * Sites are identical to the sequential reference (scan.py:226-246). */
+size_t goom_scan_selective_chain_workspace_size(int64_t T, int d,
+                                                const goom_reset_policy* policy, int block);
+int goom_scan_selective_chain_c64(const goom_c64* A, goom_c64* V, int64_t T, int d,
+                                  const goom_reset_policy* policy, int block, int64_t* sites,
+                                  int64_t* n_sites, void* ws, size_t ws_bytes, void* stream);
+
+/* Batched policy evaluation on states X[b] (d x d): fire[b] = select(X[b]).
+ * Used by the general-bias selective rounds (scan.py:255-314). */
+int goom_policy_select_c64(const goom_c64* X, int64_t batch, int d, const goom_reset_policy* policy,
+                           uint8_t* fire, void* stream);
+/* R[b] = reset(X[b]) for the policy's reset map. */
+int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
+                          const goom_reset_policy* policy, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOOM_H_ */

@@ -1,0 +1,357 @@
+"""GOOM representation and log-domain arithmetic — drop-in for `gooms.core`.
+
+A matrix of GOOMs is ONE complex64 CUDA tensor: real part log|x|, imaginary
+part 0 or pi (the paper's Complex64 GOOM). The reference
+stores the same information as two same-dtype arrays (log_mag, sign)
+(core.py:148-170); `GoomMatrix.log_mag` / `.sign` expose that view.
+
+Array work (conversions, LMME, gadd, column norms, scaled export) runs in the
+sm_100a library through `torch.ops.goom.*`. The scalar helpers (`Goom`,
+`gmul`, `gadd`, `lse_reduce`, scalar `from_real` / `to_real`) are host-side
+scalar API kept for drop-in completeness (reference core.py:16-145); they are
+not on the data-parallel path.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+
+NEG_INF = float("-inf")
+PI32 = float(np.float32(np.pi))
+BACKINGS = {32: np.float32, 64: np.float64}
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_03426_b200 needs a CUDA (sm_100a) device; there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------------------
+# scalar API (host side; core.py:21-145)
+
+
+def floor_for(bits):
+    """log(SNN^2) of a backing format (core.py:21-30)."""
+    dtype = BACKINGS[bits]
+    return 2.0 * math.log(float(np.finfo(dtype).tiny))
+
+
+@dataclass(frozen=True)
+class ZeroPolicy:
+    """Encoding of the real zero: -inf sentinel or a finite floor (core.py:33-56)."""
+
+    mode: str = "sentinel"
+    floor_value: float = NEG_INF
+
+    def __post_init__(self):
+        if self.mode not in ("sentinel", "finite_floor"):
+            raise ValueError(f"unknown zero-policy mode {self.mode!r}")
+        if self.mode == "finite_floor" and not math.isfinite(self.floor_value):
+            raise ValueError("finite_floor policy needs a finite floor_value")
+
+    @staticmethod
+    def sentinel():
+        return ZeroPolicy("sentinel", NEG_INF)
+
+    @staticmethod
+    def finite_floor(bits=64):
+        return ZeroPolicy("finite_floor", floor_for(bits))
+
+    @property
+    def zero_log(self):
+        return self.floor_value if self.mode == "finite_floor" else NEG_INF
+
+
+SENTINEL = ZeroPolicy.sentinel()
+
+
+@dataclass(frozen=True, eq=False)
+class Goom:
+    """One real as (log|x|, sign); zeros compare equal regardless of sign."""
+
+    log_mag: float
+    sign: int
+
+    def __post_init__(self):
+        if self.sign not in (1, -1):
+            raise ValueError("sign must be +1 or -1")
+        if math.isnan(self.log_mag):
+            raise ValueError("log_mag must not be NaN")
+
+    def __eq__(self, other):
+        if not isinstance(other, Goom):
+            return NotImplemented
+        if self.log_mag == NEG_INF and other.log_mag == NEG_INF:
+            return True
+        return self.log_mag == other.log_mag and self.sign == other.sign
+
+    def __hash__(self):
+        return hash((NEG_INF, 1)) if self.log_mag == NEG_INF else hash((self.log_mag, self.sign))
+
+    def as_complex(self) -> complex:
+        return complex(self.log_mag, math.pi if self.sign < 0 else 0.0)
+
+
+def from_real(x, policy=SENTINEL):
+    x = float(x)
+    if math.isnan(x):
+        raise ValueError("cannot represent NaN")
+    if math.isinf(x):
+        raise ValueError("cannot represent an infinite value")
+    if x == 0.0:
+        return Goom(policy.zero_log, 1)
+    return Goom(math.log(abs(x)), -1 if x < 0.0 else 1)
+
+
+def to_real(g):
+    if g.log_mag == NEG_INF:
+        return 0.0
+    try:
+        mag = math.exp(g.log_mag)
+    except OverflowError:
+        mag = math.inf
+    return g.sign * mag
+
+
+def gmul(a, b):
+    if a.log_mag == NEG_INF or b.log_mag == NEG_INF:
+        return Goom(NEG_INF, 1)
+    return Goom(a.log_mag + b.log_mag, a.sign * b.sign)
+
+
+def gadd(a, b, policy=SENTINEL):
+    top = max(a.log_mag, b.log_mag)
+    if top == NEG_INF:
+        return Goom(policy.zero_log, 1)
+    t = a.sign * math.exp(a.log_mag - top) + b.sign * math.exp(b.log_mag - top)
+    if t == 0.0:
+        return Goom(policy.zero_log, 1)
+    return Goom(top + math.log(abs(t)), -1 if t < 0.0 else 1)
+
+
+def lse_reduce(gooms, policy=SENTINEL):
+    gooms = list(gooms)
+    if not gooms:
+        raise ValueError("lse_reduce needs at least one element")
+    top = max(g.log_mag for g in gooms)
+    if top == NEG_INF:
+        return Goom(policy.zero_log, 1)
+    t = math.fsum(g.sign * math.exp(g.log_mag - top) for g in gooms)
+    if t == 0.0:
+        return Goom(policy.zero_log, 1)
+    return Goom(top + math.log(abs(t)), -1 if t < 0.0 else 1)
+
+
+# ---------------------------------------------------------------------------
+# tensor helpers
+
+
+def _to_tensor(x, dtype=None):
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.as_tensor(np.asarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(_device())
+
+
+def join(log_mag, sign) -> torch.Tensor:
+    """(log, sign) arrays -> complex64 GOOM tensor on the GPU."""
+    log_t = _to_tensor(log_mag)
+    if log_t.is_complex():
+        raise ValueError("log_mag must be real")
+    sign_t = _to_tensor(sign, log_t.dtype)
+    if log_t.shape != sign_t.shape:
+        raise ValueError("log_mag and sign shapes differ")
+    im = torch.where(sign_t < 0, torch.tensor(PI32, device=log_t.device),
+                     torch.tensor(0.0, device=log_t.device))
+    return torch.complex(log_t.to(torch.float32), im.to(torch.float32))
+
+
+def split(z: torch.Tensor):
+    """complex64 GOOM tensor -> (log_mag float32, sign float32 in {+1,-1})."""
+    sign = torch.where(torch.cos(z.imag) < 0, -1.0, 1.0).to(torch.float32)
+    return z.real, sign
+
+
+def _like_input(t: torch.Tensor, ref):
+    if isinstance(ref, np.ndarray):
+        return t.detach().cpu().numpy()
+    return t
+
+
+# ---------------------------------------------------------------------------
+# GoomMatrix (core.py:148-226)
+
+
+class GoomMatrix:
+    """Dense 2-D GOOM matrix backed by a complex64 CUDA tensor (`.data`)."""
+
+    __slots__ = ("data",)
+
+    def __init__(self, log_mag, sign=None):
+        if sign is None:
+            z = log_mag if isinstance(log_mag, torch.Tensor) else _to_tensor(log_mag)
+            if not z.is_complex():
+                raise ValueError("single-argument GoomMatrix takes a complex GOOM tensor")
+            z = z.to(device=_device(), dtype=torch.complex64)
+        else:
+            z = join(log_mag, sign)
+        if z.dim() != 2:
+            raise ValueError("GoomMatrix is 2-D")
+        if bool(torch.isnan(z.real).any()):
+            raise ValueError("log_mag must not contain NaN")
+        self.data = z
+
+    @classmethod
+    def _wrap(cls, z: torch.Tensor) -> "GoomMatrix":
+        obj = cls.__new__(cls)
+        obj.data = z
+        return obj
+
+    @property
+    def rows(self):
+        return self.data.shape[0]
+
+    @property
+    def cols(self):
+        return self.data.shape[1]
+
+    @property
+    def shape(self):
+        return tuple(self.data.shape)
+
+    @property
+    def dtype(self):
+        return self.data.dtype
+
+    @property
+    def log_mag(self) -> torch.Tensor:
+        return self.data.real
+
+    @property
+    def sign(self) -> torch.Tensor:
+        return split(self.data)[1]
+
+    def numpy(self):
+        """(log_mag, sign) as float64 numpy arrays (the reference's storage)."""
+        l, s = split(self.data)
+        return l.double().cpu().numpy(), s.double().cpu().numpy()
+
+    @classmethod
+    def from_real(cls, values, policy=SENTINEL, dtype=None):
+        """Elementwise real -> GOOM on the GPU (core.py:188-199)."""
+        v = _to_tensor(values)
+        if v.dtype not in (torch.float32, torch.float64):
+            v = v.to(torch.float64)
+        if dtype is not None and np.dtype(dtype) == np.float32:
+            v = v.to(torch.float32)
+        if v.dim() != 2:
+            raise ValueError("expected a 2-D array")
+        if bool(torch.isnan(v).any()):
+            raise ValueError("cannot represent NaN")
+        if bool(torch.isinf(v).any()):
+            raise ValueError("cannot represent an infinite value")
+        return cls._wrap(torch.ops.goom.from_real(v, float(policy.zero_log)))
+
+    @classmethod
+    def zeros(cls, rows, cols, policy=SENTINEL, dtype=None):
+        z = torch.full((rows, cols), complex(policy.zero_log, 0.0), dtype=torch.complex64,
+                       device=_device())
+        return cls._wrap(z)
+
+    @classmethod
+    def identity(cls, n, policy=SENTINEL, dtype=None):
+        z = torch.full((n, n), complex(policy.zero_log, 0.0), dtype=torch.complex64,
+                       device=_device())
+        z.diagonal().real.zero_()
+        return cls._wrap(z)
+
+    def to_real(self, double=False):
+        """sign * exp(log) on the GPU; overflow -> +-inf (core.py:213-216)."""
+        return torch.ops.goom.to_real(self.data, bool(double))
+
+    def __getitem__(self, idx):
+        i, j = idx
+        z = complex(self.data[i, j].item())
+        if z.real == NEG_INF:
+            return Goom(NEG_INF, 1)
+        return Goom(z.real, -1 if math.cos(z.imag) < 0 else 1)
+
+    def __repr__(self):
+        return f"GoomMatrix({self.rows}x{self.cols}, complex64 on {self.data.device})"
+
+
+# ---------------------------------------------------------------------------
+# array-level kernels (core.py:229-323)
+
+
+def _log_sign_arrays(values, policy=SENTINEL):
+    """real -> (log|v|, sign) with the zero encoding (core.py:229-239)."""
+    v = _to_tensor(values)
+    if v.dtype not in (torch.float32, torch.float64):
+        v = v.to(torch.float64)
+    z = torch.ops.goom.from_real(v.contiguous(), float(policy.zero_log))
+    l, s = split(z)
+    return _like_input(l, values), _like_input(s, values)
+
+
+def log_matmul_exp(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """LMME on complex64 GOOM tensors with np.matmul broadcasting (Eq. 9-12)."""
+    return torch.ops.goom.lmme(x, y)
+
+
+def _lmme_arrays(alog, asign, blog, bsign):
+    """Array-level LMME (core.py:242-261); returns (log, sign) like the inputs."""
+    z = torch.ops.goom.lmme(join(alog, asign), join(blog, bsign))
+    l, s = split(z)
+    return _like_input(l, alog), _like_input(s, alog)
+
+
+def _gadd_arrays(alog, asign, blog, bsign):
+    """Elementwise signed LSE (core.py:264-275)."""
+    z = torch.ops.goom.gadd(join(alog, asign), join(blog, bsign))
+    l, s = split(z)
+    return _like_input(l, alog), _like_input(s, alog)
+
+
+def lmme(a: GoomMatrix, b: GoomMatrix) -> GoomMatrix:
+    """Log-domain matrix product exp(a) @ exp(b) (core.py:278-285)."""
+    if a.cols != b.rows:
+        raise ValueError(f"dimension mismatch: {a.shape} x {b.shape}")
+    if a.dtype != b.dtype:
+        raise ValueError("operands must share a backing dtype")
+    return GoomMatrix._wrap(torch.ops.goom.lmme(a.data, b.data))
+
+
+def _col_log_norms(log_mag):
+    """Per-column log Euclidean norms over axis -2 (core.py:288-296)."""
+    l = _to_tensor(log_mag)
+    z = torch.complex(l.to(torch.float32), torch.zeros_like(l, dtype=torch.float32))
+    out = torch.ops.goom.col_log_norms(z).unsqueeze(-2)
+    return _like_input(out, log_mag)
+
+
+def log_unit_norm_columns(m: GoomMatrix):
+    """Shift columns to log-unit Euclidean norm; returns (matrix, shifts) (core.py:299-310)."""
+    nu = torch.ops.goom.col_log_norms(m.data)
+    if bool((nu == NEG_INF).any()):
+        raise ValueError("cannot normalize an all-zero column")
+    re = m.data.real
+    out_log = torch.where(re == NEG_INF, re, re - nu.unsqueeze(0))
+    z = torch.complex(out_log, m.data.imag)
+    return GoomMatrix._wrap(z), nu.double().cpu().numpy()
+
+
+def to_real_scaled(m: GoomMatrix):
+    """Eq. 29: sign*exp(log - c + 2) with c the max log (core.py:313-323)."""
+    out, c = torch.ops.goom.to_real_scaled(m.data)
+    return out, float(c.item())

@@ -1,0 +1,636 @@
+// Selective-reset product-chain scan (scan.py:342-504 + lyapunov.py:146-278).
+//
+// Structure (the reference's strided walk, scan.py:356-428, on the device):
+//   1. local products per tile of s = check_interval leaves, batched across
+//      tiles (the chain engine's phase 1; with consume_leaf also the variant
+//      whose tile starts at the identity, scan.py:317-339);
+//   2. ONE persistent CTA walks the tiles in order. Per tile it forms the tile
+//      total el = loc[p] (x) carry with a CTA-level LMME (carry resident in
+//      shared memory), evaluates the policy predicate on el in FP64, and on a
+//      fire replaces the carry by the policy's reset value and records the
+//      site p+1. The predicate and the reset are fused into the walk — no host
+//      round trip per tile;
+//   3. every position is materialised in one batched LMME, loc[t] (x) carry[t/s].
+// check_interval == 1 is the same machinery with s = 1 (every position tested):
+// the per-position walk of scan.py:431-484 collapses to the sequential fold,
+// whose reset sites the reference proves identical (scan.py:9-12).
+//
+// Policies (FP64 inside the CTA, d <= 64):
+//   colinearity: log-unit-normalised columns (lyapunov.py:255-263); fire on an
+//     all-zero column, on max_{i<j} |G_ij| > threshold (G = R^T R) or on
+//     log|det R| < log(volume_floor) / det == 0 (LU with partial pivoting, as
+//     LAPACK getrf behind np.linalg.slogdet);
+//     reset = the CGS2 orthonormal basis (lyapunov.py:175-219). It is computed
+//     as Householder QR with column signs chosen so diag(R) > 0 — the same Q
+//     (QR with positive diagonal is unique), rank-deficiency at |R_jj| < 64 eps.
+//   norm-threshold: fire when max_j log||col_j|| > threshold; reset = LAPACK-
+//     convention Householder Q of the unit-column matrix (np.linalg.qr,
+//     pkg/tests/test_scan.py:60-75).
+#include <vector>
+
+#include "goom_internal.cuh"
+
+namespace goom {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxD = 64;
+
+struct Policy {
+  int kind;
+  int interval;
+  int consume;
+  double threshold;
+  double log_floor;
+};
+
+struct Smem {
+  float2* carry;  // d*d
+  float2* el;     // d*d
+  double* R;      // d*d (aliases the f32 LMME operand buffers)
+  double* W;      // d*d
+  float* tl;      // d*d (== (float*)R)
+  float* tr;      // d*d
+  float* scal;    // 2d
+  double* vec;    // 2d
+  double* red;    // 2 * kWarps
+  int* ints;      // 8
+};
+
+__host__ __device__ inline size_t smem_bytes(int d) {
+  size_t dd = (size_t)d * d;
+  return 2 * dd * sizeof(float2) + 2 * dd * sizeof(double) + 2 * d * sizeof(float) +
+         2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + 64;
+}
+
+__device__ Smem carve(char* base, int d) {
+  Smem s;
+  size_t dd = (size_t)d * d;
+  s.carry = reinterpret_cast<float2*>(base);
+  s.el = s.carry + dd;
+  s.R = reinterpret_cast<double*>(s.el + dd);
+  s.W = s.R + dd;
+  s.tl = reinterpret_cast<float*>(s.R);
+  s.tr = s.tl + dd;
+  s.vec = s.W + dd;
+  s.red = s.vec + 2 * d;
+  s.scal = reinterpret_cast<float*>(s.red + 2 * kWarps);
+  s.ints = reinterpret_cast<int*>(s.scal + 2 * d);
+  return s;
+}
+
+__device__ double block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < kWarps; ++i) r = fmax(r, red[i]);
+  return r;
+}
+
+__device__ __forceinline__ float lmme_out_log(float acc, float a, float b) {
+  return __fadd_rn(__fadd_rn(logf(fabsf(acc)), a), b);
+}
+
+// out (smem) = Lg (global, d x d) (x) Rs (smem, d x d); Eq. 10-12 in FP32.
+__device__ void block_lmme(const float2* __restrict__ Lg, const float2* Rs, float2* out, int d,
+                           const Smem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = w; i < d; i += kWarps) {
+    float m = kNegInf;
+    for (int j = lane; j < d; j += 32) m = fmaxf(m, Lg[i * d + j].x);
+    m = warp_max(m);
+    if (lane == 0) sm.scal[i] = fmaxf(m, 0.0f);
+  }
+  for (int j = tid; j < d; j += kThreads) {
+    float m = kNegInf;
+    for (int r = 0; r < d; ++r) m = fmaxf(m, Rs[r * d + j].x);
+    sm.scal[d + j] = fmaxf(m, 0.0f);
+  }
+  __syncthreads();
+  for (int e = tid; e < d * d; e += kThreads) {
+    int i = e / d, kk = e % d;
+    float2 z = Lg[e];
+    sm.tl[kk * d + i] = goom_sign(z.y) * expf(z.x - sm.scal[i]);
+    float2 q = Rs[e];
+    sm.tr[e] = goom_sign(q.y) * expf(q.x - sm.scal[d + kk]);  // e = kk2*d + j, col j = kk here
+  }
+  __syncthreads();
+  const int ty = tid >> 4, tx = tid & 15;
+  float acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+  for (int kk = 0; kk < d; ++kk) {
+    float av[4], bv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int i = ty + 16 * r;
+      av[r] = i < d ? sm.tl[kk * d + i] : 0.0f;
+      int j = tx + 16 * r;
+      bv[r] = j < d ? sm.tr[kk * d + j] : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int i = ty + 16 * r;
+    if (i >= d) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int j = tx + 16 * c;
+      if (j >= d) continue;
+      float a = acc[r][c];
+      out[i * d + j] = make_float2(lmme_out_log(a, sm.scal[i], sm.scal[d + j]),
+                                   a < 0.0f ? kPi : 0.0f);
+    }
+  }
+  __syncthreads();
+}
+
+// Column log-norms nu_j (FP64) into sm.vec[0..d); returns true if a column is all zero.
+__device__ bool unit_columns(const float2* X, int d, const Smem& sm) {
+  const int tid = threadIdx.x;
+  if (tid == 0) sm.ints[0] = 0;
+  __syncthreads();
+  for (int j = tid; j < d; j += kThreads) {
+    float m = kNegInf;
+    for (int r = 0; r < d; ++r) m = fmaxf(m, X[r * d + j].x);
+    if (m == kNegInf) {
+      sm.ints[0] = 1;
+      sm.vec[j] = -INFINITY;
+      continue;
+    }
+    double dm = (double)m, acc = 0.0;
+    for (int r = 0; r < d; ++r) acc += exp(2.0 * ((double)X[r * d + j].x - dm));
+    sm.vec[j] = dm + 0.5 * log(acc);
+  }
+  __syncthreads();
+  bool zero = sm.ints[0] != 0;
+  if (!zero) {
+    for (int e = tid; e < d * d; e += kThreads) {
+      float2 z = X[e];
+      sm.R[e] = (double)goom_sign(z.y) * exp((double)z.x - sm.vec[e % d]);
+    }
+  }
+  __syncthreads();
+  return zero;
+}
+
+// slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor
+__device__ bool volume_deficient(int d, double log_floor, const Smem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int e = tid; e < d * d; e += kThreads) sm.W[e] = sm.R[e];
+  __syncthreads();
+  double logdet = 0.0;
+  for (int c = 0; c < d; ++c) {
+    if (w == 0) {
+      double best = -1.0;
+      int bi = c;
+      for (int r = c + lane; r < d; r += 32) {
+        double v = fabs(sm.W[r * d + c]);
+        if (v > best) { best = v; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) sm.ints[1] = bi;
+    }
+    __syncthreads();
+    const int piv = sm.ints[1];
+    const double pv = sm.W[piv * d + c];
+    if (pv == 0.0) return true;  // det_sign == 0
+    if (piv != c)
+      for (int j = tid; j < d; j += kThreads) {
+        double t = sm.W[c * d + j];
+        sm.W[c * d + j] = sm.W[piv * d + j];
+        sm.W[piv * d + j] = t;
+      }
+    __syncthreads();
+    logdet += log(fabs(pv));
+    const double inv = 1.0 / pv;
+    for (int r = c + 1 + tid; r < d; r += kThreads) sm.vec[d + r] = sm.W[r * d + c] * inv;
+    __syncthreads();
+    const int n = d - c - 1;
+    for (int e = tid; e < n * n; e += kThreads) {
+      int r = c + 1 + e / n, j = c + 1 + e % n;
+      sm.W[r * d + j] -= sm.vec[d + r] * sm.W[c * d + j];
+    }
+    __syncthreads();
+  }
+  return logdet < log_floor;
+}
+
+__device__ bool policy_select(const float2* X, int d, const Policy& pol, const Smem& sm) {
+  if (pol.kind == GOOM_POLICY_NEVER) return false;
+  bool zero = unit_columns(X, d, sm);
+  if (pol.kind == GOOM_POLICY_NORM_THRESHOLD) {
+    double m = -INFINITY;
+    for (int j = threadIdx.x; j < d; j += kThreads) m = fmax(m, sm.vec[j]);
+    return block_max(m, sm.red) > pol.threshold;
+  }
+  if (zero) return true;
+  double g = 0.0;
+  for (int e = threadIdx.x; e < d * d; e += kThreads) {
+    int i = e / d, j = e % d;
+    if (i >= j) continue;
+    double acc = 0.0;
+    for (int r = 0; r < d; ++r) acc = fma(sm.R[r * d + i], sm.R[r * d + j], acc);
+    g = fmax(g, fabs(acc));
+  }
+  if (block_max(g, sm.red) > pol.threshold) return true;
+  if (pol.log_floor == -INFINITY) return false;
+  return volume_deficient(d, pol.log_floor, sm);
+}
+
+// Householder QR of sm.R in place; Q into sm.W. positive_diag flips Q columns so
+// that diag(R) > 0 (the CGS2 basis). Returns GOOM_ERANK on a rank-deficient state.
+__device__ int householder_q(int d, bool positive_diag, const Smem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double* tau = sm.vec;      // [0, d)
+  double* diag = sm.vec + d;  // [d, 2d)
+  for (int j = 0; j < d; ++j) {
+    if (w == 0) {
+      double s = 0.0;
+      for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.R[r * d + j], s);
+      s = warp_sum_d(s);
+      if (lane == 0) {
+        double alpha = sm.R[j * d + j];
+        if (s == 0.0) {
+          tau[j] = 0.0;
+          diag[j] = alpha;
+          sm.red[0] = 0.0;
+        } else {
+          double beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
+          tau[j] = (beta - alpha) / beta;
+          diag[j] = beta;
+          sm.red[0] = 1.0 / (alpha - beta);
+          sm.R[j * d + j] = beta;
+        }
+      }
+    }
+    __syncthreads();
+    const double scale = sm.red[0];
+    const double tj = tau[j];
+    if (tj != 0.0) {
+      for (int r = j + 1 + tid; r < d; r += kThreads) sm.R[r * d + j] *= scale;  // v_r
+      __syncthreads();
+      for (int c = j + 1 + w; c < d; c += kWarps) {
+        double s = lane == 0 ? sm.R[j * d + c] : 0.0;
+        for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.R[r * d + c], s);
+        s = warp_sum_d(s) * tj;
+        if (lane == 0) sm.R[j * d + c] -= s;
+        for (int r = j + 1 + lane; r < d; r += 32) sm.R[r * d + c] -= s * sm.R[r * d + j];
+      }
+    }
+    __syncthreads();
+  }
+  // Q = H_0 ... H_{d-1} I, accumulated backwards (LAPACK dorg2r order)
+  for (int e = tid; e < d * d; e += kThreads) sm.W[e] = (e / d == e % d) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = d - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    for (int c = w; c < d; c += kWarps) {
+      double s = lane == 0 ? sm.W[j * d + c] : 0.0;
+      for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.W[r * d + c], s);
+      s = warp_sum_d(s) * tj;
+      if (lane == 0) sm.W[j * d + c] -= s;
+      for (int r = j + 1 + lane; r < d; r += 32) sm.W[r * d + c] -= s * sm.R[r * d + j];
+    }
+    __syncthreads();
+  }
+  int rc = GOOM_OK;
+  if (positive_diag) {
+    const double tiny = 64.0 * 2.220446049250313e-16;
+    for (int j = 0; j < d; ++j)
+      if (fabs(diag[j]) < tiny) rc = GOOM_ERANK;
+    if (rc == GOOM_OK)
+      for (int e = tid; e < d * d; e += kThreads)
+        if (diag[e % d] < 0.0) sm.W[e] = -sm.W[e];
+  }
+  __syncthreads();
+  return rc;
+}
+
+// reset(X) -> out (smem or global), canonical GOOMs. Returns a goom_status.
+__device__ int policy_reset(const float2* X, float2* out, int d, int kind, const Smem& sm) {
+  bool zero = unit_columns(X, d, sm);
+  if (zero) return GOOM_ERANK;
+  int rc = householder_q(d, kind == GOOM_POLICY_COLINEARITY, sm);
+  if (rc != GOOM_OK) return rc;
+  for (int e = threadIdx.x; e < d * d; e += kThreads) {
+    double q = sm.W[e];
+    out[e] = make_float2((float)log(fabs(q)), q < 0.0 ? kPi : 0.0f);
+  }
+  __syncthreads();
+  return GOOM_OK;
+}
+
+__device__ void copy_mat(const float2* src, float2* dst, int d) {
+  for (int e = threadIdx.x; e < d * d; e += kThreads) dst[e] = src[e];
+  __syncthreads();
+}
+
+// ---- the fused walk ----------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    selective_walk_kernel(const float2* __restrict__ loc0, const float2* __restrict__ loc1,
+                          float2* __restrict__ carries, int8_t* __restrict__ modes,
+                          int64_t* __restrict__ sites, int64_t* __restrict__ n_sites,
+                          int* __restrict__ status, int64_t T, int d, int s, Policy pol) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem sm = carve(smem_raw, d);
+  const int64_t mat = (int64_t)d * d;
+  const int64_t ntiles = (T + s - 1) / s;
+  int64_t nsite = 0;
+  bool have_carry = false, consumed = false;
+  for (int64_t k = 0; k < ntiles; ++k) {
+    const int64_t lo = k * s;
+    const int64_t p = (lo + s < T ? lo + s : T) - 1;
+    int8_t mode;
+    if (!have_carry) {
+      mode = 0;
+      copy_mat(loc0 + p * mat, sm.el, d);
+    } else if (consumed) {
+      mode = 2;
+      if (p == lo) copy_mat(sm.carry, sm.el, d);
+      else block_lmme(loc1 + p * mat, sm.carry, sm.el, d, sm);
+    } else {
+      mode = 1;
+      block_lmme(loc0 + p * mat, sm.carry, sm.el, d, sm);
+    }
+    if (mode > 0)
+      for (int e = threadIdx.x; e < d * d; e += kThreads) carries[k * mat + e] = sm.carry[e];
+    if (threadIdx.x == 0) modes[k] = mode;
+    consumed = false;
+    bool fire = false;
+    if ((p % s) == s - 1 && p <= T - 2) fire = policy_select(sm.el, d, pol, sm);
+    if (fire) {
+      int rc = policy_reset(sm.el, sm.carry, d, pol.kind, sm);
+      if (rc != GOOM_OK) {
+        if (threadIdx.x == 0) *status = rc;
+        break;
+      }
+      if (threadIdx.x == 0) sites[nsite] = p + 1;
+      ++nsite;
+      consumed = pol.consume != 0;
+    } else {
+      copy_mat(sm.el, sm.carry, d);
+    }
+    have_carry = true;
+  }
+  if (threadIdx.x == 0) *n_sites = nsite;
+}
+
+// mode-2 tiles: loc0[tile] <- loc1[tile] (before materialisation)
+__global__ void adopt_loc1_kernel(float2* loc0, const float2* loc1, const int8_t* modes,
+                                  int64_t T, int d, int s) {
+  const int64_t k = blockIdx.x;
+  if (modes[k] != 2) return;
+  const int64_t mat = (int64_t)d * d;
+  int64_t lo = k * s, hi = lo + s < T ? lo + s : T;
+  for (int64_t e = threadIdx.x; e < (hi - lo) * mat; e += blockDim.x)
+    loc0[lo * mat + e] = loc1[lo * mat + e];
+}
+
+// mode-2 tiles: V[k*s] <- carry[k] (the consuming reset's own slot, scan.py:423-427)
+__global__ void fix_reset_slots_kernel(float2* V, const float2* carries, const int8_t* modes,
+                                       int d, int s) {
+  const int64_t k = blockIdx.x;
+  if (modes[k] != 2) return;
+  const int64_t mat = (int64_t)d * d;
+  for (int64_t e = threadIdx.x; e < mat; e += blockDim.x) V[k * s * mat + e] = carries[k * mat + e];
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    policy_select_kernel(const float2* X, int d, Policy pol, uint8_t* fire) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem sm = carve(smem_raw, d);
+  const int64_t mat = (int64_t)d * d;
+  copy_mat(X + blockIdx.x * mat, sm.el, d);
+  bool f = policy_select(sm.el, d, pol, sm);
+  if (threadIdx.x == 0) fire[blockIdx.x] = f ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    policy_reset_kernel(const float2* X, float2* R, int d, int kind, int* status) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem sm = carve(smem_raw, d);
+  const int64_t mat = (int64_t)d * d;
+  copy_mat(X + blockIdx.x * mat, sm.el, d);
+  int rc = policy_reset(sm.el, R + blockIdx.x * mat, d, kind, sm);
+  if (rc != GOOM_OK && threadIdx.x == 0) *status = rc;
+}
+
+inline size_t round_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+int check_policy(const goom_reset_policy* p, int d) {
+  if (!p) return fail(GOOM_EINVAL, "null policy");
+  if (p->check_interval < 1) return fail(GOOM_EINVAL, "check_interval must be >= 1");
+  if (p->kind < GOOM_POLICY_NEVER || p->kind > GOOM_POLICY_NORM_THRESHOLD)
+    return fail(GOOM_EINVAL, "unknown policy kind");
+  if (d > kMaxD && p->kind != GOOM_POLICY_NEVER)
+    return fail(GOOM_EUNSUPPORTED, "built-in reset policies run in one CTA: d <= 64");
+  return GOOM_OK;
+}
+
+Policy to_policy(const goom_reset_policy* p) {
+  return Policy{p->kind, p->check_interval, p->consume_leaf, p->threshold, p->log_volume_floor};
+}
+
+int set_smem(const void* fn, int d) {
+  size_t need = smem_bytes(d);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) !=
+      cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "selective smem attribute");
+  return GOOM_OK;
+}
+
+// L[k*s] = first ? I : A[k*s];  L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]   (scan.py:317-339)
+int local_products(const float2* A, float2* L, int64_t T, int d, int64_t s, bool skip_first,
+                   void* lws, size_t lws_bytes, cudaStream_t st) {
+  const int64_t mat = (int64_t)d * d;
+  const int64_t nb = (T + s - 1) / s;
+  if (cudaMemcpy2DAsync(L, sizeof(float2) * mat * s, A, sizeof(float2) * mat * s,
+                        sizeof(float2) * mat, nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "local products copy");
+  if (skip_first) {
+    // identity at every tile start
+    GOOM_TRY(launch_identity(L, nb, d, s * mat, st));
+  }
+  for (int64_t i = 1; i < s; ++i) {
+    int64_t cnt = (T - i + s - 1) / s;
+    if (cnt <= 0) break;
+    LmmeProblem p{};
+    p.A = Operand{A + i * mat, s * mat, 1};
+    p.B = Operand{L + (i - 1) * mat, s * mat, 1};
+    p.D = Operand{nullptr, 0, 1};
+    p.C = L + i * mat;
+    p.strideC = s * mat;
+    p.batch = cnt;
+    p.n = p.k = p.m = d;
+    p.rowA = Scales{nullptr, 0, 1};
+    p.colB = Scales{nullptr, 0, 1};
+    GOOM_TRY(lmme_run(p, lws, lws_bytes, st));
+  }
+  return GOOM_OK;
+}
+
+size_t lmme_ws_bytes(int64_t batch, int d) {
+  return round_up(sizeof(float) * (size_t)batch * d) * 2;
+}
+
+}  // namespace
+}  // namespace goom
+
+using namespace goom;
+
+extern "C" {
+
+size_t goom_scan_selective_chain_workspace_size(int64_t T, int d, const goom_reset_policy* policy,
+                                                int block) {
+  (void)block;
+  if (T < 1 || d < 1 || !policy || policy->check_interval < 1) return 0;
+  int64_t s = policy->check_interval < T ? policy->check_interval : T;
+  int64_t nt = (T + s - 1) / s;
+  size_t mat = (size_t)d * d * sizeof(float2);
+  size_t b = round_up(mat * T);                       // loc0
+  if (policy->consume_leaf && s > 1) b += round_up(mat * T);  // loc1
+  b += round_up(mat * nt) + round_up(nt) + round_up(sizeof(int) * 4);
+  b += lmme_ws_bytes(T, d);
+  return b;
+}
+
+int goom_scan_selective_chain_c64(const goom_c64* A_, goom_c64* V_, int64_t T, int d,
+                                  const goom_reset_policy* policy, int block, int64_t* sites,
+                                  int64_t* n_sites, void* ws, size_t ws_bytes, void* stream) {
+  if (T < 1) return fail(GOOM_EINVAL, "scan of an empty sequence");
+  if (block < 1) return fail(GOOM_EINVAL, "block_size must be >= 1");
+  if (d < 1) return fail(GOOM_ESHAPE, "d must be >= 1");
+  if (!A_ || !V_ || !sites || !n_sites) return fail(GOOM_EINVAL, "null pointer");
+  GOOM_TRY(check_policy(policy, d));
+  size_t need = goom_scan_selective_chain_workspace_size(T, d, policy, block);
+  if (ws_bytes < need || !ws) return fail(GOOM_EWORKSPACE, "selective workspace too small");
+  cudaStream_t st = as_stream(stream);
+  const float2* A = reinterpret_cast<const float2*>(A_);
+  float2* V = reinterpret_cast<float2*>(V_);
+  const int64_t s = policy->check_interval < T ? policy->check_interval : T;
+  const int64_t nt = (T + s - 1) / s;
+  const int64_t mat = (int64_t)d * d;
+  const bool need_loc1 = policy->consume_leaf && s > 1;
+
+  char* base = reinterpret_cast<char*>(ws);
+  size_t off = 0;
+  float2* loc0 = reinterpret_cast<float2*>(base + off);
+  off += round_up(sizeof(float2) * mat * T);
+  float2* loc1 = nullptr;
+  if (need_loc1) {
+    loc1 = reinterpret_cast<float2*>(base + off);
+    off += round_up(sizeof(float2) * mat * T);
+  }
+  float2* carries = reinterpret_cast<float2*>(base + off);
+  off += round_up(sizeof(float2) * mat * nt);
+  int8_t* modes = reinterpret_cast<int8_t*>(base + off);
+  off += round_up(nt);
+  int* status = reinterpret_cast<int*>(base + off);
+  off += round_up(sizeof(int) * 4);
+  void* lws = base + off;
+  size_t lws_bytes = ws_bytes - off;
+
+  // 1. local products
+  GOOM_TRY(local_products(A, loc0, T, d, s, false, lws, lws_bytes, st));
+  if (need_loc1) GOOM_TRY(local_products(A, loc1, T, d, s, true, lws, lws_bytes, st));
+  // 2. fused walk
+  if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "status reset");
+  GOOM_TRY(set_smem((const void*)selective_walk_kernel, d));
+  selective_walk_kernel<<<1, kThreads, smem_bytes(d), st>>>(
+      loc0, loc1 ? loc1 : loc0, carries, modes, sites, n_sites, status, T, d, (int)s,
+      to_policy(policy));
+  GOOM_CHECK_LAUNCH("selective_walk_kernel");
+  // 3. materialise: tile 0 = loc0; tile k>0: loc[t] (x) carry[k]
+  if (need_loc1) {
+    adopt_loc1_kernel<<<(unsigned)nt, 256, 0, st>>>(loc0, loc1, modes, T, d, (int)s);
+    GOOM_CHECK_LAUNCH("adopt_loc1_kernel");
+  }
+  const int64_t first = s < T ? s : T;
+  if (cudaMemcpyAsync(V, loc0, sizeof(float2) * mat * first, cudaMemcpyDeviceToDevice, st) !=
+      cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "materialise tile 0");
+  if (T > s) {
+    LmmeProblem p{};
+    p.A = Operand{loc0 + s * mat, mat, 1};
+    p.B = Operand{carries + mat, mat, s};
+    p.D = Operand{nullptr, 0, 1};
+    p.C = V + s * mat;
+    p.strideC = mat;
+    p.batch = T - s;
+    p.n = p.k = p.m = d;
+    p.rowA = Scales{nullptr, 0, 1};
+    p.colB = Scales{nullptr, 0, 1};
+    GOOM_TRY(lmme_run(p, lws, lws_bytes, st));
+  }
+  if (policy->consume_leaf) {
+    fix_reset_slots_kernel<<<(unsigned)nt, 256, 0, st>>>(V, carries, modes, d, (int)s);
+    GOOM_CHECK_LAUNCH("fix_reset_slots_kernel");
+  }
+  // surface a rank-deficient reset as ValueError (lyapunov.py:191-192, 212-213)
+  int host_status = 0;
+  if (cudaMemcpyAsync(&host_status, status, sizeof(int), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "selective status read");
+  if (host_status != GOOM_OK)
+    return fail(host_status, "rank-deficient state cannot be orthonormalized (or all-zero column)");
+  return GOOM_OK;
+}
+
+int goom_policy_select_c64(const goom_c64* X, int64_t batch, int d, const goom_reset_policy* policy,
+                           uint8_t* fire, void* stream) {
+  if (batch < 0 || d < 1) return fail(GOOM_EINVAL, "bad shape");
+  GOOM_TRY(check_policy(policy, d));
+  if (batch == 0) return GOOM_OK;
+  GOOM_TRY(set_smem((const void*)policy_select_kernel, d));
+  policy_select_kernel<<<(unsigned)batch, kThreads, smem_bytes(d), as_stream(stream)>>>(
+      reinterpret_cast<const float2*>(X), d, to_policy(policy), fire);
+  GOOM_CHECK_LAUNCH("policy_select_kernel");
+  return GOOM_OK;
+}
+
+int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
+                          const goom_reset_policy* policy, void* stream) {
+  if (batch < 0 || d < 1) return fail(GOOM_EINVAL, "bad shape");
+  GOOM_TRY(check_policy(policy, d));
+  if (batch == 0) return GOOM_OK;
+  if (policy->kind == GOOM_POLICY_NEVER) return fail(GOOM_EINVAL, "never-policy has no reset");
+  cudaStream_t st = as_stream(stream);
+  int* status = nullptr;
+  if (cudaMallocAsync(&status, sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "reset status");
+  GOOM_TRY(set_smem((const void*)policy_reset_kernel, d));
+  policy_reset_kernel<<<(unsigned)batch, kThreads, smem_bytes(d), st>>>(
+      reinterpret_cast<const float2*>(X), reinterpret_cast<float2*>(R), d, policy->kind, status);
+  GOOM_CHECK_LAUNCH("policy_reset_kernel");
+  int host_status = 0;
+  cudaMemcpyAsync(&host_status, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(status, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_fail(cudaGetLastError(), "reset sync");
+  if (host_status != GOOM_OK)
+    return fail(host_status, "rank-deficient state cannot be orthonormalized (or all-zero column)");
+  return GOOM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+"""GPU parity of the scan engines against the oracle and the reference's golden scans.
+
+Mirrors pkg/tests/test_scan.py (TestScanParallel, TestSelectiveScan,
+TestGoldenThreeStep) plus the SURVEY §8c chain criterion: per position,
+err(GPU complex64 vs float64 oracle) <= max(4 * err(reference float32 vs
+float64 oracle), 1e-4) in _rel_log_diff, signs exact where |x| is not near 0.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from goom_testlib import NEG_INF, load_golden, rel_log_diff_per, to_np
+from oracle import gooms_port as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2510_03426_b200 as goom
+
+    goom._lib.load()
+    return goom
+
+
+def cz(log, sign):
+    import paper_2510_03426_b200 as goom
+
+    return goom.join(log, sign)
+
+
+def calibrated_ok(got_log, want64, ref32, floor=1e-4, factor=4.0):
+    e_gpu = rel_log_diff_per(got_log, want64)
+    e_ref = rel_log_diff_per(ref32, want64)
+    bound = np.maximum(factor * e_ref, floor)
+    bad = np.flatnonzero(e_gpu > bound)
+    return bad, e_gpu, e_ref
+
+
+# ---------------------------------------------------------------------------
+# product chains / affine scans
+
+
+@pytest.mark.parametrize("block", [1, 16, 32, 64, 1000])
+def test_config1_chain_d8_T1000(g, block):
+    """Config 1: 1,000 random-normal 8x8 leaves, all prefixes (golden from the reference)."""
+    z = load_golden("config1_chain")
+    al, as_ = G.log_sign(z["mats"])
+    out = g.scan_chain(cz(al, as_), block_size=block)
+    gl, gs = to_np(out)
+    want64 = z["seq_f64"][0]
+    ref32 = z["seq_f32"][0].astype(np.float64)
+    bad, e_gpu, e_ref = calibrated_ok(gl, want64, ref32)
+    assert bad.size == 0, (bad[:10], e_gpu[bad[:10]], e_ref[bad[:10]])
+    # signs agree with the float64 oracle wherever the reference float32 run agrees
+    ref_ok = z["seq_f32"][1] == z["seq_f64"][1]
+    assert np.mean((gs == z["seq_f64"][1])[ref_ok]) > 0.999
+
+
+def test_block_ge_T_is_sequential_fold_bitwise(g):
+    """scan.py:217-225: block >= T degenerates to the sequential fold (same combines)."""
+    rng = np.random.default_rng(38)
+    A = cz(*G.log_sign(rng.standard_normal((7, 3, 3))))
+    B = cz(*G.log_sign(rng.standard_normal((7, 3, 3))))
+    st = g._Stack(A, B)
+    par = g._scan_affine_stack(st, 7)
+    seq = g._Stack(A.clone(), B.clone())
+    for t in range(1, 7):
+        seq.A[t] = torch.ops.goom.lmme(A[t], seq.A[t - 1])
+        seq.B[t] = torch.ops.goom.lmme_gadd(A[t], seq.B[t - 1], B[t])
+    assert torch.equal(par.A, seq.A) and torch.equal(par.B, seq.B)
+
+
+def test_affine_golden_T64_d4(g):
+    z = load_golden("affine_T64_d4")
+    st = g._Stack(cz(z["alog"], z["asign"]), cz(z["blog"], z["bsign"]))
+    for block, key in ((64, "seq"), (8, "par8")):
+        out = g._scan_affine_stack(st, block)
+        gl, gs = to_np(out.A)
+        bl, bs = to_np(out.B)
+        ref = z[key]
+        assert G.rel_log_diff(gl, ref[0]) < 1e-4
+        assert G.rel_log_diff(bl, ref[2]) < 1e-4
+        assert np.mean(gs == ref[1]) > 0.999 and np.mean(bs == ref[3]) > 0.999
+
+
+def test_1024_leaves_across_block_sizes(g):
+    """test_scan.py:227-237 at complex64: blocks {4,16,64} vs the f64 sequential oracle."""
+    rng = np.random.default_rng(39)
+    T, d = 1024, 8
+    st64 = G.random_stack(rng, T, d, biases=True)
+    seq = G.scan_sequential(st64)
+    st32 = G.Stack(*(x.astype(np.float32) for x in (st64.alog, st64.asign, st64.blog, st64.bsign)),
+                   st64.flags.copy())
+    ref32 = G.scan_sequential(st32)
+    st = g._Stack(cz(st64.alog, st64.asign), cz(st64.blog, st64.bsign))
+    for bs in (4, 16, 64):
+        out = g._scan_affine_stack(st, bs)
+        for slot, want, r32 in ((out.A, seq.alog, ref32.alog), (out.B, seq.blog, ref32.blog)):
+            gl, _ = to_np(slot)
+            bad, e_gpu, e_ref = calibrated_ok(gl, want, r32.astype(np.float64))
+            assert bad.size == 0, (bs, bad[:5], e_gpu[bad[:5]], e_ref[bad[:5]])
+
+
+def test_zero_bias_affine_is_product_chain(g):
+    """test_scan.py:328-337: zero biases -> pure product chain; bias slot stays zero."""
+    rng = np.random.default_rng(48)
+    mats = rng.standard_normal((12, 3, 3))
+    leaves = [g.ScanPair(g.GoomMatrix.from_real(m), g.GoomMatrix.zeros(3, 3)) for m in mats]
+    out = g.scan_parallel(leaves, g.combine_affine, block_size=4)
+    prod = np.eye(3)
+    for m, pair in zip(mats, out):
+        prod = m @ prod
+        np.testing.assert_allclose(pair.A.to_real(True).cpu().numpy(), prod, rtol=1e-5, atol=1e-6)
+        assert bool((pair.B.log_mag == NEG_INF).all())
+
+
+def test_chain_with_carry_in(g):
+    rng = np.random.default_rng(9)
+    T, d = 40, 6
+    al, as_ = G.log_sign(rng.standard_normal((T, d, d)))
+    cl, cs = G.log_sign(rng.standard_normal((d, d)))
+    out = g.scan_chain(cz(al, as_), block_size=8, carry=cz(cl, cs))
+    # oracle: prefix products times the carry on the right
+    st = G.Stack(np.concatenate([cl[None], al]), np.concatenate([cs[None], as_]),
+                 np.full((T + 1, d, d), NEG_INF), np.ones((T + 1, d, d)), np.zeros(T + 1, bool))
+    want = G.scan_sequential(st)
+    gl, _ = to_np(out)
+    assert G.rel_log_diff(gl, want.alog[1:]) < 1e-4
+
+
+def test_pairs_api_and_sequential(g):
+    rng = np.random.default_rng(37)
+    mats = [rng.standard_normal((3, 3)) for _ in range(16)]
+    bias = [rng.standard_normal((3, 3)) for _ in range(16)]
+    leaves = [g.ScanPair(g.GoomMatrix.from_real(a), g.GoomMatrix.from_real(b))
+              for a, b in zip(mats, bias)]
+    out = g.scan_sequential(leaves, g.combine_affine)
+    x = np.eye(3)
+    for a, b, pair in zip(mats, bias, out):
+        x = a @ x + b
+        got = pair.A.to_real(True).cpu().numpy() + pair.B.to_real(True).cpu().numpy()
+        np.testing.assert_allclose(got, x, rtol=1e-4, atol=1e-5)
+    with pytest.raises(ValueError):
+        g.scan_parallel(leaves, g.combine_affine, block_size=0)
+
+
+# ---------------------------------------------------------------------------
+# selective scans
+
+
+def _chain_states(V):
+    return to_np(V)
+
+
+def test_selective_norm_threshold_sites_golden(g):
+    z = load_golden("sel_norm_T300_d4")
+    A = cz(z["alog"], z["asign"])
+    want_sites = list(z["sites"])
+    for block in (2, 4, 7, 32):
+        V, sites = g._selective_chain_core(A, g.norm_threshold_policy(12.0), block)
+        assert sites == want_sites
+        gl, gs = _chain_states(V)
+        assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+    # pair API: flags monotone from the first site (test_scan.py:306-314)
+    leaves = [g.ScanPair(g.GoomMatrix(z["alog"][i], z["asign"][i]),
+                         g.GoomMatrix.zeros(4, 4)) for i in range(len(z["alog"]))]
+    states, sites = g.scan_selective(leaves, g.norm_threshold_policy(12.0), block_size=8)
+    flags = np.array([s.reset_applied for s in states])
+    assert sites == want_sites
+    assert np.array_equal(flags, np.arange(len(flags)) >= sites[0])
+    np.testing.assert_array_equal(flags, z["seq_flags"])
+
+
+def test_selective_interval_8(g):
+    z = load_golden("sel_norm_interval8")
+    V, sites = g._selective_chain_core(cz(z["alog"], z["asign"]),
+                                       g.norm_threshold_policy(5.0, interval=8), 16)
+    assert sites == list(z["sites"])
+    assert all(s % 8 == 0 for s in sites)
+    gl, _ = _chain_states(V)
+    assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+
+
+def test_selective_with_biases_rounds(g):
+    z = load_golden("sel_norm_bias")
+    st = g._Stack(cz(z["alog"], z["asign"]), cz(z["blog"], z["bsign"]))
+    for block in (4, 16, 64):
+        out, sites = g.scan_selective(st, g.norm_threshold_policy(12.0), block_size=block)
+        assert sites == list(z["sites"])
+        np.testing.assert_array_equal(out.flags.cpu().numpy(), z["seq_flags"])
+        gl, _ = to_np(out.states())
+        assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+
+
+def test_colinearity_lorenz_sites(g):
+    """spectrum_parallel stage (a) on a Lorenz chain: sites identical to the reference."""
+    z = load_golden("sel_colin_lorenz")
+    A = cz(z["alog"], z["asign"])
+    V, sites = g._selective_chain_core(A, g.colinearity_policy(0.99, 12), 256)
+    assert sites == list(z["sites"])
+    gl, gs = to_np(V)
+    want = z["Vlog"]
+    assert G.rel_log_diff(gl, want) < 1e-3
+    w = load_golden("sel_colin_lorenz_walk")
+    V1, s1 = g._selective_chain_core(A[:600], g.colinearity_policy(0.99, 1), 64)
+    assert s1 == list(w["sites"])
+
+
+def test_colinearity_predicate_and_reset_kats(g):
+    """pkg/tests/test_lyapunov.py:164-215 on the device policy."""
+    import math
+
+    m = g.GoomMatrix.from_real(np.eye(3))
+    assert g.colinearity_select(m, 0.1) is False
+    assert g.colinearity_select(g.GoomMatrix.from_real(np.array([[1.0, 1.0], [2.0, 2.0]])), 0.999)
+    th = math.radians(0.5)
+    m = g.GoomMatrix.from_real(np.array([[1.0, math.cos(th)], [0.0, math.sin(th)]]))
+    assert g.colinearity_select(m, 0.99) is True
+    assert g.colinearity_select(m, 0.99999) is False
+    assert g.colinearity_select(g.GoomMatrix.from_real(np.array([[1.0, 0.0], [0.0, 0.0]])), 0.5)
+    assert g.colinearity_select(g.GoomMatrix.from_real(np.array([[1.0, -2.0], [1.0, -2.0]])), 0.99)
+    z = load_golden("orthonormal_reset")
+    out = g.orthonormal_reset(g.GoomMatrix(z["qlog"], z["qsign"])).to_real(True).cpu().numpy()
+    want = G.to_real(z["rlog"], z["rsign"])
+    np.testing.assert_allclose(out, want, atol=1e-6)
+    np.testing.assert_allclose(out.T @ out, np.eye(4), atol=1e-5)
+    huge = g.orthonormal_reset(g.GoomMatrix(z["hlog"], np.ones((2, 2)))).to_real(True)
+    assert bool(torch.isfinite(huge).all())
+    with pytest.raises(ValueError):
+        g.orthonormal_reset(g.GoomMatrix.from_real(np.array([[1.0, 1.0], [1.0, 1.0]])))
+
+
+def test_appendix_c_callable_policy(g):
+    """Appendix C worked example (test_scan.py:142-178) with host-callable select/reset."""
+    z = load_golden("appendix_c")
+    target = z["a1"] @ z["x0"]
+
+    def select(m):
+        real = m.to_real(True).cpu().numpy()
+        return real.shape == target.shape and np.allclose(real, target, rtol=1e-5)
+
+    def reset(m):
+        x = m.to_real(True).cpu().numpy()
+        return g.GoomMatrix.from_real(x / (1.0 + np.linalg.norm(x)))
+
+    pol = g.ResetPolicy(select=select, reset=reset)
+    leaves = [g.ScanPair(g.GoomMatrix.from_real(x), g.GoomMatrix.zeros(3, 3))
+              for x in (z["x0"], z["a1"], z["a2"], z["a3"])]
+    for block in (None, 1, 2, 3, 4):
+        states, sites = g.scan_selective(leaves, pol, block_size=block)
+        assert sites == [2]
+        for i, key in ((1, "want1"), (2, "want2"), (3, "want3")):
+            np.testing.assert_allclose(states[i].state.to_real(True).cpu().numpy(), z[key],
+                                       rtol=1e-5, atol=1e-6)
+        assert [s.reset_applied for s in states] == [False, False, True, True]
+
+
+def test_never_firing_equals_affine(g):
+    """test_scan.py:255-265: a never-firing selective scan equals the affine scan."""
+    rng = np.random.default_rng(42)
+    T, d = 200, 3
+    A = cz(*G.log_sign(rng.standard_normal((T, d, d))))
+    st = g._Stack(A, torch.full_like(A, complex(NEG_INF, 0.0)))
+    aff = g._scan_affine_stack(st, 16)
+    V, sites = g._selective_chain_core(A, g.never_policy(16), 16)
+    assert sites == []
+    assert torch.equal(V, aff.A)
+
+
+def test_parenthesizations_length_six(g):
+    rng = np.random.default_rng(47)
+    mats = []
+    for _ in range(6):
+        q, _ = np.linalg.qr(rng.standard_normal((2, 2)))
+        mats.append(np.exp(rng.normal(1.0, 0.2)) * q)
+    al, as_ = G.log_sign(np.array(mats))
+    want_states, want_sites = G.selective_sequential(
+        G.Stack(al, as_, np.full_like(al, NEG_INF), np.ones_like(as_), np.zeros(6, bool)),
+        G.norm_threshold_policy(1.0))
+    for block in range(1, 7):
+        V, sites = g._selective_chain_core(cz(al, as_), g.norm_threshold_policy(1.0), block)
+        assert sites == want_sites
+        gl, _ = to_np(V[-1])
+        assert G.rel_log_diff(gl, want_states.state(5)[0]) < 1e-4
