@@ -37,6 +37,10 @@ extern "C" {
 #endif
 
 typedef struct goom_c64 { float re, im; } goom_c64;
+/* complex128 GOOM: float64 log-magnitude, the precision of the reference's
+ * default float64 backing (core.py:189). Every _c128 entry point is the
+ * FP64 twin of the _c64 one documented next to it. */
+typedef struct goom_c128 { double re, im; } goom_c128;
 
 typedef enum goom_status {
   GOOM_OK = 0,
@@ -60,20 +64,28 @@ int goom_device_supported(int device);
  * NaN/inf inputs are NOT checked here (the Python layer raises like core.py:194-197). */
 int goom_from_real_f32(const float* x, goom_c64* out, int64_t n, float zero_log, void* stream);
 int goom_from_real_f64(const double* x, goom_c64* out, int64_t n, double zero_log, void* stream);
+int goom_from_real_c128(const double* x, goom_c128* out, int64_t n, double zero_log, void* stream);
 /* sign * exp(log), overflow -> +-inf.  GoomMatrix.to_real core.py:213-216. */
 int goom_to_real_f32(const goom_c64* z, float* out, int64_t n, void* stream);
 int goom_to_real_f64(const goom_c64* z, double* out, int64_t n, void* stream);
+int goom_to_real_c128(const goom_c128* z, double* out, int64_t n, void* stream);
 /* Per matrix b of `batch` (each `n` elements): c_b = max log (0 if all zero),
  * out = sign * exp(log - c_b + 2).  to_real_scaled core.py:313-323.
  * c is a device array of `batch` floats. */
 int goom_to_real_scaled_f32(const goom_c64* z, float* out, float* c, int64_t batch, int64_t n,
                             void* stream);
+int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t batch, int64_t n,
+                             void* stream);
 /* Elementwise signed log-sum-exp, bitwise commutative.  _gadd_arrays core.py:264-275. */
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream);
+int goom_gadd_c128(const goom_c128* a, const goom_c128* b, goom_c128* out, int64_t n,
+                   void* stream);
 /* Per-column log Euclidean norms of batch x (rows x cols) -> batch x cols floats.
  * _col_log_norms core.py:288-296. */
 int goom_col_log_norms_c64(const goom_c64* z, float* out, int64_t batch, int rows, int cols,
                            void* stream);
+int goom_col_log_norms_c128(const goom_c128* z, double* out, int64_t batch, int rows, int cols,
+                            void* stream);
 
 /* ---- LMME (core.py:242-285, Eq. 10-12) ------------------------------------- */
 /* C[b] = A[b] (x) B[b]  for b < batch;  A: n x k, B: k x m, C: n x m.
@@ -82,12 +94,13 @@ int goom_col_log_norms_c64(const goom_c64* z, float* out, int64_t batch, int row
  * C = (log|I| + a) + b, sign(I).  Operand b addresses base + (b/div)*stride.
  * C must not alias A or B. */
 typedef struct goom_operand {
-  const goom_c64* ptr;
+  const void* ptr;  /* goom_c64* for _c64 calls, goom_c128* for _c128 calls */
   int64_t stride;  /* elements between consecutive matrices (0 = broadcast) */
   int64_t div;     /* matrix index = b / div (>= 1)                          */
 } goom_operand;
 
 size_t goom_lmme_workspace_size(int64_t batch, int n, int k, int m);
+size_t goom_lmme_workspace_size_c128(int64_t batch, int n, int k, int m);
 int goom_lmme_c64(goom_operand A, goom_operand B, goom_c64* C, int64_t strideC, int64_t batch,
                   int n, int k, int m, void* ws, size_t ws_bytes, void* stream);
 /* Fused combine step: C[b] = (A[b] (x) B[b]) (+) D[b]   (_combine_arrays bias slot,
@@ -95,6 +108,12 @@ int goom_lmme_c64(goom_operand A, goom_operand B, goom_c64* C, int64_t strideC, 
 int goom_lmme_gadd_c64(goom_operand A, goom_operand B, goom_operand D, goom_c64* C,
                        int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
                        size_t ws_bytes, void* stream);
+/* FP64 SIMT twins (complex128 GOOMs) */
+int goom_lmme_c128(goom_operand A, goom_operand B, goom_c128* C, int64_t strideC, int64_t batch,
+                   int n, int k, int m, void* ws, size_t ws_bytes, void* stream);
+int goom_lmme_gadd_c128(goom_operand A, goom_operand B, goom_operand D, goom_c128* C,
+                        int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
+                        size_t ws_bytes, void* stream);
 /* Force a kernel family for testing: 0 auto, 1 SIMT, 2 tcgen05 3xTF32. Returns the
  * previous value. Process-wide. */
 int goom_set_lmme_backend(int backend);
@@ -106,6 +125,9 @@ int goom_set_lmme_backend(int backend);
 size_t goom_scan_chain_workspace_size(int64_t T, int d, int block);
 int goom_scan_chain_c64(const goom_c64* A, goom_c64* out, int64_t T, int d, int block,
                         const goom_c64* carry_in, void* ws, size_t ws_bytes, void* stream);
+size_t goom_scan_chain_workspace_size_c128(int64_t T, int d, int block);
+int goom_scan_chain_c128(const goom_c128* A, goom_c128* out, int64_t T, int d, int block,
+                         const goom_c128* carry_in, void* ws, size_t ws_bytes, void* stream);
 
 /* Inclusive affine scan of pairs (A_t: d x d, B_t: d x m, flag_t) under
  * combine_affine (scan.py:92-103): (A,B) <- (A_t A, A_t B (+) B_t), flag OR.
@@ -114,6 +136,10 @@ size_t goom_scan_affine_workspace_size(int64_t T, int d, int m, int block);
 int goom_scan_affine_c64(const goom_c64* A, const goom_c64* B, const uint8_t* flags_in,
                          goom_c64* outA, goom_c64* outB, uint8_t* flags_out, int64_t T, int d,
                          int m, int block, void* ws, size_t ws_bytes, void* stream);
+size_t goom_scan_affine_workspace_size_c128(int64_t T, int d, int m, int block);
+int goom_scan_affine_c128(const goom_c128* A, const goom_c128* B, const uint8_t* flags_in,
+                          goom_c128* outA, goom_c128* outB, uint8_t* flags_out, int64_t T, int d,
+                          int m, int block, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- selective resetting (scan.py:342-484, lyapunov.py:146-278) ------------- */
 typedef enum goom_policy_kind {
@@ -145,6 +171,13 @@ size_t goom_scan_selective_chain_workspace_size(int64_t T, int d,
 int goom_scan_selective_chain_c64(const goom_c64* A, goom_c64* V, int64_t T, int d,
                                   const goom_reset_policy* policy, int block, int64_t* sites,
                                   int64_t* n_sites, void* ws, size_t ws_bytes, void* stream);
+/* complex128 twin: the reference's spectrum_parallel runs this path in float64
+ * (lyapunov.py:336); volume-test decisions (logdet < log 1e-9) need FP64 states. */
+size_t goom_scan_selective_chain_workspace_size_c128(int64_t T, int d,
+                                                     const goom_reset_policy* policy, int block);
+int goom_scan_selective_chain_c128(const goom_c128* A, goom_c128* V, int64_t T, int d,
+                                   const goom_reset_policy* policy, int block, int64_t* sites,
+                                   int64_t* n_sites, void* ws, size_t ws_bytes, void* stream);
 
 /* Batched policy evaluation on states X[b] (d x d): fire[b] = select(X[b]).
  * Used by the general-bias selective rounds (scan.py:255-314). */
@@ -153,6 +186,10 @@ int goom_policy_select_c64(const goom_c64* X, int64_t batch, int d, const goom_r
 /* R[b] = reset(X[b]) for the policy's reset map. */
 int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
                           const goom_reset_policy* policy, void* stream);
+int goom_policy_select_c128(const goom_c128* X, int64_t batch, int d,
+                            const goom_reset_policy* policy, uint8_t* fire, void* stream);
+int goom_policy_reset_c128(const goom_c128* X, goom_c128* R, int64_t batch, int d,
+                           const goom_reset_policy* policy, void* stream);
 
 #ifdef __cplusplus
 }

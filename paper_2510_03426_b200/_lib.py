@@ -86,7 +86,44 @@ SIGNATURES = {
     ),
     "goom_policy_select_c64": (_I, [_P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P, _P]),
     "goom_policy_reset_c64": (_I, [_P, _P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P]),
+    # complex128 (FP64) twins
+    "goom_from_real_c128": (_I, [_P, _P, _I64, ctypes.c_double, _P]),
+    "goom_to_real_c128": (_I, [_P, _P, _I64, _P]),
+    "goom_to_real_scaled_c128": (_I, [_P, _P, _P, _I64, _I64, _P]),
+    "goom_gadd_c128": (_I, [_P, _P, _P, _I64, _P]),
+    "goom_col_log_norms_c128": (_I, [_P, _P, _I64, _I, _I, _P]),
+    "goom_lmme_workspace_size_c128": (_SZ, [_I64, _I, _I, _I]),
+    "goom_lmme_c128": (_I, [goom_operand, goom_operand, _P, _I64, _I64, _I, _I, _I, _P, _SZ, _P]),
+    "goom_lmme_gadd_c128": (
+        _I,
+        [goom_operand, goom_operand, goom_operand, _P, _I64, _I64, _I, _I, _I, _P, _SZ, _P],
+    ),
+    "goom_scan_chain_workspace_size_c128": (_SZ, [_I64, _I, _I]),
+    "goom_scan_chain_c128": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
+    "goom_scan_affine_workspace_size_c128": (_SZ, [_I64, _I, _I, _I]),
+    "goom_scan_affine_c128": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _SZ, _P]),
+    "goom_scan_selective_chain_workspace_size_c128": (
+        _SZ,
+        [_I64, _I, ctypes.POINTER(goom_reset_policy), _I],
+    ),
+    "goom_scan_selective_chain_c128": (
+        _I,
+        [_P, _P, _I64, _I, ctypes.POINTER(goom_reset_policy), _I, _P, _P, _P, _SZ, _P],
+    ),
+    "goom_policy_select_c128": (_I, [_P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P, _P]),
+    "goom_policy_reset_c128": (_I, [_P, _P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P]),
 }
+
+
+def fn(base: str, dtype) -> str:
+    """ABI name for a complex dtype: base_c64 / base_c128 (torch.complex64/128)."""
+    import torch
+
+    if dtype == torch.complex64:
+        return base + "_c64"
+    if dtype == torch.complex128:
+        return base + "_c128"
+    raise ValueError(f"GOOM tensors are complex64 or complex128, got {dtype}")
 
 _lib = None
 _lock = threading.Lock()

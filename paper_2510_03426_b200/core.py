@@ -163,23 +163,46 @@ def _to_tensor(x, dtype=None):
     return t.to(_device())
 
 
-def join(log_mag, sign) -> torch.Tensor:
-    """(log, sign) arrays -> complex64 GOOM tensor on the GPU."""
+def complex_dtype(dtype=None, like=None):
+    """GOOM dtype: complex64 by default (the paper's Complex64 GOOM); complex128
+    for float64 / complex128 requests (the reference's float64 backing)."""
+    if dtype is None and like is not None:
+        dtype = like
+    if dtype is None:
+        return torch.complex64
+    if isinstance(dtype, torch.dtype):
+        if dtype in (torch.float64, torch.complex128):
+            return torch.complex128
+        return torch.complex64
+    return torch.complex128 if np.dtype(dtype) in (np.float64, np.complex128) else torch.complex64
+
+
+def join(log_mag, sign, dtype=None) -> torch.Tensor:
+    """(log, sign) arrays -> GOOM tensor on the GPU (complex64 unless dtype says 128)."""
+    cd = complex_dtype(dtype)
+    rt = torch.float64 if cd == torch.complex128 else torch.float32
     log_t = _to_tensor(log_mag)
     if log_t.is_complex():
         raise ValueError("log_mag must be real")
     sign_t = _to_tensor(sign, log_t.dtype)
     if log_t.shape != sign_t.shape:
         raise ValueError("log_mag and sign shapes differ")
-    im = torch.where(sign_t < 0, torch.tensor(PI32, device=log_t.device),
-                     torch.tensor(0.0, device=log_t.device))
-    return torch.complex(log_t.to(torch.float32), im.to(torch.float32))
+    pi = math.pi if rt == torch.float64 else PI32
+    im = torch.where(sign_t < 0, torch.tensor(pi, device=log_t.device, dtype=rt),
+                     torch.tensor(0.0, device=log_t.device, dtype=rt))
+    return torch.complex(log_t.to(rt), im)
 
 
 def split(z: torch.Tensor):
-    """complex64 GOOM tensor -> (log_mag float32, sign float32 in {+1,-1})."""
-    sign = torch.where(torch.cos(z.imag) < 0, -1.0, 1.0).to(torch.float32)
+    """GOOM tensor -> (log_mag, sign in {+1,-1}) in the matching real dtype."""
+    sign = torch.where(torch.cos(z.imag) < 0, -1.0, 1.0).to(z.real.dtype)
     return z.real, sign
+
+
+def _dtype_of_arrays(x):
+    """Array-level entry points keep the reference's dtype: float64 -> complex128."""
+    dt = x.dtype if isinstance(x, (np.ndarray, torch.Tensor)) else np.asarray(x).dtype
+    return complex_dtype(dt)
 
 
 def _like_input(t: torch.Tensor, ref):
@@ -197,14 +220,14 @@ class GoomMatrix:
 
     __slots__ = ("data",)
 
-    def __init__(self, log_mag, sign=None):
+    def __init__(self, log_mag, sign=None, dtype=None):
         if sign is None:
             z = log_mag if isinstance(log_mag, torch.Tensor) else _to_tensor(log_mag)
             if not z.is_complex():
                 raise ValueError("single-argument GoomMatrix takes a complex GOOM tensor")
-            z = z.to(device=_device(), dtype=torch.complex64)
+            z = z.to(device=_device(), dtype=complex_dtype(dtype, z.dtype))
         else:
-            z = join(log_mag, sign)
+            z = join(log_mag, sign, dtype)
         if z.dim() != 2:
             raise ValueError("GoomMatrix is 2-D")
         if bool(torch.isnan(z.real).any()):
@@ -260,17 +283,18 @@ class GoomMatrix:
             raise ValueError("cannot represent NaN")
         if bool(torch.isinf(v).any()):
             raise ValueError("cannot represent an infinite value")
-        return cls._wrap(torch.ops.goom.from_real(v, float(policy.zero_log)))
+        double = complex_dtype(dtype) == torch.complex128
+        return cls._wrap(torch.ops.goom.from_real(v, float(policy.zero_log), double))
 
     @classmethod
     def zeros(cls, rows, cols, policy=SENTINEL, dtype=None):
-        z = torch.full((rows, cols), complex(policy.zero_log, 0.0), dtype=torch.complex64,
+        z = torch.full((rows, cols), complex(policy.zero_log, 0.0), dtype=complex_dtype(dtype),
                        device=_device())
         return cls._wrap(z)
 
     @classmethod
     def identity(cls, n, policy=SENTINEL, dtype=None):
-        z = torch.full((n, n), complex(policy.zero_log, 0.0), dtype=torch.complex64,
+        z = torch.full((n, n), complex(policy.zero_log, 0.0), dtype=complex_dtype(dtype),
                        device=_device())
         z.diagonal().real.zero_()
         return cls._wrap(z)
@@ -299,7 +323,7 @@ def _log_sign_arrays(values, policy=SENTINEL):
     v = _to_tensor(values)
     if v.dtype not in (torch.float32, torch.float64):
         v = v.to(torch.float64)
-    z = torch.ops.goom.from_real(v.contiguous(), float(policy.zero_log))
+    z = torch.ops.goom.from_real(v.contiguous(), float(policy.zero_log), v.dtype == torch.float64)
     l, s = split(z)
     return _like_input(l, values), _like_input(s, values)
 
@@ -311,14 +335,16 @@ def log_matmul_exp(x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
 
 def _lmme_arrays(alog, asign, blog, bsign):
     """Array-level LMME (core.py:242-261); returns (log, sign) like the inputs."""
-    z = torch.ops.goom.lmme(join(alog, asign), join(blog, bsign))
+    dt = _dtype_of_arrays(alog)
+    z = torch.ops.goom.lmme(join(alog, asign, dt), join(blog, bsign, dt))
     l, s = split(z)
     return _like_input(l, alog), _like_input(s, alog)
 
 
 def _gadd_arrays(alog, asign, blog, bsign):
     """Elementwise signed LSE (core.py:264-275)."""
-    z = torch.ops.goom.gadd(join(alog, asign), join(blog, bsign))
+    dt = _dtype_of_arrays(alog)
+    z = torch.ops.goom.gadd(join(alog, asign, dt), join(blog, bsign, dt))
     l, s = split(z)
     return _like_input(l, alog), _like_input(s, alog)
 
@@ -335,7 +361,8 @@ def lmme(a: GoomMatrix, b: GoomMatrix) -> GoomMatrix:
 def _col_log_norms(log_mag):
     """Per-column log Euclidean norms over axis -2 (core.py:288-296)."""
     l = _to_tensor(log_mag)
-    z = torch.complex(l.to(torch.float32), torch.zeros_like(l, dtype=torch.float32))
+    rt = torch.float64 if l.dtype == torch.float64 else torch.float32
+    z = torch.complex(l.to(rt), torch.zeros_like(l, dtype=rt))
     out = torch.ops.goom.col_log_norms(z).unsqueeze(-2)
     return _like_input(out, log_mag)
 

@@ -1,9 +1,8 @@
 // Elementwise GOOM kernels: real<->GOOM maps, scaled export, signed LSE (gadd),
 // column log-norms, and the LMME scale pre-pass (row / column maxima).
 //
-// All are HBM-bound streaming kernels: 8 B (complex64) per element plus the
-// real side; grid-stride loops sized to a multiple of the SM count.
-#include "goom_common.cuh"
+// All are HBM-bound streaming kernels (8 or 16 B per complex element plus the
+// real side); grid-stride loops sized to a multiple of the SM count.
 #include "goom_internal.cuh"
 
 namespace goom {
@@ -19,101 +18,87 @@ inline int stream_grid(int64_t n) {
   return blocks < 1 ? 1 : (int)blocks;
 }
 
-__global__ void from_real_f32_kernel(const float* __restrict__ x, float2* __restrict__ out,
-                                     int64_t n, float zero_log) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float v = x[i];
-    out[i] = (v == 0.0f) ? make_float2(zero_log, 0.0f) : goom_from_value(v);
-  }
-}
+#define GRID_STRIDE(i, n)                                                                   \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n);                 \
+       i += (int64_t)gridDim.x * blockDim.x)
 
-__global__ void from_real_f64_kernel(const double* __restrict__ x, float2* __restrict__ out,
-                                     int64_t n, double zero_log) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double v = x[i];
-    if (v == 0.0) {
-      out[i] = make_float2((float)zero_log, 0.0f);
+template <class X, class R>
+__global__ void from_real_kernel(const X* __restrict__ x, Cx<R>* __restrict__ out, int64_t n,
+                                 X zero_log) {
+  GRID_STRIDE(i, n) {
+    X v = x[i];
+    if (v == X(0)) {
+      out[i] = cx<R>((R)zero_log, R(0));
     } else {
-      out[i] = make_float2((float)log(fabs(v)), v < 0.0 ? kPi : 0.0f);
+      out[i] = cx<R>((R)glog(fabs(v)), v < X(0) ? pi_of<R>() : R(0));
     }
   }
 }
 
-__global__ void to_real_f32_kernel(const float2* __restrict__ z, float* __restrict__ out,
-                                   int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float2 v = z[i];
-    out[i] = goom_sign(v.y) * expf(v.x);
+template <class R, class X>
+__global__ void to_real_kernel(const Cx<R>* __restrict__ z, X* __restrict__ out, int64_t n) {
+  GRID_STRIDE(i, n) {
+    Cx<R> v = z[i];
+    out[i] = (X)goom_sign_t<R>(v.y) * gexp((X)v.x);
   }
 }
 
-__global__ void to_real_f64_kernel(const float2* __restrict__ z, double* __restrict__ out,
-                                   int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float2 v = z[i];
-    out[i] = (double)goom_sign(v.y) * exp((double)v.x);
-  }
-}
-
-// one CTA per matrix: max log, then the shifted export
-__global__ void to_real_scaled_kernel(const float2* __restrict__ z, float* __restrict__ out,
-                                      float* __restrict__ cvec, int64_t n) {
+// one CTA per matrix: max log, then the shifted export (core.py:313-323)
+template <class R>
+__global__ void to_real_scaled_kernel(const Cx<R>* __restrict__ z, R* __restrict__ out,
+                                      R* __restrict__ cvec, int64_t n) {
   const int64_t b = blockIdx.x;
-  const float2* zb = z + b * n;
-  float* ob = out + b * n;
-  __shared__ float red[32];
-  float m = kNegInf;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, zb[i].x);
-  m = warp_max(m);
+  const Cx<R>* zb = z + b * n;
+  R* ob = out + b * n;
+  __shared__ R red[32];
+  R m = R(-INFINITY);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = gmax(m, zb[i].x);
+  m = warp_max_t(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : kNegInf;
-    v = warp_max(v);
+    R v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : R(-INFINITY);
+    v = warp_max_t(v);
     if (threadIdx.x == 0) red[0] = v;
   }
   __syncthreads();
-  float c = red[0];
-  if (c == kNegInf || n == 0) c = 0.0f;
+  R c = red[0];
+  if (c == R(-INFINITY) || n == 0) c = R(0);
   if (threadIdx.x == 0) cvec[b] = c;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-    float2 v = zb[i];
-    ob[i] = goom_sign(v.y) * expf(__fadd_rn(__fsub_rn(v.x, c), 2.0f));
+    Cx<R> v = zb[i];
+    ob[i] = goom_sign_t<R>(v.y) * gexp(add_rn(sub_rn(v.x, c), R(2)));
   }
 }
 
-__global__ void gadd_kernel(const float2* __restrict__ a, const float2* __restrict__ b,
-                            float2* __restrict__ out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    out[i] = gadd_elem(a[i], b[i]);
-  }
+template <class R>
+__global__ void gadd_kernel(const Cx<R>* __restrict__ a, const Cx<R>* __restrict__ b,
+                            Cx<R>* __restrict__ out, int64_t n) {
+  GRID_STRIDE(i, n) { out[i] = gadd_elem_t<R>(a[i], b[i]); }
 }
 
 // one thread per (batch, column); rows looped (columns are contiguous across threads)
-__global__ void col_log_norms_kernel(const float2* __restrict__ z, float* __restrict__ out,
+template <class R>
+__global__ void col_log_norms_kernel(const Cx<R>* __restrict__ z, R* __restrict__ out,
                                      int64_t batch, int rows, int cols) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= batch * cols) return;
   int64_t b = t / cols;
   int c = (int)(t % cols);
-  const float2* zb = z + b * (int64_t)rows * cols + c;
-  float top = kNegInf;
-  for (int r = 0; r < rows; ++r) top = fmaxf(top, zb[(int64_t)r * cols].x);
-  bool live = top != kNegInf;
-  float shift = live ? top : 0.0f;
-  float acc = 0.0f;
-  for (int r = 0; r < rows; ++r) acc += expf(2.0f * (zb[(int64_t)r * cols].x - shift));
-  out[t] = live ? __fadd_rn(shift, 0.5f * logf(acc)) : kNegInf;
+  const Cx<R>* zb = z + b * (int64_t)rows * cols + c;
+  R top = R(-INFINITY);
+  for (int r = 0; r < rows; ++r) top = gmax(top, zb[(int64_t)r * cols].x);
+  bool live = top != R(-INFINITY);
+  R shift = live ? top : R(0);
+  R acc = R(0);
+  for (int r = 0; r < rows; ++r) acc += gexp(R(2) * (zb[(int64_t)r * cols].x - shift));
+  out[t] = live ? add_rn(shift, R(0.5) * glog(acc)) : R(-INFINITY);
 }
 
 // ---- LMME scale pre-pass ---------------------------------------------------
 // rows: one warp per (batch, row) -> max(max_j Re A[i, j], 0)
-__global__ void row_scale_kernel(Operand A, float* __restrict__ out, int64_t batch, int n,
+template <class R>
+__global__ void row_scale_kernel(OperandT<Cx<R>> A, R* __restrict__ out, int64_t batch, int n,
                                  int k) {
   const int warps = blockDim.x >> 5;
   int64_t w = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5);
@@ -121,40 +106,40 @@ __global__ void row_scale_kernel(Operand A, float* __restrict__ out, int64_t bat
   if (w >= batch * n) return;
   int64_t b = w / n;
   int i = (int)(w % n);
-  const float2* row = A.at(b) + (int64_t)i * k;
-  float m = kNegInf;
-  for (int j = lane; j < k; j += 32) m = fmaxf(m, row[j].x);
-  m = warp_max(m);
-  if (lane == 0) out[w] = fmaxf(m, 0.0f);
+  const Cx<R>* row = A.at(b) + (int64_t)i * k;
+  R m = R(-INFINITY);
+  for (int j = lane; j < k; j += 32) m = gmax(m, row[j].x);
+  m = warp_max_t(m);
+  if (lane == 0) out[w] = gmax(m, R(0));
 }
 
 // columns: one thread per (batch, column) -> max(max_j Re B[j, c], 0)
-__global__ void col_scale_kernel(Operand B, float* __restrict__ out, int64_t batch, int k,
+template <class R>
+__global__ void col_scale_kernel(OperandT<Cx<R>> B, R* __restrict__ out, int64_t batch, int k,
                                  int m) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= batch * m) return;
   int64_t b = t / m;
   int c = (int)(t % m);
-  const float2* col = B.at(b) + c;
-  float v = kNegInf;
-  for (int j = 0; j < k; ++j) v = fmaxf(v, col[(int64_t)j * m].x);
-  out[t] = fmaxf(v, 0.0f);
+  const Cx<R>* col = B.at(b) + c;
+  R v = R(-INFINITY);
+  for (int j = 0; j < k; ++j) v = gmax(v, col[(int64_t)j * m].x);
+  out[t] = gmax(v, R(0));
 }
 
-__global__ void identity_kernel(float2* __restrict__ out, int64_t batch, int d, int64_t stride) {
+template <class R>
+__global__ void identity_kernel(Cx<R>* __restrict__ out, int64_t batch, int d, int64_t stride) {
   const int64_t mat = (int64_t)d * d;
-  int64_t n = batch * mat;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  GRID_STRIDE(i, batch * mat) {
     int64_t b = i / mat, e = i % mat;
     int r = (int)(e / d), c = (int)(e % d);
-    out[b * stride + e] = make_float2(r == c ? 0.0f : kNegInf, 0.0f);
+    out[b * stride + e] = cx<R>(r == c ? R(0) : R(-INFINITY), R(0));
   }
 }
 
 __global__ void flags_or_scan_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                                      int64_t T) {
-  // single CTA: chunked OR-scan (T is the number of scan elements; tiny vs matrix work)
+  // single CTA: chunked OR-scan (T scan elements; negligible next to the matrix work)
   __shared__ int carry;
   __shared__ int warp_any[32];
   if (threadIdx.x == 0) carry = 0;
@@ -162,7 +147,6 @@ __global__ void flags_or_scan_kernel(const uint8_t* __restrict__ in, uint8_t* __
   for (int64_t base = 0; base < T; base += blockDim.x) {
     int64_t i = base + threadIdx.x;
     int v = (i < T && in) ? (in[i] != 0) : 0;
-    // inclusive OR-scan inside the CTA via ballots
     unsigned ballot = __ballot_sync(0xffffffffu, v);
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int mine = (ballot & ((2u << lane) - 1u)) != 0;
@@ -184,27 +168,39 @@ __global__ void flags_or_scan_kernel(const uint8_t* __restrict__ in, uint8_t* __
 }  // namespace
 
 // ---- host launchers --------------------------------------------------------
-int launch_row_scales(Operand A, float* out, int64_t batch, int n, int k, cudaStream_t s) {
+template <class R>
+int launch_row_scales(OperandT<Cx<R>> A, R* out, int64_t batch, int n, int k, cudaStream_t s) {
   int64_t warps = batch * n;
   int per_block = 8;
-  row_scale_kernel<<<(unsigned)((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
+  row_scale_kernel<R><<<(unsigned)((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
       A, out, batch, n, k);
   GOOM_CHECK_LAUNCH("row_scale_kernel");
   return GOOM_OK;
 }
 
-int launch_col_scales(Operand B, float* out, int64_t batch, int k, int m, cudaStream_t s) {
+template <class R>
+int launch_col_scales(OperandT<Cx<R>> B, R* out, int64_t batch, int k, int m, cudaStream_t s) {
   int64_t t = batch * m;
-  col_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(B, out, batch, k, m);
+  col_scale_kernel<R><<<(unsigned)((t + 255) / 256), 256, 0, s>>>(B, out, batch, k, m);
   GOOM_CHECK_LAUNCH("col_scale_kernel");
   return GOOM_OK;
 }
 
-int launch_identity(float2* out, int64_t batch, int d, int64_t stride, cudaStream_t s) {
-  identity_kernel<<<stream_grid(batch * d * d), kThreads, 0, s>>>(out, batch, d, stride);
+template <class R>
+int launch_identity(Cx<R>* out, int64_t batch, int d, int64_t stride, cudaStream_t s) {
+  identity_kernel<R><<<stream_grid(batch * d * d), kThreads, 0, s>>>(out, batch, d, stride);
   GOOM_CHECK_LAUNCH("identity_kernel");
   return GOOM_OK;
 }
+
+template int launch_row_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t);
+template int launch_row_scales<double>(OperandT<double2>, double*, int64_t, int, int,
+                                       cudaStream_t);
+template int launch_col_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t);
+template int launch_col_scales<double>(OperandT<double2>, double*, int64_t, int, int,
+                                       cudaStream_t);
+template int launch_identity<float>(float2*, int64_t, int, int64_t, cudaStream_t);
+template int launch_identity<double>(double2*, int64_t, int, int64_t, cudaStream_t);
 
 int launch_flags_or_scan(const uint8_t* in, uint8_t* out, int64_t T, cudaStream_t s) {
   flags_or_scan_kernel<<<1, 1024, 0, s>>>(in, out, T);
@@ -212,13 +208,65 @@ int launch_flags_or_scan(const uint8_t* in, uint8_t* out, int64_t T, cudaStream_
   return GOOM_OK;
 }
 
-int launch_gadd(const float2* a, const float2* b, float2* out, int64_t n, cudaStream_t s) {
+namespace {
+
+template <class X, class R>
+int from_real(const X* x, void* out, int64_t n, X zero_log, void* stream) {
+  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
   if (n == 0) return GOOM_OK;
-  gadd_kernel<<<stream_grid(n), kThreads, 0, s>>>(a, b, out, n);
-  GOOM_CHECK_LAUNCH("gadd_kernel");
+  if (!x || !out) return fail(GOOM_EINVAL, "null pointer");
+  from_real_kernel<X, R><<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
+      x, reinterpret_cast<Cx<R>*>(out), n, zero_log);
+  GOOM_CHECK_LAUNCH("from_real");
   return GOOM_OK;
 }
 
+template <class R, class X>
+int to_real(const void* z, X* out, int64_t n, void* stream) {
+  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
+  if (n == 0) return GOOM_OK;
+  if (!z || !out) return fail(GOOM_EINVAL, "null pointer");
+  to_real_kernel<R, X><<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
+      reinterpret_cast<const Cx<R>*>(z), out, n);
+  GOOM_CHECK_LAUNCH("to_real");
+  return GOOM_OK;
+}
+
+template <class R>
+int to_real_scaled(const void* z, R* out, R* c, int64_t batch, int64_t n, void* stream) {
+  if (batch < 0 || n < 0) return fail(GOOM_EINVAL, "batch and n must be >= 0");
+  if (batch == 0) return GOOM_OK;
+  if (!z || !out || !c) return fail(GOOM_EINVAL, "null pointer");
+  to_real_scaled_kernel<R><<<(unsigned)batch, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const Cx<R>*>(z), out, c, n);
+  GOOM_CHECK_LAUNCH("to_real_scaled");
+  return GOOM_OK;
+}
+
+template <class R>
+int gadd(const void* a, const void* b, void* out, int64_t n, void* stream) {
+  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
+  if (n == 0) return GOOM_OK;
+  if (!a || !b || !out) return fail(GOOM_EINVAL, "null pointer");
+  gadd_kernel<R><<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
+      reinterpret_cast<const Cx<R>*>(a), reinterpret_cast<const Cx<R>*>(b),
+      reinterpret_cast<Cx<R>*>(out), n);
+  GOOM_CHECK_LAUNCH("gadd");
+  return GOOM_OK;
+}
+
+template <class R>
+int col_log_norms(const void* z, R* out, int64_t batch, int rows, int cols, void* stream) {
+  if (batch < 0 || rows < 1 || cols < 1) return fail(GOOM_EINVAL, "bad shape");
+  if (batch == 0) return GOOM_OK;
+  int64_t t = batch * cols;
+  col_log_norms_kernel<R><<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const Cx<R>*>(z), out, batch, rows, cols);
+  GOOM_CHECK_LAUNCH("col_log_norms");
+  return GOOM_OK;
+}
+
+}  // namespace
 }  // namespace goom
 
 using namespace goom;
@@ -226,72 +274,46 @@ using namespace goom;
 extern "C" {
 
 int goom_from_real_f32(const float* x, goom_c64* out, int64_t n, float zero_log, void* stream) {
-  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
-  if (n == 0) return GOOM_OK;
-  if (!x || !out) return fail(GOOM_EINVAL, "null pointer");
-  from_real_f32_kernel<<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
-      x, reinterpret_cast<float2*>(out), n, zero_log);
-  GOOM_CHECK_LAUNCH("from_real_f32");
-  return GOOM_OK;
+  return from_real<float, float>(x, out, n, zero_log, stream);
 }
-
 int goom_from_real_f64(const double* x, goom_c64* out, int64_t n, double zero_log, void* stream) {
-  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
-  if (n == 0) return GOOM_OK;
-  if (!x || !out) return fail(GOOM_EINVAL, "null pointer");
-  from_real_f64_kernel<<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
-      x, reinterpret_cast<float2*>(out), n, zero_log);
-  GOOM_CHECK_LAUNCH("from_real_f64");
-  return GOOM_OK;
+  return from_real<double, float>(x, out, n, zero_log, stream);
 }
-
+int goom_from_real_c128(const double* x, goom_c128* out, int64_t n, double zero_log,
+                        void* stream) {
+  return from_real<double, double>(x, out, n, zero_log, stream);
+}
 int goom_to_real_f32(const goom_c64* z, float* out, int64_t n, void* stream) {
-  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
-  if (n == 0) return GOOM_OK;
-  if (!z || !out) return fail(GOOM_EINVAL, "null pointer");
-  to_real_f32_kernel<<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float2*>(z), out, n);
-  GOOM_CHECK_LAUNCH("to_real_f32");
-  return GOOM_OK;
+  return to_real<float, float>(z, out, n, stream);
 }
-
 int goom_to_real_f64(const goom_c64* z, double* out, int64_t n, void* stream) {
-  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
-  if (n == 0) return GOOM_OK;
-  if (!z || !out) return fail(GOOM_EINVAL, "null pointer");
-  to_real_f64_kernel<<<stream_grid(n), kThreads, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float2*>(z), out, n);
-  GOOM_CHECK_LAUNCH("to_real_f64");
-  return GOOM_OK;
+  return to_real<float, double>(z, out, n, stream);
 }
-
+int goom_to_real_c128(const goom_c128* z, double* out, int64_t n, void* stream) {
+  return to_real<double, double>(z, out, n, stream);
+}
 int goom_to_real_scaled_f32(const goom_c64* z, float* out, float* c, int64_t batch, int64_t n,
                             void* stream) {
-  if (batch < 0 || n < 0) return fail(GOOM_EINVAL, "batch and n must be >= 0");
-  if (batch == 0) return GOOM_OK;
-  if (!z || !out || !c) return fail(GOOM_EINVAL, "null pointer");
-  to_real_scaled_kernel<<<(unsigned)batch, 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float2*>(z), out, c, n);
-  GOOM_CHECK_LAUNCH("to_real_scaled");
-  return GOOM_OK;
+  return to_real_scaled<float>(z, out, c, batch, n, stream);
 }
-
+int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t batch, int64_t n,
+                             void* stream) {
+  return to_real_scaled<double>(z, out, c, batch, n, stream);
+}
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream) {
-  if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
-  if (n && (!a || !b || !out)) return fail(GOOM_EINVAL, "null pointer");
-  return launch_gadd(reinterpret_cast<const float2*>(a), reinterpret_cast<const float2*>(b),
-                     reinterpret_cast<float2*>(out), n, as_stream(stream));
+  return gadd<float>(a, b, out, n, stream);
 }
-
+int goom_gadd_c128(const goom_c128* a, const goom_c128* b, goom_c128* out, int64_t n,
+                   void* stream) {
+  return gadd<double>(a, b, out, n, stream);
+}
 int goom_col_log_norms_c64(const goom_c64* z, float* out, int64_t batch, int rows, int cols,
                            void* stream) {
-  if (batch < 0 || rows < 1 || cols < 1) return fail(GOOM_EINVAL, "bad shape");
-  if (batch == 0) return GOOM_OK;
-  int64_t t = batch * cols;
-  col_log_norms_kernel<<<(unsigned)((t + 255) / 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const float2*>(z), out, batch, rows, cols);
-  GOOM_CHECK_LAUNCH("col_log_norms");
-  return GOOM_OK;
+  return col_log_norms<float>(z, out, batch, rows, cols, stream);
+}
+int goom_col_log_norms_c128(const goom_c128* z, double* out, int64_t batch, int rows, int cols,
+                            void* stream) {
+  return col_log_norms<double>(z, out, batch, rows, cols, stream);
 }
 
 }  // extern "C"

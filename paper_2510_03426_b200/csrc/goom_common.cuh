@@ -75,15 +75,61 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// ---- precision-generic helpers (complex64 = float2, complex128 = double2) -------
+template <class R> struct CxOf;
+template <> struct CxOf<float> { using type = float2; };
+template <> struct CxOf<double> { using type = double2; };
+template <class R> using Cx = typename CxOf<R>::type;
+
+template <class R> __host__ __device__ __forceinline__ R pi_of();
+template <> __host__ __device__ __forceinline__ float pi_of<float>() { return kPi; }
+template <> __host__ __device__ __forceinline__ double pi_of<double>() {
+  return 3.14159265358979323846;
+}
+
+__device__ __forceinline__ float gexp(float x) { return expf(x); }
+__device__ __forceinline__ double gexp(double x) { return exp(x); }
+__device__ __forceinline__ float glog(float x) { return logf(x); }
+__device__ __forceinline__ double glog(double x) { return log(x); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float gfma(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double gfma(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float gmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double gmax(double a, double b) { return fmax(a, b); }
+
+template <class R> __device__ __forceinline__ R goom_sign_t(R im) {
+  if (im == R(0)) return R(1);
+  if (im == pi_of<R>()) return R(-1);
+  return cos(im) < R(0) ? R(-1) : R(1);
+}
+template <class R> __device__ __forceinline__ Cx<R> cx(R re, R im) {
+  Cx<R> z;
+  z.x = re;
+  z.y = im;
+  return z;
+}
+template <class R> __device__ __forceinline__ R warp_max_t(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = gmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 // ---- operand addressing -----------------------------------------------------
-struct Operand {
-  const float2* ptr;
+template <class C>
+struct OperandT {
+  const C* ptr;
   int64_t stride;
   int64_t div;
-  __host__ __device__ __forceinline__ const float2* at(int64_t b) const {
+  __host__ __device__ __forceinline__ const C* at(int64_t b) const {
     return ptr + (b / div) * stride;
   }
 };
+using Operand = OperandT<float2>;
 
 inline Operand make_operand(const goom_c64* p, int64_t stride, int64_t div) {
   return Operand{reinterpret_cast<const float2*>(p), stride, div < 1 ? 1 : div};

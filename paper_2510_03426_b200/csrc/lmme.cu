@@ -1,4 +1,6 @@
 // LMME dispatch: scale pre-pass + kernel-family selection + ABI entry points.
+//   complex64 : tcgen05 3xTF32 (n, m % 128 == 0, k % 32 == 0) > SIMT small (<= 32) > SIMT tiled
+//   complex128: SIMT FP64 small / tiled
 #include <atomic>
 
 #include "goom_internal.cuh"
@@ -8,96 +10,135 @@ namespace goom {
 namespace {
 std::atomic<int> g_backend{0};  // 0 auto, 1 SIMT, 2 tcgen05
 
-inline int64_t distinct(const Operand& o, int64_t batch) {
-  if (o.stride == 0 || batch == 0) return 1;
-  return (batch - 1) / o.div + 1;
+inline int64_t distinct(int64_t stride, int64_t div, int64_t batch) {
+  if (stride == 0 || batch == 0) return 1;
+  return (batch - 1) / (div < 1 ? 1 : div) + 1;
 }
 inline size_t round_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+template <class R>
+bool small_shape(int n, int k, int m) {
+  return n <= 32 && k <= 32 && m <= 32;
+}
 }  // namespace
 
 int lmme_backend() { return g_backend.load(); }
 
-size_t lmme_workspace_bytes(int64_t batch, int n, int k, int m, const Operand& A,
-                            const Operand& B) {
-  (void)k;
-  if (n <= 32 && k <= 32 && m <= 32 && g_backend.load() != 2) return 0;  // small kernel: in-kernel
-  return round_up(sizeof(float) * (size_t)distinct(A, batch) * n) +
-         round_up(sizeof(float) * (size_t)distinct(B, batch) * m);
+template <class R>
+size_t lmme_workspace_bytes(int64_t batch, int n, int k, int m, int64_t strideA, int64_t divA,
+                            int64_t strideB, int64_t divB) {
+  if (small_shape<R>(n, k, m)) return 0;  // small kernel: scales in-kernel
+  return round_up(sizeof(R) * (size_t)distinct(strideA, divA, batch) * n) +
+         round_up(sizeof(R) * (size_t)distinct(strideB, divB, batch) * m);
 }
 
-int lmme_run(LmmeProblem p, void* ws, size_t ws_bytes, cudaStream_t s) {
+template <class R>
+int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (p.batch == 0 || p.n == 0 || p.m == 0) return GOOM_OK;
   const int backend = g_backend.load();
-  const bool small = p.n <= 32 && p.k <= 32 && p.m <= 32;
-  if (small && backend != 2 && !p.rowA.ptr) return lmme_simt_small(p, s);
+  const bool small = small_shape<R>(p.n, p.k, p.m);
+  if (small && !p.rowA.ptr) return lmme_simt_small<R>(p, s);
   if (!p.rowA.ptr || !p.colB.ptr) {
-    size_t need = lmme_workspace_bytes(p.batch, p.n, p.k, p.m, p.A, p.B);
+    size_t need = lmme_workspace_bytes<R>(p.batch, p.n, p.k, p.m, p.A.stride, p.A.div,
+                                          p.B.stride, p.B.div);
     if (ws_bytes < need || (need && !ws))
       return fail(GOOM_EWORKSPACE, "lmme workspace too small (need " + std::to_string(need) +
                                        " bytes)");
-    int64_t nA = distinct(p.A, p.batch), nB = distinct(p.B, p.batch);
-    float* ra = reinterpret_cast<float*>(ws);
-    float* cb = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
-                                         round_up(sizeof(float) * (size_t)nA * p.n));
-    GOOM_TRY(launch_row_scales(Operand{p.A.ptr, p.A.stride, 1}, ra, nA, p.n, p.k, s));
-    GOOM_TRY(launch_col_scales(Operand{p.B.ptr, p.B.stride, 1}, cb, nB, p.k, p.m, s));
-    p.rowA = Scales{ra, p.A.stride == 0 ? 0 : (int64_t)p.n, p.A.div};
-    p.colB = Scales{cb, p.B.stride == 0 ? 0 : (int64_t)p.m, p.B.div};
+    int64_t nA = distinct(p.A.stride, p.A.div, p.batch), nB = distinct(p.B.stride, p.B.div, p.batch);
+    R* ra = reinterpret_cast<R*>(ws);
+    R* cb = reinterpret_cast<R*>(reinterpret_cast<char*>(ws) + round_up(sizeof(R) * (size_t)nA * p.n));
+    GOOM_TRY(launch_row_scales<R>(OperandT<Cx<R>>{p.A.ptr, p.A.stride, 1}, ra, nA, p.n, p.k, s));
+    GOOM_TRY(launch_col_scales<R>(OperandT<Cx<R>>{p.B.ptr, p.B.stride, 1}, cb, nB, p.k, p.m, s));
+    p.rowA = ScalesT<R>{ra, p.A.stride == 0 ? 0 : (int64_t)p.n, p.A.div};
+    p.colB = ScalesT<R>{cb, p.B.stride == 0 ? 0 : (int64_t)p.m, p.B.div};
   }
-  if (backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)) {
-    int rc = lmme_tc(p, s);
-    if (rc != GOOM_EUNSUPPORTED) return rc;
+  if constexpr (sizeof(R) == 4) {
+    if (backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)) {
+      int rc = lmme_tc(p, s);
+      if (rc != GOOM_EUNSUPPORTED) return rc;
+    }
+    if (backend == 2 && !small)
+      return fail(GOOM_EUNSUPPORTED, "tcgen05 LMME needs n,m multiples of 128 and k of 32");
   }
-  if (backend == 2 && !lmme_tc_eligible(p.n, p.k, p.m) && !small)
-    return fail(GOOM_EUNSUPPORTED, "tcgen05 LMME needs n,m multiples of 128 and k of 32");
-  return lmme_simt_tiled(p, s);
+  return lmme_simt_tiled<R>(p, s);
 }
+
+template size_t lmme_workspace_bytes<float>(int64_t, int, int, int, int64_t, int64_t, int64_t,
+                                            int64_t);
+template size_t lmme_workspace_bytes<double>(int64_t, int, int, int, int64_t, int64_t, int64_t,
+                                             int64_t);
+template int lmme_run<float>(LmmeProblemT<float>, void*, size_t, cudaStream_t);
+template int lmme_run<double>(LmmeProblemT<double>, void*, size_t, cudaStream_t);
 
 }  // namespace goom
 
 using namespace goom;
 
 namespace {
-int check_lmme_args(const goom_operand& A, const goom_operand& B, const goom_c64* C,
-                    int64_t batch, int n, int k, int m) {
+
+int check_lmme_args(const goom_operand& A, const goom_operand& B, const void* C, int64_t batch,
+                    int n, int k, int m) {
   if (batch < 0) return fail(GOOM_EINVAL, "batch must be >= 0");
   if (n < 1 || k < 1 || m < 1) return fail(GOOM_ESHAPE, "lmme dimensions must be >= 1");
   if (batch > 0 && (!A.ptr || !B.ptr || !C)) return fail(GOOM_EINVAL, "null pointer");
   if (A.stride < 0 || B.stride < 0) return fail(GOOM_EINVAL, "negative stride");
   return GOOM_OK;
 }
-}  // namespace
 
-extern "C" {
-
-size_t goom_lmme_workspace_size(int64_t batch, int n, int k, int m) {
-  Operand a{nullptr, 1, 1}, b{nullptr, 1, 1};
-  return lmme_workspace_bytes(batch, n, k, m, a, b);
+template <class R>
+OperandT<Cx<R>> op(const goom_operand& o) {
+  return OperandT<Cx<R>>{reinterpret_cast<const Cx<R>*>(o.ptr), o.stride, o.div < 1 ? 1 : o.div};
 }
 
-int goom_lmme_c64(goom_operand A, goom_operand B, goom_c64* C, int64_t strideC, int64_t batch,
-                  int n, int k, int m, void* ws, size_t ws_bytes, void* stream) {
-  goom_operand D{nullptr, 0, 1};
-  return goom_lmme_gadd_c64(A, B, D, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
-}
-
-int goom_lmme_gadd_c64(goom_operand A, goom_operand B, goom_operand D, goom_c64* C,
-                       int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
-                       size_t ws_bytes, void* stream) {
+template <class R>
+int lmme_entry(goom_operand A, goom_operand B, goom_operand D, void* C, int64_t strideC,
+               int64_t batch, int n, int k, int m, void* ws, size_t ws_bytes, void* stream) {
   GOOM_TRY(check_lmme_args(A, B, C, batch, n, k, m));
-  LmmeProblem p{};
-  p.A = make_operand(A.ptr, A.stride, A.div);
-  p.B = make_operand(B.ptr, B.stride, B.div);
-  p.D = make_operand(D.ptr, D.stride, D.div);
-  p.C = reinterpret_cast<float2*>(C);
+  LmmeProblemT<R> p{};
+  p.A = op<R>(A);
+  p.B = op<R>(B);
+  p.D = op<R>(D);
+  p.C = reinterpret_cast<Cx<R>*>(C);
   p.strideC = strideC;
   p.batch = batch;
   p.n = n;
   p.k = k;
   p.m = m;
-  p.rowA = Scales{nullptr, 0, 1};
-  p.colB = Scales{nullptr, 0, 1};
-  return lmme_run(p, ws, ws_bytes, as_stream(stream));
+  p.rowA = ScalesT<R>{nullptr, 0, 1};
+  p.colB = ScalesT<R>{nullptr, 0, 1};
+  return lmme_run<R>(p, ws, ws_bytes, as_stream(stream));
+}
+
+const goom_operand kNoAddend{nullptr, 0, 1};
+
+}  // namespace
+
+extern "C" {
+
+size_t goom_lmme_workspace_size(int64_t batch, int n, int k, int m) {
+  return lmme_workspace_bytes<float>(batch, n, k, m, 1, 1, 1, 1);
+}
+size_t goom_lmme_workspace_size_c128(int64_t batch, int n, int k, int m) {
+  return lmme_workspace_bytes<double>(batch, n, k, m, 1, 1, 1, 1);
+}
+
+int goom_lmme_c64(goom_operand A, goom_operand B, goom_c64* C, int64_t strideC, int64_t batch,
+                  int n, int k, int m, void* ws, size_t ws_bytes, void* stream) {
+  return lmme_entry<float>(A, B, kNoAddend, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
+}
+int goom_lmme_gadd_c64(goom_operand A, goom_operand B, goom_operand D, goom_c64* C,
+                       int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return lmme_entry<float>(A, B, D, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
+}
+int goom_lmme_c128(goom_operand A, goom_operand B, goom_c128* C, int64_t strideC, int64_t batch,
+                   int n, int k, int m, void* ws, size_t ws_bytes, void* stream) {
+  return lmme_entry<double>(A, B, kNoAddend, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
+}
+int goom_lmme_gadd_c128(goom_operand A, goom_operand B, goom_operand D, goom_c128* C,
+                        int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
+                        size_t ws_bytes, void* stream) {
+  return lmme_entry<double>(A, B, D, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
 }
 
 int goom_set_lmme_backend(int backend) {

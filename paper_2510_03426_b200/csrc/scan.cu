@@ -1,4 +1,4 @@
-// Blocked prefix-scan engines over LMME combines.
+// Blocked prefix-scan engines over LMME combines (complex64 and complex128).
 //
 // Both engines use the reference's two-level tree (_scan_affine_stack,
 // scan.py:181-214) with block s, restructured for the GPU:
@@ -33,15 +33,17 @@ struct Carve {
   }
 };
 
-size_t lmme_ws(int64_t batch, int n, int k, int m) {
+template <class R>
+size_t lmme_ws(int64_t batch, int n, int m) {
   // worst case: every operand distinct
-  return round_up(sizeof(float) * (size_t)batch * n) + round_up(sizeof(float) * (size_t)batch * m);
+  return round_up(sizeof(R) * (size_t)batch * n) + round_up(sizeof(R) * (size_t)batch * m);
 }
 
-// out[b] = A(b) (x) B(b) (+) D(b)
-int lmme_call(Operand A, Operand B, Operand D, float2* C, int64_t strideC, int64_t batch, int n,
-              int k, int m, void* ws, size_t ws_bytes, cudaStream_t s) {
-  LmmeProblem p{};
+// C[b] = A(b) (x) B(b) (+) D(b)
+template <class R>
+int lmme_call(OperandT<Cx<R>> A, OperandT<Cx<R>> B, OperandT<Cx<R>> D, Cx<R>* C, int64_t strideC,
+              int64_t batch, int n, int k, int m, void* ws, size_t ws_bytes, cudaStream_t s) {
+  LmmeProblemT<R> p{};
   p.A = A;
   p.B = B;
   p.D = D;
@@ -51,153 +53,202 @@ int lmme_call(Operand A, Operand B, Operand D, float2* C, int64_t strideC, int64
   p.n = n;
   p.k = k;
   p.m = m;
-  p.rowA = Scales{nullptr, 0, 1};
-  p.colB = Scales{nullptr, 0, 1};
-  return lmme_run(p, ws, ws_bytes, s);
+  p.rowA = ScalesT<R>{nullptr, 0, 1};
+  p.colB = ScalesT<R>{nullptr, 0, 1};
+  return lmme_run<R>(p, ws, ws_bytes, s);
 }
 
-const Operand kNone{nullptr, 0, 1};
+template <class C>
+OperandT<C> opnd(const C* p, int64_t stride, int64_t div = 1) {
+  return OperandT<C>{p, stride, div};
+}
+
+template <class C>
+int copy_d2d(C* dst, const C* src, size_t count, cudaStream_t st, const char* what) {
+  if (count && cudaMemcpyAsync(dst, src, sizeof(C) * count, cudaMemcpyDeviceToDevice, st) !=
+                   cudaSuccess)
+    return cuda_fail(cudaGetLastError(), what);
+  return GOOM_OK;
+}
+
+// dst[k*pitch .. +width) = src[k*pitch .. +width) for k < rows (elements)
+template <class C>
+int copy_strided(C* dst, const C* src, size_t width, size_t pitch, size_t rows, cudaStream_t st,
+                 const char* what) {
+  if (cudaMemcpy2DAsync(dst, sizeof(C) * pitch, src, sizeof(C) * pitch, sizeof(C) * width, rows,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), what);
+  return GOOM_OK;
+}
 
 }  // namespace
 
+template <class R>
 size_t chain_workspace_bytes(int64_t T, int d, int block) {
   int64_t s = block < T ? block : T;
   int64_t nb = (T + s - 1) / s;
   size_t mat = (size_t)d * d;
-  size_t lm = lmme_ws(T, d, d, d);
-  return round_up(sizeof(float2) * mat * T) + round_up(sizeof(float2) * mat * (nb + 1)) + lm;
+  return round_up(sizeof(Cx<R>) * mat * T) + round_up(sizeof(Cx<R>) * mat * (nb + 1)) +
+         lmme_ws<R>(T, d, d);
 }
 
-// Product chain with optional right carry (see header comment).
-int chain_scan(const float2* A, float2* out, int64_t T, int d, int block, const float2* carry_in,
+template <class R>
+int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx<R>* carry_in,
                void* ws, size_t ws_bytes, cudaStream_t st) {
+  using C = Cx<R>;
   const int64_t s = block < T ? block : T;
   const int64_t nb = (T + s - 1) / s;
   const int64_t mat = (int64_t)d * d;
-  if (ws_bytes < chain_workspace_bytes(T, d, block))
+  if (ws_bytes < chain_workspace_bytes<R>(T, d, block))
     return fail(GOOM_EWORKSPACE, "chain scan workspace too small");
   Carve cv{reinterpret_cast<char*>(ws)};
-  float2* L = cv.take<float2>((size_t)mat * T);
-  float2* Cx = cv.take<float2>((size_t)mat * (nb + 1));
+  C* L = cv.take<C>((size_t)mat * T);
+  C* Cx_ = cv.take<C>((size_t)mat * (nb + 1));
   void* lws = cv.base + cv.off;
   size_t lws_bytes = ws_bytes - cv.off;
+  const OperandT<C> none{nullptr, 0, 1};
 
   // phase 1: L[k*s] = A[k*s]; L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]
-  if (cudaMemcpy2DAsync(L, sizeof(float2) * mat * s, A, sizeof(float2) * mat * s,
-                        sizeof(float2) * mat, nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-    return cuda_fail(cudaGetLastError(), "chain phase-1 copy");
+  GOOM_TRY(copy_strided(L, A, mat, mat * s, nb, st, "chain phase-1 copy"));
   for (int64_t i = 1; i < s; ++i) {
     int64_t cnt = (T - i + s - 1) / s;  // blocks whose length exceeds i
     if (cnt <= 0) break;
-    GOOM_TRY(lmme_call(Operand{A + i * mat, s * mat, 1}, Operand{L + (i - 1) * mat, s * mat, 1},
-                       kNone, L + i * mat, s * mat, cnt, d, d, d, lws, lws_bytes, st));
+    GOOM_TRY(lmme_call<R>(opnd(A + i * mat, s * mat), opnd<C>(L + (i - 1) * mat, s * mat), none,
+                          L + i * mat, s * mat, cnt, d, d, d, lws, lws_bytes, st));
   }
   // phase 2: Cx[0] = carry_in; Cx[k+1] = L[last of block k] (x) Cx[k]
-  for (int64_t kb = 0; kb < nb; ++kb) {
-    int64_t last = (kb * s + s < T ? kb * s + s : T) - 1;
+  for (int64_t kb = 0; kb + 1 < nb || (kb == 0 && !carry_in); ++kb) {
+    int64_t last = kb * s + s - 1;
     if (kb == 0 && !carry_in) {
-      if (cudaMemcpyAsync(Cx + mat, L + last * mat, sizeof(float2) * mat,
-                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return cuda_fail(cudaGetLastError(), "chain carry copy");
+      GOOM_TRY(copy_d2d(Cx_ + mat, L + last * mat, mat, st, "chain carry copy"));
+      if (nb == 1) break;
       continue;
     }
-    const float2* prev = (kb == 0) ? carry_in : Cx + kb * mat;
-    if (kb == nb - 1) break;  // the last block's carry-out is produced by phase 3
-    GOOM_TRY(lmme_call(Operand{L + last * mat, 0, 1}, Operand{prev, 0, 1}, kNone,
-                       Cx + (kb + 1) * mat, 0, 1, d, d, d, lws, lws_bytes, st));
+    const C* prev = (kb == 0) ? carry_in : Cx_ + kb * mat;
+    GOOM_TRY(lmme_call<R>(opnd<C>(L + last * mat, 0), opnd(prev, 0), none, Cx_ + (kb + 1) * mat,
+                          0, 1, d, d, d, lws, lws_bytes, st));
   }
   // phase 3: out[b] = L[b] (x) Cx[b/s]  (block 0 needs a carry only with carry_in)
   if (carry_in) {
-    if (cudaMemcpyAsync(Cx, carry_in, sizeof(float2) * mat, cudaMemcpyDeviceToDevice, st) !=
-        cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "chain carry-in copy");
-    GOOM_TRY(lmme_call(Operand{L, mat, 1}, Operand{Cx, mat, s}, kNone, out, mat, T, d, d, d, lws,
-                       lws_bytes, st));
+    GOOM_TRY(copy_d2d(Cx_, carry_in, mat, st, "chain carry-in copy"));
+    GOOM_TRY(lmme_call<R>(opnd<C>(L, mat), opnd<C>(Cx_, mat, s), none, out, mat, T, d, d, d, lws,
+                          lws_bytes, st));
   } else {
-    if (cudaMemcpyAsync(out, L, sizeof(float2) * mat * s, cudaMemcpyDeviceToDevice, st) !=
-        cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "chain block-0 copy");
+    GOOM_TRY(copy_d2d(out, L, (size_t)mat * s, st, "chain block-0 copy"));
     if (T > s)
-      GOOM_TRY(lmme_call(Operand{L + s * mat, mat, 1}, Operand{Cx + mat, mat, s}, kNone,
-                         out + s * mat, mat, T - s, d, d, d, lws, lws_bytes, st));
+      GOOM_TRY(lmme_call<R>(opnd<C>(L + s * mat, mat), opnd<C>(Cx_ + mat, mat, s), none,
+                            out + s * mat, mat, T - s, d, d, d, lws, lws_bytes, st));
   }
   return GOOM_OK;
 }
 
+template size_t chain_workspace_bytes<float>(int64_t, int, int);
+template size_t chain_workspace_bytes<double>(int64_t, int, int);
+template int chain_scan<float>(const float2*, float2*, int64_t, int, int, const float2*, void*,
+                               size_t, cudaStream_t);
+template int chain_scan<double>(const double2*, double2*, int64_t, int, int, const double2*,
+                                void*, size_t, cudaStream_t);
+
+namespace {
+
+template <class R>
 size_t affine_workspace_bytes(int64_t T, int d, int m, int block) {
   int64_t s = block < T ? block : T;
   int64_t nb = (T + s - 1) / s;
-  size_t lm = lmme_ws(T, d, d, d > m ? d : m);
-  return round_up(sizeof(float2) * (size_t)d * d * T) + round_up(sizeof(float2) * (size_t)d * m * T) +
-         round_up(sizeof(float2) * (size_t)d * d * (nb + 1)) +
-         round_up(sizeof(float2) * (size_t)d * m * (nb + 1)) + lm;
+  const size_t e = sizeof(Cx<R>);
+  return round_up(e * (size_t)d * d * T) + round_up(e * (size_t)d * m * T) +
+         round_up(e * (size_t)d * d * (nb + 1)) + round_up(e * (size_t)d * m * (nb + 1)) +
+         lmme_ws<R>(T, d, d > m ? d : m);
 }
 
-int affine_scan(const float2* A, const float2* B, const uint8_t* flags_in, float2* outA,
-                float2* outB, uint8_t* flags_out, int64_t T, int d, int m, int block, void* ws,
+template <class R>
+int affine_scan(const Cx<R>* A, const Cx<R>* B, const uint8_t* flags_in, Cx<R>* outA,
+                Cx<R>* outB, uint8_t* flags_out, int64_t T, int d, int m, int block, void* ws,
                 size_t ws_bytes, cudaStream_t st) {
+  using C = Cx<R>;
   const int64_t s = block < T ? block : T;
   const int64_t nb = (T + s - 1) / s;
   const int64_t ma = (int64_t)d * d, mb = (int64_t)d * m;
-  if (ws_bytes < affine_workspace_bytes(T, d, m, block))
+  if (ws_bytes < affine_workspace_bytes<R>(T, d, m, block))
     return fail(GOOM_EWORKSPACE, "affine scan workspace too small");
   Carve cv{reinterpret_cast<char*>(ws)};
-  float2* LA = cv.take<float2>((size_t)ma * T);
-  float2* LB = cv.take<float2>((size_t)mb * T);
-  float2* CA = cv.take<float2>((size_t)ma * (nb + 1));
-  float2* CB = cv.take<float2>((size_t)mb * (nb + 1));
+  C* LA = cv.take<C>((size_t)ma * T);
+  C* LB = cv.take<C>((size_t)mb * T);
+  C* CA = cv.take<C>((size_t)ma * (nb + 1));
+  C* CB = cv.take<C>((size_t)mb * (nb + 1));
   void* lws = cv.base + cv.off;
   size_t lws_bytes = ws_bytes - cv.off;
+  const OperandT<C> none{nullptr, 0, 1};
 
-  if (cudaMemcpy2DAsync(LA, sizeof(float2) * ma * s, A, sizeof(float2) * ma * s,
-                        sizeof(float2) * ma, nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-      cudaMemcpy2DAsync(LB, sizeof(float2) * mb * s, B, sizeof(float2) * mb * s,
-                        sizeof(float2) * mb, nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-    return cuda_fail(cudaGetLastError(), "affine phase-1 copy");
-  // phase 1 (combine_affine, scan.py:173-178): A slot then fused bias slot
+  GOOM_TRY(copy_strided(LA, A, ma, ma * s, nb, st, "affine phase-1 copy"));
+  GOOM_TRY(copy_strided(LB, B, mb, mb * s, nb, st, "affine phase-1 copy"));
+  // phase 1 (combine_affine, scan.py:173-178): A slot, then the fused bias slot
   for (int64_t i = 1; i < s; ++i) {
     int64_t cnt = (T - i + s - 1) / s;
     if (cnt <= 0) break;
-    Operand cur{A + i * ma, s * ma, 1};
-    GOOM_TRY(lmme_call(cur, Operand{LA + (i - 1) * ma, s * ma, 1}, kNone, LA + i * ma, s * ma, cnt,
-                       d, d, d, lws, lws_bytes, st));
-    GOOM_TRY(lmme_call(cur, Operand{LB + (i - 1) * mb, s * mb, 1}, Operand{B + i * mb, s * mb, 1},
-                       LB + i * mb, s * mb, cnt, d, d, m, lws, lws_bytes, st));
+    auto cur = opnd(A + i * ma, s * ma);
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(LA + (i - 1) * ma, s * ma), none, LA + i * ma, s * ma, cnt,
+                          d, d, d, lws, lws_bytes, st));
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(LB + (i - 1) * mb, s * mb), opnd(B + i * mb, s * mb),
+                          LB + i * mb, s * mb, cnt, d, d, m, lws, lws_bytes, st));
   }
-  // phase 2: carries
+  // phase 2: carries of blocks 0 .. nb-2
   for (int64_t kb = 0; kb + 1 < nb; ++kb) {
     int64_t last = kb * s + s - 1;
     if (kb == 0) {
-      if (cudaMemcpyAsync(CA + ma, LA + last * ma, sizeof(float2) * ma, cudaMemcpyDeviceToDevice,
-                          st) != cudaSuccess ||
-          cudaMemcpyAsync(CB + mb, LB + last * mb, sizeof(float2) * mb, cudaMemcpyDeviceToDevice,
-                          st) != cudaSuccess)
-        return cuda_fail(cudaGetLastError(), "affine carry copy");
+      GOOM_TRY(copy_d2d(CA + ma, LA + last * ma, ma, st, "affine carry copy"));
+      GOOM_TRY(copy_d2d(CB + mb, LB + last * mb, mb, st, "affine carry copy"));
       continue;
     }
-    Operand cur{LA + last * ma, 0, 1};
-    GOOM_TRY(lmme_call(cur, Operand{CA + kb * ma, 0, 1}, kNone, CA + (kb + 1) * ma, 0, 1, d, d, d,
-                       lws, lws_bytes, st));
-    GOOM_TRY(lmme_call(cur, Operand{CB + kb * mb, 0, 1}, Operand{LB + last * mb, 0, 1},
-                       CB + (kb + 1) * mb, 0, 1, d, d, m, lws, lws_bytes, st));
+    auto cur = opnd<C>(LA + last * ma, 0);
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(CA + kb * ma, 0), none, CA + (kb + 1) * ma, 0, 1, d, d, d,
+                          lws, lws_bytes, st));
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(CB + kb * mb, 0), opnd<C>(LB + last * mb, 0),
+                          CB + (kb + 1) * mb, 0, 1, d, d, m, lws, lws_bytes, st));
   }
   // phase 3
-  if (cudaMemcpyAsync(outA, LA, sizeof(float2) * ma * s, cudaMemcpyDeviceToDevice, st) !=
-          cudaSuccess ||
-      cudaMemcpyAsync(outB, LB, sizeof(float2) * mb * s, cudaMemcpyDeviceToDevice, st) !=
-          cudaSuccess)
-    return cuda_fail(cudaGetLastError(), "affine block-0 copy");
+  GOOM_TRY(copy_d2d(outA, LA, (size_t)ma * s, st, "affine block-0 copy"));
+  GOOM_TRY(copy_d2d(outB, LB, (size_t)mb * s, st, "affine block-0 copy"));
   if (T > s) {
-    Operand cur{LA + s * ma, ma, 1};
-    GOOM_TRY(lmme_call(cur, Operand{CA + ma, ma, s}, kNone, outA + s * ma, ma, T - s, d, d, d, lws,
-                       lws_bytes, st));
-    GOOM_TRY(lmme_call(cur, Operand{CB + mb, mb, s}, Operand{LB + s * mb, mb, 1}, outB + s * mb,
-                       mb, T - s, d, d, m, lws, lws_bytes, st));
+    auto cur = opnd<C>(LA + s * ma, ma);
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(CA + ma, ma, s), none, outA + s * ma, ma, T - s, d, d, d,
+                          lws, lws_bytes, st));
+    GOOM_TRY(lmme_call<R>(cur, opnd<C>(CB + mb, mb, s), opnd<C>(LB + s * mb, mb), outB + s * mb,
+                          mb, T - s, d, d, m, lws, lws_bytes, st));
   }
   if (flags_out) GOOM_TRY(launch_flags_or_scan(flags_in, flags_out, T, st));
   return GOOM_OK;
 }
 
+int check_scan(int64_t T, int block, int d, int m) {
+  if (T < 1) return fail(GOOM_EINVAL, "scan of an empty sequence");
+  if (block < 1) return fail(GOOM_EINVAL, "block_size must be >= 1");
+  if (d < 1 || m < 1) return fail(GOOM_ESHAPE, "d and m must be >= 1");
+  return GOOM_OK;
+}
+
+template <class R>
+int chain_entry(const void* A, void* out, int64_t T, int d, int block, const void* carry_in,
+                void* ws, size_t ws_bytes, void* stream) {
+  GOOM_TRY(check_scan(T, block, d, 1));
+  if (!A || !out) return fail(GOOM_EINVAL, "null pointer");
+  return chain_scan<R>(reinterpret_cast<const Cx<R>*>(A), reinterpret_cast<Cx<R>*>(out), T, d,
+                       block, reinterpret_cast<const Cx<R>*>(carry_in), ws, ws_bytes,
+                       as_stream(stream));
+}
+
+template <class R>
+int affine_entry(const void* A, const void* B, const uint8_t* flags_in, void* outA, void* outB,
+                 uint8_t* flags_out, int64_t T, int d, int m, int block, void* ws,
+                 size_t ws_bytes, void* stream) {
+  GOOM_TRY(check_scan(T, block, d, m));
+  if (!A || !B || !outA || !outB) return fail(GOOM_EINVAL, "null pointer");
+  return affine_scan<R>(reinterpret_cast<const Cx<R>*>(A), reinterpret_cast<const Cx<R>*>(B),
+                        flags_in, reinterpret_cast<Cx<R>*>(outA), reinterpret_cast<Cx<R>*>(outB),
+                        flags_out, T, d, m, block, ws, ws_bytes, as_stream(stream));
+}
+
+}  // namespace
 }  // namespace goom
 
 using namespace goom;
@@ -206,35 +257,40 @@ extern "C" {
 
 size_t goom_scan_chain_workspace_size(int64_t T, int d, int block) {
   if (T < 1 || d < 1 || block < 1) return 0;
-  return chain_workspace_bytes(T, d, block);
+  return chain_workspace_bytes<float>(T, d, block);
 }
-
+size_t goom_scan_chain_workspace_size_c128(int64_t T, int d, int block) {
+  if (T < 1 || d < 1 || block < 1) return 0;
+  return chain_workspace_bytes<double>(T, d, block);
+}
 int goom_scan_chain_c64(const goom_c64* A, goom_c64* out, int64_t T, int d, int block,
                         const goom_c64* carry_in, void* ws, size_t ws_bytes, void* stream) {
-  if (T < 1) return fail(GOOM_EINVAL, "scan of an empty sequence");
-  if (block < 1) return fail(GOOM_EINVAL, "block_size must be >= 1");
-  if (d < 1) return fail(GOOM_ESHAPE, "d must be >= 1");
-  if (!A || !out) return fail(GOOM_EINVAL, "null pointer");
-  return chain_scan(reinterpret_cast<const float2*>(A), reinterpret_cast<float2*>(out), T, d,
-                    block, reinterpret_cast<const float2*>(carry_in), ws, ws_bytes,
-                    as_stream(stream));
+  return chain_entry<float>(A, out, T, d, block, carry_in, ws, ws_bytes, stream);
+}
+int goom_scan_chain_c128(const goom_c128* A, goom_c128* out, int64_t T, int d, int block,
+                         const goom_c128* carry_in, void* ws, size_t ws_bytes, void* stream) {
+  return chain_entry<double>(A, out, T, d, block, carry_in, ws, ws_bytes, stream);
 }
 
 size_t goom_scan_affine_workspace_size(int64_t T, int d, int m, int block) {
   if (T < 1 || d < 1 || m < 1 || block < 1) return 0;
-  return affine_workspace_bytes(T, d, m, block);
+  return affine_workspace_bytes<float>(T, d, m, block);
 }
-
+size_t goom_scan_affine_workspace_size_c128(int64_t T, int d, int m, int block) {
+  if (T < 1 || d < 1 || m < 1 || block < 1) return 0;
+  return affine_workspace_bytes<double>(T, d, m, block);
+}
 int goom_scan_affine_c64(const goom_c64* A, const goom_c64* B, const uint8_t* flags_in,
                          goom_c64* outA, goom_c64* outB, uint8_t* flags_out, int64_t T, int d,
                          int m, int block, void* ws, size_t ws_bytes, void* stream) {
-  if (T < 1) return fail(GOOM_EINVAL, "scan of an empty sequence");
-  if (block < 1) return fail(GOOM_EINVAL, "block_size must be >= 1");
-  if (d < 1 || m < 1) return fail(GOOM_ESHAPE, "d and m must be >= 1");
-  if (!A || !B || !outA || !outB) return fail(GOOM_EINVAL, "null pointer");
-  return affine_scan(reinterpret_cast<const float2*>(A), reinterpret_cast<const float2*>(B),
-                     flags_in, reinterpret_cast<float2*>(outA), reinterpret_cast<float2*>(outB),
-                     flags_out, T, d, m, block, ws, ws_bytes, as_stream(stream));
+  return affine_entry<float>(A, B, flags_in, outA, outB, flags_out, T, d, m, block, ws, ws_bytes,
+                             stream);
+}
+int goom_scan_affine_c128(const goom_c128* A, const goom_c128* B, const uint8_t* flags_in,
+                          goom_c128* outA, goom_c128* outB, uint8_t* flags_out, int64_t T, int d,
+                          int m, int block, void* ws, size_t ws_bytes, void* stream) {
+  return affine_entry<double>(A, B, flags_in, outA, outB, flags_out, T, d, m, block, ws, ws_bytes,
+                              stream);
 }
 
 }  // extern "C"

@@ -46,37 +46,41 @@ struct Policy {
   double log_floor;
 };
 
+// Shared-memory carve-up of the walk CTA; Rt is the chain's backing precision.
+template <class Rt>
 struct Smem {
-  float2* carry;  // d*d
-  float2* el;     // d*d
-  double* R;      // d*d (aliases the f32 LMME operand buffers)
+  Cx<Rt>* carry;  // d*d
+  Cx<Rt>* el;     // d*d
+  double* R;      // d*d  (R and W also host the LMME operand planes tl / tr)
   double* W;      // d*d
-  float* tl;      // d*d (== (float*)R)
-  float* tr;      // d*d
-  float* scal;    // 2d
+  Rt* tl;         // d*d (aliases R)
+  Rt* tr;         // d*d
+  Rt* scal;       // 2d
   double* vec;    // 2d
   double* red;    // 2 * kWarps
   int* ints;      // 8
 };
 
-__host__ __device__ inline size_t smem_bytes(int d) {
+template <class Rt>
+inline size_t smem_bytes(int d) {
   size_t dd = (size_t)d * d;
-  return 2 * dd * sizeof(float2) + 2 * dd * sizeof(double) + 2 * d * sizeof(float) +
+  return 2 * dd * sizeof(Cx<Rt>) + 2 * dd * sizeof(double) + 2 * d * sizeof(Rt) +
          2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + 64;
 }
 
-__device__ Smem carve(char* base, int d) {
-  Smem s;
+template <class Rt>
+__device__ Smem<Rt> carve(char* base, int d) {
+  Smem<Rt> s;
   size_t dd = (size_t)d * d;
-  s.carry = reinterpret_cast<float2*>(base);
+  s.carry = reinterpret_cast<Cx<Rt>*>(base);
   s.el = s.carry + dd;
   s.R = reinterpret_cast<double*>(s.el + dd);
   s.W = s.R + dd;
-  s.tl = reinterpret_cast<float*>(s.R);
+  s.tl = reinterpret_cast<Rt*>(s.R);
   s.tr = s.tl + dd;
   s.vec = s.W + dd;
   s.red = s.vec + 2 * d;
-  s.scal = reinterpret_cast<float*>(s.red + 2 * kWarps);
+  s.scal = reinterpret_cast<Rt*>(s.red + 2 * kWarps);
   s.ints = reinterpret_cast<int*>(s.scal + 2 * d);
   return s;
 }
@@ -93,53 +97,51 @@ __device__ double block_max(double v, double* red) {
   return r;
 }
 
-__device__ __forceinline__ float lmme_out_log(float acc, float a, float b) {
-  return __fadd_rn(__fadd_rn(logf(fabsf(acc)), a), b);
-}
-
-// out (smem) = Lg (global, d x d) (x) Rs (smem, d x d); Eq. 10-12 in FP32.
-__device__ void block_lmme(const float2* __restrict__ Lg, const float2* Rs, float2* out, int d,
-                           const Smem& sm) {
+// out (smem) = Lg (global, d x d) (x) Rs (smem, d x d); Eq. 10-12 at the chain's precision,
+// same per-output FMA order as the SIMT kernels (bitwise-identical products).
+template <class Rt>
+__device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<Rt>* out, int d,
+                           const Smem<Rt>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = w; i < d; i += kWarps) {
-    float m = kNegInf;
-    for (int j = lane; j < d; j += 32) m = fmaxf(m, Lg[i * d + j].x);
-    m = warp_max(m);
-    if (lane == 0) sm.scal[i] = fmaxf(m, 0.0f);
+    Rt m = Rt(-INFINITY);
+    for (int j = lane; j < d; j += 32) m = gmax(m, Lg[i * d + j].x);
+    m = warp_max_t(m);
+    if (lane == 0) sm.scal[i] = gmax(m, Rt(0));
   }
   for (int j = tid; j < d; j += kThreads) {
-    float m = kNegInf;
-    for (int r = 0; r < d; ++r) m = fmaxf(m, Rs[r * d + j].x);
-    sm.scal[d + j] = fmaxf(m, 0.0f);
+    Rt m = Rt(-INFINITY);
+    for (int r = 0; r < d; ++r) m = gmax(m, Rs[r * d + j].x);
+    sm.scal[d + j] = gmax(m, Rt(0));
   }
   __syncthreads();
   for (int e = tid; e < d * d; e += kThreads) {
-    int i = e / d, kk = e % d;
-    float2 z = Lg[e];
-    sm.tl[kk * d + i] = goom_sign(z.y) * expf(z.x - sm.scal[i]);
-    float2 q = Rs[e];
-    sm.tr[e] = goom_sign(q.y) * expf(q.x - sm.scal[d + kk]);  // e = kk2*d + j, col j = kk here
+    int i = e / d, j = e % d;
+    Cx<Rt> z = Lg[e];  // left operand, row i, column j (= k index)
+    sm.tl[j * d + i] = goom_sign_t<Rt>(z.y) * gexp(z.x - sm.scal[i]);
+    Cx<Rt> q = Rs[e];  // right operand, row i (= k index), column j
+    sm.tr[e] = goom_sign_t<Rt>(q.y) * gexp(q.x - sm.scal[d + j]);
   }
   __syncthreads();
   const int ty = tid >> 4, tx = tid & 15;
-  float acc[4][4];
+  Rt acc[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0f;
+    for (int c = 0; c < 4; ++c) acc[r][c] = Rt(0);
   for (int kk = 0; kk < d; ++kk) {
-    float av[4], bv[4];
+    Rt av[4], bv[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       int i = ty + 16 * r;
-      av[r] = i < d ? sm.tl[kk * d + i] : 0.0f;
+      av[r] = i < d ? sm.tl[kk * d + i] : Rt(0);
       int j = tx + 16 * r;
-      bv[r] = j < d ? sm.tr[kk * d + j] : 0.0f;
+      bv[r] = j < d ? sm.tr[kk * d + j] : Rt(0);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+      for (int c = 0; c < 4; ++c) acc[r][c] = gfma(av[r], bv[c], acc[r][c]);
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -149,23 +151,22 @@ __device__ void block_lmme(const float2* __restrict__ Lg, const float2* Rs, floa
     for (int c = 0; c < 4; ++c) {
       int j = tx + 16 * c;
       if (j >= d) continue;
-      float a = acc[r][c];
-      out[i * d + j] = make_float2(lmme_out_log(a, sm.scal[i], sm.scal[d + j]),
-                                   a < 0.0f ? kPi : 0.0f);
+      out[i * d + j] = lmme_out<Rt>(acc[r][c], sm.scal[i], sm.scal[d + j]);
     }
   }
   __syncthreads();
 }
 
 // Column log-norms nu_j (FP64) into sm.vec[0..d); returns true if a column is all zero.
-__device__ bool unit_columns(const float2* X, int d, const Smem& sm) {
+template <class Rt>
+__device__ bool unit_columns(const Cx<Rt>* X, int d, const Smem<Rt>& sm) {
   const int tid = threadIdx.x;
   if (tid == 0) sm.ints[0] = 0;
   __syncthreads();
   for (int j = tid; j < d; j += kThreads) {
-    float m = kNegInf;
-    for (int r = 0; r < d; ++r) m = fmaxf(m, X[r * d + j].x);
-    if (m == kNegInf) {
+    double m = -INFINITY;
+    for (int r = 0; r < d; ++r) m = fmax(m, (double)X[r * d + j].x);
+    if (m == -INFINITY) {
       sm.ints[0] = 1;
       sm.vec[j] = -INFINITY;
       continue;
@@ -178,8 +179,8 @@ __device__ bool unit_columns(const float2* X, int d, const Smem& sm) {
   bool zero = sm.ints[0] != 0;
   if (!zero) {
     for (int e = tid; e < d * d; e += kThreads) {
-      float2 z = X[e];
-      sm.R[e] = (double)goom_sign(z.y) * exp((double)z.x - sm.vec[e % d]);
+      Cx<Rt> z = X[e];
+      sm.R[e] = (double)goom_sign_t<Rt>(z.y) * exp((double)z.x - sm.vec[e % d]);
     }
   }
   __syncthreads();
@@ -187,7 +188,8 @@ __device__ bool unit_columns(const float2* X, int d, const Smem& sm) {
 }
 
 // slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor
-__device__ bool volume_deficient(int d, double log_floor, const Smem& sm) {
+template <class Rt>
+__device__ bool volume_deficient(int d, double log_floor, const Smem<Rt>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int e = tid; e < d * d; e += kThreads) sm.W[e] = sm.R[e];
   __syncthreads();
@@ -211,6 +213,7 @@ __device__ bool volume_deficient(int d, double log_floor, const Smem& sm) {
     __syncthreads();
     const int piv = sm.ints[1];
     const double pv = sm.W[piv * d + c];
+    __syncthreads();  // every thread holds pv before the row swap overwrites it
     if (pv == 0.0) return true;  // det_sign == 0
     if (piv != c)
       for (int j = tid; j < d; j += kThreads) {
@@ -233,7 +236,8 @@ __device__ bool volume_deficient(int d, double log_floor, const Smem& sm) {
   return logdet < log_floor;
 }
 
-__device__ bool policy_select(const float2* X, int d, const Policy& pol, const Smem& sm) {
+template <class Rt>
+__device__ bool policy_select(const Cx<Rt>* X, int d, const Policy& pol, const Smem<Rt>& sm) {
   if (pol.kind == GOOM_POLICY_NEVER) return false;
   bool zero = unit_columns(X, d, sm);
   if (pol.kind == GOOM_POLICY_NORM_THRESHOLD) {
@@ -257,7 +261,8 @@ __device__ bool policy_select(const float2* X, int d, const Policy& pol, const S
 
 // Householder QR of sm.R in place; Q into sm.W. positive_diag flips Q columns so
 // that diag(R) > 0 (the CGS2 basis). Returns GOOM_ERANK on a rank-deficient state.
-__device__ int householder_q(int d, bool positive_diag, const Smem& sm) {
+template <class Rt>
+__device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double* tau = sm.vec;      // [0, d)
   double* diag = sm.vec + d;  // [d, 2d)
@@ -326,32 +331,35 @@ __device__ int householder_q(int d, bool positive_diag, const Smem& sm) {
 }
 
 // reset(X) -> out (smem or global), canonical GOOMs. Returns a goom_status.
-__device__ int policy_reset(const float2* X, float2* out, int d, int kind, const Smem& sm) {
+template <class Rt>
+__device__ int policy_reset(const Cx<Rt>* X, Cx<Rt>* out, int d, int kind, const Smem<Rt>& sm) {
   bool zero = unit_columns(X, d, sm);
   if (zero) return GOOM_ERANK;
   int rc = householder_q(d, kind == GOOM_POLICY_COLINEARITY, sm);
   if (rc != GOOM_OK) return rc;
   for (int e = threadIdx.x; e < d * d; e += kThreads) {
     double q = sm.W[e];
-    out[e] = make_float2((float)log(fabs(q)), q < 0.0 ? kPi : 0.0f);
+    out[e] = cx<Rt>((Rt)log(fabs(q)), q < 0.0 ? pi_of<Rt>() : Rt(0));
   }
   __syncthreads();
   return GOOM_OK;
 }
 
-__device__ void copy_mat(const float2* src, float2* dst, int d) {
+template <class C>
+__device__ void copy_mat(const C* src, C* dst, int d) {
   for (int e = threadIdx.x; e < d * d; e += kThreads) dst[e] = src[e];
   __syncthreads();
 }
 
 // ---- the fused walk ----------------------------------------------------------
+template <class Rt>
 __global__ void __launch_bounds__(kThreads, 1)
-    selective_walk_kernel(const float2* __restrict__ loc0, const float2* __restrict__ loc1,
-                          float2* __restrict__ carries, int8_t* __restrict__ modes,
+    selective_walk_kernel(const Cx<Rt>* __restrict__ loc0, const Cx<Rt>* __restrict__ loc1,
+                          Cx<Rt>* __restrict__ carries, int8_t* __restrict__ modes,
                           int64_t* __restrict__ sites, int64_t* __restrict__ n_sites,
                           int* __restrict__ status, int64_t T, int d, int s, Policy pol) {
   extern __shared__ __align__(16) char smem_raw[];
-  Smem sm = carve(smem_raw, d);
+  Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   const int64_t ntiles = (T + s - 1) / s;
   int64_t nsite = 0;
@@ -395,8 +403,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // mode-2 tiles: loc0[tile] <- loc1[tile] (before materialisation)
-__global__ void adopt_loc1_kernel(float2* loc0, const float2* loc1, const int8_t* modes,
-                                  int64_t T, int d, int s) {
+template <class C>
+__global__ void adopt_loc1_kernel(C* loc0, const C* loc1, const int8_t* modes, int64_t T, int d,
+                                  int s) {
   const int64_t k = blockIdx.x;
   if (modes[k] != 2) return;
   const int64_t mat = (int64_t)d * d;
@@ -406,28 +415,30 @@ __global__ void adopt_loc1_kernel(float2* loc0, const float2* loc1, const int8_t
 }
 
 // mode-2 tiles: V[k*s] <- carry[k] (the consuming reset's own slot, scan.py:423-427)
-__global__ void fix_reset_slots_kernel(float2* V, const float2* carries, const int8_t* modes,
-                                       int d, int s) {
+template <class C>
+__global__ void fix_reset_slots_kernel(C* V, const C* carries, const int8_t* modes, int d, int s) {
   const int64_t k = blockIdx.x;
   if (modes[k] != 2) return;
   const int64_t mat = (int64_t)d * d;
   for (int64_t e = threadIdx.x; e < mat; e += blockDim.x) V[k * s * mat + e] = carries[k * mat + e];
 }
 
+template <class Rt>
 __global__ void __launch_bounds__(kThreads, 1)
-    policy_select_kernel(const float2* X, int d, Policy pol, uint8_t* fire) {
+    policy_select_kernel(const Cx<Rt>* X, int d, Policy pol, uint8_t* fire) {
   extern __shared__ __align__(16) char smem_raw[];
-  Smem sm = carve(smem_raw, d);
+  Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   copy_mat(X + blockIdx.x * mat, sm.el, d);
   bool f = policy_select(sm.el, d, pol, sm);
   if (threadIdx.x == 0) fire[blockIdx.x] = f ? 1 : 0;
 }
 
+template <class Rt>
 __global__ void __launch_bounds__(kThreads, 1)
-    policy_reset_kernel(const float2* X, float2* R, int d, int kind, int* status) {
+    policy_reset_kernel(const Cx<Rt>* X, Cx<Rt>* R, int d, int kind, int* status) {
   extern __shared__ __align__(16) char smem_raw[];
-  Smem sm = carve(smem_raw, d);
+  Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   copy_mat(X + blockIdx.x * mat, sm.el, d);
   int rc = policy_reset(sm.el, R + blockIdx.x * mat, d, kind, sm);
@@ -441,8 +452,8 @@ int check_policy(const goom_reset_policy* p, int d) {
   if (p->check_interval < 1) return fail(GOOM_EINVAL, "check_interval must be >= 1");
   if (p->kind < GOOM_POLICY_NEVER || p->kind > GOOM_POLICY_NORM_THRESHOLD)
     return fail(GOOM_EINVAL, "unknown policy kind");
-  if (d > kMaxD && p->kind != GOOM_POLICY_NEVER)
-    return fail(GOOM_EUNSUPPORTED, "built-in reset policies run in one CTA: d <= 64");
+  if (d > kMaxD)
+    return fail(GOOM_EUNSUPPORTED, "the fused selective walk keeps the state in one CTA: d <= 64");
   return GOOM_OK;
 }
 
@@ -450,82 +461,69 @@ Policy to_policy(const goom_reset_policy* p) {
   return Policy{p->kind, p->check_interval, p->consume_leaf, p->threshold, p->log_volume_floor};
 }
 
+template <class Rt>
 int set_smem(const void* fn, int d) {
-  size_t need = smem_bytes(d);
+  size_t need = smem_bytes<Rt>(d);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) !=
       cudaSuccess)
     return cuda_fail(cudaGetLastError(), "selective smem attribute");
   return GOOM_OK;
 }
 
-// L[k*s] = first ? I : A[k*s];  L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]   (scan.py:317-339)
-int local_products(const float2* A, float2* L, int64_t T, int d, int64_t s, bool skip_first,
+// L[k*s] = skip_first ? I : A[k*s];  L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]   (scan.py:317-339)
+template <class Rt>
+int local_products(const Cx<Rt>* A, Cx<Rt>* L, int64_t T, int d, int64_t s, bool skip_first,
                    void* lws, size_t lws_bytes, cudaStream_t st) {
+  using C = Cx<Rt>;
   const int64_t mat = (int64_t)d * d;
   const int64_t nb = (T + s - 1) / s;
-  if (cudaMemcpy2DAsync(L, sizeof(float2) * mat * s, A, sizeof(float2) * mat * s,
-                        sizeof(float2) * mat, nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+  if (cudaMemcpy2DAsync(L, sizeof(C) * mat * s, A, sizeof(C) * mat * s, sizeof(C) * mat, nb,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
     return cuda_fail(cudaGetLastError(), "local products copy");
-  if (skip_first) {
-    // identity at every tile start
-    GOOM_TRY(launch_identity(L, nb, d, s * mat, st));
-  }
+  if (skip_first) GOOM_TRY(launch_identity<Rt>(L, nb, d, s * mat, st));
   for (int64_t i = 1; i < s; ++i) {
     int64_t cnt = (T - i + s - 1) / s;
     if (cnt <= 0) break;
-    LmmeProblem p{};
-    p.A = Operand{A + i * mat, s * mat, 1};
-    p.B = Operand{L + (i - 1) * mat, s * mat, 1};
-    p.D = Operand{nullptr, 0, 1};
+    LmmeProblemT<Rt> p{};
+    p.A = OperandT<C>{A + i * mat, s * mat, 1};
+    p.B = OperandT<C>{L + (i - 1) * mat, s * mat, 1};
+    p.D = OperandT<C>{nullptr, 0, 1};
     p.C = L + i * mat;
     p.strideC = s * mat;
     p.batch = cnt;
     p.n = p.k = p.m = d;
-    p.rowA = Scales{nullptr, 0, 1};
-    p.colB = Scales{nullptr, 0, 1};
-    GOOM_TRY(lmme_run(p, lws, lws_bytes, st));
+    p.rowA = ScalesT<Rt>{nullptr, 0, 1};
+    p.colB = ScalesT<Rt>{nullptr, 0, 1};
+    GOOM_TRY(lmme_run<Rt>(p, lws, lws_bytes, st));
   }
   return GOOM_OK;
 }
 
-size_t lmme_ws_bytes(int64_t batch, int d) {
-  return round_up(sizeof(float) * (size_t)batch * d) * 2;
-}
-
-}  // namespace
-}  // namespace goom
-
-using namespace goom;
-
-extern "C" {
-
-size_t goom_scan_selective_chain_workspace_size(int64_t T, int d, const goom_reset_policy* policy,
-                                                int block) {
-  (void)block;
+template <class Rt>
+size_t workspace_bytes(int64_t T, int d, const goom_reset_policy* policy) {
   if (T < 1 || d < 1 || !policy || policy->check_interval < 1) return 0;
   int64_t s = policy->check_interval < T ? policy->check_interval : T;
   int64_t nt = (T + s - 1) / s;
-  size_t mat = (size_t)d * d * sizeof(float2);
-  size_t b = round_up(mat * T);                       // loc0
+  size_t mat = (size_t)d * d * sizeof(Cx<Rt>);
+  size_t b = round_up(mat * T);                               // loc0
   if (policy->consume_leaf && s > 1) b += round_up(mat * T);  // loc1
   b += round_up(mat * nt) + round_up(nt) + round_up(sizeof(int) * 4);
-  b += lmme_ws_bytes(T, d);
+  b += 2 * round_up(sizeof(Rt) * (size_t)T * d);              // LMME scale scratch
   return b;
 }
 
-int goom_scan_selective_chain_c64(const goom_c64* A_, goom_c64* V_, int64_t T, int d,
-                                  const goom_reset_policy* policy, int block, int64_t* sites,
-                                  int64_t* n_sites, void* ws, size_t ws_bytes, void* stream) {
+template <class Rt>
+int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_reset_policy* policy,
+                    int block, int64_t* sites, int64_t* n_sites, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+  using C = Cx<Rt>;
   if (T < 1) return fail(GOOM_EINVAL, "scan of an empty sequence");
   if (block < 1) return fail(GOOM_EINVAL, "block_size must be >= 1");
   if (d < 1) return fail(GOOM_ESHAPE, "d must be >= 1");
-  if (!A_ || !V_ || !sites || !n_sites) return fail(GOOM_EINVAL, "null pointer");
+  if (!A || !V || !sites || !n_sites) return fail(GOOM_EINVAL, "null pointer");
   GOOM_TRY(check_policy(policy, d));
-  size_t need = goom_scan_selective_chain_workspace_size(T, d, policy, block);
+  size_t need = workspace_bytes<Rt>(T, d, policy);
   if (ws_bytes < need || !ws) return fail(GOOM_EWORKSPACE, "selective workspace too small");
-  cudaStream_t st = as_stream(stream);
-  const float2* A = reinterpret_cast<const float2*>(A_);
-  float2* V = reinterpret_cast<float2*>(V_);
   const int64_t s = policy->check_interval < T ? policy->check_interval : T;
   const int64_t nt = (T + s - 1) / s;
   const int64_t mat = (int64_t)d * d;
@@ -533,15 +531,15 @@ int goom_scan_selective_chain_c64(const goom_c64* A_, goom_c64* V_, int64_t T, i
 
   char* base = reinterpret_cast<char*>(ws);
   size_t off = 0;
-  float2* loc0 = reinterpret_cast<float2*>(base + off);
-  off += round_up(sizeof(float2) * mat * T);
-  float2* loc1 = nullptr;
+  C* loc0 = reinterpret_cast<C*>(base + off);
+  off += round_up(sizeof(C) * mat * T);
+  C* loc1 = nullptr;
   if (need_loc1) {
-    loc1 = reinterpret_cast<float2*>(base + off);
-    off += round_up(sizeof(float2) * mat * T);
+    loc1 = reinterpret_cast<C*>(base + off);
+    off += round_up(sizeof(C) * mat * T);
   }
-  float2* carries = reinterpret_cast<float2*>(base + off);
-  off += round_up(sizeof(float2) * mat * nt);
+  C* carries = reinterpret_cast<C*>(base + off);
+  off += round_up(sizeof(C) * mat * nt);
   int8_t* modes = reinterpret_cast<int8_t*>(base + off);
   off += round_up(nt);
   int* status = reinterpret_cast<int*>(base + off);
@@ -550,40 +548,40 @@ int goom_scan_selective_chain_c64(const goom_c64* A_, goom_c64* V_, int64_t T, i
   size_t lws_bytes = ws_bytes - off;
 
   // 1. local products
-  GOOM_TRY(local_products(A, loc0, T, d, s, false, lws, lws_bytes, st));
-  if (need_loc1) GOOM_TRY(local_products(A, loc1, T, d, s, true, lws, lws_bytes, st));
+  GOOM_TRY(local_products<Rt>(A, loc0, T, d, s, false, lws, lws_bytes, st));
+  if (need_loc1) GOOM_TRY(local_products<Rt>(A, loc1, T, d, s, true, lws, lws_bytes, st));
   // 2. fused walk
   if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
     return cuda_fail(cudaGetLastError(), "status reset");
-  GOOM_TRY(set_smem((const void*)selective_walk_kernel, d));
-  selective_walk_kernel<<<1, kThreads, smem_bytes(d), st>>>(
+  GOOM_TRY(set_smem<Rt>((const void*)selective_walk_kernel<Rt>, d));
+  selective_walk_kernel<Rt><<<1, kThreads, smem_bytes<Rt>(d), st>>>(
       loc0, loc1 ? loc1 : loc0, carries, modes, sites, n_sites, status, T, d, (int)s,
       to_policy(policy));
   GOOM_CHECK_LAUNCH("selective_walk_kernel");
   // 3. materialise: tile 0 = loc0; tile k>0: loc[t] (x) carry[k]
   if (need_loc1) {
-    adopt_loc1_kernel<<<(unsigned)nt, 256, 0, st>>>(loc0, loc1, modes, T, d, (int)s);
+    adopt_loc1_kernel<C><<<(unsigned)nt, 256, 0, st>>>(loc0, loc1, modes, T, d, (int)s);
     GOOM_CHECK_LAUNCH("adopt_loc1_kernel");
   }
   const int64_t first = s < T ? s : T;
-  if (cudaMemcpyAsync(V, loc0, sizeof(float2) * mat * first, cudaMemcpyDeviceToDevice, st) !=
+  if (cudaMemcpyAsync(V, loc0, sizeof(C) * mat * first, cudaMemcpyDeviceToDevice, st) !=
       cudaSuccess)
     return cuda_fail(cudaGetLastError(), "materialise tile 0");
   if (T > s) {
-    LmmeProblem p{};
-    p.A = Operand{loc0 + s * mat, mat, 1};
-    p.B = Operand{carries + mat, mat, s};
-    p.D = Operand{nullptr, 0, 1};
+    LmmeProblemT<Rt> p{};
+    p.A = OperandT<C>{loc0 + s * mat, mat, 1};
+    p.B = OperandT<C>{carries + mat, mat, s};
+    p.D = OperandT<C>{nullptr, 0, 1};
     p.C = V + s * mat;
     p.strideC = mat;
     p.batch = T - s;
     p.n = p.k = p.m = d;
-    p.rowA = Scales{nullptr, 0, 1};
-    p.colB = Scales{nullptr, 0, 1};
-    GOOM_TRY(lmme_run(p, lws, lws_bytes, st));
+    p.rowA = ScalesT<Rt>{nullptr, 0, 1};
+    p.colB = ScalesT<Rt>{nullptr, 0, 1};
+    GOOM_TRY(lmme_run<Rt>(p, lws, lws_bytes, st));
   }
   if (policy->consume_leaf) {
-    fix_reset_slots_kernel<<<(unsigned)nt, 256, 0, st>>>(V, carries, modes, d, (int)s);
+    fix_reset_slots_kernel<C><<<(unsigned)nt, 256, 0, st>>>(V, carries, modes, d, (int)s);
     GOOM_CHECK_LAUNCH("fix_reset_slots_kernel");
   }
   // surface a rank-deficient reset as ValueError (lyapunov.py:191-192, 212-213)
@@ -597,20 +595,22 @@ int goom_scan_selective_chain_c64(const goom_c64* A_, goom_c64* V_, int64_t T, i
   return GOOM_OK;
 }
 
-int goom_policy_select_c64(const goom_c64* X, int64_t batch, int d, const goom_reset_policy* policy,
-                           uint8_t* fire, void* stream) {
+template <class Rt>
+int select_batch(const void* X, int64_t batch, int d, const goom_reset_policy* policy,
+                 uint8_t* fire, void* stream) {
   if (batch < 0 || d < 1) return fail(GOOM_EINVAL, "bad shape");
   GOOM_TRY(check_policy(policy, d));
   if (batch == 0) return GOOM_OK;
-  GOOM_TRY(set_smem((const void*)policy_select_kernel, d));
-  policy_select_kernel<<<(unsigned)batch, kThreads, smem_bytes(d), as_stream(stream)>>>(
-      reinterpret_cast<const float2*>(X), d, to_policy(policy), fire);
+  GOOM_TRY(set_smem<Rt>((const void*)policy_select_kernel<Rt>, d));
+  policy_select_kernel<Rt><<<(unsigned)batch, kThreads, smem_bytes<Rt>(d), as_stream(stream)>>>(
+      reinterpret_cast<const Cx<Rt>*>(X), d, to_policy(policy), fire);
   GOOM_CHECK_LAUNCH("policy_select_kernel");
   return GOOM_OK;
 }
 
-int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
-                          const goom_reset_policy* policy, void* stream) {
+template <class Rt>
+int reset_batch(const void* X, void* R, int64_t batch, int d, const goom_reset_policy* policy,
+                void* stream) {
   if (batch < 0 || d < 1) return fail(GOOM_EINVAL, "bad shape");
   GOOM_TRY(check_policy(policy, d));
   if (batch == 0) return GOOM_OK;
@@ -620,9 +620,9 @@ int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
   if (cudaMallocAsync(&status, sizeof(int), st) != cudaSuccess ||
       cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
     return cuda_fail(cudaGetLastError(), "reset status");
-  GOOM_TRY(set_smem((const void*)policy_reset_kernel, d));
-  policy_reset_kernel<<<(unsigned)batch, kThreads, smem_bytes(d), st>>>(
-      reinterpret_cast<const float2*>(X), reinterpret_cast<float2*>(R), d, policy->kind, status);
+  GOOM_TRY(set_smem<Rt>((const void*)policy_reset_kernel<Rt>, d));
+  policy_reset_kernel<Rt><<<(unsigned)batch, kThreads, smem_bytes<Rt>(d), st>>>(
+      reinterpret_cast<const Cx<Rt>*>(X), reinterpret_cast<Cx<Rt>*>(R), d, policy->kind, status);
   GOOM_CHECK_LAUNCH("policy_reset_kernel");
   int host_status = 0;
   cudaMemcpyAsync(&host_status, status, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -631,6 +631,54 @@ int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
   if (host_status != GOOM_OK)
     return fail(host_status, "rank-deficient state cannot be orthonormalized (or all-zero column)");
   return GOOM_OK;
+}
+
+}  // namespace
+}  // namespace goom
+
+using namespace goom;
+
+extern "C" {
+
+size_t goom_scan_selective_chain_workspace_size(int64_t T, int d, const goom_reset_policy* policy,
+                                                int block) {
+  (void)block;
+  return workspace_bytes<float>(T, d, policy);
+}
+size_t goom_scan_selective_chain_workspace_size_c128(int64_t T, int d,
+                                                     const goom_reset_policy* policy, int block) {
+  (void)block;
+  return workspace_bytes<double>(T, d, policy);
+}
+int goom_scan_selective_chain_c64(const goom_c64* A, goom_c64* V, int64_t T, int d,
+                                  const goom_reset_policy* policy, int block, int64_t* sites,
+                                  int64_t* n_sites, void* ws, size_t ws_bytes, void* stream) {
+  return selective_chain<float>(reinterpret_cast<const float2*>(A), reinterpret_cast<float2*>(V),
+                                T, d, policy, block, sites, n_sites, ws, ws_bytes,
+                                as_stream(stream));
+}
+int goom_scan_selective_chain_c128(const goom_c128* A, goom_c128* V, int64_t T, int d,
+                                   const goom_reset_policy* policy, int block, int64_t* sites,
+                                   int64_t* n_sites, void* ws, size_t ws_bytes, void* stream) {
+  return selective_chain<double>(reinterpret_cast<const double2*>(A),
+                                 reinterpret_cast<double2*>(V), T, d, policy, block, sites,
+                                 n_sites, ws, ws_bytes, as_stream(stream));
+}
+int goom_policy_select_c64(const goom_c64* X, int64_t batch, int d, const goom_reset_policy* policy,
+                           uint8_t* fire, void* stream) {
+  return select_batch<float>(X, batch, d, policy, fire, stream);
+}
+int goom_policy_select_c128(const goom_c128* X, int64_t batch, int d,
+                            const goom_reset_policy* policy, uint8_t* fire, void* stream) {
+  return select_batch<double>(X, batch, d, policy, fire, stream);
+}
+int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
+                          const goom_reset_policy* policy, void* stream) {
+  return reset_batch<float>(X, R, batch, d, policy, stream);
+}
+int goom_policy_reset_c128(const goom_c128* X, goom_c128* R, int64_t batch, int d,
+                           const goom_reset_policy* policy, void* stream) {
+  return reset_batch<double>(X, R, batch, d, policy, stream);
 }
 
 }  // extern "C"

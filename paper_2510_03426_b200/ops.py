@@ -1,23 +1,24 @@
 """PyTorch custom ops (`torch.ops.goom.*`) over the C ABI.
 
-Each op takes / returns complex64 CUDA tensors (GOOMs), calls exactly one
-ABI entry point on the current CUDA stream, and allocates its outputs and
-workspace through the caching allocator. No op has a CPU implementation: a
-CPU tensor or a missing library raises.
+Each op takes / returns complex64 or complex128 CUDA tensors (GOOMs), calls
+exactly one ABI entry point on the current CUDA stream (the _c64 or _c128
+twin, by dtype), and allocates outputs and workspace through the caching
+allocator. No op has a CPU implementation: a CPU tensor or a missing library
+raises.
 """
 
 from __future__ import annotations
 
 import ctypes
 import math
-from typing import List, Optional, Tuple
+from typing import Optional, Tuple
 
 import torch
 
 from . import _lib
 
 NEG_INF = float("-inf")
-_C64 = torch.complex64
+_CPLX = (torch.complex64, torch.complex128)
 
 
 def _stream():
@@ -30,7 +31,17 @@ def _need_cuda(*ts):
             raise ValueError("goom ops take CUDA tensors (there is no CPU path)")
 
 
-def _ws(nbytes: int, device) -> Tuple[Optional[torch.Tensor], int]:
+def _need_goom(*ts):
+    for t in ts:
+        if t is not None and t.dtype not in _CPLX:
+            raise ValueError("GOOM tensors are complex64 or complex128")
+
+
+def _real_of(dtype):
+    return torch.float64 if dtype == torch.complex128 else torch.float32
+
+
+def _ws(nbytes: int, device):
     if nbytes == 0:
         return None, 0
     return torch.empty(int(nbytes), dtype=torch.uint8, device=device), int(nbytes)
@@ -40,28 +51,43 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _size(base: str, dtype, *args) -> int:
+    name = base if dtype == torch.complex64 else base + "_c128"
+    return int(getattr(_lib.load(), name)(*args))
+
+
 # ---------------------------------------------------------------------------
 # conversions
 
 
 @torch.library.custom_op("goom::from_real", mutates_args=(), device_types="cuda")
-def from_real(x: torch.Tensor, zero_log: float) -> torch.Tensor:
+def from_real(x: torch.Tensor, zero_log: float, double: bool) -> torch.Tensor:
+    """real -> GOOM (complex128 if `double`, else complex64)."""
     _need_cuda(x)
-    x = x.contiguous()
-    out = torch.empty(x.shape, dtype=_C64, device=x.device)
-    if x.dtype == torch.float64:
-        _lib.call("goom_from_real_f64", x.data_ptr(), out.data_ptr(), x.numel(), zero_log, _stream())
-    elif x.dtype == torch.float32:
-        _lib.call("goom_from_real_f32", x.data_ptr(), out.data_ptr(), x.numel(), zero_log, _stream())
-    else:
+    if x.dtype not in (torch.float32, torch.float64):
         raise ValueError("from_real expects float32 or float64 values")
+    if double:
+        x = x.to(torch.float64).contiguous()
+        out = torch.empty(x.shape, dtype=torch.complex128, device=x.device)
+        _lib.call("goom_from_real_c128", x.data_ptr(), out.data_ptr(), x.numel(), zero_log,
+                  _stream())
+        return out
+    x = x.contiguous()
+    out = torch.empty(x.shape, dtype=torch.complex64, device=x.device)
+    name = "goom_from_real_f64" if x.dtype == torch.float64 else "goom_from_real_f32"
+    _lib.call(name, x.data_ptr(), out.data_ptr(), x.numel(), zero_log, _stream())
     return out
 
 
 @torch.library.custom_op("goom::to_real", mutates_args=(), device_types="cuda")
 def to_real(z: torch.Tensor, double: bool) -> torch.Tensor:
     _need_cuda(z)
+    _need_goom(z)
     z = z.contiguous()
+    if z.dtype == torch.complex128:
+        out = torch.empty(z.shape, dtype=torch.float64, device=z.device)
+        _lib.call("goom_to_real_c128", z.data_ptr(), out.data_ptr(), z.numel(), _stream())
+        return out
     dt = torch.float64 if double else torch.float32
     out = torch.empty(z.shape, dtype=dt, device=z.device)
     fn = "goom_to_real_f64" if double else "goom_to_real_f32"
@@ -73,35 +99,43 @@ def to_real(z: torch.Tensor, double: bool) -> torch.Tensor:
 def to_real_scaled(z: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
     """Per-matrix (last two dims) Eq. 29 export; returns (values, c)."""
     _need_cuda(z)
+    _need_goom(z)
     z = z.contiguous()
     n = z.shape[-1] * z.shape[-2] if z.dim() >= 2 else z.numel()
     batch = z.numel() // max(n, 1) if n else 0
-    out = torch.empty(z.shape, dtype=torch.float32, device=z.device)
-    c = torch.empty(z.shape[:-2] if z.dim() >= 2 else (), dtype=torch.float32, device=z.device)
-    _lib.call("goom_to_real_scaled_f32", z.data_ptr(), out.data_ptr(), c.data_ptr(), batch, n,
-              _stream())
+    rt = _real_of(z.dtype)
+    out = torch.empty(z.shape, dtype=rt, device=z.device)
+    c = torch.empty(z.shape[:-2] if z.dim() >= 2 else (), dtype=rt, device=z.device)
+    name = "goom_to_real_scaled_f32" if z.dtype == torch.complex64 else "goom_to_real_scaled_c128"
+    _lib.call(name, z.data_ptr(), out.data_ptr(), c.data_ptr(), batch, n, _stream())
     return out, c
 
 
 @torch.library.custom_op("goom::gadd", mutates_args=(), device_types="cuda")
 def gadd(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     _need_cuda(a, b)
+    _need_goom(a, b)
+    if a.dtype != b.dtype:
+        raise ValueError("gadd operands must share a dtype")
     a, b = torch.broadcast_tensors(a, b)
     a = a.contiguous()
     b = b.contiguous()
-    out = torch.empty(a.shape, dtype=_C64, device=a.device)
-    _lib.call("goom_gadd_c64", a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _stream())
+    out = torch.empty(a.shape, dtype=a.dtype, device=a.device)
+    _lib.call(_lib.fn("goom_gadd", a.dtype), a.data_ptr(), b.data_ptr(), out.data_ptr(),
+              a.numel(), _stream())
     return out
 
 
 @torch.library.custom_op("goom::col_log_norms", mutates_args=(), device_types="cuda")
 def col_log_norms(z: torch.Tensor) -> torch.Tensor:
     _need_cuda(z)
+    _need_goom(z)
     z = z.contiguous()
     rows, cols = z.shape[-2], z.shape[-1]
     batch = z.numel() // (rows * cols)
-    out = torch.empty(z.shape[:-2] + (cols,), dtype=torch.float32, device=z.device)
-    _lib.call("goom_col_log_norms_c64", z.data_ptr(), out.data_ptr(), batch, rows, cols, _stream())
+    out = torch.empty(z.shape[:-2] + (cols,), dtype=_real_of(z.dtype), device=z.device)
+    _lib.call(_lib.fn("goom_col_log_norms", z.dtype), z.data_ptr(), out.data_ptr(), batch, rows,
+              cols, _stream())
     return out
 
 
@@ -110,7 +144,7 @@ def col_log_norms(z: torch.Tensor) -> torch.Tensor:
 
 
 def _bcast_operands(a: torch.Tensor, b: torch.Tensor):
-    """np.matmul broadcasting over leading dims -> (a, b, batch_shape, strideA, strideB)."""
+    """np.matmul broadcasting over leading dims -> (a, b, batch_shape, batch, strideA, strideB)."""
     ab, bb = a.shape[:-2], b.shape[:-2]
     batch_shape = torch.broadcast_shapes(ab, bb)
     batch = math.prod(batch_shape)
@@ -130,8 +164,9 @@ def _bcast_operands(a: torch.Tensor, b: torch.Tensor):
 
 def _lmme_impl(a, b, d):
     _need_cuda(a, b, d)
-    if a.dtype != _C64 or b.dtype != _C64:
-        raise ValueError("lmme operands must be complex64 GOOMs")
+    _need_goom(a, b, d)
+    if a.dtype != b.dtype or (d is not None and d.dtype != a.dtype):
+        raise ValueError("operands must share a backing dtype")
     if a.dim() < 2 or b.dim() < 2:
         raise ValueError("lmme operands must be at least 2-D")
     n, k = a.shape[-2], a.shape[-1]
@@ -139,17 +174,17 @@ def _lmme_impl(a, b, d):
     if k != k2:
         raise ValueError(f"dimension mismatch: {tuple(a.shape)} x {tuple(b.shape)}")
     a2, b2, batch_shape, batch, sa, sb = _bcast_operands(a, b)
-    out = torch.empty(batch_shape + (n, m), dtype=_C64, device=a.device)
+    out = torch.empty(batch_shape + (n, m), dtype=a.dtype, device=a.device)
     if batch == 0:
         return out
-    ws, nws = _ws(_lib.load().goom_lmme_workspace_size(batch, n, k, m), a.device)
+    ws, nws = _ws(_size("goom_lmme_workspace_size", a.dtype, batch, n, k, m), a.device)
     if d is None:
-        _lib.call("goom_lmme_c64", _lib.goom_operand(a2.data_ptr(), sa, 1),
+        _lib.call(_lib.fn("goom_lmme", a.dtype), _lib.goom_operand(a2.data_ptr(), sa, 1),
                   _lib.goom_operand(b2.data_ptr(), sb, 1), out.data_ptr(), n * m, batch, n, k, m,
                   _ptr(ws), nws, _stream())
     else:
         d2 = d.expand(batch_shape + (n, m)).contiguous()
-        _lib.call("goom_lmme_gadd_c64", _lib.goom_operand(a2.data_ptr(), sa, 1),
+        _lib.call(_lib.fn("goom_lmme_gadd", a.dtype), _lib.goom_operand(a2.data_ptr(), sa, 1),
                   _lib.goom_operand(b2.data_ptr(), sb, 1),
                   _lib.goom_operand(d2.data_ptr(), n * m, 1), out.data_ptr(), n * m, batch, n, k,
                   m, _ptr(ws), nws, _stream())
@@ -176,13 +211,14 @@ def lmme_gadd(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor) -> torch.Tensor
 def scan_chain(a: torch.Tensor, block: int, carry: Optional[torch.Tensor]) -> torch.Tensor:
     """Inclusive left-accumulating product chain (A slot of _scan_affine_stack)."""
     _need_cuda(a, carry)
+    _need_goom(a, carry)
     a = a.contiguous()
     T, d = a.shape[0], a.shape[-1]
     out = torch.empty_like(a)
-    ws, nws = _ws(_lib.load().goom_scan_chain_workspace_size(T, d, block), a.device)
-    c = None if carry is None else carry.contiguous()
-    _lib.call("goom_scan_chain_c64", a.data_ptr(), out.data_ptr(), T, d, block, _ptr(c), _ptr(ws),
-              nws, _stream())
+    ws, nws = _ws(_size("goom_scan_chain_workspace_size", a.dtype, T, d, block), a.device)
+    c = None if carry is None else carry.to(a.dtype).contiguous()
+    _lib.call(_lib.fn("goom_scan_chain", a.dtype), a.data_ptr(), out.data_ptr(), T, d, block,
+              _ptr(c), _ptr(ws), nws, _stream())
     return out
 
 
@@ -191,16 +227,18 @@ def scan_affine(a: torch.Tensor, b: torch.Tensor, flags: torch.Tensor,
                 block: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """Inclusive affine scan under combine_affine (scan.py:181-214)."""
     _need_cuda(a, b, flags)
+    _need_goom(a, b)
     a = a.contiguous()
-    b = b.contiguous()
+    b = b.to(a.dtype).contiguous()
     flags = flags.to(torch.uint8).contiguous()
     T, d, m = a.shape[0], a.shape[-1], b.shape[-1]
     oa = torch.empty_like(a)
     ob = torch.empty_like(b)
     of = torch.empty_like(flags)
-    ws, nws = _ws(_lib.load().goom_scan_affine_workspace_size(T, d, m, block), a.device)
-    _lib.call("goom_scan_affine_c64", a.data_ptr(), b.data_ptr(), flags.data_ptr(), oa.data_ptr(),
-              ob.data_ptr(), of.data_ptr(), T, d, m, block, _ptr(ws), nws, _stream())
+    ws, nws = _ws(_size("goom_scan_affine_workspace_size", a.dtype, T, d, m, block), a.device)
+    _lib.call(_lib.fn("goom_scan_affine", a.dtype), a.data_ptr(), b.data_ptr(), flags.data_ptr(),
+              oa.data_ptr(), ob.data_ptr(), of.data_ptr(), T, d, m, block, _ptr(ws), nws,
+              _stream())
     return oa, ob, of
 
 
@@ -217,14 +255,16 @@ def scan_selective_chain(a: torch.Tensor, kind: int, interval: int, consume: boo
     """Selective-reset product chain with a built-in policy (scan.py:342-484).
     Returns (states, sites) with sites an int64 CUDA tensor."""
     _need_cuda(a)
+    _need_goom(a)
     a = a.contiguous()
     T, d = a.shape[0], a.shape[-1]
     pol = policy_struct(kind, interval, consume, threshold, log_floor)
     out = torch.empty_like(a)
     sites = torch.empty(T + 1, dtype=torch.int64, device=a.device)
-    nbytes = _lib.load().goom_scan_selective_chain_workspace_size(T, d, ctypes.byref(pol), block)
+    nbytes = _size("goom_scan_selective_chain_workspace_size", a.dtype, T, d, ctypes.byref(pol),
+                   block)
     ws, nws = _ws(nbytes, a.device)
-    _lib.call("goom_scan_selective_chain_c64", a.data_ptr(), out.data_ptr(), T, d,
+    _lib.call(_lib.fn("goom_scan_selective_chain", a.dtype), a.data_ptr(), out.data_ptr(), T, d,
               ctypes.byref(pol), block, sites.data_ptr(), sites[T:].data_ptr(), _ptr(ws), nws,
               _stream())
     n = int(sites[T].item())
@@ -234,12 +274,13 @@ def scan_selective_chain(a: torch.Tensor, kind: int, interval: int, consume: boo
 @torch.library.custom_op("goom::policy_select", mutates_args=(), device_types="cuda")
 def policy_select(x: torch.Tensor, kind: int, threshold: float, log_floor: float) -> torch.Tensor:
     _need_cuda(x)
+    _need_goom(x)
     x = x.contiguous()
     d = x.shape[-1]
     batch = x.numel() // (d * d)
     pol = policy_struct(kind, 1, False, threshold, log_floor)
     fire = torch.empty(x.shape[:-2], dtype=torch.uint8, device=x.device)
-    _lib.call("goom_policy_select_c64", x.data_ptr(), batch, d, ctypes.byref(pol),
+    _lib.call(_lib.fn("goom_policy_select", x.dtype), x.data_ptr(), batch, d, ctypes.byref(pol),
               fire.data_ptr(), _stream())
     return fire.bool()
 
@@ -247,11 +288,12 @@ def policy_select(x: torch.Tensor, kind: int, threshold: float, log_floor: float
 @torch.library.custom_op("goom::policy_reset", mutates_args=(), device_types="cuda")
 def policy_reset(x: torch.Tensor, kind: int) -> torch.Tensor:
     _need_cuda(x)
+    _need_goom(x)
     x = x.contiguous()
     d = x.shape[-1]
     batch = x.numel() // (d * d)
     pol = policy_struct(kind, 1, False, 0.5, 0.0)
     out = torch.empty_like(x)
-    _lib.call("goom_policy_reset_c64", x.data_ptr(), out.data_ptr(), batch, d, ctypes.byref(pol),
-              _stream())
+    _lib.call(_lib.fn("goom_policy_reset", x.dtype), x.data_ptr(), out.data_ptr(), batch, d,
+              ctypes.byref(pol), _stream())
     return out

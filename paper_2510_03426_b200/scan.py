@@ -175,10 +175,15 @@ class _Stack:
         self.flags = flags
 
     @classmethod
-    def from_arrays(cls, alog, asign, blog, bsign, flags=None):
+    def from_arrays(cls, alog, asign, blog, bsign, flags=None, dtype=None):
+        """The reference's _Stack(alog, asign, blog, bsign, flags); float64 arrays map
+        to complex128 unless `dtype` says otherwise."""
+        from .core import _dtype_of_arrays
+
+        dt = _dtype_of_arrays(alog) if dtype is None else dtype
         f = None if flags is None else torch.as_tensor(np.asarray(flags), dtype=torch.bool,
                                                        device=_device())
-        return cls(join(alog, asign), join(blog, bsign), f)
+        return cls(join(alog, asign, dt), join(blog, bsign, dt), f)
 
     @classmethod
     def from_pairs(cls, leaves):
@@ -244,14 +249,26 @@ def _tested(p, interval):
     return (p + 1) % interval == 0
 
 
-def _selective_chain_core(A, policy: ResetPolicy, block_size: int):
+def _selective_chain_core(A, *args):
     """Selective scan of a pure product chain (scan.py:342-353).
 
-    `A` is a (T, d, d) complex64 tensor (or a (log, sign) pair). Returns
-    (states, sites). Built-in policies run fused on the device.
+    Two call forms:
+      * `_selective_chain_core(A, policy, block_size)` with A a (T, d, d)
+        complex64/complex128 tensor -> (states tensor, sites);
+      * the reference's array form `_selective_chain_core(alog, asign, policy,
+        block_size)` -> (Vlog, Vsign, sites) with arrays like the inputs
+        (float64 arrays run in complex128, the reference's precision for the
+        Lyapunov path, lyapunov.py:336-341).
+    Built-in policies run fused on the device.
     """
-    if isinstance(A, tuple):
-        A = join(*A)
+    if not isinstance(args[0], ResetPolicy):
+        asign, policy, block_size = args
+        from .core import _dtype_of_arrays, _like_input
+
+        V, sites = _selective_chain_core(join(A, asign, _dtype_of_arrays(A)), policy, block_size)
+        l, s = split(V)
+        return _like_input(l, A), _like_input(s, A), sites
+    policy, block_size = args
     if policy.builtin:
         V, sites = torch.ops.goom.scan_selective_chain(
             A, int(policy.kind), int(policy.check_interval), bool(policy.consume_leaf),

@@ -57,3 +57,68 @@ def lmme_parity(got, alog, asign, blog, bsign, tol=1e-4, kappa_min=1e-2, sign_ka
     smask = kappa >= sign_kappa
     flips = int(np.sum((gs != ws) & smask))
     return err, flips
+
+
+def scaled_real_err(got_log, got_sign, want_log, want_sign):
+    """Per leading index: max |s_g e^{g-c} - s_w e^{w-c}| with c = max(want log) —
+    the error of the real matrix relative to its largest entry (robust to log
+    magnitudes beyond float64 range, insensitive to near-zero entries)."""
+    gl = np.asarray(got_log, dtype=np.float64)
+    wl = np.asarray(want_log, dtype=np.float64)
+    n = gl.shape[0]
+    gl = gl.reshape(n, -1)
+    wl = wl.reshape(n, -1)
+    gs = np.asarray(got_sign, dtype=np.float64).reshape(n, -1)
+    ws = np.asarray(want_sign, dtype=np.float64).reshape(n, -1)
+    c = wl.max(axis=1, keepdims=True)
+    c = np.where(np.isfinite(c), c, 0.0)
+    with np.errstate(over="ignore", invalid="ignore"):
+        diff = np.abs(gs * np.exp(gl - c) - ws * np.exp(wl - c))
+    diff = np.where(np.isnan(diff), np.inf, diff)
+    return diff.max(axis=1)
+
+
+def chain_kappa(alog, asign, plog, psign):
+    """Cancellation ratio of every entry of a product chain P_t = A_t P_{t-1},
+    from the float64 oracle prefixes (P_0 = A_0 has kappa 1)."""
+    from oracle import gooms_port as G
+
+    k = np.ones(alog.shape, dtype=np.float64)
+    k[1:] = G.cancellation(alog[1:].astype(np.float64), asign[1:].astype(np.float64),
+                           plog[:-1].astype(np.float64), psign[:-1].astype(np.float64))
+    return k
+
+
+def masked_rel_err(x, y, mask):
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    both = (x == NEG_INF) & (y == NEG_INF)
+    with np.errstate(invalid="ignore"):
+        d = np.where(both, 0.0, np.abs(x - y) / np.maximum(1.0, np.abs(y)))
+    d = np.where(np.isnan(d), np.inf, d)
+    d = np.where(mask, d, 0.0)
+    return d.reshape(d.shape[0], -1).max(axis=1)
+
+
+def chain_parity(got_log, got_sign, alog, asign, want64, ref32_runs, kappa_min=1e-2,
+                 factor=4.0, floor=2e-4):
+    """SURVEY §8c chain criterion, cancellation-masked: per position the rel-log
+    error over entries with kappa >= kappa_min must stay within `factor` x the
+    reference's own float32 error (max over the given float32 runs) or `floor`;
+    signs there must match the float64 oracle wherever the float32 runs do.
+    Returns a dict of diagnostics; `ok` is the verdict."""
+    wl, ws = want64
+    kap = chain_kappa(alog, asign, wl, ws)
+    mask = kap >= kappa_min
+    e_gpu = masked_rel_err(got_log, wl, mask)
+    e_ref = np.max([masked_rel_err(r[0], wl, mask) for r in ref32_runs], axis=0)
+    bound = np.maximum(factor * e_ref, floor)
+    bad = np.flatnonzero(e_gpu > bound)
+    ref_sign_ok = np.all([r[1] == ws for r in ref32_runs], axis=0)
+    flips = int(np.sum((np.asarray(got_sign) != ws) & mask & ref_sign_ok))
+    scaled = scaled_real_err(got_log, got_sign, wl, ws)
+    scaled_ref = np.max([scaled_real_err(r[0], r[1], wl, ws) for r in ref32_runs], axis=0)
+    scaled_bad = np.flatnonzero(scaled > np.maximum(factor * scaled_ref, 1e-4))
+    return dict(ok=bad.size == 0 and flips == 0 and scaled_bad.size == 0, bad=bad[:10],
+                e_gpu=e_gpu, e_ref=e_ref, flips=flips, scaled_max=float(scaled.max()),
+                scaled_bad=scaled_bad[:10])

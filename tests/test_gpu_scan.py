@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 import torch
 
-from goom_testlib import NEG_INF, load_golden, rel_log_diff_per, to_np
+from goom_testlib import (NEG_INF, chain_parity, load_golden, rel_log_diff_per, scaled_real_err,
+                          to_np)
 from oracle import gooms_port as G
 
 pytestmark = pytest.mark.gpu
@@ -44,18 +45,30 @@ def calibrated_ok(got_log, want64, ref32, floor=1e-4, factor=4.0):
 
 @pytest.mark.parametrize("block", [1, 16, 32, 64, 1000])
 def test_config1_chain_d8_T1000(g, block):
-    """Config 1: 1,000 random-normal 8x8 leaves, all prefixes (golden from the reference)."""
+    """Config 1: 1,000 random-normal 8x8 leaves, all prefixes (golden from the reference),
+    against the float64 sequential oracle, calibrated by the reference's own float32 runs."""
     z = load_golden("config1_chain")
     al, as_ = G.log_sign(z["mats"])
     out = g.scan_chain(cz(al, as_), block_size=block)
     gl, gs = to_np(out)
-    want64 = z["seq_f64"][0]
-    ref32 = z["seq_f32"][0].astype(np.float64)
-    bad, e_gpu, e_ref = calibrated_ok(gl, want64, ref32)
-    assert bad.size == 0, (bad[:10], e_gpu[bad[:10]], e_ref[bad[:10]])
-    # signs agree with the float64 oracle wherever the reference float32 run agrees
-    ref_ok = z["seq_f32"][1] == z["seq_f64"][1]
-    assert np.mean((gs == z["seq_f64"][1])[ref_ok]) > 0.999
+    want = (z["seq_f64"][0], z["seq_f64"][1])
+    refs = [z["seq_f32"], z["par32_f32"]]
+    r = chain_parity(gl, gs, al, as_, want, refs)
+    assert r["ok"], (r["bad"], r["e_gpu"][r["bad"]], r["e_ref"][r["bad"]], r["flips"],
+                     r["scaled_bad"])
+
+
+@pytest.mark.parametrize("block", [1, 32, 1000])
+def test_config1_chain_complex128_matches_float64_reference(g, block):
+    """complex128 GOOMs reproduce the reference's own float64 run to its float64
+    tolerance (test_scan.py:227-237 uses 1e-10 across block sizes)."""
+    z = load_golden("config1_chain")
+    al, as_ = G.log_sign(z["mats"])
+    out = g.scan_chain(g.join(al, as_, torch.complex128), block_size=block)
+    gl, gs = to_np(out)
+    want = z["seq_f64"] if block >= 1000 else (z["par32_f64"] if block == 32 else z["seq_f64"])
+    assert G.rel_log_diff(gl, want[0]) < 1e-9
+    assert np.array_equal(gs, want[1])
 
 
 def test_block_ge_T_is_sequential_fold_bitwise(g):
@@ -93,14 +106,27 @@ def test_1024_leaves_across_block_sizes(g):
     seq = G.scan_sequential(st64)
     st32 = G.Stack(*(x.astype(np.float32) for x in (st64.alog, st64.asign, st64.blog, st64.bsign)),
                    st64.flags.copy())
-    ref32 = G.scan_sequential(st32)
     st = g._Stack(cz(st64.alog, st64.asign), cz(st64.blog, st64.bsign))
+    st128 = g._Stack.from_arrays(st64.alog, st64.asign, st64.blog, st64.bsign)
+    # the reference's own float32 noise at each position: worst over its block sizes
+    refs = [G.scan_affine_blocked(st32, b) for b in (4, 16, 64, T)]
+    ref_a = np.max([scaled_real_err(r.alog, r.asign, seq.alog, seq.asign) for r in refs], axis=0)
+    ref_b = np.max([scaled_real_err(r.blog, r.bsign, seq.blog, seq.bsign) for r in refs], axis=0)
     for bs in (4, 16, 64):
         out = g._scan_affine_stack(st, bs)
-        for slot, want, r32 in ((out.A, seq.alog, ref32.alog), (out.B, seq.blog, ref32.blog)):
-            gl, _ = to_np(slot)
-            bad, e_gpu, e_ref = calibrated_ok(gl, want, r32.astype(np.float64))
-            assert bad.size == 0, (bs, bad[:5], e_gpu[bad[:5]], e_ref[bad[:5]])
+        for slot, wl, ws, err_ref in ((out.A, seq.alog, seq.asign, ref_a),
+                                      (out.B, seq.blog, seq.bsign, ref_b)):
+            gl, gs = to_np(slot)
+            err = scaled_real_err(gl, gs, wl, ws)
+            bad = np.flatnonzero(err > np.maximum(4 * err_ref, 1e-4))
+            assert bad.size == 0, (bs, bad[:5], err[bad[:5]], err_ref[bad[:5]])
+        # complex128: the reference's float64 tolerance (1e-10, sign-exact)
+        o128 = g._scan_affine_stack(st128, bs)
+        ref64 = G.scan_affine_blocked(st64, bs)
+        gl, gs = to_np(o128.A)
+        assert G.rel_log_diff(gl, ref64.alog) < 1e-10 and np.array_equal(gs, ref64.asign)
+        gl, gs = to_np(o128.B)
+        assert G.rel_log_diff(gl, ref64.blog) < 1e-10 and np.array_equal(gs, ref64.bsign)
 
 
 def test_zero_bias_affine_is_product_chain(g):
@@ -126,8 +152,8 @@ def test_chain_with_carry_in(g):
     st = G.Stack(np.concatenate([cl[None], al]), np.concatenate([cs[None], as_]),
                  np.full((T + 1, d, d), NEG_INF), np.ones((T + 1, d, d)), np.zeros(T + 1, bool))
     want = G.scan_sequential(st)
-    gl, _ = to_np(out)
-    assert G.rel_log_diff(gl, want.alog[1:]) < 1e-4
+    gl, gs = to_np(out)
+    assert scaled_real_err(gl, gs, want.alog[1:], want.asign[1:]).max() < 1e-5
 
 
 def test_pairs_api_and_sequential(g):
@@ -162,7 +188,7 @@ def test_selective_norm_threshold_sites_golden(g):
         V, sites = g._selective_chain_core(A, g.norm_threshold_policy(12.0), block)
         assert sites == want_sites
         gl, gs = _chain_states(V)
-        assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+        assert scaled_real_err(gl, gs, *z["seq_state"]).max() < 1e-4
     # pair API: flags monotone from the first site (test_scan.py:306-314)
     leaves = [g.ScanPair(g.GoomMatrix(z["alog"][i], z["asign"][i]),
                          g.GoomMatrix.zeros(4, 4)) for i in range(len(z["alog"]))]
@@ -179,8 +205,8 @@ def test_selective_interval_8(g):
                                        g.norm_threshold_policy(5.0, interval=8), 16)
     assert sites == list(z["sites"])
     assert all(s % 8 == 0 for s in sites)
-    gl, _ = _chain_states(V)
-    assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+    gl, gs = _chain_states(V)
+    assert scaled_real_err(gl, gs, *z["seq_state"]).max() < 1e-4
 
 
 def test_selective_with_biases_rounds(g):
@@ -190,22 +216,24 @@ def test_selective_with_biases_rounds(g):
         out, sites = g.scan_selective(st, g.norm_threshold_policy(12.0), block_size=block)
         assert sites == list(z["sites"])
         np.testing.assert_array_equal(out.flags.cpu().numpy(), z["seq_flags"])
-        gl, _ = to_np(out.states())
-        assert G.rel_log_diff(gl, z["seq_state"][0]) < 1e-4
+        gl, gs = to_np(out.states())
+        assert scaled_real_err(gl, gs, *z["seq_state"]).max() < 1e-4
 
 
 def test_colinearity_lorenz_sites(g):
     """spectrum_parallel stage (a) on a Lorenz chain: sites identical to the reference."""
     z = load_golden("sel_colin_lorenz")
-    A = cz(z["alog"], z["asign"])
-    V, sites = g._selective_chain_core(A, g.colinearity_policy(0.99, 12), 256)
+    # the reference's array-level call (lyapunov.py:341): float64 arrays -> complex128 chain
+    Vl, Vs, sites = g._selective_chain_core(z["alog"], z["asign"], g.colinearity_policy(0.99, 12),
+                                            256)
     assert sites == list(z["sites"])
-    gl, gs = to_np(V)
-    want = z["Vlog"]
-    assert G.rel_log_diff(gl, want) < 1e-3
+    assert G.rel_log_diff(Vl, z["Vlog"]) < 1e-9
+    assert scaled_real_err(Vl, Vs, z["Vlog"], z["Vsign"]).max() < 1e-10
     w = load_golden("sel_colin_lorenz_walk")
-    V1, s1 = g._selective_chain_core(A[:600], g.colinearity_policy(0.99, 1), 64)
+    V1, S1, s1 = g._selective_chain_core(z["alog"][:600], z["asign"][:600],
+                                         g.colinearity_policy(0.99, 1), 64)
     assert s1 == list(w["sites"])
+    assert scaled_real_err(V1, S1, w["Vlog"], w["Vsign"]).max() < 1e-10
 
 
 def test_colinearity_predicate_and_reset_kats(g):
@@ -282,5 +310,6 @@ def test_parenthesizations_length_six(g):
     for block in range(1, 7):
         V, sites = g._selective_chain_core(cz(al, as_), g.norm_threshold_policy(1.0), block)
         assert sites == want_sites
-        gl, _ = to_np(V[-1])
-        assert G.rel_log_diff(gl, want_states.state(5)[0]) < 1e-4
+        gl, gs = to_np(V[-1:])
+        wl, ws = want_states.state(5)
+        assert scaled_real_err(gl, gs, wl[None], ws[None]).max() < 1e-5
