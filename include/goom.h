@@ -191,6 +191,18 @@ int goom_policy_select_c128(const goom_c128* X, int64_t batch, int d,
 int goom_policy_reset_c128(const goom_c128* X, goom_c128* R, int64_t batch, int d,
                            const goom_reset_policy* policy, void* stream);
 
+/* ---- long-chain harness (SPEC.md:391-455 run_chain) -------- */
+/* n random-normal reals as GOOMs, element i drawn from Philox4x32-10 keyed (seed,
+ * offset + i): chain leaf t of a d x d chain uses offset t*d*d on any GPU or shard.
+ * offset must be a multiple of 4. */
+int goom_random_normal_c64(goom_c64* out, int64_t n, uint64_t seed, uint64_t offset,
+                           void* stream);
+/* Per matrix b (n elements each): out4[4b..4b+3] = {max log|x|, log ||x||_F,
+ * 1 if every log-magnitude is finite or -inf else 0, 0}. */
+int goom_digest_c64(const goom_c64* X, int64_t batch, int64_t n, float* out4, void* stream);
+/* Kernels libgoom has launched in this process (bench accounting). */
+long long goom_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

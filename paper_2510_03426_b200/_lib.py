@@ -112,6 +112,10 @@ SIGNATURES = {
     ),
     "goom_policy_select_c128": (_I, [_P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P, _P]),
     "goom_policy_reset_c128": (_I, [_P, _P, _I64, _I, ctypes.POINTER(goom_reset_policy), _P]),
+    # long-chain harness
+    "goom_random_normal_c64": (_I, [_P, _I64, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    "goom_digest_c64": (_I, [_P, _I64, _I64, _P, _P]),
+    "goom_kernel_launches": (ctypes.c_longlong, []),
 }
 
 

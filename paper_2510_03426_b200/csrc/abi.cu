@@ -1,4 +1,5 @@
 // Library plumbing: thread-local error messages, version, device checks.
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -8,7 +9,10 @@ namespace goom {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
 }
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -51,3 +55,5 @@ int goom_device_supported(int device) {
 }
 
 }  // extern "C"
+
+extern "C" long long goom_kernel_launches(void) { return goom::g_launches.load(); }

@@ -97,9 +97,15 @@ __global__ void col_log_norms_kernel(const Cx<R>* __restrict__ z, R* __restrict_
 
 // ---- LMME scale pre-pass ---------------------------------------------------
 // rows: one warp per (batch, row) -> max(max_j Re A[i, j], 0)
+// canonical phase: exactly 0 or pi (what every libgoom kernel emits)
+template <class R>
+__device__ __forceinline__ bool canonical_phase(R y) {
+  return y == R(0) || y == pi_of<R>();
+}
+
 template <class R>
 __global__ void row_scale_kernel(OperandT<Cx<R>> A, R* __restrict__ out, int64_t batch, int n,
-                                 int k) {
+                                 int k, int* __restrict__ noncanon) {
   const int warps = blockDim.x >> 5;
   int64_t w = blockIdx.x * (int64_t)warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -108,23 +114,36 @@ __global__ void row_scale_kernel(OperandT<Cx<R>> A, R* __restrict__ out, int64_t
   int i = (int)(w % n);
   const Cx<R>* row = A.at(b) + (int64_t)i * k;
   R m = R(-INFINITY);
-  for (int j = lane; j < k; j += 32) m = gmax(m, row[j].x);
+  bool odd = false;
+  for (int j = lane; j < k; j += 32) {
+    const Cx<R> z = row[j];
+    m = gmax(m, z.x);
+    odd |= !canonical_phase(z.y);
+  }
   m = warp_max_t(m);
   if (lane == 0) out[w] = gmax(m, R(0));
+  if (noncanon && __any_sync(0xffffffffu, odd) && lane == 0) atomicOr(noncanon, 1);
 }
 
 // columns: one thread per (batch, column) -> max(max_j Re B[j, c], 0)
 template <class R>
 __global__ void col_scale_kernel(OperandT<Cx<R>> B, R* __restrict__ out, int64_t batch, int k,
-                                 int m) {
+                                 int m, int* __restrict__ noncanon) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= batch * m) return;
-  int64_t b = t / m;
-  int c = (int)(t % m);
-  const Cx<R>* col = B.at(b) + c;
-  R v = R(-INFINITY);
-  for (int j = 0; j < k; ++j) v = gmax(v, col[(int64_t)j * m].x);
-  out[t] = gmax(v, R(0));
+  bool odd = false;
+  if (t < batch * m) {
+    int64_t b = t / m;
+    int c = (int)(t % m);
+    const Cx<R>* col = B.at(b) + c;
+    R v = R(-INFINITY);
+    for (int j = 0; j < k; ++j) {
+      const Cx<R> z = col[(int64_t)j * m];
+      v = gmax(v, z.x);
+      odd |= !canonical_phase(z.y);
+    }
+    out[t] = gmax(v, R(0));
+  }
+  if (noncanon && __any_sync(0xffffffffu, odd) && (threadIdx.x & 31) == 0) atomicOr(noncanon, 1);
 }
 
 template <class R>
@@ -169,19 +188,21 @@ __global__ void flags_or_scan_kernel(const uint8_t* __restrict__ in, uint8_t* __
 
 // ---- host launchers --------------------------------------------------------
 template <class R>
-int launch_row_scales(OperandT<Cx<R>> A, R* out, int64_t batch, int n, int k, cudaStream_t s) {
+int launch_row_scales(OperandT<Cx<R>> A, R* out, int64_t batch, int n, int k, cudaStream_t s,
+                      int* noncanon) {
   int64_t warps = batch * n;
   int per_block = 8;
   row_scale_kernel<R><<<(unsigned)((warps + per_block - 1) / per_block), per_block * 32, 0, s>>>(
-      A, out, batch, n, k);
+      A, out, batch, n, k, noncanon);
   GOOM_CHECK_LAUNCH("row_scale_kernel");
   return GOOM_OK;
 }
 
 template <class R>
-int launch_col_scales(OperandT<Cx<R>> B, R* out, int64_t batch, int k, int m, cudaStream_t s) {
+int launch_col_scales(OperandT<Cx<R>> B, R* out, int64_t batch, int k, int m, cudaStream_t s,
+                      int* noncanon) {
   int64_t t = batch * m;
-  col_scale_kernel<R><<<(unsigned)((t + 255) / 256), 256, 0, s>>>(B, out, batch, k, m);
+  col_scale_kernel<R><<<(unsigned)((t + 255) / 256), 256, 0, s>>>(B, out, batch, k, m, noncanon);
   GOOM_CHECK_LAUNCH("col_scale_kernel");
   return GOOM_OK;
 }
@@ -193,12 +214,14 @@ int launch_identity(Cx<R>* out, int64_t batch, int d, int64_t stride, cudaStream
   return GOOM_OK;
 }
 
-template int launch_row_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t);
+template int launch_row_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t,
+                                      int*);
 template int launch_row_scales<double>(OperandT<double2>, double*, int64_t, int, int,
-                                       cudaStream_t);
-template int launch_col_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t);
+                                       cudaStream_t, int*);
+template int launch_col_scales<float>(OperandT<float2>, float*, int64_t, int, int, cudaStream_t,
+                                      int*);
 template int launch_col_scales<double>(OperandT<double2>, double*, int64_t, int, int,
-                                       cudaStream_t);
+                                       cudaStream_t, int*);
 template int launch_identity<float>(float2*, int64_t, int, int64_t, cudaStream_t);
 template int launch_identity<double>(double2*, int64_t, int, int64_t, cudaStream_t);
 

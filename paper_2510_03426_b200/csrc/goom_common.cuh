@@ -19,8 +19,12 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 
+// every kernel launch site goes through this: error check + the launch counter
+// behind goom_kernel_launches() (bench.py reports it as gpu_launches)
+void count_launch();
 #define GOOM_CHECK_LAUNCH(where)                                   \
   do {                                                             \
+    ::goom::count_launch();                                        \
     cudaError_t _e = cudaGetLastError();                           \
     if (_e != cudaSuccess) return ::goom::cuda_fail(_e, (where));  \
   } while (0)
@@ -32,12 +36,19 @@ int cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 // ---- GOOM element helpers ---------------------------------------------------
-// sign parity from the imaginary part: -1 iff cos(imag) < 0 (canonical 0 / pi fast)
-__device__ __forceinline__ float goom_sign(float im) {
-  if (im == 0.0f) return 1.0f;
-  if (im == kPi) return -1.0f;
-  return cosf(im) < 0.0f ? -1.0f : 1.0f;
+// Sign parity from the imaginary part: negative iff the phase lies within a quarter
+// turn of pi (== cos(imag) < 0, the reference adapter's rule, except exactly at
+// +-pi/2 where the phase carries no sign). Branch-free: FMUL, FRND, FADD, FSETP —
+// no cosf range reduction on the hot path, any 2*pi multiple accepted.
+__device__ __forceinline__ bool phase_negative(float im) {
+  const float t = im * 0.15915494309189535f;  // 1 / (2 pi)
+  return fabsf(t - rintf(t)) > 0.25f;
 }
+__device__ __forceinline__ bool phase_negative(double im) {
+  const double t = im * 0.15915494309189535;
+  return fabs(t - rint(t)) > 0.25;
+}
+__device__ __forceinline__ float goom_sign(float im) { return phase_negative(im) ? -1.0f : 1.0f; }
 
 __device__ __forceinline__ float2 goom_make(float log_mag, bool negative) {
   return make_float2(log_mag, negative ? kPi : 0.0f);
@@ -103,9 +114,7 @@ __device__ __forceinline__ float gmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double gmax(double a, double b) { return fmax(a, b); }
 
 template <class R> __device__ __forceinline__ R goom_sign_t(R im) {
-  if (im == R(0)) return R(1);
-  if (im == pi_of<R>()) return R(-1);
-  return cos(im) < R(0) ? R(-1) : R(1);
+  return phase_negative(im) ? R(-1) : R(1);
 }
 template <class R> __device__ __forceinline__ Cx<R> cx(R re, R im) {
   Cx<R> z;

@@ -50,14 +50,18 @@ struct LmmeProblemT {
   int64_t batch;
   int n, k, m;
   ScalesT<R> rowA, colB;    // ptr null -> computed by the pre-pass into workspace
+  const int* noncanon;      // device flag from the pre-pass (null: phases unknown)
 };
 using LmmeProblem = LmmeProblemT<float>;
 
 // ---- launchers (elementwise.cu) ---------------------------------------------
+// noncanon (nullable): set to 1 if any imaginary part is not exactly 0 or pi
 template <class R>
-int launch_row_scales(OperandT<Cx<R>> A, R* out, int64_t batch, int n, int k, cudaStream_t s);
+int launch_row_scales(OperandT<Cx<R>> A, R* out, int64_t batch, int n, int k, cudaStream_t s,
+                      int* noncanon = nullptr);
 template <class R>
-int launch_col_scales(OperandT<Cx<R>> B, R* out, int64_t batch, int k, int m, cudaStream_t s);
+int launch_col_scales(OperandT<Cx<R>> B, R* out, int64_t batch, int k, int m, cudaStream_t s,
+                      int* noncanon = nullptr);
 // identity matrices at out + b*stride (elements), b < batch
 template <class R>
 int launch_identity(Cx<R>* out, int64_t batch, int d, int64_t stride, cudaStream_t s);

@@ -29,7 +29,7 @@ size_t lmme_workspace_bytes(int64_t batch, int n, int k, int m, int64_t strideA,
                             int64_t strideB, int64_t divB) {
   if (small_shape<R>(n, k, m)) return 0;  // small kernel: scales in-kernel
   return round_up(sizeof(R) * (size_t)distinct(strideA, divA, batch) * n) +
-         round_up(sizeof(R) * (size_t)distinct(strideB, divB, batch) * m);
+         round_up(sizeof(R) * (size_t)distinct(strideB, divB, batch) * m) + 256 /*phase flag*/;
 }
 
 template <class R>
@@ -45,10 +45,20 @@ int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
       return fail(GOOM_EWORKSPACE, "lmme workspace too small (need " + std::to_string(need) +
                                        " bytes)");
     int64_t nA = distinct(p.A.stride, p.A.div, p.batch), nB = distinct(p.B.stride, p.B.div, p.batch);
-    R* ra = reinterpret_cast<R*>(ws);
-    R* cb = reinterpret_cast<R*>(reinterpret_cast<char*>(ws) + round_up(sizeof(R) * (size_t)nA * p.n));
-    GOOM_TRY(launch_row_scales<R>(OperandT<Cx<R>>{p.A.ptr, p.A.stride, 1}, ra, nA, p.n, p.k, s));
-    GOOM_TRY(launch_col_scales<R>(OperandT<Cx<R>>{p.B.ptr, p.B.stride, 1}, cb, nB, p.k, p.m, s));
+    char* w = reinterpret_cast<char*>(ws);
+    R* ra = reinterpret_cast<R*>(w);
+    w += round_up(sizeof(R) * (size_t)nA * p.n);
+    R* cb = reinterpret_cast<R*>(w);
+    w += round_up(sizeof(R) * (size_t)nB * p.m);
+    int* flag = nullptr;
+    if (sizeof(R) == 4 && backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)) {
+      flag = reinterpret_cast<int*>(w);  // lets the tcgen05 transform take the 0 / pi fast path
+      if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "phase flag reset");
+    }
+    GOOM_TRY(launch_row_scales<R>(OperandT<Cx<R>>{p.A.ptr, p.A.stride, 1}, ra, nA, p.n, p.k, s, flag));
+    GOOM_TRY(launch_col_scales<R>(OperandT<Cx<R>>{p.B.ptr, p.B.stride, 1}, cb, nB, p.k, p.m, s, flag));
+    p.noncanon = flag;
     p.rowA = ScalesT<R>{ra, p.A.stride == 0 ? 0 : (int64_t)p.n, p.A.div};
     p.colB = ScalesT<R>{cb, p.B.stride == 0 ? 0 : (int64_t)p.m, p.B.div};
   }

@@ -36,7 +36,7 @@ struct Carve {
 template <class R>
 size_t lmme_ws(int64_t batch, int n, int m) {
   // worst case: every operand distinct
-  return round_up(sizeof(R) * (size_t)batch * n) + round_up(sizeof(R) * (size_t)batch * m);
+  return round_up(sizeof(R) * (size_t)batch * n) + round_up(sizeof(R) * (size_t)batch * m) + 256;
 }
 
 // C[b] = A(b) (x) B(b) (+) D(b)

@@ -508,7 +508,7 @@ size_t workspace_bytes(int64_t T, int d, const goom_reset_policy* policy) {
   size_t b = round_up(mat * T);                               // loc0
   if (policy->consume_leaf && s > 1) b += round_up(mat * T);  // loc1
   b += round_up(mat * nt) + round_up(nt) + round_up(sizeof(int) * 4);
-  b += 2 * round_up(sizeof(Rt) * (size_t)T * d);              // LMME scale scratch
+  b += 2 * round_up(sizeof(Rt) * (size_t)T * d) + 256;        // LMME scale scratch + flag
   return b;
 }
 

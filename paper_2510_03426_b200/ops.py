@@ -297,3 +297,36 @@ def policy_reset(x: torch.Tensor, kind: int) -> torch.Tensor:
     _lib.call(_lib.fn("goom_policy_reset", x.dtype), x.data_ptr(), out.data_ptr(), batch, d,
               ctypes.byref(pol), _stream())
     return out
+
+
+# ---------------------------------------------------------------------------
+# long-chain harness
+
+
+@torch.library.custom_op("goom::random_normal", mutates_args=(), device_types="cuda")
+def random_normal(like: torch.Tensor, T: int, d: int, seed: int, t0: int) -> torch.Tensor:
+    """(T, d, d) complex64 GOOMs of N(0,1) reals; leaf t is keyed (seed, (t0 + t) * d * d)
+    so any window / shard regenerates the same chain. `like` only fixes the device."""
+    out = torch.empty((T, d, d), dtype=torch.complex64, device=like.device)
+    _lib.call("goom_random_normal_c64", out.data_ptr(), out.numel(), int(seed),
+              int(t0) * d * d, _stream())
+    return out
+
+
+@torch.library.custom_op("goom::digest", mutates_args=(), device_types="cuda")
+def digest(x: torch.Tensor) -> torch.Tensor:
+    """Per matrix: (max log|x|, log Frobenius norm, finite flag, 0) as float32 (batch, 4)."""
+    _need_cuda(x)
+    if x.dtype != torch.complex64:
+        raise ValueError("digest takes complex64 GOOMs")
+    x = x.contiguous()
+    n = x.shape[-1] * x.shape[-2]
+    batch = x.numel() // n
+    out = torch.empty((batch, 4), dtype=torch.float32, device=x.device)
+    _lib.call("goom_digest_c64", x.data_ptr(), batch, n, out.data_ptr(), _stream())
+    return out
+
+
+def kernel_launches() -> int:
+    """libgoom kernel launches so far in this process."""
+    return int(_lib.load().goom_kernel_launches())

@@ -1,0 +1,64 @@
+"""Time-sharded LMME chain scan over the GPUs of one node.
+
+Rank g owns leaves [g*T/G, (g+1)*T/G). The only exchange is one all-gather of
+the G chunk totals (d x d GOOMs, 2 MiB each at d = 512):
+
+  1. local total  tot_g = A_{end-1} ... A_{start}   (pairwise tree of batched LMMEs)
+  2. all-gather   tot_0 .. tot_{G-1}                (NCCL over NVLink; gloo in CPU tests)
+  3. carry        C_g = tot_{g-1} ... tot_0         (products accumulate on the LEFT,
+                                                     so the carry multiplies on the right)
+  4. local scan   P_t = (A_t ... A_start) (x) C_g   (the chain engine's carry-in)
+
+Results are deterministic for a fixed (G, window, block) but not bitwise equal
+across G (different trees). The orchestration takes the LMME / scan / total
+functions as arguments so the same code runs in the gloo CPU tests with the
+numpy oracle standing in for the GPU.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(T: int, rank: int, world: int) -> Tuple[int, int]:
+    """(first leaf, count) of `rank`'s contiguous shard; earlier ranks take the remainder."""
+    base, rem = divmod(T, world)
+    start = rank * base + min(rank, rem)
+    return start, base + (1 if rank < rem else 0)
+
+
+def exclusive_carry(local_total: torch.Tensor, lmme: Callable, group=None) -> Optional[torch.Tensor]:
+    """All-gather the chunk totals and fold the ones before this rank (None on rank 0)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    real = torch.view_as_real(local_total.contiguous())
+    gathered = [torch.empty_like(real) for _ in range(world)]
+    dist.all_gather(gathered, real, group=group)
+    carry = None
+    for r in range(rank):
+        tot = torch.view_as_complex(gathered[r])
+        carry = tot if carry is None else lmme(tot, carry)
+    return carry
+
+
+def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
+                      group=None, snapshot_every: int = 0):
+    """Rank-local part of a time-sharded chain run; returns (t0, ChainRun)."""
+    from .harness import chain_total, random_chain, run_chain
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    t0, n = shard_range(T, rank, world)
+    carry = None
+    if world > 1:
+        total = None
+        for w0 in range(0, n, window):
+            m = min(window, n - w0)
+            wt = chain_total(random_chain(m, d, seed, t0 + w0))
+            total = wt if total is None else torch.ops.goom.lmme(wt, total)
+        carry = exclusive_carry(total, torch.ops.goom.lmme, group)
+    return t0, run_chain(n, d, seed, window, block, t0=t0, carry=carry,
+                         snapshot_every=snapshot_every)
