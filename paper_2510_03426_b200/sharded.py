@@ -30,6 +30,14 @@ def shard_range(T: int, rank: int, world: int) -> Tuple[int, int]:
     return start, base + (1 if rank < rem else 0)
 
 
+def fold_carry(totals, rank: int, lmme: Callable) -> Optional[torch.Tensor]:
+    """C_rank = tot_{rank-1} (x) ... (x) tot_0 (None for rank 0): later chunks on the left."""
+    carry = None
+    for r in range(rank):
+        carry = totals[r] if carry is None else lmme(totals[r], carry)
+    return carry
+
+
 def exclusive_carry(local_total: torch.Tensor, lmme: Callable, group=None) -> Optional[torch.Tensor]:
     """All-gather the chunk totals and fold the ones before this rank (None on rank 0)."""
     world = dist.get_world_size(group)
@@ -37,11 +45,7 @@ def exclusive_carry(local_total: torch.Tensor, lmme: Callable, group=None) -> Op
     real = torch.view_as_real(local_total.contiguous())
     gathered = [torch.empty_like(real) for _ in range(world)]
     dist.all_gather(gathered, real, group=group)
-    carry = None
-    for r in range(rank):
-        tot = torch.view_as_complex(gathered[r])
-        carry = tot if carry is None else lmme(tot, carry)
-    return carry
+    return fold_carry([torch.view_as_complex(g) for g in gathered], rank, lmme)
 
 
 def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,

@@ -1,0 +1,104 @@
+"""GPU tests of the long-chain harness (config 3 machinery) and the sharded path on one GPU."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from goom_testlib import scaled_real_err, to_np
+from oracle import gooms_port as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def h():
+    from paper_2510_03426_b200 import harness
+
+    return harness
+
+
+def test_random_chain_is_keyed_by_leaf_index(h):
+    a = h.random_chain(20, 16, seed=5)
+    b = h.random_chain(10, 16, seed=5, t0=5)
+    assert torch.equal(a[5:15], b)
+    c = h.random_chain(10, 16, seed=6, t0=5)
+    assert not torch.equal(b, c)
+    x = torch.ops.goom.to_real(h.random_chain(64, 64, seed=1), True).cpu().numpy().ravel()
+    assert abs(x.mean()) < 0.01 and abs(x.std() - 1.0) < 0.01  # N(0, 1)
+    assert set(np.unique(a.imag.cpu().numpy())) <= {0.0, np.float32(np.pi)}  # canonical
+
+
+def test_digest_matches_oracle(h):
+    X = h.random_chain(6, 32, seed=2)
+    dg = torch.ops.goom.digest(X).cpu().numpy()
+    l, s = to_np(X)
+    for i in range(6):
+        assert abs(dg[i, 0] - l[i].max()) < 1e-6
+        want = 0.5 * np.log(np.sum(np.exp(2 * l[i])))
+        assert abs(dg[i, 1] - want) < 1e-5
+        assert dg[i, 2] == 1.0
+
+
+@pytest.mark.parametrize("d,window,block", [(8, 100, 16), (64, 64, 8), (128, 96, 32)])
+def test_windowed_run_matches_oracle(h, d, window, block):
+    """Windows chained by carries == one scan of the whole chain (oracle, float64)."""
+    T = 300
+    A = h.random_chain(T, d, seed=11)
+    run = h.run_chain(T, d, seed=11, window=window, block=block, snapshot_every=50)
+    al, as_ = to_np(A)
+    st = G.Stack(al, as_, np.full_like(al, -np.inf), np.ones_like(as_), np.zeros(T, bool))
+    want = G.scan_sequential(st)
+    # digests vs the float64 oracle's own prefixes
+    lf = 0.5 * np.log(np.sum(np.exp(2 * (want.alog - want.alog.max(axis=(1, 2), keepdims=True))),
+                             axis=(1, 2))) + want.alog.max(axis=(1, 2))
+    dg = run.digests.double().cpu().numpy()
+    assert np.max(np.abs(dg[:, 1] - lf) / np.maximum(1, np.abs(lf))) < 1e-4
+    assert np.all(dg[:, 2] == 1.0)
+    for t, P in run.snapshots.items():
+        gl, gs = to_np(P[None])
+        assert scaled_real_err(gl, gs, want.alog[t:t + 1], want.asign[t:t + 1]).max() < 1e-2
+    gl, gs = to_np(run.final[None])
+    assert scaled_real_err(gl, gs, want.alog[-1:], want.asign[-1:]).max() < 1e-2
+
+
+def test_growth_rate_matches_lyapunov_theory(h):
+    """log||P_t|| grows at (ln 2 + psi(d/2)) / 2 per step for N(0,1) leaves."""
+    d, T = 64, 2000
+    run = h.run_chain(T, d, seed=3, window=512, block=32)
+    rate = h.growth_rate(run.digests)
+    psi = math.log(d / 2) - 1 / d - 1 / (12 * (d / 2) ** 2)
+    expected = 0.5 * (math.log(2) + psi)
+    assert abs(rate - expected) < 0.02 * expected
+
+
+def test_chain_total_and_sharded_fold_on_one_gpu(h):
+    """The sharded algorithm (totals -> exclusive carries -> local scans), run shard by
+    shard on one GPU, equals the single-GPU chain."""
+    from paper_2510_03426_b200 import sharded
+
+    T, d, world = 257, 128, 3
+    full = h.run_chain(T, d, seed=9, window=128, block=16)
+    totals, runs = [], []
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        totals.append(h.chain_total(h.random_chain(n, d, 9, t0)))
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        carry = sharded.fold_carry(totals, r, torch.ops.goom.lmme)
+        runs.append(h.run_chain(n, d, seed=9, window=128, block=16, t0=t0, carry=carry))
+    dg = torch.cat([r.digests for r in runs]).double().cpu().numpy()
+    ref = full.digests.double().cpu().numpy()
+    assert np.max(np.abs(dg[:, 1] - ref[:, 1]) / np.maximum(1, np.abs(ref[:, 1]))) < 1e-4
+    gl, gs = to_np(runs[-1].final[None])
+    rl, rs = to_np(full.final[None])
+    assert scaled_real_err(gl, gs, rl, rs).max() < 1e-2
+
+
+def test_kernel_launch_counter_moves(h):
+    from paper_2510_03426_b200 import ops
+
+    n0 = ops.kernel_launches()
+    h.random_chain(4, 8)
+    assert ops.kernel_launches() > n0

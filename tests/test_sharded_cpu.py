@@ -1,0 +1,111 @@
+"""Multi-process (gloo, world size 2 and 3) tests of the time-sharding host logic.
+
+The GPU kernels are replaced by the numpy oracle (the orchestration in
+paper_2510_03426_b200/sharded.py takes the LMME as an argument), so the
+shard partition, the all-gather of chunk totals and the carry fold — the only
+cross-GPU logic of the path — are exercised here on CPU with real
+torch.distributed process groups.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import gooms_port as G
+
+
+def oracle_lmme(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    al, as_ = G.split_complex(a.numpy())
+    bl, bs = G.split_complex(b.numpy())
+    ol, os_ = G.lmme(al, as_, bl, bs)
+    return torch.from_numpy(G.join_complex(ol, os_, np.complex128))
+
+
+def leaves(T, d, seed=3):
+    rng = np.random.default_rng(seed)
+    al, as_ = G.log_sign(rng.standard_normal((T, d, d)))
+    return al, as_
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, T, d, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_03426_b200 import sharded
+
+        al, as_ = leaves(T, d)
+        t0, n = sharded.shard_range(T, rank, world)
+        L, S = G.chain_blocked(al[t0:t0 + n], as_[t0:t0 + n], n)  # local prefixes
+        local_total = torch.from_numpy(G.join_complex(L[-1], S[-1], np.complex128))
+        carry = sharded.exclusive_carry(local_total, oracle_lmme)
+        if carry is not None:
+            cl, cs = G.split_complex(carry.numpy())
+            L, S = G.lmme(L, S, np.broadcast_to(cl, L.shape), np.broadcast_to(cs, S.shape))
+        q.put((rank, t0, L, S))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T", [(2, 17), (3, 25)])
+def test_sharded_chain_matches_sequential(world, T):
+    d = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, d, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts.sort()
+    got_l = np.concatenate([p[2] for p in parts])
+    got_s = np.concatenate([p[3] for p in parts])
+    al, as_ = leaves(T, d)
+    st = G.Stack(al, as_, np.full_like(al, -np.inf), np.ones_like(as_), np.zeros(T, bool))
+    want = G.scan_sequential(st)
+    assert G.rel_log_diff(got_l, want.alog) < 1e-10
+    np.testing.assert_array_equal(got_s, want.asign)
+
+
+def test_shard_range_partitions():
+    from paper_2510_03426_b200 import sharded
+
+    for T in (1, 7, 8, 1000, 1 << 20):
+        for world in (1, 2, 3, 4, 8):
+            spans = [sharded.shard_range(T, r, world) for r in range(world)]
+            assert spans[0][0] == 0
+            for (a, n), (b, _) in zip(spans, spans[1:]):
+                assert a + n == b
+            assert spans[-1][0] + spans[-1][1] == T
+            assert max(n for _, n in spans) - min(n for _, n in spans) <= 1
+
+
+def test_fold_carry_order():
+    """Products accumulate on the left: C_2 = tot_1 (x) tot_0."""
+    from paper_2510_03426_b200 import sharded
+
+    calls = []
+
+    def fake(a, b):
+        calls.append((a, b))
+        return f"({a}*{b})"
+
+    assert sharded.fold_carry(["t0", "t1", "t2"], 0, fake) is None
+    assert sharded.fold_carry(["t0", "t1", "t2"], 1, fake) == "t0"
+    assert sharded.fold_carry(["t0", "t1", "t2"], 3, fake) == "(t2*(t1*t0))"
