@@ -51,6 +51,13 @@ struct LmmeProblemT {
   int n, k, m;
   ScalesT<R> rowA, colB;    // ptr null -> computed by the pre-pass into workspace
   const int* noncanon;      // device flag from the pre-pass (null: phases unknown)
+  // optional (tcgen05 path): clamped row maxima of C into emitRow[b*emitRowStride + i] and
+  // column maxima into emitCol[b*emitColStride + j] (atomicMax on the bits; the caller
+  // zero-fills), i.e. the scales the next LMME needs when C is its left / right operand
+  R* emitRow;
+  int64_t emitRowStride;
+  R* emitCol;
+  int64_t emitColStride;
 };
 using LmmeProblem = LmmeProblemT<float>;
 

@@ -89,8 +89,109 @@ size_t chain_workspace_bytes(int64_t T, int d, int block) {
   int64_t nb = (T + s - 1) / s;
   size_t mat = (size_t)d * d;
   return round_up(sizeof(Cx<R>) * mat * T) + round_up(sizeof(Cx<R>) * mat * (nb + 1)) +
-         lmme_ws<R>(T, d, d);
+         lmme_ws<R>(T, d, d) +
+         // fused-scale tcgen05 path: row/col scales of leaves and local products, carries
+         4 * round_up(sizeof(R) * (size_t)T * d) + 2 * round_up(sizeof(R) * (size_t)(nb + 1) * d) +
+         256;
 }
+
+namespace {
+
+// complex64 chain on the tcgen05 kernel with the scale reductions fused into the producing
+// epilogues: only the leaves (and carry_in) get a scale pre-pass; every local product and
+// carry arrives with its row / column maxima already reduced by the kernel that wrote it.
+// Same tree and same LMME kernel as the generic path; only where the scales come from differs.
+int chain_scan_tc(const float2* A, float2* out, int64_t T, int d, int64_t s, int64_t nb,
+                  const float2* carry_in, float2* L, float2* Cx_, char* sbase, size_t sbytes,
+                  cudaStream_t st) {
+  using C = float2;
+  const int64_t mat = (int64_t)d * d;
+  Carve cv{sbase};
+  float* rA = cv.take<float>((size_t)T * d);   // row scales of the leaves
+  float* cA = cv.take<float>((size_t)T * d);   // column scales of the block-start leaves
+  float* rL = cv.take<float>((size_t)T * d);   // emitted: row scales of L
+  float* cL = cv.take<float>((size_t)T * d);   // emitted: column scales of L
+  float* rC = cv.take<float>((size_t)(nb + 1) * d);
+  float* cC = cv.take<float>((size_t)(nb + 1) * d);  // emitted: column scales of the carries
+  int* flag = cv.take<int>(1);
+  if (cv.off > sbytes) return fail(GOOM_EWORKSPACE, "chain scan workspace too small");
+  (void)rC;
+  if (cudaMemsetAsync(sbase, 0, cv.off, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "scale workspace reset");
+  // leaf pre-pass (also tells the kernel whether every phase is exactly 0 / pi)
+  GOOM_TRY(launch_row_scales<float>(OperandT<C>{A, mat, 1}, rA, T, d, d, st, flag));
+  GOOM_TRY(launch_col_scales<float>(OperandT<C>{A, s * mat, 1}, cA, nb, d, d, st, flag));
+  // L[k*s] = A[k*s]: its scales are the leaf's
+  if (cudaMemcpy2DAsync(rL, sizeof(float) * d * s, rA, sizeof(float) * d * s, sizeof(float) * d,
+                        nb, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemcpy2DAsync(cL, sizeof(float) * d * s, cA, sizeof(float) * d, sizeof(float) * d, nb,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "block-start scales");
+  if (carry_in)
+    GOOM_TRY(launch_col_scales<float>(OperandT<C>{carry_in, 0, 1}, cC, 1, d, d, st, flag));
+
+  auto run = [&](OperandT<C> a, ScalesT<float> ra, OperandT<C> b, ScalesT<float> cb, C* c,
+                 int64_t strideC, int64_t batch, float* er, int64_t ers, float* ec,
+                 int64_t ecs) {
+    LmmeProblemT<float> p{};
+    p.A = a;
+    p.B = b;
+    p.D = OperandT<C>{nullptr, 0, 1};
+    p.C = c;
+    p.strideC = strideC;
+    p.batch = batch;
+    p.n = p.k = p.m = d;
+    p.rowA = ra;
+    p.colB = cb;
+    p.noncanon = flag;
+    p.emitRow = er;
+    p.emitRowStride = ers;
+    p.emitCol = ec;
+    p.emitColStride = ecs;
+    return lmme_tc(p, st);
+  };
+  // phase 1: L[k*s+i] = A[k*s+i] (x) L[k*s+i-1], emitting the scales of L[k*s+i]
+  for (int64_t i = 1; i < s; ++i) {
+    int64_t cnt = (T - i + s - 1) / s;
+    if (cnt <= 0) break;
+    GOOM_TRY(run({A + i * mat, s * mat, 1}, {rA + i * d, s * d, 1}, {L + (i - 1) * mat, s * mat, 1},
+                 {cL + (i - 1) * d, s * d, 1}, L + i * mat, s * mat, cnt, rL + i * d, s * d,
+                 cL + i * d, s * d));
+  }
+  // phase 2: Cx[k+1] = L[last of block k] (x) Cx[k], emitting the carries' column scales
+  for (int64_t kb = 0; kb + 1 < nb || (kb == 0 && !carry_in); ++kb) {
+    int64_t last = kb * s + s - 1;
+    if (kb == 0 && !carry_in) {
+      GOOM_TRY(copy_d2d(Cx_ + mat, L + last * mat, mat, st, "chain carry copy"));
+      GOOM_TRY(copy_d2d(cC + d, cL + last * d, d, st, "chain carry scale copy"));
+      if (nb == 1) break;
+      continue;
+    }
+    const C* prev = (kb == 0) ? carry_in : Cx_ + kb * mat;
+    GOOM_TRY(run({L + last * mat, 0, 1}, {rL + last * d, 0, 1}, {prev, 0, 1}, {cC + kb * d, 0, 1},
+                 Cx_ + (kb + 1) * mat, 0, 1, nullptr, 0, cC + (kb + 1) * d, 0));
+  }
+  // phase 3: out[b] = L[b] (x) Cx[b/s]
+  if (carry_in) {
+    GOOM_TRY(copy_d2d(Cx_, carry_in, mat, st, "chain carry-in copy"));
+    GOOM_TRY(run({L, mat, 1}, {rL, d, 1}, {Cx_, mat, s}, {cC, d, s}, out, mat, T, nullptr, 0,
+                 nullptr, 0));
+  } else {
+    GOOM_TRY(copy_d2d(out, L, (size_t)mat * s, st, "chain block-0 copy"));
+    if (T > s)
+      GOOM_TRY(run({L + s * mat, mat, 1}, {rL + s * d, d, 1}, {Cx_ + mat, mat, s}, {cC + d, d, s},
+                   out + s * mat, mat, T - s, nullptr, 0, nullptr, 0));
+  }
+  return GOOM_OK;
+}
+
+bool fused_scale_path(const float2* A, const float2* carry_in, int d) {
+  return lmme_backend() != 1 && lmme_tc_eligible(d, d, d) &&
+         ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(carry_in)) & 15) == 0;
+}
+bool fused_scale_path(const double2*, const double2*, int) { return false; }
+
+}  // namespace
 
 template <class R>
 int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx<R>* carry_in,
@@ -110,6 +211,11 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
 
   // phase 1: L[k*s] = A[k*s]; L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]
   GOOM_TRY(copy_strided(L, A, mat, mat * s, nb, st, "chain phase-1 copy"));
+  if constexpr (sizeof(R) == 4) {
+    if (fused_scale_path(A, carry_in, d))
+      return chain_scan_tc(A, out, T, d, s, nb, carry_in, L, Cx_, reinterpret_cast<char*>(lws),
+                           lws_bytes, st);
+  }
   for (int64_t i = 1; i < s; ++i) {
     int64_t cnt = (T - i + s - 1) / s;  // blocks whose length exceeds i
     if (cnt <= 0) break;

@@ -313,3 +313,24 @@ def test_parenthesizations_length_six(g):
         gl, gs = to_np(V[-1:])
         wl, ws = want_states.state(5)
         assert scaled_real_err(gl, gs, wl[None], ws[None]).max() < 1e-5
+
+
+@pytest.mark.parametrize("d,T,block", [(128, 100, 8), (256, 40, 16), (128, 33, 64)])
+def test_chain_fused_scales_match_prepass_path(g, d, T, block):
+    """The tcgen05 chain with scales emitted by the producing epilogues equals the same
+    chain scanned with the pre-pass (SIMT backend), within float32 noise; also with a carry."""
+    rng = np.random.default_rng(d + T)
+    A = cz(*G.log_sign(rng.standard_normal((T, d, d)).astype(np.float32)))
+    carry = cz(*G.log_sign(rng.standard_normal((d, d)).astype(np.float32)))
+    for c in (None, carry):
+        fused = g.scan_chain(A, block, c)
+        prev = g._lib.set_backend(1)
+        try:
+            ref = g.scan_chain(A, block, c)
+        finally:
+            g._lib.set_backend(prev)
+        fl, fs = to_np(fused)
+        rl, rs = to_np(ref)
+        # 3xTF32 vs FP32 SIMT differ by ~1e-6 per step; over T steps that accumulates
+        assert scaled_real_err(fl, fs, rl, rs).max() < 1e-3
+        assert np.isfinite(fl).all()

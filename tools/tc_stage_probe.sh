@@ -1,6 +1,6 @@
 #!/bin/bash
 # Time the TC kernel with stages disabled (GOOM_TC_DEBUG) to find the bottleneck.
-for dbg in 0 1 2 3 4; do
+for dbg in ${DBGS:-0 1 2 3 4}; do
   echo "GOOM_TC_DEBUG=$dbg"
   GOOM_TC_DEBUG=$dbg timeout 120 python - <<'PY'
 import sys, torch
