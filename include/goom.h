@@ -114,6 +114,12 @@ int goom_lmme_c128(goom_operand A, goom_operand B, goom_c128* C, int64_t strideC
 int goom_lmme_gadd_c128(goom_operand A, goom_operand B, goom_operand D, goom_c128* C,
                         int64_t strideC, int64_t batch, int n, int k, int m, void* ws,
                         size_t ws_bytes, void* stream);
+/* LMME with caller-provided clamped scales (no pre-pass): rowA[(b/divA)*rowA_stride + i]
+ * = max(max_j Re A[b][i][j], 0), colB[(b/divB)*colB_stride + j] likewise for the columns
+ * of B (e.g. emitted by the kernel that produced the operand). No workspace. */
+int goom_lmme_scaled_c64(goom_operand A, const float* rowA, int64_t rowA_stride, goom_operand B,
+                         const float* colB, int64_t colB_stride, goom_c64* C, int64_t strideC,
+                         int64_t batch, int n, int k, int m, void* stream);
 /* Force a kernel family for testing: 0 auto, 1 SIMT, 2 tcgen05 3xTF32. Returns the
  * previous value. Process-wide. */
 int goom_set_lmme_backend(int backend);

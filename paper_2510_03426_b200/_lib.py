@@ -72,6 +72,10 @@ SIGNATURES = {
         [goom_operand, goom_operand, goom_operand, _P, _I64, _I64, _I, _I, _I, _P, _SZ, _P],
     ),
     "goom_set_lmme_backend": (_I, [_I]),
+    "goom_lmme_scaled_c64": (
+        _I,
+        [goom_operand, _P, _I64, goom_operand, _P, _I64, _P, _I64, _I64, _I, _I, _I, _P],
+    ),
     "goom_scan_chain_workspace_size": (_SZ, [_I64, _I, _I]),
     "goom_scan_chain_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
     "goom_scan_affine_workspace_size": (_SZ, [_I64, _I, _I, _I]),

@@ -95,5 +95,9 @@ size_t chain_workspace_bytes(int64_t T, int d, int block);
 template <class R>
 int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx<R>* carry_in,
                void* ws, size_t ws_bytes, cudaStream_t st);
+// d <= 32 warp-resident variant (scan_small.cu): L = local products (T), Cx_ = carries (nb+1)
+template <class R>
+int chain_scan_small(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int64_t s,
+                     const Cx<R>* carry_in, Cx<R>* L, Cx<R>* Cx_, cudaStream_t st);
 
 }  // namespace goom

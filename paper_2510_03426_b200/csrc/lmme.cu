@@ -151,6 +151,26 @@ int goom_lmme_gadd_c128(goom_operand A, goom_operand B, goom_operand D, goom_c12
   return lmme_entry<double>(A, B, D, C, strideC, batch, n, k, m, ws, ws_bytes, stream);
 }
 
+int goom_lmme_scaled_c64(goom_operand A, const float* rowA, int64_t rowA_stride, goom_operand B,
+                         const float* colB, int64_t colB_stride, goom_c64* C, int64_t strideC,
+                         int64_t batch, int n, int k, int m, void* stream) {
+  GOOM_TRY(check_lmme_args(A, B, C, batch, n, k, m));
+  if (!rowA || !colB) return fail(GOOM_EINVAL, "null scale array");
+  LmmeProblemT<float> p{};
+  p.A = op<float>(A);
+  p.B = op<float>(B);
+  p.D = OperandT<float2>{nullptr, 0, 1};
+  p.C = reinterpret_cast<float2*>(C);
+  p.strideC = strideC;
+  p.batch = batch;
+  p.n = n;
+  p.k = k;
+  p.m = m;
+  p.rowA = ScalesT<float>{rowA, rowA_stride, p.A.div};
+  p.colB = ScalesT<float>{colB, colB_stride, p.B.div};
+  return lmme_run<float>(p, nullptr, 0, as_stream(stream));
+}
+
 int goom_set_lmme_backend(int backend) {
   if (backend < 0 || backend > 2) return g_backend.load();
   return g_backend.exchange(backend);

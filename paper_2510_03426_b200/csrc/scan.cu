@@ -209,6 +209,9 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
   size_t lws_bytes = ws_bytes - cv.off;
   const OperandT<C> none{nullptr, 0, 1};
 
+  // d <= 32: the warp-resident scan (scan_small.cu), same tree, three launches
+  if (d <= 32) return chain_scan_small<R>(A, out, T, d, s, carry_in, L, Cx_, st);
+
   // phase 1: L[k*s] = A[k*s]; L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]
   GOOM_TRY(copy_strided(L, A, mat, mat * s, nb, st, "chain phase-1 copy"));
   if constexpr (sizeof(R) == 4) {

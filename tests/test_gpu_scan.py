@@ -236,6 +236,22 @@ def test_colinearity_lorenz_sites(g):
     assert scaled_real_err(V1, S1, w["Vlog"], w["Vsign"]).max() < 1e-10
 
 
+def test_colinearity_lorenz96_d64_sites(g):
+    """SURVEY §8d config 4 at reduced T: Lorenz-96 d=64 Jacobians (oracle/systems_port,
+    pinned by the lorenz96_d16 golden), colinearity(0.99, 12) — sites identical to the
+    reference algorithm, states within f64 tolerance."""
+    from oracle import systems_port as S
+
+    f, df, x0, dt = S.lorenz96(64)
+    leaves = S.spectrum_leaves(S.integrate_chain(f, df, x0, dt, burn_in=200, T=1200, seed=0))
+    al, asg = G.log_sign(leaves)
+    Vc, Sc, sites_ref = G.selective_chain(al, asg, G.colinearity_policy(0.99, 12), 256)
+    assert sites_ref, "the workload must exercise resets"
+    Vl, Vs, sites = g._selective_chain_core(al, asg, g.colinearity_policy(0.99, 12), 256)
+    assert sites == sites_ref
+    assert scaled_real_err(Vl, Vs, Vc, Sc).max() < 1e-9
+
+
 def test_colinearity_predicate_and_reset_kats(g):
     """pkg/tests/test_lyapunov.py:164-215 on the device policy."""
     import math
@@ -334,3 +350,28 @@ def test_chain_fused_scales_match_prepass_path(g, d, T, block):
         # 3xTF32 vs FP32 SIMT differ by ~1e-6 per step; over T steps that accumulates
         assert scaled_real_err(fl, fs, rl, rs).max() < 1e-3
         assert np.isfinite(fl).all()
+
+
+@pytest.mark.parametrize("d,T,block", [(3, 50, 4), (8, 1000, 32), (16, 300, 17), (32, 200, 64),
+                                       (8, 5, 8)])
+@pytest.mark.parametrize("c128", [False, True])
+def test_warp_resident_small_chain_is_bitwise_the_blocked_tree(g, d, T, block, c128):
+    """d <= 32 chains run on the warp-resident kernels (scan_small.cu); their A slot must be
+    bitwise the generic multi-launch blocked tree (the affine engine's A slot)."""
+    rng = np.random.default_rng(d * T)
+    dt = torch.complex128 if c128 else torch.complex64
+    A = g.join(*G.log_sign(rng.standard_normal((T, d, d))), dt)
+    Bz = g.join(*G.log_sign(rng.standard_normal((T, d, 1))), dt)
+    flags = torch.zeros(T, dtype=torch.uint8, device=A.device)
+    small = g.scan_chain(A, block)
+    generic, _, _ = torch.ops.goom.scan_affine(A, Bz, flags, block)
+    assert torch.equal(small, generic)
+    carry = g.join(*G.log_sign(rng.standard_normal((d, d))), dt)
+    with_carry = g.scan_chain(A, block, carry)
+    cl, cs = to_np(carry[None])
+    al, as_ = to_np(A)
+    want = G.scan_sequential(G.Stack(np.concatenate([cl, al]), np.concatenate([cs, as_]),
+                                     np.full((T + 1, d, d), -np.inf), np.ones((T + 1, d, d)),
+                                     np.zeros(T + 1, bool)))
+    wl, ws = to_np(with_carry)
+    assert scaled_real_err(wl, ws, want.alog[1:], want.asign[1:]).max() < (1e-9 if c128 else 5e-3)

@@ -202,3 +202,13 @@ def test_complex_adapters_round_trip():
     # non-canonical phases: 2*pi is positive, 3*pi negative
     w = np.array([1 + 2j * np.pi, 1 + 3j * np.pi], dtype=np.complex64)
     assert list(G.split_complex(w)[1]) == [1.0, -1.0]
+
+
+def test_lorenz96_jacobians_match_reference_machinery():
+    """oracle/systems_port.py vs the reference's systems._flow_system (golden, d=16)."""
+    from oracle import systems_port as S
+
+    z = load_golden("lorenz96_d16")
+    f, df, x0, dt = S.lorenz96(16)
+    mats = S.integrate_chain(f, df, x0, dt, burn_in=200, T=40, seed=0)
+    np.testing.assert_allclose(mats, z["mats"], rtol=1e-12, atol=1e-12)
