@@ -88,6 +88,10 @@ template <class R> int lmme_simt_tiled(const LmmeProblemT<R>& p, cudaStream_t s)
 // tcgen05 3xTF32 (lmme_tc.cu), complex64 only; GOOM_EUNSUPPORTED if not tileable
 int lmme_tc(const LmmeProblem& p, cudaStream_t s);
 bool lmme_tc_eligible(int n, int k, int m);
+// cta_group::2 pair-tile variant (lmme_tc2.cu) for n, m multiples of 256; lmme_tc() prefers
+// it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
+int lmme_tc2(const LmmeProblem& p, cudaStream_t s);
+bool lmme_tc2_eligible(int n, int k, int m);
 
 // ---- scans (scan.cu) --------------------------------------------------------
 template <class R>
