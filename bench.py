@@ -230,32 +230,33 @@ def main():
     growth = harness.growth_rate(dg) if run.digests.shape[0] > 2 else float("nan")
 
     # ---- roofline of the dominant kernel: the phase-3 batched LMME of a window ----
+    # out[b] = L[b] (x) Cx[b / block] with the digest epilogue: exactly the chain engine's
+    # phase-3 launch (chain_ts.cu) on tile-scaled operands; algorithmic 2 d^3 flop/product
     pk, src = measured_peaks()
-    # out[b] = L[b] (x) C[b / block], exactly the chain engine's phase-3 launch (scan.cu)
-    nb = args.window - args.block
-    L = harness.random_chain(nb, d, args.seed, 0, dev)
-    C = harness.random_chain(nb // args.block + 1, d, args.seed + 1, 0, dev)
-    P = torch.empty_like(L)
-    lib = goom._lib
-    strm = ops._stream()
-    # the scan feeds this launch scales emitted by the producing epilogues: time the kernel
-    # alone with precomputed scales (goom_lmme_scaled_c64)
-    rowL = L.real.amax(dim=2).clamp_min(0).contiguous()
-    colC = C.real.amax(dim=1).clamp_min(0).contiguous()
+    nb = args.window
+    if ops.ts_eligible(d):
+        L = ops.ts_random_normal(nb, d, args.seed, 0, dev)
+        C = ops.ts_random_normal(nb // args.block, d, args.seed + 1, 0, dev)
 
-    def phase3():
-        lib.call("goom_lmme_scaled_c64", lib.goom_operand(L.data_ptr(), d * d, 1),
-                 rowL.data_ptr(), d, lib.goom_operand(C.data_ptr(), d * d, args.block),
-                 colC.data_ptr(), d, P.data_ptr(), d * d, nb, d, d, d, strm)
+        def phase3():
+            ops.lmme_ts(L, C, 2, b_div=args.block)
+        kname = "lmme_ts_kernel<digest> (tcgen05 cta_group::2 3xTF32, tile-scaled fp32 operands)"
+    else:
+        L = harness.random_chain(nb, d, args.seed, 0, dev)
+        C = harness.random_chain(nb // args.block, d, args.seed + 1, 0, dev)
 
+        def phase3():
+            torch.ops.goom.lmme(L, torch.repeat_interleave(C, args.block, 0))
+        kname = "lmme (complex64 tcgen05)"
+    strm = torch.cuda.current_stream()
     phase3()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 3
-    s.record()
+    s.record(strm)
     for _ in range(reps):
         phase3()
-    e.record()
+    e.record(strm)
     torch.cuda.synchronize()
     lmme_ms = s.elapsed_time(e) / reps
     tflops = 2.0 * d ** 3 * nb / (lmme_ms / 1e3) / 1e12
@@ -265,7 +266,7 @@ def main():
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    del L, C, P, rowL, colC
+    del L, C
     torch.cuda.empty_cache()
 
     # ---- e2e through the public API: host leaves -> H2D -> scan -> digests D2H ----
@@ -315,9 +316,8 @@ def main():
                        "l2": "no flush: every window (>= 16 GiB) exceeds the 126 MB L2"},
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak_3xtf32,
                          "unit": "TFLOP/s", "frac": tflops / peak_3xtf32, "traffic": traffic,
-                         "kernel": "lmme_tc_kernel (tcgen05 3xTF32, scales given), phase-3 shape "
-                                   f"batch={nb}, {lmme_ms:.2f} ms/launch; algorithmic 2*d^3 "
-                                   "flop/product",
+                         "kernel": f"{kname}, phase-3 shape batch={nb} (carry per {args.block}), "
+                                   f"{lmme_ms:.2f} ms/launch; algorithmic 2*d^3 flop/product",
                          "peak_source": f"{src} bf16 {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 "
                                         "(3xTF32 split)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * d * d * 8,

@@ -206,6 +206,39 @@ int goom_random_normal_c64(goom_c64* out, int64_t n, uint64_t seed, uint64_t off
 /* Per matrix b (n elements each): out4[4b..4b+3] = {max log|x|, log ||x||_F,
  * 1 if every log-magnitude is finite or -inf else 0, 0}. */
 int goom_digest_c64(const goom_c64* X, int64_t batch, int64_t n, float* out4, void* stream);
+/* ---- tile-scaled fp32 chain engine (d % 256 == 0; lmme_ts.cu, chain_ts.cu) ----
+ * The scan's internal matrix format: X_ij = U_ij * exp(q[i][j/256]) (U fp32 d x d,
+ * q fp32 d x d/256) and G[J] = max_i q[i][J] as order-preserving uint bits (0 = unset).
+ * Between scan phases no exp/log runs per element; the public complex64 chain scan
+ * (goom_scan_chain_c64) imports leaves into it and exports prefixes from it. */
+/* Leaves t0 .. t0+T-1 of the goom_random_normal_c64 chain, directly tile-scaled. */
+int goom_random_normal_ts(float* U, float* q, uint32_t* G, int64_t T, int d, uint64_t seed,
+                          uint64_t t0, void* stream);
+/* complex64 (batch, rows, cols) <-> tile-scaled. */
+int goom_ts_from_c64(const goom_c64* X, int64_t batch, int rows, int cols, float* U, float* q,
+                     uint32_t* G, void* stream);
+int goom_ts_to_c64(const float* U, const float* q, int64_t batch, int rows, int cols, goom_c64* X,
+                   void* stream);
+/* C[b] = A(b) (x) B(b) on tile-scaled operands (x_stride 0 broadcasts one matrix, else
+ * contiguous; matrix index b / x_div). kind 0: complex64 C; 1: tile-scaled oU/oq/oG (oG
+ * zero-filled by the caller); 2: digests4 (b: max log, log ||.||_F, finite, 0) with
+ * parts_ws >= batch * (n/32) * (m/256) float4 of scratch. */
+int goom_lmme_ts(const float* aU, const float* aq, const uint32_t* aG, int64_t a_stride,
+                 int64_t a_div, const float* bU, const float* bq, const uint32_t* bG,
+                 int64_t b_stride, int64_t b_div, int kind, goom_c64* C, float* oU, float* oq,
+                 uint32_t* oG, float* digests4, float* parts_ws, int64_t batch, int n, int k,
+                 int m, void* stream);
+/* One window of the long-chain harness: the blocked chain scan (block = `block`, the
+ * reference's tree, scan.py:181-214) of T tile-scaled leaves with an optional
+ * tile-scaled right carry (cU/cq/cG, may be NULL); writes complex64 prefixes to `out`
+ * and/or per-prefix digests (as goom_digest_c64) to digests4, and the last prefix
+ * (tile-scaled) to oU/oq/oG when non-NULL. */
+size_t goom_chain_ts_workspace_size(int64_t T, int d, int block);
+int goom_chain_ts(const float* U, const float* q, const uint32_t* G, int64_t T, int d, int block,
+                  const float* cU, const float* cq, const uint32_t* cG, goom_c64* out,
+                  float* digests4, float* oU, float* oq, uint32_t* oG, void* ws, size_t ws_bytes,
+                  void* stream);
+
 /* Kernels libgoom has launched in this process (bench accounting). */
 long long goom_kernel_launches(void);
 

@@ -120,6 +120,20 @@ SIGNATURES = {
     "goom_random_normal_c64": (_I, [_P, _I64, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "goom_digest_c64": (_I, [_P, _I64, _I64, _P, _P]),
     "goom_kernel_launches": (ctypes.c_longlong, []),
+    # tile-scaled fp32 chain engine
+    "goom_random_normal_ts": (_I, [_P, _P, _P, _I64, _I, ctypes.c_uint64, ctypes.c_uint64, _P]),
+    "goom_ts_from_c64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
+    "goom_ts_to_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P]),
+    "goom_lmme_ts": (
+        _I,
+        [_P, _P, _P, _I64, _I64, _P, _P, _P, _I64, _I64, _I, _P, _P, _P, _P, _P, _P, _I64, _I,
+         _I, _I, _P],
+    ),
+    "goom_chain_ts_workspace_size": (_SZ, [_I64, _I, _I]),
+    "goom_chain_ts": (
+        _I,
+        [_P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+    ),
 }
 
 

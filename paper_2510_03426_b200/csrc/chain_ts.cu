@@ -1,0 +1,281 @@
+// Chain scan over tile-scaled fp32 matrices (lmme_ts.cu) for d a multiple of 256.
+//
+// Same two-level tree as the reference's _scan_affine_stack A slot (scan.py:181-214) and
+// as chain_scan (scan.cu) for the same block size s:
+//   phase 1  L[ks+i] = A[ks+i] (x) L[ks+i-1], batched over blocks (s-1 launches);
+//   phase 2  Cx[k+1] = L[last of block k] (x) Cx[k] (sequential fold; Cx[0] = carry-in, or
+//            the identity when there is none, so every prefix is L_t (x) Cx[k]);
+//   phase 3  P_t = L_t (x) Cx[t / s], one batched launch, written as complex64 GOOMs (the
+//            public scan) or reduced on the fly to per-prefix digests (the long-chain
+//            harness: 2 TiB of d = 512 prefixes are never stored).
+// Cx[nb] = P_{T-1} is the carry-out of a window. Between phases every matrix stays
+// tile-scaled: no exp/log per element except the leaf import and the final export.
+#include "goom_internal.cuh"
+
+namespace goom {
+
+namespace {
+
+inline size_t rup(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct TsBuf {  // T tile-scaled d x d matrices, contiguous
+  float* U;
+  float* q;
+  uint32_t* G;
+  int d, nJ;
+  TsIn in(int64_t first = 0, int64_t stride_mats = 1, int64_t div = 1) const {
+    const int64_t mat = (int64_t)d * d, qm = (int64_t)d * nJ;
+    return TsIn{U + first * mat, q + first * qm, G + first * nJ, stride_mats * mat,
+                stride_mats * qm, stride_mats * nJ, div};
+  }
+  TsOut out(int64_t first = 0, int64_t stride_mats = 1) const {
+    const int64_t mat = (int64_t)d * d, qm = (int64_t)d * nJ;
+    return TsOut{U + first * mat, q + first * qm, G + first * nJ, stride_mats * mat,
+                 stride_mats * qm, stride_mats * nJ};
+  }
+};
+
+size_t ts_bytes(int64_t mats, int d) {
+  const int nJ = d / 256;
+  return rup(sizeof(float) * (size_t)mats * d * d) + rup(sizeof(float) * (size_t)mats * d * nJ) +
+         rup(sizeof(uint32_t) * (size_t)mats * nJ);
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <class X>
+  X* take(size_t count) {
+    X* p = reinterpret_cast<X*>(base + off);
+    off += rup(sizeof(X) * count);
+    return p;
+  }
+  TsBuf ts(int64_t mats, int d) {
+    const int nJ = d / 256;
+    TsBuf b;
+    b.d = d;
+    b.nJ = nJ;
+    b.U = take<float>((size_t)mats * d * d);
+    b.q = take<float>((size_t)mats * d * nJ);
+    b.G = take<uint32_t>((size_t)mats * nJ);
+    return b;
+  }
+};
+
+int copy_ts(const TsBuf& dst, int64_t dfirst, const TsBuf& src, int64_t sfirst, int64_t count,
+            int64_t sstride, cudaStream_t st) {
+  // count matrices src[sfirst + i*sstride] -> dst[dfirst + i*sstride]
+  const size_t mat = (size_t)src.d * src.d, qm = (size_t)src.d * src.nJ;
+  const size_t w[3] = {mat * 4, qm * 4, (size_t)src.nJ * 4};
+  const char* s[3] = {reinterpret_cast<const char*>(src.U + sfirst * mat),
+                      reinterpret_cast<const char*>(src.q + sfirst * qm),
+                      reinterpret_cast<const char*>(src.G + sfirst * src.nJ)};
+  char* d[3] = {reinterpret_cast<char*>(dst.U + dfirst * mat),
+                reinterpret_cast<char*>(dst.q + dfirst * qm),
+                reinterpret_cast<char*>(dst.G + dfirst * dst.nJ)};
+  for (int i = 0; i < 3; ++i)
+    if (cudaMemcpy2DAsync(d[i], w[i] * sstride, s[i], w[i] * sstride, w[i], count,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "tile-scaled copy");
+  return GOOM_OK;
+}
+
+int lmme_ts_call(TsIn a, TsIn b, int kind, float2* C, int64_t strideC, TsOut T, float4* parts,
+                 int64_t batch, int d, cudaStream_t st) {
+  TsProblem p{};
+  p.A = a;
+  p.B = b;
+  p.kind = kind;
+  p.C = C;
+  p.strideC = strideC;
+  p.T = T;
+  p.parts = parts;
+  p.batch = batch;
+  p.n = p.k = p.m = d;
+  return lmme_ts(p, st);
+}
+
+}  // namespace
+
+size_t chain_ts_workspace_bytes(int64_t T, int d, int block, bool leaves_given_ts) {
+  const int64_t s = block < T ? block : T;
+  const int64_t nb = (T + s - 1) / s;
+  return (leaves_given_ts ? 0 : ts_bytes(T, d)) + ts_bytes(T, d) + ts_bytes(nb + 1, d) +
+         rup(sizeof(float2) * (size_t)d * d) +                       // identity (complex64)
+         rup(sizeof(float4) * (size_t)T * (d / 32) * (d / 256)) +    // digest partials
+         1024;
+}
+
+// A (tile-scaled leaves, T of them) -> out (complex64 prefixes) or digests (T float4);
+// carry_in / carry_out tile-scaled (may be null).
+int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_in,
+                  float2* out, float4* digests, TsBuf* carry_out, char* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  const int64_t s = block < T ? block : T;
+  const int64_t nb = (T + s - 1) / s;
+  Carve cv{ws};
+  TsBuf L = cv.ts(T, d);
+  TsBuf Cx = cv.ts(nb + 1, d);
+  float2* ident = cv.take<float2>((size_t)d * d);
+  float4* parts = cv.take<float4>((size_t)T * (d / 32) * (d / 256));
+  if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "tile-scaled chain workspace too small");
+  const int nJ = d / 256;
+  // every G slot that an epilogue max-reduces starts at "unset" (0)
+  if (cudaMemsetAsync(L.G, 0, sizeof(uint32_t) * (size_t)T * nJ, st) != cudaSuccess ||
+      cudaMemsetAsync(Cx.G, 0, sizeof(uint32_t) * (size_t)(nb + 1) * nJ, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "tile-scaled G reset");
+  // Cx[0]: carry-in or the identity
+  if (carry_in) {
+    GOOM_TRY(copy_ts(Cx, 0, *carry_in, 0, 1, 1, st));
+  } else {
+    GOOM_TRY(launch_identity<float>(ident, 1, d, (int64_t)d * d, st));
+    GOOM_TRY(launch_goom_to_ts(ident, 0, Cx.out(0), 1, d, d, st));
+  }
+  // phase 1
+  GOOM_TRY(copy_ts(L, 0, A, 0, nb, s, st));  // L[ks] = A[ks]
+  for (int64_t i = 1; i < s; ++i) {
+    const int64_t cnt = (T - i + s - 1) / s;
+    if (cnt <= 0) break;
+    GOOM_TRY(lmme_ts_call(A.in(i, s), L.in(i - 1, s), kTsOutTs, nullptr, 0, L.out(i, s), nullptr,
+                          cnt, d, st));
+  }
+  // phase 2: Cx[k+1] = L[last of block k] (x) Cx[k]
+  for (int64_t kb = 0; kb < nb; ++kb) {
+    const int64_t last = kb * s + s - 1 < T ? kb * s + s - 1 : T - 1;
+    if (kb == 0 && !carry_in) {
+      GOOM_TRY(copy_ts(Cx, 1, L, last, 1, 1, st));
+      continue;
+    }
+    GOOM_TRY(lmme_ts_call(L.in(last, 0), Cx.in(kb, 0), kTsOutTs, nullptr, 0, Cx.out(kb + 1, 0),
+                          nullptr, 1, d, st));
+  }
+  // phase 3: P_t = L_t (x) Cx[t / s]
+  if (out)
+    GOOM_TRY(lmme_ts_call(L.in(0, 1), Cx.in(0, 1, s), kTsOutGoom, out, (int64_t)d * d, TsOut{},
+                          nullptr, T, d, st));
+  if (digests) {
+    GOOM_TRY(lmme_ts_call(L.in(0, 1), Cx.in(0, 1, s), kTsOutDigest, nullptr, 0, TsOut{}, parts, T,
+                          d, st));
+    GOOM_TRY(launch_digest_reduce(parts, (d / 32) * nJ, digests, T, st));
+  }
+  if (carry_out) GOOM_TRY(copy_ts(*carry_out, 0, Cx, nb, 1, 1, st));
+  return GOOM_OK;
+}
+
+// complex64 leaves -> tile-scaled -> chain_scan_ts (the public chain scan for d % 256 == 0)
+int chain_scan_c64_ts(const float2* A, float2* out, int64_t T, int d, int block,
+                      const float2* carry_in, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Carve cv{reinterpret_cast<char*>(ws)};
+  TsBuf At = cv.ts(T, d);
+  TsBuf Ci = cv.ts(1, d);
+  const int nJ = d / 256;
+  if (cudaMemsetAsync(At.G, 0, sizeof(uint32_t) * (size_t)T * nJ, st) != cudaSuccess ||
+      cudaMemsetAsync(Ci.G, 0, sizeof(uint32_t) * nJ, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "tile-scaled G reset");
+  GOOM_TRY(launch_goom_to_ts(A, (int64_t)d * d, At.out(0), T, d, d, st));
+  if (carry_in) GOOM_TRY(launch_goom_to_ts(carry_in, 0, Ci.out(0), 1, d, d, st));
+  if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "chain workspace too small");
+  return chain_scan_ts(At, T, d, block, carry_in ? &Ci : nullptr, out, nullptr, nullptr,
+                       cv.base + cv.off, ws_bytes - cv.off, st);
+}
+
+size_t chain_c64_ts_workspace_bytes(int64_t T, int d, int block) {
+  return ts_bytes(T, d) + ts_bytes(1, d) + chain_ts_workspace_bytes(T, d, block, true);
+}
+
+}  // namespace goom
+
+using namespace goom;
+
+namespace {
+TsBuf ts_of(float* U, float* q, uint32_t* G, int d) {
+  TsBuf b;
+  b.U = U;
+  b.q = q;
+  b.G = G;
+  b.d = d;
+  b.nJ = d / 256;
+  return b;
+}
+}  // namespace
+
+extern "C" {
+
+size_t goom_chain_ts_workspace_size(int64_t T, int d, int block) {
+  if (T < 1 || d < 256 || d % 256 || block < 1) return 0;
+  return chain_ts_workspace_bytes(T, d, block, true);
+}
+
+int goom_chain_ts(const float* U, const float* q, const uint32_t* G, int64_t T, int d, int block,
+                  const float* cU, const float* cq, const uint32_t* cG, goom_c64* out,
+                  float* digests4, float* oU, float* oq, uint32_t* oG, void* ws, size_t ws_bytes,
+                  void* stream) {
+  if (T < 1 || block < 1) return fail(GOOM_EINVAL, "T and block must be >= 1");
+  if (d < 256 || d % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled chain needs d % 256 == 0");
+  if (!U || !q || !G || !ws) return fail(GOOM_EINVAL, "null pointer");
+  const TsBuf A = ts_of(const_cast<float*>(U), const_cast<float*>(q), const_cast<uint32_t*>(G), d);
+  TsBuf ci = ts_of(const_cast<float*>(cU), const_cast<float*>(cq), const_cast<uint32_t*>(cG), d);
+  TsBuf co = ts_of(oU, oq, oG, d);
+  return chain_scan_ts(A, T, d, block, cU ? &ci : nullptr, reinterpret_cast<float2*>(out),
+                       reinterpret_cast<float4*>(digests4), oU ? &co : nullptr,
+                       reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream));
+}
+
+int goom_ts_from_c64(const goom_c64* X, int64_t batch, int rows, int cols, float* U, float* q,
+                     uint32_t* G, void* stream) {
+  if (batch < 0 || rows < 1 || cols < 256 || cols % 256)
+    return fail(GOOM_EUNSUPPORTED, "tile-scaled format needs cols % 256 == 0");
+  if (batch == 0) return GOOM_OK;
+  const int nJ = cols / 256;
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemsetAsync(G, 0, sizeof(uint32_t) * (size_t)batch * nJ, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "G reset");
+  return launch_goom_to_ts(reinterpret_cast<const float2*>(X), (int64_t)rows * cols,
+                           TsOut{U, q, G, (int64_t)rows * cols, (int64_t)rows * nJ, nJ}, batch,
+                           rows, cols, st);
+}
+
+int goom_ts_to_c64(const float* U, const float* q, int64_t batch, int rows, int cols, goom_c64* X,
+                   void* stream) {
+  if (batch < 0 || rows < 1 || cols < 256 || cols % 256)
+    return fail(GOOM_EUNSUPPORTED, "tile-scaled format needs cols % 256 == 0");
+  if (batch == 0) return GOOM_OK;
+  const int nJ = cols / 256;
+  return launch_ts_to_goom(TsIn{U, q, nullptr, (int64_t)rows * cols, (int64_t)rows * nJ, nJ, 1},
+                           reinterpret_cast<float2*>(X), (int64_t)rows * cols, batch, rows, cols,
+                           as_stream(stream));
+}
+
+// C[b] = A(b) (x) B(b) on tile-scaled operands (matrix index b / div, stride 0 broadcasts);
+// kind 0: complex64 C; 1: tile-scaled (oU, oq, oG zero-filled by the caller); 2: digests4
+int goom_lmme_ts(const float* aU, const float* aq, const uint32_t* aG, int64_t a_stride,
+                 int64_t a_div, const float* bU, const float* bq, const uint32_t* bG,
+                 int64_t b_stride, int64_t b_div, int kind, goom_c64* C, float* oU, float* oq,
+                 uint32_t* oG, float* digests4, float* parts_ws, int64_t batch, int n, int k,
+                 int m, void* stream) {
+  if (batch < 0) return fail(GOOM_EINVAL, "batch must be >= 0");
+  if (!lmme_ts_eligible(n, k, m)) return fail(GOOM_EUNSUPPORTED, "lmme_ts needs n, k, m % 256");
+  if (batch == 0) return GOOM_OK;
+  const int64_t am = a_stride ? 1 : 0, bm = b_stride ? 1 : 0;
+  TsProblem p{};
+  p.A = TsIn{aU, aq, aG, am * (int64_t)n * k, am * (int64_t)n * (k / 256), am * (k / 256),
+             a_div < 1 ? 1 : a_div};
+  p.B = TsIn{bU, bq, bG, bm * (int64_t)k * m, bm * (int64_t)k * (m / 256), bm * (m / 256),
+             b_div < 1 ? 1 : b_div};
+  p.kind = kind;
+  p.C = reinterpret_cast<float2*>(C);
+  p.strideC = (int64_t)n * m;
+  p.T = TsOut{oU, oq, oG, (int64_t)n * m, (int64_t)n * (m / 256), m / 256};
+  p.parts = reinterpret_cast<float4*>(parts_ws);
+  p.batch = batch;
+  p.n = n;
+  p.k = k;
+  p.m = m;
+  GOOM_TRY(lmme_ts(p, as_stream(stream)));
+  if (kind == kTsOutDigest)
+    GOOM_TRY(launch_digest_reduce(p.parts, (n / 32) * (m / 256),
+                                  reinterpret_cast<float4*>(digests4), batch, as_stream(stream)));
+  return GOOM_OK;
+}
+
+}  // extern "C"

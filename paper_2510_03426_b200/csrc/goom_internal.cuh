@@ -61,6 +61,53 @@ struct LmmeProblemT {
 };
 using LmmeProblem = LmmeProblemT<float>;
 
+// ---- tile-scaled fp32 matrices (lmme_ts.cu) ----------------------------------
+// The chain engine's internal format: X_ij = U_ij * exp(q[i][j / 256]) with U fp32
+// (|U| <= 1 per (row, 256-column block) when produced by an LMME epilogue) and
+// G[J] = max_i q[i][J] kept as order-preserving uint bits (float_to_ordered; 0 = unset).
+// An LMME of two such matrices needs no exp/log per element: the left operand is
+// rescaled per (row, block) by exp(q - rowmax q), the right one per row by exp(q - G),
+// and the product's natural scales are rowmax q (left) + G (right).
+struct TsIn {
+  const float* U;
+  const float* q;
+  const uint32_t* G;
+  int64_t sU, sq, sG;  // per-matrix strides in elements (0 broadcasts one matrix)
+  int64_t div;         // matrix index = b / div
+};
+struct TsOut {
+  float* U;
+  float* q;
+  uint32_t* G;  // caller zero-fills
+  int64_t sU, sq, sG;
+};
+// LMME epilogue targets of the tile-scaled kernel
+enum TsOutKind { kTsOutGoom = 0, kTsOutTs = 1, kTsOutDigest = 2 };
+struct TsProblem {
+  TsIn A, B;
+  int kind;
+  float2* C;          // kTsOutGoom: complex64 (batch, n, m)
+  int64_t strideC;
+  TsOut T;            // kTsOutTs
+  float4* parts;      // kTsOutDigest: [batch][n / 32][m / 256] (max log, lfro top, sum, bad)
+  int64_t batch;
+  int n, k, m;
+};
+bool lmme_ts_eligible(int n, int k, int m);
+int lmme_ts(const TsProblem& p, cudaStream_t s);
+// complex64 GOOM <-> tile-scaled (elementwise, one warp per (row, 256-column block))
+int launch_goom_to_ts(const float2* X, int64_t strideX, TsOut out, int64_t batch, int rows,
+                      int cols, cudaStream_t s);
+int launch_ts_to_goom(TsIn in, float2* X, int64_t strideX, int64_t batch, int rows, int cols,
+                      cudaStream_t s);
+// the public chain scan on the tile-scaled engine (chain_ts.cu), d % 256 == 0
+size_t chain_c64_ts_workspace_bytes(int64_t T, int d, int block);
+int chain_scan_c64_ts(const float2* A, float2* out, int64_t T, int d, int block,
+                      const float2* carry_in, void* ws, size_t ws_bytes, cudaStream_t st);
+// digest partials [batch][parts] -> float4 (max log, log ||.||_F, finite, 0) per matrix
+int launch_digest_reduce(const float4* parts, int parts_per, float4* out, int64_t batch,
+                         cudaStream_t s);
+
 // ---- launchers (elementwise.cu) ---------------------------------------------
 // noncanon (nullable): set to 1 if any imaginary part is not exactly 0 or pi
 template <class R>

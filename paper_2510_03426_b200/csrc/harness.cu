@@ -30,25 +30,54 @@ __device__ __forceinline__ float2 goom_of(float v) {
   return make_float2(logf(fabsf(v)), v < 0.0f ? kPi : 0.0f);
 }
 
+// 4 normals per Philox counter g (Box-Muller on two uniform pairs); MUFU log / sincos:
+// the generator is HBM-bound (the accurate libm paths made it 3x slower than its store).
+__device__ __forceinline__ float4 normals4(uint64_t g, uint2 key) {
+  const uint4 r = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0x474F4F4Du, 0u), key);
+  const float a = sqrtf(-2.0f * __logf(u01(r.x))), t0 = 6.283185307179586f * u01(r.y);
+  const float b = sqrtf(-2.0f * __logf(u01(r.z))), t1 = 6.283185307179586f * u01(r.w);
+  float s0, c0, s1, c1;
+  __sincosf(t0, &s0, &c0);
+  __sincosf(t1, &s1, &c1);
+  return make_float4(a * c0, a * s0, b * c1, b * s1);
+}
+
 __global__ void random_normal_kernel(float2* __restrict__ out, int64_t n, uint64_t seed,
                                      uint64_t offset) {
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q * 4 < n;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = (offset / 4) + (uint64_t)q;  // 4 normals per counter
-    const uint4 r = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0x474F4F4Du, 0u), key);
-    const float a = sqrtf(-2.0f * logf(u01(r.x))), t0 = 6.283185307179586f * u01(r.y);
-    const float b = sqrtf(-2.0f * logf(u01(r.z))), t1 = 6.283185307179586f * u01(r.w);
-    float s0, c0, s1, c1;
-    sincosf(t0, &s0, &c0);
-    sincosf(t1, &s1, &c1);
-    const float z[4] = {a * c0, a * s0, b * c1, b * s1};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t i = q * 4 + j;
-      if (i < n) out[i] = goom_of(z[j]);
+    const float4 z = normals4((offset / 4) + (uint64_t)q, key);  // 4 normals per counter
+    if (q * 4 + 3 < n) {
+      float4* o = reinterpret_cast<float4*>(out + q * 4);
+      const float2 g0 = goom_of(z.x), g1 = goom_of(z.y), g2 = goom_of(z.z), g3 = goom_of(z.w);
+      o[0] = make_float4(g0.x, g0.y, g1.x, g1.y);
+      o[1] = make_float4(g2.x, g2.y, g3.x, g3.y);
+    } else {
+      const float zz[4] = {z.x, z.y, z.z, z.w};
+      for (int j = 0; j < 4 && q * 4 + j < n; ++j) out[q * 4 + j] = goom_of(zz[j]);
     }
   }
+}
+
+// the same leaves as tile-scaled fp32 (chain_ts.cu): U = the normals, q = 0, G = bits(0)
+__global__ void random_normal_ts_kernel(float* __restrict__ U, float* __restrict__ qv,
+                                        uint32_t* __restrict__ G, int64_t n, int64_t nq,
+                                        int64_t ng, uint64_t seed, uint64_t offset) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = tid; q * 4 < n; q += stride) {
+    const float4 z = normals4((offset / 4) + (uint64_t)q, key);
+    if (q * 4 + 3 < n) {
+      reinterpret_cast<float4*>(U)[q] = z;
+    } else {
+      const float zz[4] = {z.x, z.y, z.z, z.w};
+      for (int j = 0; j < 4 && q * 4 + j < n; ++j) U[q * 4 + j] = zz[j];
+    }
+  }
+  for (int64_t i = tid; i < nq; i += stride) qv[i] = 0.0f;
+  for (int64_t i = tid; i < ng; i += stride) G[i] = float_to_ordered(0.0f);
 }
 
 // one CTA per matrix: {max log, log Frobenius norm, finite(1/0), 0}
@@ -109,6 +138,22 @@ int goom_random_normal_c64(goom_c64* out, int64_t n, uint64_t seed, uint64_t off
   random_normal_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       reinterpret_cast<float2*>(out), n, seed, offset);
   GOOM_CHECK_LAUNCH("random_normal_kernel");
+  return GOOM_OK;
+}
+
+int goom_random_normal_ts(float* U, float* q, uint32_t* G, int64_t T, int d, uint64_t seed,
+                          uint64_t t0, void* stream) {
+  if (T < 0 || d < 256 || d % 256) return fail(GOOM_EINVAL, "tile-scaled leaves need d % 256 == 0");
+  if (T == 0) return GOOM_OK;
+  if (!U || !q || !G) return fail(GOOM_EINVAL, "null pointer");
+  const int64_t n = T * d * d, offset = (int64_t)t0 * d * d;
+  if (offset % 4) return fail(GOOM_EINVAL, "offset must be a multiple of 4");
+  int64_t blocks = (n / 4 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  random_normal_ts_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      U, q, G, n, T * d * (d / 256), T * (d / 256), seed, (uint64_t)offset);
+  GOOM_CHECK_LAUNCH("random_normal_ts_kernel");
   return GOOM_OK;
 }
 

@@ -1,0 +1,658 @@
+// Tile-scaled LMME on CTA pairs: the chain engine's combine for d a multiple of 256.
+//
+// Same product as Eq. 10-12 (core.py:242-261), with the operands kept between scan
+// phases as tile-scaled fp32 (goom_internal.cuh: X_ij = U_ij exp(q[i][j/256]), G[J] =
+// max_i q[i][J]) instead of complex64 logs. Why (measured, lmme_tc2.cu stage probes on
+// B200): with complex64 operands the pair kernel moves 8 B per operand element through
+// TMA, LDS and STS and spends an ex2 per element in the transform and an lg2 per output
+// element in the epilogue; the load path alone takes as long as the MMAs. Here
+//   * operands are 4 B/element: half the L2->SMEM and LDS bytes;
+//   * the transform is one FMUL per element by a per-(row, block) factor exp(q - rowmax q)
+//     (left operand) or a per-row factor exp(q - G) (right operand), then the 3xTF32 split;
+//   * the epilogue writes U = S * 2^-e (exact power-of-two row normalisation of the
+//     accumulator S within its 256-column block) and q = rowmax_A + G_B + e ln 2: no log;
+//   * or, for prefixes that are only digested, it reduces (max log, log Frobenius,
+//     finiteness) per 32 rows and never writes the product.
+// The scale choice differs from the reference's clamped per-row/per-column maxima only
+// in how intermediate values are rounded and where they underflow (a column more than
+// e^87 below the largest entry of its 256-column block flushes), not in the product.
+//
+// Pipeline per CTA (pair tile 256 x 256, full K, cta_group::2 like lmme_tc2.cu):
+//   warp 0       TMA: raw fp32 K-block (A [128 rows][16 k], B [16 k][128 cols]) into a
+//                4-deep raw ring;
+//   warps 2..17  transform raw -> (big, small) TF32 planes (64B-swizzled, K-major) in a
+//                4-deep plane ring; arrive on the leader's plane_ready;
+//   warp 1       (leader) 6 x tcgen05.mma.cta_group::2.kind::tf32 (M=N=256, K=8) per
+//                K-block into a double-buffered TMEM accumulator;
+//   warps 18..21 epilogue (GOOM complex64 | tile-scaled fp32 | digest partials).
+#include <cstdlib>
+
+#include "tc_ptx.cuh"
+
+namespace goom {
+
+namespace {
+using namespace tc;
+
+constexpr int kRowsCta = 128;
+constexpr int kPairN = 256;
+constexpr int BK = 16;
+constexpr int kRawStages = 4;
+constexpr int kPlStages = 4;
+constexpr int kXformWarps = 16;
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + (kXformWarps + kEpiWarps) * 32;  // 704
+constexpr int kRawA = kRowsCta * BK * 4;                       // 8 KB  [128 rows][16 k]
+constexpr int kRawB = BK * (kPairN / 2) * 4;                   // 8 KB  [16 k][128 cols]
+constexpr int kRaw = kRawA + kRawB;
+constexpr int kPlA = (kRowsCta / 8) * kGroupBytes;             // 16 KB: 16 groups (big | small)
+constexpr int kPl = 2 * kPlA;                                  // 32 KB
+constexpr int kOutStage = 4096;                                // 32 rows x 128 B
+constexpr int kOutBytes = kEpiWarps * 2 * kOutStage;           // 32 KB
+constexpr int kPlOff = kRawStages * kRaw;                      // 64 KB
+constexpr int kOutOff = kPlOff + kPlStages * kPl;              // 192 KB
+constexpr int kBarOff = kOutOff + kOutBytes;                   // 224 KB
+constexpr int kSmem = kBarOff + 512 + 1024;
+constexpr int kTmemCols = 2 * kPairN;
+
+template <int N>
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++s == N) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+__device__ __forceinline__ float lds32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// exp(q - ref) for q <= ref; exact zero for an all-zero row / block (q = -inf)
+__device__ __forceinline__ float scale_factor(float q, float ref) {
+  return q == kNegInf ? 0.0f : ex2_approx(__fsub_rn(q, ref) * kLog2e);
+}
+__device__ __forceinline__ float decode_g(uint32_t g) {
+  return g == 0u ? kNegInf : ordered_to_float(g);
+}
+
+// v -> (big, small) TF32 bit patterns: big = RN-to-TF32(v), small = v - big (exact in FP32;
+// the tensor core reads it truncated to TF32)
+__device__ __forceinline__ void split_tf32(float v, uint32_t& big, uint32_t& small) {
+  big = tf32_round(v);
+  small = __float_as_uint(v - __uint_as_float(big));
+}
+
+struct PairGrid {
+  int nct, nrt;
+  int64_t tiles;
+  __device__ __forceinline__ void at(int64_t t, int64_t& b, int& prow0, int& pcol0) const {
+    const int ct = (int)(t % nct);
+    const int64_t q = t / nct;
+    prow0 = (int)(q % nrt) * 256;
+    pcol0 = ct * kPairN;
+    b = q / nrt;
+  }
+};
+
+template <int kOut>
+__global__ void __launch_bounds__(kThreads, 1)
+    lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
+                   float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* raw_full = bars;                        // [R] local, TMA tx
+  uint64_t* raw_free = raw_full + kRawStages;       // [R] local, 16 transform warps
+  uint64_t* pl_ready = raw_free + kRawStages;       // [P] leader, 32 transform warps
+  uint64_t* pl_free = pl_ready + kPlStages;         // [P] local, MMA commit (multicast)
+  uint64_t* acc_full = pl_free + kPlStages;         // [2] local, MMA commit (multicast)
+  uint64_t* acc_empty = acc_full + 2;               // [2] leader, 8 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cta_rank();
+  const int64_t cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int nk = k / BK;
+  const int nJk = k / 256, nJm = m / 256;
+
+  if (tid == 0) {
+    for (int s = 0; s < kRawStages; ++s) {
+      mbar_init(smem_u32(&raw_full[s]), 1);
+      mbar_init(smem_u32(&raw_free[s]), kXformWarps);
+    }
+    for (int s = 0; s < kPlStages; ++s) {
+      mbar_init(smem_u32(&pl_ready[s]), 2 * kXformWarps);
+      mbar_init(smem_u32(&pl_free[s]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t base = smem_u32(smem);
+
+  if (warp == 0) {
+    // ------------------------------ TMA loader ------------------------------
+    if (lane == 0) {
+      Ring<kRawStages> rr;
+      for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
+        int64_t b;
+        int prow0, pcol0;
+        grid.at(t, b, prow0, pcol0);
+        const int row0 = prow0 + (int)rank * kRowsCta;
+        const int col0 = pcol0 + (int)rank * (kPairN / 2);
+        const int ma = A.sU == 0 ? 0 : (int)(b / A.div);
+        const int mb = B.sU == 0 ? 0 : (int)(b / B.div);
+        for (int kb = 0; kb < nk; ++kb, rr.next()) {
+          mbar_wait(smem_u32(&raw_free[rr.s]), rr.ph ^ 1u);
+          const uint32_t bar = smem_u32(&raw_full[rr.s]);
+          mbar_expect_tx(bar, kRaw);
+          const uint32_t dst = base + rr.s * kRaw;
+          tma_load_3d(dst, &mapA, kb * BK, row0, ma, bar);           // [128 rows][16 k]
+          tma_load_3d(dst + kRawA, &mapB, col0, kb * BK, mb, bar);   // [16 k][128 cols]
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer (leader) ------------------------------
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN);
+      Ring<kPlStages> pr;
+      int lt = 0;
+      for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
+        const int buf = lt & 1;
+        mbar_wait(smem_u32(&acc_empty[buf]), (uint32_t)((lt >> 1) & 1) ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * kPairN);
+        for (int kb = 0; kb < nk; ++kb, pr.next()) {
+          mbar_wait(smem_u32(&pl_ready[pr.s]), pr.ph);
+          tc_fence_after();
+          if (debug != 2) {
+            const uint32_t pb = base + kPlOff + pr.s * kPl;
+            const uint64_t dAb = sw64_desc(pb), dAs = sw64_desc(pb + 512);
+            const uint64_t dBb = sw64_desc(pb + kPlA), dBs = sw64_desc(pb + kPlA + 512);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+              mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, (kb | kk) != 0);
+              mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
+              mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, 1);
+            }
+          }
+          mma_commit_pair(smem_u32(&pl_free[pr.s]));
+        }
+        mma_commit_pair(smem_u32(&acc_full[buf]));
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + kXformWarps) {
+    // ------------------------------ transform ------------------------------
+    // A: warp xw owns group xw (rows 8xw..8xw+7); lane -> row ar = lane/4, k-quad akq = lane%4
+    // (one LDS.128 of a contiguous 512 B group, one STS.128 per plane: conflict-free).
+    // B: warp xw owns columns 32 (xw%4) + lane and k-quad xw/4 (four LDS.32 of 128 B rows,
+    // one STS.128 per plane into group column/8: conflict-free); its 4 k rows are uniform
+    // across the warp, so are their factors.
+    const int xw = warp - 2;
+    const int ar = lane >> 2, akq = lane & 3;
+    const int bkq = xw >> 2, bn = (xw & 3) * 32 + lane;
+    const uint32_t pl_ready0 = smem_u32(&pl_ready[0]);
+    Ring<kRawStages> rr;
+    Ring<kPlStages> pr;
+    for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
+      int64_t b;
+      int prow0, pcol0;
+      grid.at(t, b, prow0, pcol0);
+      const int arow = prow0 + (int)rank * kRowsCta + xw * 8 + ar;   // A row of this lane
+      const float* qa = A.q + (b / A.div) * A.sq + (int64_t)arow * nJk;
+      float rho = kNegInf;
+      for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
+      const int JB = pcol0 / 256;
+      const float* qb = B.q + (b / B.div) * B.sq + JB;
+      const float gB = decode_g(B.G[(b / B.div) * B.sG + JB]);
+      float fa = 0.0f;
+      int curJ = -1;
+      float qn[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) qn[j] = qb[(int64_t)(4 * bkq + j) * nJm];
+      for (int kb = 0; kb < nk; ++kb, rr.next(), pr.next()) {
+        const int J = (kb * BK) >> 8;
+        if (J != curJ) {
+          fa = scale_factor(qa[J], rho);
+          curJ = J;
+        }
+        float fb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fb[j] = scale_factor(qn[j], gB);
+        if (kb + 1 < nk) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) qn[j] = qb[(int64_t)((kb + 1) * BK + 4 * bkq + j) * nJm];
+        }
+        mbar_wait(smem_u32(&raw_full[rr.s]), rr.ph);
+        const uint32_t rb = base + rr.s * kRaw;
+        const float4 va = ld_shared_v4(rb + xw * 512 + lane * 16);
+        float vb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vb[j] = lds32(rb + kRawA + (4 * bkq + j) * 512 + bn * 4);
+        uint32_t ha[4], la[4], hb[4], lb[4];
+        split_tf32(va.x * fa, ha[0], la[0]);
+        split_tf32(va.y * fa, ha[1], la[1]);
+        split_tf32(va.z * fa, ha[2], la[2]);
+        split_tf32(va.w * fa, ha[3], la[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(vb[j] * fb[j], hb[j], lb[j]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&raw_free[rr.s]));
+        mbar_wait(smem_u32(&pl_free[pr.s]), pr.ph ^ 1u);
+        const uint32_t pb = base + kPlOff + pr.s * kPl;
+        if (debug != 1) {
+          const uint32_t ga = pb + xw * kGroupBytes + sw64_off(ar, akq);
+          st_shared_v4(ga, ha[0], ha[1], ha[2], ha[3]);
+          st_shared_v4(ga + 512, la[0], la[1], la[2], la[3]);
+          const uint32_t gb = pb + kPlA + (bn >> 3) * kGroupBytes + sw64_off(bn & 7, bkq);
+          st_shared_v4(gb, hb[0], hb[1], hb[2], hb[3]);
+          st_shared_v4(gb + 512, lb[0], lb[1], lb[2], lb[3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_rank(pl_ready0 + pr.s * 8, 0);
+      }
+    }
+  } else {
+    // ------------------------------ epilogue ------------------------------
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t acc_empty0 = smem_u32(&acc_empty[0]);
+    const uint32_t obuf = base + kOutOff + (uint32_t)(warp - 2 - kXformWarps) * 2 * kOutStage;
+    int lt = 0;
+    for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
+      int64_t b;
+      int prow0, pcol0;
+      grid.at(t, b, prow0, pcol0);
+      const int buf = lt & 1;
+      const int grow = prow0 + (int)rank * kRowsCta + row;
+      const int wrow0 = prow0 + (int)rank * kRowsCta + quad * 32;
+      const int JB = pcol0 / 256;
+      // product scales: rowmax q of the left operand's row, G of the right operand's block
+      const float* qa = A.q + (b / A.div) * A.sq + (int64_t)grow * nJk;
+      float rho = kNegInf;
+      for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
+      const float gB = decode_g(B.G[(b / B.div) * B.sG + JB]);
+      mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
+      tc_fence_after();
+      const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * kPairN);
+      if constexpr (kOut == kTsOutGoom) {
+#pragma unroll 1
+        for (int col = 0; col < kPairN; col += 32) {
+          uint32_t v[32];
+          tmem_ld32(tacc + col, v);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t sbuf = obuf + (uint32_t)h * kOutStage;
+            if (lane == 0) tma_store_wait_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float2 o0 = tc_out(__uint_as_float(v[16 * h + j]), rho, gB);
+              const float2 o1 = tc_out(__uint_as_float(v[16 * h + j + 1]), rho, gB);
+              const float2 o2 = tc_out(__uint_as_float(v[16 * h + j + 2]), rho, gB);
+              const float2 o3 = tc_out(__uint_as_float(v[16 * h + j + 3]), rho, gB);
+              const uint32_t rb = sbuf + (uint32_t)lane * 128;
+              st_shared_v4(rb + ((((j >> 1) + 0) ^ (lane & 7)) << 4), __float_as_uint(o0.x),
+                           __float_as_uint(o0.y), __float_as_uint(o1.x), __float_as_uint(o1.y));
+              st_shared_v4(rb + ((((j >> 1) + 1) ^ (lane & 7)) << 4), __float_as_uint(o2.x),
+                           __float_as_uint(o2.y), __float_as_uint(o3.x), __float_as_uint(o3.y));
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tma_store_3d(&mapOut, sbuf, pcol0 + col + 16 * h, wrow0, (int)b);
+          }
+        }
+      } else {
+        // pass 1: max |S| over this row's 256 columns
+        float mx = 0.0f;
+        bool bad = false;
+#pragma unroll 1
+        for (int col = 0; col < kPairN; col += 32) {
+          uint32_t v[32];
+          tmem_ld32(tacc + col, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float a = fabsf(__uint_as_float(v[j]));
+            bad |= !(a <= 3.0e38f);  // inf or NaN
+            mx = fmaxf(mx, a);
+          }
+        }
+        // exact power-of-two normalisation: mx * 2^-e in [0.5, 1)
+        const uint32_t ex = (__float_as_uint(mx) >> 23) & 0xFFu;
+        const bool norm = mx > 0.0f && ex >= 2u && ex <= 252u;
+        const int e = norm ? (int)ex - 126 : 0;
+        const float sc = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e
+        const float qrow = mx > 0.0f ? __fadd_rn(__fadd_rn(rho, gB), (float)e * kLn2) : kNegInf;
+        if constexpr (kOut == kTsOutTs) {
+#pragma unroll 1
+          for (int col = 0; col < kPairN; col += 32) {
+            uint32_t v[32];
+            tmem_ld32(tacc + col, v);
+            const uint32_t sbuf = obuf + (uint32_t)((col >> 5) & 1) * kOutStage;
+            if (lane == 0) tma_store_wait_read<1>();
+            __syncwarp();
+            const uint32_t rb = sbuf + (uint32_t)lane * 128;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              st_shared_v4(rb + (((j >> 2) ^ (lane & 7)) << 4),
+                           __float_as_uint(__uint_as_float(v[j]) * sc),
+                           __float_as_uint(__uint_as_float(v[j + 1]) * sc),
+                           __float_as_uint(__uint_as_float(v[j + 2]) * sc),
+                           __float_as_uint(__uint_as_float(v[j + 3]) * sc));
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tma_store_3d(&mapOut, sbuf, pcol0 + col, wrow0, (int)b);
+          }
+          T.q[b * T.sq + (int64_t)grow * nJm + JB] = qrow;
+          const float gmax = warp_max(qrow);
+          if (lane == 0 && gmax != kNegInf)
+            atomicMax(&T.G[b * T.sG + JB], float_to_ordered(gmax));
+        } else {
+          // digest: this row's max log and log Frobenius norm, reduced over the warp's 32 rows
+          float ss = 0.0f;
+#pragma unroll 1
+          for (int col = 0; col < kPairN; col += 32) {
+            uint32_t v[32];
+            tmem_ld32(tacc + col, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float a = __uint_as_float(v[j]) * sc;
+              ss = fmaf(a, a, ss);
+            }
+          }
+          const float lmax = mx > 0.0f ? __fadd_rn(qrow, logf(mx * sc)) : kNegInf;
+          const float lfro = mx > 0.0f ? __fadd_rn(qrow, 0.5f * logf(ss)) : kNegInf;
+          const float wmax = warp_max(lmax);
+          const float top = warp_max(lfro);
+          const float w = top == kNegInf ? 0.0f : expf(2.0f * (lfro - top));
+          const float sum = warp_sum(w);
+          const bool wbad = __any_sync(0xffffffffu, bad || !(rho < INFINITY) || !(gB < INFINITY));
+          if (lane == 0)
+            parts[(b * (n / 32) + wrow0 / 32) * nJm + JB] =
+                make_float4(wmax, top, sum, wbad ? 1.0f : 0.0f);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_rank(acc_empty0 + buf * 8, 0);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+int ts_debug() {
+  static int v = [] {
+    const char* e = getenv("GOOM_TS_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int kOut>
+int max_clusters() {
+  static int v = [] {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 74);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, lmme_ts_kernel<kOut>, &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    return n;
+  }();
+  return v;
+}
+
+template <int kOut>
+int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
+           const CUtensorMap& mapOut, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmem) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "lmme_ts smem attribute");
+    attr_set = true;
+  }
+  PairGrid pg;
+  pg.nct = p.m / kPairN;
+  pg.nrt = p.n / 256;
+  pg.tiles = p.batch * pg.nct * pg.nrt;
+  const int64_t mc = max_clusters<kOut>();
+  const int64_t clusters = pg.tiles < mc ? pg.tiles : mc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut>, mapA, mapB, mapOut, p.A, p.B, p.T, p.parts, pg,
+                     p.n, p.k, p.m, ts_debug());
+  GOOM_CHECK_LAUNCH("lmme_ts_kernel");
+  return GOOM_OK;
+}
+
+inline int64_t mats(int64_t stride, int64_t div, int64_t batch) {
+  return stride == 0 ? 1 : (batch - 1) / div + 1;
+}
+
+}  // namespace
+
+bool lmme_ts_eligible(int n, int k, int m) {
+  return n > 0 && k > 0 && m > 0 && n % 256 == 0 && k % 256 == 0 && m % 256 == 0;
+}
+
+int lmme_ts(const TsProblem& p, cudaStream_t s) {
+  if (!lmme_ts_eligible(p.n, p.k, p.m)) return fail(GOOM_EUNSUPPORTED, "lmme_ts: n, k, m % 256");
+  if (p.batch == 0) return GOOM_OK;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(p.A.U) | reinterpret_cast<uintptr_t>(p.B.U);
+  if ((al & 15) || ((p.A.sU | p.B.sU) & 3)) return fail(GOOM_EINVAL, "lmme_ts: operand alignment");
+  alignas(64) CUtensorMap mapA, mapB, mapOut;
+  {  // A fp32 (k, n, matrix), box 16 k x 128 rows
+    cuuint64_t dims[3] = {(cuuint64_t)p.k, (cuuint64_t)p.n,
+                          (cuuint64_t)mats(p.A.sU, p.A.div, p.batch)};
+    cuuint64_t strides[2] = {(cuuint64_t)p.k * 4,
+                             (cuuint64_t)(p.A.sU ? p.A.sU : (int64_t)p.n * p.k) * 4};
+    cuuint32_t box[3] = {BK, kRowsCta, 1};
+    GOOM_TRY(encode_raw(&mapA, p.A.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box));
+  }
+  {  // B fp32 (m, k, matrix), box 128 cols x 16 k
+    cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.k,
+                          (cuuint64_t)mats(p.B.sU, p.B.div, p.batch)};
+    cuuint64_t strides[2] = {(cuuint64_t)p.m * 4,
+                             (cuuint64_t)(p.B.sU ? p.B.sU : (int64_t)p.k * p.m) * 4};
+    cuuint32_t box[3] = {kPairN / 2, BK, 1};
+    GOOM_TRY(encode_raw(&mapB, p.B.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box));
+  }
+  if (p.kind == kTsOutGoom) {
+    if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.strideC & 1))
+      return fail(GOOM_EINVAL, "lmme_ts: output alignment");
+    const int64_t cb = p.strideC == 0 ? 1 : p.batch;
+    const int64_t cs = p.strideC == 0 ? (int64_t)p.n * p.m : p.strideC;
+    cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.n, (cuuint64_t)cb};
+    cuuint64_t strides[2] = {(cuuint64_t)p.m * 8, (cuuint64_t)cs * 8};
+    cuuint32_t box[3] = {16, 32, 1};
+    GOOM_TRY(encode_raw(&mapOut, p.C, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, dims, strides, box,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    return launch<kTsOutGoom>(p, mapA, mapB, mapOut, s);
+  }
+  if (p.kind == kTsOutTs) {
+    if ((reinterpret_cast<uintptr_t>(p.T.U) & 15) || (p.T.sU & 3))
+      return fail(GOOM_EINVAL, "lmme_ts: output alignment");
+    const int64_t cb = p.T.sU == 0 ? 1 : p.batch;
+    const int64_t cs = p.T.sU == 0 ? (int64_t)p.n * p.m : p.T.sU;
+    cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.n, (cuuint64_t)cb};
+    cuuint64_t strides[2] = {(cuuint64_t)p.m * 4, (cuuint64_t)cs * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    GOOM_TRY(encode_raw(&mapOut, p.T.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    return launch<kTsOutTs>(p, mapA, mapB, mapOut, s);
+  }
+  mapOut = mapA;  // unused by the digest epilogue
+  return launch<kTsOutDigest>(p, mapA, mapB, mapOut, s);
+}
+
+// ---- conversions ------------------------------------------------------------------
+
+namespace {
+
+// one warp per (matrix, row, 256-column block): q = max log (clamped below by nothing: the
+// block's own maximum), U = sign * exp(log - q); G via ordered atomicMax
+__global__ void goom_to_ts_kernel(const float2* __restrict__ X, int64_t sX, TsOut out,
+                                  int64_t batch, int rows, int cols) {
+  const int nJ = cols / 256;
+  const int64_t units = batch * rows * nJ;
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < units;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int J = (int)(u % nJ);
+    const int64_t r = (u / nJ) % rows;
+    const int64_t b = u / ((int64_t)nJ * rows);
+    const float2* x = X + b * sX + r * cols + J * 256;
+    float2 v[8];
+    float mx = kNegInf;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = x[i * 32 + lane];
+      mx = fmaxf(mx, v[i].x);
+    }
+    mx = warp_max(mx);
+    float* U = out.U + b * out.sU + r * cols + J * 256;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float e = mx == kNegInf ? 0.0f : expf(v[i].x - mx);
+      U[i * 32 + lane] = phase_negative(v[i].y) ? -e : e;
+    }
+    if (lane == 0) {
+      out.q[b * out.sq + r * nJ + J] = mx;
+      if (mx != kNegInf) atomicMax(&out.G[b * out.sG + J], float_to_ordered(mx));
+    }
+  }
+}
+
+__global__ void ts_to_goom_kernel(TsIn in, float2* __restrict__ X, int64_t sX, int64_t batch,
+                                  int rows, int cols) {
+  const int nJ = cols / 256;
+  const int64_t n = batch * rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cols);
+    const int64_t r = (i / cols) % rows;
+    const int64_t b = i / ((int64_t)cols * rows);
+    const int64_t mb = b / in.div;
+    const float u = in.U[mb * in.sU + r * cols + c];
+    const float q = in.q[mb * in.sq + r * nJ + c / 256];
+    X[b * sX + r * cols + c] = make_float2(u == 0.0f ? kNegInf : __fadd_rn(logf(fabsf(u)), q),
+                                           u < 0.0f ? kPi : 0.0f);
+  }
+}
+
+// per matrix: combine (max log, lfro top, sum e^{2(lfro - top)}, bad) partials
+__global__ void digest_reduce_kernel(const float4* __restrict__ parts, int per,
+                                     float4* __restrict__ out, int64_t batch) {
+  const int64_t b = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= batch) return;
+  const float4* p = parts + b * per;
+  float mx = kNegInf, top = kNegInf;
+  bool bad = false;
+  for (int i = lane; i < per; i += 32) {
+    mx = fmaxf(mx, p[i].x);
+    top = fmaxf(top, p[i].y);
+    bad |= p[i].w != 0.0f;
+  }
+  mx = warp_max(mx);
+  top = warp_max(top);
+  float s = 0.0f;
+  if (top != kNegInf)
+    for (int i = lane; i < per; i += 32)
+      if (p[i].y != kNegInf) s += p[i].z * expf(2.0f * (p[i].y - top));
+  s = warp_sum(s);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0)
+    out[b] = make_float4(mx, top == kNegInf ? kNegInf : top + 0.5f * logf(s),
+                         bad || !(mx < INFINITY) ? 0.0f : 1.0f, 0.0f);
+}
+
+int grid_for(int64_t threads) {
+  int64_t b = (threads + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+int launch_goom_to_ts(const float2* X, int64_t strideX, TsOut out, int64_t batch, int rows,
+                      int cols, cudaStream_t s) {
+  if (cols % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled format needs cols % 256 == 0");
+  goom_to_ts_kernel<<<grid_for(batch * rows * (cols / 256) * 32), 256, 0, s>>>(X, strideX, out,
+                                                                                batch, rows, cols);
+  GOOM_CHECK_LAUNCH("goom_to_ts_kernel");
+  return GOOM_OK;
+}
+
+int launch_ts_to_goom(TsIn in, float2* X, int64_t strideX, int64_t batch, int rows, int cols,
+                      cudaStream_t s) {
+  ts_to_goom_kernel<<<grid_for(batch * rows * cols), 256, 0, s>>>(in, X, strideX, batch, rows,
+                                                                   cols);
+  GOOM_CHECK_LAUNCH("ts_to_goom_kernel");
+  return GOOM_OK;
+}
+
+int launch_digest_reduce(const float4* parts, int parts_per, float4* out, int64_t batch,
+                         cudaStream_t s) {
+  const int blocks = (int)((batch + 7) / 8);
+  digest_reduce_kernel<<<blocks, 256, 0, s>>>(parts, parts_per, out, batch);
+  GOOM_CHECK_LAUNCH("digest_reduce_kernel");
+  return GOOM_OK;
+}
+
+}  // namespace goom

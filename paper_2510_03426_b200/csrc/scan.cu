@@ -14,6 +14,8 @@
 //
 // Buffers: local products L (T matrices) and carries Cx (nblocks+1) live in the
 // caller's workspace; the input is never written; out may not alias the input.
+#include <cstdlib>
+
 #include "goom_internal.cuh"
 
 namespace goom {
@@ -83,8 +85,17 @@ int copy_strided(C* dst, const C* src, size_t width, size_t pitch, size_t rows, 
 
 }  // namespace
 
+bool chain_ts_path(int d) {
+  static const bool on = [] {
+    const char* e = getenv("GOOM_CHAIN_TS");
+    return !(e && atoi(e) == 0);
+  }();
+  return on && lmme_backend() != 1 && lmme_ts_eligible(d, d, d);
+}
+
 template <class R>
 size_t chain_workspace_bytes(int64_t T, int d, int block) {
+  if (sizeof(R) == 4 && chain_ts_path(d)) return chain_c64_ts_workspace_bytes(T, d, block);
   int64_t s = block < T ? block : T;
   int64_t nb = (T + s - 1) / s;
   size_t mat = (size_t)d * d;
@@ -202,6 +213,10 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
   const int64_t mat = (int64_t)d * d;
   if (ws_bytes < chain_workspace_bytes<R>(T, d, block))
     return fail(GOOM_EWORKSPACE, "chain scan workspace too small");
+  if constexpr (sizeof(R) == 4) {
+    if (chain_ts_path(d))
+      return chain_scan_c64_ts(A, out, T, d, block, carry_in, ws, ws_bytes, st);
+  }
   Carve cv{reinterpret_cast<char*>(ws)};
   C* L = cv.take<C>((size_t)mat * T);
   C* Cx_ = cv.take<C>((size_t)mat * (nb + 1));

@@ -17,7 +17,7 @@ from typing import Dict, Optional
 
 import torch
 
-from . import ops  # noqa: F401  (registers torch.ops.goom.*)
+from . import ops  # registers torch.ops.goom.*
 
 
 @dataclass
@@ -36,7 +36,14 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
               t0: int = 0, carry: Optional[torch.Tensor] = None, snapshot_every: int = 0,
               leaves: Optional[torch.Tensor] = None) -> ChainRun:
     """Scan leaves t0 .. t0+T-1 (generated, or the given `leaves` tensor) with an
-    optional right carry; returns per-prefix digests, the final prefix, snapshots."""
+    optional right carry; returns per-prefix digests, the final prefix, snapshots.
+
+    d % 256 == 0 runs on the tile-scaled engine (ops.chain_ts): leaves are generated
+    (or imported) tile-scaled, prefixes are digested inside the phase-3 LMME epilogue
+    and the carry between windows stays tile-scaled. Other d use the complex64 scan +
+    digest kernels."""
+    if ops.ts_eligible(d):
+        return _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves)
     dev = torch.device("cuda", torch.cuda.current_device())
     digests = torch.empty((T, 4), dtype=torch.float32, device=dev)
     snaps: Dict[int, torch.Tensor] = {}
@@ -52,6 +59,29 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
         carry = P[n - 1].clone()
         del P, A
     return ChainRun(digests, carry, snaps)
+
+
+def _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves) -> ChainRun:
+    dev = torch.device("cuda", torch.cuda.current_device())
+    digests = torch.empty((T, 4), dtype=torch.float32, device=dev)
+    snaps: Dict[int, torch.Tensor] = {}
+    c = ops.ts_from_goom(carry.reshape(1, d, d)) if carry is not None else None
+    for w0 in range(0, T, window):
+        n = min(window, T - w0)
+        if leaves is not None:
+            A = ops.ts_from_goom(leaves[w0:w0 + n])
+        else:
+            A = ops.ts_random_normal(n, d, seed, t0 + w0, dev)
+        want = bool(snapshot_every) and any((t0 + t) % snapshot_every == 0
+                                            for t in range(w0, w0 + n))
+        P, dg, c = ops.chain_ts(A, block, c, out=want, digests=True, carry_out=True)
+        digests[w0:w0 + n] = dg
+        if want:
+            for t in range(w0, w0 + n):
+                if (t0 + t) % snapshot_every == 0:
+                    snaps[t0 + t] = P[t - w0].clone()
+        del P, A
+    return ChainRun(digests, ops.ts_to_goom(c)[0], snaps)
 
 
 def chain_total(A: torch.Tensor) -> torch.Tensor:

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import math
-from typing import Optional, Tuple
+from typing import NamedTuple, Optional, Tuple
 
 import torch
 
@@ -330,3 +330,116 @@ def digest(x: torch.Tensor) -> torch.Tensor:
 def kernel_launches() -> int:
     """libgoom kernel launches so far in this process."""
     return int(_lib.load().goom_kernel_launches())
+
+
+# ---------------------------------------------------------------------------
+# tile-scaled fp32 chain engine (include/goom.h; d % 256 == 0)
+
+
+class TsMats(NamedTuple):
+    """T tile-scaled d x d matrices: X_ij = U_ij exp(q[i][j // 256]); G[J] = max_i q[i][J]
+    as order-preserving uint bits stored in int32 (0 = unset)."""
+    U: torch.Tensor  # (T, d, d) float32
+    q: torch.Tensor  # (T, d, d // 256) float32
+    G: torch.Tensor  # (T, d // 256) int32
+
+    @property
+    def T(self) -> int:
+        return self.U.shape[0]
+
+    def __getitem__(self, i):  # slice of matrices
+        return TsMats(self.U[i], self.q[i], self.G[i])
+
+
+def ts_eligible(d: int) -> bool:
+    return d >= 256 and d % 256 == 0
+
+
+def ts_empty(T: int, d: int, device) -> TsMats:
+    if not ts_eligible(d):
+        raise ValueError(f"tile-scaled matrices need d % 256 == 0, got {d}")
+    return TsMats(torch.empty((T, d, d), dtype=torch.float32, device=device),
+                  torch.empty((T, d, d // 256), dtype=torch.float32, device=device),
+                  torch.zeros((T, d // 256), dtype=torch.int32, device=device))
+
+
+def ts_random_normal(T: int, d: int, seed: int, t0: int, device) -> TsMats:
+    """Leaves t0 .. t0+T-1 of the random_normal chain, tile-scaled (same values)."""
+    m = ts_empty(T, d, device)
+    _lib.call("goom_random_normal_ts", m.U.data_ptr(), m.q.data_ptr(), m.G.data_ptr(), T, d,
+              int(seed), int(t0), _stream())
+    return m
+
+
+def ts_from_goom(x: torch.Tensor) -> TsMats:
+    _need_cuda(x)
+    if x.dtype != torch.complex64:
+        raise ValueError("tile-scaled import takes complex64 GOOMs")
+    x = x.contiguous()
+    d = x.shape[-1]
+    if x.shape[-2] != d:
+        raise ValueError("square matrices expected")
+    xb = x.reshape(-1, d, d)
+    m = ts_empty(xb.shape[0], d, x.device)
+    _lib.call("goom_ts_from_c64", xb.data_ptr(), xb.shape[0], d, d, m.U.data_ptr(), m.q.data_ptr(),
+              m.G.data_ptr(), _stream())
+    return m
+
+
+def ts_to_goom(m: TsMats) -> torch.Tensor:
+    T, d = m.U.shape[0], m.U.shape[-1]
+    out = torch.empty((T, d, d), dtype=torch.complex64, device=m.U.device)
+    _lib.call("goom_ts_to_c64", m.U.data_ptr(), m.q.data_ptr(), T, d, d, out.data_ptr(), _stream())
+    return out
+
+
+def lmme_ts(a: TsMats, b: TsMats, kind: int = 0, b_div: int = 1):
+    """C[i] = a[i] (x) b[i // b_div] on tile-scaled operands (a single-matrix operand
+    broadcasts). kind 0 -> complex64 (T, d, d); 1 -> TsMats; 2 -> digests (T, 4)."""
+    d = a.U.shape[-1]
+    batch = max(a.T, b.T * b_div if b.T > 1 else a.T)
+    dev = a.U.device
+    a_stride = 1 if a.T > 1 else 0
+    b_stride = 1 if b.T > 1 else 0
+    C = oU = oq = oG = dg = parts = None
+    if kind == 0:
+        C = torch.empty((batch, d, d), dtype=torch.complex64, device=dev)
+    elif kind == 1:
+        res = ts_empty(batch, d, dev)
+        oU, oq, oG = res.U, res.q, res.G
+    else:
+        dg = torch.empty((batch, 4), dtype=torch.float32, device=dev)
+        parts = torch.empty((batch * (d // 32) * (d // 256), 4), dtype=torch.float32, device=dev)
+
+    def p(t):
+        return None if t is None else t.data_ptr()
+
+    _lib.call("goom_lmme_ts", a.U.data_ptr(), a.q.data_ptr(), a.G.data_ptr(), a_stride, 1,
+              b.U.data_ptr(), b.q.data_ptr(), b.G.data_ptr(), b_stride, int(b_div), int(kind),
+              p(C), p(oU), p(oq), p(oG), p(dg), p(parts), batch, d, d, d, _stream())
+    if kind == 0:
+        return C
+    if kind == 1:
+        return res
+    return dg
+
+
+def chain_ts(leaves: TsMats, block: int, carry: Optional[TsMats] = None, out: bool = False,
+             digests: bool = True, carry_out: bool = True):
+    """One window of the long-chain scan on tile-scaled leaves: returns
+    (prefixes complex64 or None, digests (T, 4) or None, last prefix TsMats or None)."""
+    T, d = leaves.U.shape[0], leaves.U.shape[-1]
+    dev = leaves.U.device
+    ws, nws = _ws(int(_lib.load().goom_chain_ts_workspace_size(T, d, int(block))), dev)
+    P = torch.empty((T, d, d), dtype=torch.complex64, device=dev) if out else None
+    dg = torch.empty((T, 4), dtype=torch.float32, device=dev) if digests else None
+    co = ts_empty(1, d, dev) if carry_out else None
+
+    def p(t):
+        return None if t is None else t.data_ptr()
+
+    _lib.call("goom_chain_ts", leaves.U.data_ptr(), leaves.q.data_ptr(), leaves.G.data_ptr(), T, d,
+              int(block), p(carry.U if carry else None), p(carry.q if carry else None),
+              p(carry.G if carry else None), p(P), p(dg), p(co.U if co else None),
+              p(co.q if co else None), p(co.G if co else None), ws.data_ptr(), nws, _stream())
+    return P, dg, co
