@@ -87,6 +87,10 @@ __device__ __forceinline__ void split_tf32(float v, uint32_t& big, uint32_t& sma
   big = tf32_round(v);
   small = __float_as_uint(v - __uint_as_float(big));
 }
+__device__ __forceinline__ void split_tf32_rn(float v, uint32_t& big, uint32_t& small) {
+  big = tf32_round(v);
+  small = tf32_round(v - __uint_as_float(big));
+}
 
 struct PairGrid {
   int nct, nrt;
@@ -188,16 +192,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb, pr.next()) {
           mbar_wait(smem_u32(&pl_ready[pr.s]), pr.ph);
           tc_fence_after();
-          if (debug != 2) {
+          if ((debug & 15) != 2) {
             const uint32_t pb = base + kPlOff + pr.s * kPl;
             const uint64_t dAb = sw64_desc(pb), dAs = sw64_desc(pb + 512);
             const uint64_t dBb = sw64_desc(pb + kPlA), dBs = sw64_desc(pb + kPlA + 512);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-              mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, (kb | kk) != 0);
-              mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
-              mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, 1);
+              if (debug & 64) {  // plain TF32 (precision probe only)
+                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, (kb | kk) != 0);
+              } else if (debug & 32) {
+                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, (kb | kk) != 0);
+                mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, 1);
+                mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
+              } else {
+                mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, (kb | kk) != 0);
+                mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
+                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, 1);
+              }
             }
           }
           mma_commit_pair(smem_u32(&pl_free[pr.s]));
@@ -255,17 +267,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) vb[j] = lds32(rb + kRawA + (4 * bkq + j) * 512 + bn * 4);
         uint32_t ha[4], la[4], hb[4], lb[4];
-        split_tf32(va.x * fa, ha[0], la[0]);
-        split_tf32(va.y * fa, ha[1], la[1]);
-        split_tf32(va.z * fa, ha[2], la[2]);
-        split_tf32(va.w * fa, ha[3], la[3]);
+        if (debug & 16) {
+          split_tf32_rn(va.x * fa, ha[0], la[0]);
+          split_tf32_rn(va.y * fa, ha[1], la[1]);
+          split_tf32_rn(va.z * fa, ha[2], la[2]);
+          split_tf32_rn(va.w * fa, ha[3], la[3]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) split_tf32(vb[j] * fb[j], hb[j], lb[j]);
+          for (int j = 0; j < 4; ++j) split_tf32_rn(vb[j] * fb[j], hb[j], lb[j]);
+        } else {
+          split_tf32(va.x * fa, ha[0], la[0]);
+          split_tf32(va.y * fa, ha[1], la[1]);
+          split_tf32(va.z * fa, ha[2], la[2]);
+          split_tf32(va.w * fa, ha[3], la[3]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split_tf32(vb[j] * fb[j], hb[j], lb[j]);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&raw_free[rr.s]));
         mbar_wait(smem_u32(&pl_free[pr.s]), pr.ph ^ 1u);
         const uint32_t pb = base + kPlOff + pr.s * kPl;
-        if (debug != 1) {
+        if ((debug & 15) != 1) {
           const uint32_t ga = pb + xw * kGroupBytes + sw64_off(ar, akq);
           st_shared_v4(ga, ha[0], ha[1], ha[2], ha[3]);
           st_shared_v4(ga + 512, la[0], la[1], la[2], la[3]);

@@ -78,6 +78,15 @@ def scaled_real_err(got_log, got_sign, want_log, want_sign):
     return diff.max(axis=1)
 
 
+def tc_chain_scaled_floor(d, T):
+    """Scaled-real error floor for chains on the tcgen05 3xTF32 kernels. The tensor core's
+    FP32 accumulation into TMEM truncates, so each LMME of inner dimension k shrinks
+    |result| by ~6e-9 * k on average (measured on B200, tools/bias_probe.py: -1.5e-6 at
+    k = 256, -3.1e-6 at k = 512; numpy float32 is unbiased at 3e-7 rms). Along a chain this
+    bias adds up linearly: allow twice the measured drift, 1.2e-8 * k per step."""
+    return max(1e-4, 1.2e-8 * d * T)
+
+
 def chain_kappa(alog, asign, plog, psign):
     """Cancellation ratio of every entry of a product chain P_t = A_t P_{t-1},
     from the float64 oracle prefixes (P_0 = A_0 has kappa 1)."""
@@ -101,7 +110,7 @@ def masked_rel_err(x, y, mask):
 
 
 def chain_parity(got_log, got_sign, alog, asign, want64, ref32_runs, kappa_min=1e-2,
-                 factor=4.0, floor=2e-4):
+                 factor=4.0, floor=2e-4, scaled_floor=1e-4):
     """SURVEY §8c chain criterion, cancellation-masked: per position the rel-log
     error over entries with kappa >= kappa_min must stay within `factor` x the
     reference's own float32 error (max over the given float32 runs) or `floor`;
@@ -118,7 +127,7 @@ def chain_parity(got_log, got_sign, alog, asign, want64, ref32_runs, kappa_min=1
     flips = int(np.sum((np.asarray(got_sign) != ws) & mask & ref_sign_ok))
     scaled = scaled_real_err(got_log, got_sign, wl, ws)
     scaled_ref = np.max([scaled_real_err(r[0], r[1], wl, ws) for r in ref32_runs], axis=0)
-    scaled_bad = np.flatnonzero(scaled > np.maximum(factor * scaled_ref, 1e-4))
+    scaled_bad = np.flatnonzero(scaled > np.maximum(factor * scaled_ref, scaled_floor))
     return dict(ok=bad.size == 0 and flips == 0 and scaled_bad.size == 0, bad=bad[:10],
                 e_gpu=e_gpu, e_ref=e_ref, flips=flips, scaled_max=float(scaled.max()),
                 scaled_bad=scaled_bad[:10])

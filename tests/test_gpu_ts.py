@@ -11,7 +11,8 @@ import numpy as np
 import pytest
 import torch
 
-from goom_testlib import chain_parity, lmme_parity, scaled_real_err, to_np
+from goom_testlib import (chain_parity, lmme_parity, scaled_real_err, tc_chain_scaled_floor,
+                          to_np)
 from oracle import gooms_port as G
 
 pytestmark = pytest.mark.gpu
@@ -119,10 +120,11 @@ def test_lmme_ts_edge_cases(g, ops):
     sl, ss = G.lmme(al[1:2].astype(np.float64) - 5000.0, as_[1:2].astype(np.float64),
                     bl[1:2].astype(np.float64) + 3000.0, bs[1:2].astype(np.float64))
     assert np.isfinite(gl[1]).all()
-    err = np.max(np.abs(gl[1] - (sl[0] + 2000.0)) / np.abs(sl[0] + 2000.0))
     kap = G.cancellation(al[1:2].astype(np.float64) - 5000.0, as_[1:2].astype(np.float64),
                          bl[1:2].astype(np.float64) + 3000.0, bs[1:2].astype(np.float64))[0]
-    assert err < 1e-4 and np.all((gs[1] == ss[0]) | (kap < 1e-4))
+    rel = np.abs(gl[1] - (sl[0] + 2000.0)) / np.abs(sl[0] + 2000.0)
+    assert np.max(np.where(kap >= 1e-2, rel, 0.0)) < 1e-4
+    assert np.all((gs[1] == ss[0]) | (kap < 1e-4))
 
 
 @pytest.mark.parametrize("d,T,block", [(256, 64, 8), (256, 33, 64), (512, 24, 5)])
@@ -137,7 +139,7 @@ def test_chain_ts_matches_float64_oracle(g, ops, d, T, block):
     want = G.chain_blocked(al, as_, T)
     l32, s32 = G.log_sign(mats.astype(np.float32))
     refs = [G.chain_blocked(l32, s32, block), G.chain_blocked(l32, s32, T)]
-    r = chain_parity(gl, gs, al, as_, want, refs)
+    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=tc_chain_scaled_floor(d, T))
     assert r["ok"], (r["bad"], r["flips"], r["scaled_bad"])
 
 
@@ -154,7 +156,9 @@ def test_chain_ts_carry_digests_and_windows(g, ops):
     assert torch.allclose(dg[:, :3], dref[:, :3], rtol=1e-5, atol=1e-4)
     cl, cs = to_np(ops.ts_to_goom(c))
     pl, ps = to_np(P[-1:])
-    assert scaled_real_err(cl, cs, pl, ps).max() < 1e-6
+    # same product, tile-scaled vs complex64 epilogue: q = rowmax + G + e ln 2 rounds at
+    # ulp(|log|) ~ 1.5e-5 for the logs ~130 reached here
+    assert scaled_real_err(cl, cs, pl, ps).max() < 1e-4
     P1, _, c1 = ops.chain_ts(leaves[0:20], block, None, out=True, digests=False, carry_out=True)
     P2, _, _ = ops.chain_ts(leaves[20:48], block, c1, out=True, digests=False, carry_out=False)
     got = torch.cat([P1, P2])
