@@ -63,8 +63,9 @@ struct Carve {
 };
 
 int copy_ts(const TsBuf& dst, int64_t dfirst, const TsBuf& src, int64_t sfirst, int64_t count,
-            int64_t sstride, cudaStream_t st) {
-  // count matrices src[sfirst + i*sstride] -> dst[dfirst + i*sstride]
+            int64_t sstride, cudaStream_t st, int64_t dstride = 0) {
+  // count matrices src[sfirst + i*sstride] -> dst[dfirst + i*dstride] (dstride 0: = sstride)
+  if (dstride == 0) dstride = sstride;
   const size_t mat = (size_t)src.d * src.d, qm = (size_t)src.d * src.nJ;
   const size_t w[3] = {mat * 4, qm * 4, (size_t)src.nJ * 4};
   const char* s[3] = {reinterpret_cast<const char*>(src.U + sfirst * mat),
@@ -74,7 +75,7 @@ int copy_ts(const TsBuf& dst, int64_t dfirst, const TsBuf& src, int64_t sfirst, 
                 reinterpret_cast<char*>(dst.q + dfirst * qm),
                 reinterpret_cast<char*>(dst.G + dfirst * dst.nJ)};
   for (int i = 0; i < 3; ++i)
-    if (cudaMemcpy2DAsync(d[i], w[i] * sstride, s[i], w[i] * sstride, w[i], count,
+    if (cudaMemcpy2DAsync(d[i], w[i] * dstride, s[i], w[i] * sstride, w[i], count,
                           cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return cuda_fail(cudaGetLastError(), "tile-scaled copy");
   return GOOM_OK;
@@ -100,22 +101,26 @@ int lmme_ts_call(TsIn a, TsIn b, int kind, float2* C, int64_t strideC, TsOut T, 
 size_t chain_ts_workspace_bytes(int64_t T, int d, int block, bool leaves_given_ts) {
   const int64_t s = block < T ? block : T;
   const int64_t nb = (T + s - 1) / s;
-  return (leaves_given_ts ? 0 : ts_bytes(T, d)) + ts_bytes(T, d) + ts_bytes(nb + 1, d) +
+  return (leaves_given_ts ? 0 : ts_bytes(T, d)) + ts_bytes(T, d) + 2 * ts_bytes(nb + 1, d) +
          rup(sizeof(float2) * (size_t)d * d) +                       // identity (complex64)
          rup(sizeof(float4) * (size_t)T * (d / 32) * (d / 256)) +    // digest partials
          1024;
 }
 
 // A (tile-scaled leaves, T of them) -> out (complex64 prefixes) or digests (T float4);
-// carry_in / carry_out tile-scaled (may be null).
+// carry_in / carry_out tile-scaled (may be null). tree_carries: phase 2 as a Kogge-Stone
+// scan of the block totals (ceil(log2 nb) batched launches, ~nb log2 nb products) instead
+// of the reference's sequential fold (nb dependent single-product launches, each on 8 of
+// the 148 SMs at d = 512); a different but fixed combine tree, deterministic per (T, block).
 int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_in,
                   float2* out, float4* digests, TsBuf* carry_out, char* ws, size_t ws_bytes,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool tree_carries) {
   const int64_t s = block < T ? block : T;
   const int64_t nb = (T + s - 1) / s;
   Carve cv{ws};
   TsBuf L = cv.ts(T, d);
   TsBuf Cx = cv.ts(nb + 1, d);
+  TsBuf Cy = cv.ts(nb + 1, d);  // Kogge-Stone ping-pong buffer
   float2* ident = cv.take<float2>((size_t)d * d);
   float4* parts = cv.take<float4>((size_t)T * (d / 32) * (d / 256));
   if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "tile-scaled chain workspace too small");
@@ -140,14 +145,44 @@ int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carr
                           cnt, d, st));
   }
   // phase 2: Cx[k+1] = L[last of block k] (x) Cx[k]
-  for (int64_t kb = 0; kb < nb; ++kb) {
-    const int64_t last = kb * s + s - 1 < T ? kb * s + s - 1 : T - 1;
-    if (kb == 0 && !carry_in) {
-      GOOM_TRY(copy_ts(Cx, 1, L, last, 1, 1, st));
-      continue;
+  if (tree_carries && nb > 1) {
+    // X[k] (block k's carry-out, stored at Cx[k+1]) starts as the block total L[last of k]
+    // (block 0: L[s-1] (x) Cx[0]); level j: X[k] <- X[k] (x) X[k - 2^j] for k >= 2^j
+    if (cudaMemsetAsync(Cy.G, 0, sizeof(uint32_t) * (size_t)(nb + 1) * nJ, st) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "tile-scaled G reset");
+    GOOM_TRY(copy_ts(Cx, 1, L, s - 1, nb - 1, s, st, 1));  // totals of blocks 0 .. nb-2
+    const int64_t lastT = T - 1;                          // block nb-1 may be partial
+    GOOM_TRY(copy_ts(Cx, nb, L, lastT, 1, 1, st));
+    if (carry_in) {
+      GOOM_TRY(lmme_ts_call(L.in(s - 1, 0), Cx.in(0, 0), kTsOutTs, nullptr, 0, Cy.out(1, 0),
+                            nullptr, 1, d, st));
+      GOOM_TRY(copy_ts(Cx, 1, Cy, 1, 1, 1, st));
     }
-    GOOM_TRY(lmme_ts_call(L.in(last, 0), Cx.in(kb, 0), kTsOutTs, nullptr, 0, Cx.out(kb + 1, 0),
-                          nullptr, 1, d, st));
+    TsBuf* X = &Cx;
+    TsBuf* Y = &Cy;
+    for (int64_t h = 1; h < nb; h <<= 1) {
+      // Y[1 + k] = X[1 + k] (x) X[1 + k - h] for k >= h; Y[1 + k] = X[1 + k] below
+      if (cudaMemsetAsync(Y->G + (1 + h) * nJ, 0, sizeof(uint32_t) * (size_t)(nb - h) * nJ, st) !=
+          cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "tile-scaled G reset");
+      GOOM_TRY(lmme_ts_call(X->in(1 + h, 1), X->in(1, 1), kTsOutTs, nullptr, 0, Y->out(1 + h, 1),
+                            nullptr, nb - h, d, st));
+      GOOM_TRY(copy_ts(*Y, 1, *X, 1, h, 1, st));
+      TsBuf* tmp = X;
+      X = Y;
+      Y = tmp;
+    }
+    if (X != &Cx) GOOM_TRY(copy_ts(Cx, 1, *X, 1, nb, 1, st));
+  } else {
+    for (int64_t kb = 0; kb < nb; ++kb) {
+      const int64_t last = kb * s + s - 1 < T ? kb * s + s - 1 : T - 1;
+      if (kb == 0 && !carry_in) {
+        GOOM_TRY(copy_ts(Cx, 1, L, last, 1, 1, st));
+        continue;
+      }
+      GOOM_TRY(lmme_ts_call(L.in(last, 0), Cx.in(kb, 0), kTsOutTs, nullptr, 0,
+                            Cx.out(kb + 1, 0), nullptr, 1, d, st));
+    }
   }
   // phase 3: P_t = L_t (x) Cx[t / s]
   if (out)
@@ -176,7 +211,7 @@ int chain_scan_c64_ts(const float2* A, float2* out, int64_t T, int d, int block,
   if (carry_in) GOOM_TRY(launch_goom_to_ts(carry_in, 0, Ci.out(0), 1, d, d, st));
   if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "chain workspace too small");
   return chain_scan_ts(At, T, d, block, carry_in ? &Ci : nullptr, out, nullptr, nullptr,
-                       cv.base + cv.off, ws_bytes - cv.off, st);
+                       cv.base + cv.off, ws_bytes - cv.off, st, /*tree_carries=*/false);
 }
 
 size_t chain_c64_ts_workspace_bytes(int64_t T, int d, int block) {
@@ -218,7 +253,8 @@ int goom_chain_ts(const float* U, const float* q, const uint32_t* G, int64_t T, 
   TsBuf co = ts_of(oU, oq, oG, d);
   return chain_scan_ts(A, T, d, block, cU ? &ci : nullptr, reinterpret_cast<float2*>(out),
                        reinterpret_cast<float4*>(digests4), oU ? &co : nullptr,
-                       reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream));
+                       reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream),
+                       /*tree_carries=*/true);
 }
 
 int goom_ts_from_c64(const goom_c64* X, int64_t batch, int rows, int cols, float* U, float* q,

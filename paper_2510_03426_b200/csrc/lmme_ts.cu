@@ -37,23 +37,47 @@ using namespace tc;
 constexpr int kRowsCta = 128;
 constexpr int kPairN = 256;
 constexpr int BK = 16;
-constexpr int kRawStages = 4;
-constexpr int kPlStages = 4;
 constexpr int kXformWarps = 16;
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 64 + (kXformWarps + kEpiWarps) * 32;  // 704
-constexpr int kRawA = kRowsCta * BK * 4;                       // 8 KB  [128 rows][16 k]
-constexpr int kRawB = BK * (kPairN / 2) * 4;                   // 8 KB  [16 k][128 cols]
-constexpr int kRaw = kRawA + kRawB;
-constexpr int kPlA = (kRowsCta / 8) * kGroupBytes;             // 16 KB: 16 groups (big | small)
-constexpr int kPl = 2 * kPlA;                                  // 32 KB
+// One ring of stages, operands landed by TMA directly in the UMMA layouts and turned into
+// (big, small) TF32 planes IN PLACE (big overwrites the raw value, small goes to its twin):
+//   [A big 8 KB | A small 8 KB]  K-major, 64B swizzle: 16 atoms of 8 rows x 64 B (SBO 512)
+//   [B big 8 KB | B small 8 KB]  MN-major, 128B swizzle: 4 column chunks of 32 (LBO 2 KB) x
+//                                2 atoms of 8 k-rows x 128 B (SBO 1 KB)
+// so there is no separate raw ring and every transform LDS/STS is a contiguous 512 B per warp.
+constexpr int kHalf = 8192;
+constexpr int kStage = 4 * kHalf;                              // 32 KB
+constexpr int kOffAs = kHalf, kOffBb = 2 * kHalf, kOffBs = 3 * kHalf;
 constexpr int kOutStage = 4096;                                // 32 rows x 128 B
-constexpr int kOutBytes = kEpiWarps * 2 * kOutStage;           // 32 KB
-constexpr int kPlOff = kRawStages * kRaw;                      // 64 KB
-constexpr int kOutOff = kPlOff + kPlStages * kPl;              // 192 KB
-constexpr int kBarOff = kOutOff + kOutBytes;                   // 224 KB
-constexpr int kSmem = kBarOff + 512 + 1024;
+constexpr int kMaxK = 1024;
+// shared memory: ring (S x 32 KB) | output staging (32 KB, not used by the digest epilogue) |
+// per-tile right-operand row factors (2 x kMaxK floats) | barriers
+template <int kOut, int S>
+struct Lay {
+  static constexpr int kStages = S;
+  static constexpr int kOutBytes = kOut == kTsOutDigest ? 0 : kEpiWarps * 2 * kOutStage;
+  static constexpr int kOutOff = S * kStage;
+  static constexpr int kFacOff = kOutOff + kOutBytes;
+  static constexpr int kBarOff = kFacOff + 2 * kMaxK * 4;
+  static constexpr int kSmem = kBarOff + 512 + 1024;
+  static_assert(kSmem <= 232448, "shared memory budget");
+};
 constexpr int kTmemCols = 2 * kPairN;
+
+// K-major 64B-swizzled operand: 8-row atoms 512 B apart
+__device__ __forceinline__ uint64_t kmaj_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | (1ull << 16) | ((uint64_t)(512 >> 4) << 32) |
+         (1ull << 46) | (4ull << 61);
+}
+// MN-major TF32 operand in the 128B_BASE32B layout (the only MN-major smem layout tcgen05
+// accepts for 32-bit types; CUTLASS sm100_common.inl): 128 B rows along N, 32-byte chunks
+// swizzled with the row index mod 4, 4-row atoms SBO = 512 B apart along K, 32-column chunks
+// LBO = 2 KB apart along N. TMA lands it with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t mnmaj_sw128_32b(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(2048 >> 4) << 16) |
+         ((uint64_t)(512 >> 4) << 32) | (1ull << 46) | (1ull << 61);
+}
 
 template <int N>
 struct Ring {
@@ -87,10 +111,7 @@ __device__ __forceinline__ void split_tf32(float v, uint32_t& big, uint32_t& sma
   big = tf32_round(v);
   small = __float_as_uint(v - __uint_as_float(big));
 }
-__device__ __forceinline__ void split_tf32_rn(float v, uint32_t& big, uint32_t& small) {
-  big = tf32_round(v);
-  small = tf32_round(v - __uint_as_float(big));
-}
+
 
 struct PairGrid {
   int nct, nrt;
@@ -104,19 +125,20 @@ struct PairGrid {
   }
 };
 
-template <int kOut>
+template <int kOut, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
                    float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug) {
+  using Y = Lay<kOut, S>;
+  constexpr int kStages = S, kOutOff = Y::kOutOff;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
-  uint64_t* raw_full = bars;                        // [R] local, TMA tx
-  uint64_t* raw_free = raw_full + kRawStages;       // [R] local, 16 transform warps
-  uint64_t* pl_ready = raw_free + kRawStages;       // [P] leader, 32 transform warps
-  uint64_t* pl_free = pl_ready + kPlStages;         // [P] local, MMA commit (multicast)
-  uint64_t* acc_full = pl_free + kPlStages;         // [2] local, MMA commit (multicast)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Y::kBarOff);
+  uint64_t* full = bars;                            // [S] local, TMA tx
+  uint64_t* ready = full + kStages;                 // [S] leader, 32 transform warps
+  uint64_t* freed = ready + kStages;                // [S] local, MMA commit (multicast)
+  uint64_t* acc_full = freed + kStages;             // [2] local, MMA commit (multicast)
   uint64_t* acc_empty = acc_full + 2;               // [2] leader, 8 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -128,13 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nJk = k / 256, nJm = m / 256;
 
   if (tid == 0) {
-    for (int s = 0; s < kRawStages; ++s) {
-      mbar_init(smem_u32(&raw_full[s]), 1);
-      mbar_init(smem_u32(&raw_free[s]), kXformWarps);
-    }
-    for (int s = 0; s < kPlStages; ++s) {
-      mbar_init(smem_u32(&pl_ready[s]), 2 * kXformWarps);
-      mbar_init(smem_u32(&pl_free[s]), 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&ready[s]), 2 * kXformWarps);
+      mbar_init(smem_u32(&freed[s]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
@@ -158,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------ TMA loader ------------------------------
     if (lane == 0) {
-      Ring<kRawStages> rr;
+      Ring<kStages> rr;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
         int64_t b;
         int prow0, pcol0;
@@ -168,12 +187,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ma = A.sU == 0 ? 0 : (int)(b / A.div);
         const int mb = B.sU == 0 ? 0 : (int)(b / B.div);
         for (int kb = 0; kb < nk; ++kb, rr.next()) {
-          mbar_wait(smem_u32(&raw_free[rr.s]), rr.ph ^ 1u);
-          const uint32_t bar = smem_u32(&raw_full[rr.s]);
-          mbar_expect_tx(bar, kRaw);
-          const uint32_t dst = base + rr.s * kRaw;
-          tma_load_3d(dst, &mapA, kb * BK, row0, ma, bar);           // [128 rows][16 k]
-          tma_load_3d(dst + kRawA, &mapB, col0, kb * BK, mb, bar);   // [16 k][128 cols]
+          mbar_wait(smem_u32(&freed[rr.s]), rr.ph ^ 1u);
+          const uint32_t bar = smem_u32(&full[rr.s]);
+          mbar_expect_tx(bar, 2 * kHalf);
+          const uint32_t dst = base + rr.s * kStage;
+          tma_load_3d(dst, &mapA, kb * BK, row0, ma, bar);                      // A big
+          tma_load_4d(dst + kOffBb, &mapB, 0, kb * BK, col0 / 32, mb, bar);     // B big
         }
       }
     }
@@ -181,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------ MMA issuer (leader) ------------------------------
     if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN);
-      Ring<kPlStages> pr;
+      constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN) | (1u << 16);  // B MN-major
+      Ring<kStages> pr;
       int lt = 0;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
         const int buf = lt & 1;
@@ -190,29 +209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * kPairN);
         for (int kb = 0; kb < nk; ++kb, pr.next()) {
-          mbar_wait(smem_u32(&pl_ready[pr.s]), pr.ph);
+          mbar_wait(smem_u32(&ready[pr.s]), pr.ph);
           tc_fence_after();
           if ((debug & 15) != 2) {
-            const uint32_t pb = base + kPlOff + pr.s * kPl;
-            const uint64_t dAb = sw64_desc(pb), dAs = sw64_desc(pb + 512);
-            const uint64_t dBb = sw64_desc(pb + kPlA), dBs = sw64_desc(pb + kPlA + 512);
+            const uint32_t sb = base + pr.s * kStage;
+            const uint64_t dAb = kmaj_sw64(sb), dAs = kmaj_sw64(sb + kOffAs);
+            const uint64_t dBb = mnmaj_sw128_32b(sb + kOffBb), dBs = mnmaj_sw128_32b(sb + kOffBs);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t adv = (uint64_t)(kk * 32) >> 4;
-              if (debug & 64) {  // plain TF32 (precision probe only)
-                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, (kb | kk) != 0);
-              } else if (debug & 32) {
-                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, (kb | kk) != 0);
-                mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, 1);
-                mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
-              } else {
-                mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, (kb | kk) != 0);
-                mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
-                mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, 1);
-              }
+              const uint64_t aadv = (uint64_t)(kk * 32) >> 4;     // 8 TF32 along the 64 B row
+              const uint64_t badv = (uint64_t)(kk * 1024) >> 4;   // 8 k rows further
+              mma_tf32_pair(acc, dAs + aadv, dBb + badv, idesc, (kb | kk) != 0);
+              mma_tf32_pair(acc, dAb + aadv, dBs + badv, idesc, 1);
+              mma_tf32_pair(acc, dAb + aadv, dBb + badv, idesc, 1);
             }
           }
-          mma_commit_pair(smem_u32(&pl_free[pr.s]));
+          mma_commit_pair(smem_u32(&freed[pr.s]));
         }
         mma_commit_pair(smem_u32(&acc_full[buf]));
       }
@@ -220,83 +232,86 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp < 2 + kXformWarps) {
     // ------------------------------ transform ------------------------------
-    // A: warp xw owns group xw (rows 8xw..8xw+7); lane -> row ar = lane/4, k-quad akq = lane%4
-    // (one LDS.128 of a contiguous 512 B group, one STS.128 per plane: conflict-free).
-    // B: warp xw owns columns 32 (xw%4) + lane and k-quad xw/4 (four LDS.32 of 128 B rows,
-    // one STS.128 per plane into group column/8: conflict-free); its 4 k rows are uniform
-    // across the warp, so are their factors.
+    // Thread u = 32 xw + lane owns byte 16u of each operand half: A row u/4 (4 k values),
+    // B k-row (u % 128) / 8 of column chunk u / 128 (4 n values). It reads its 16 B of the
+    // raw fp32, multiplies by the factor, rounds big to TF32 in place and writes small to
+    // the twin plane: contiguous 512 B per warp, the swizzle is irrelevant in place.
     const int xw = warp - 2;
-    const int ar = lane >> 2, akq = lane & 3;
-    const int bkq = xw >> 2, bn = (xw & 3) * 32 + lane;
-    const uint32_t pl_ready0 = smem_u32(&pl_ready[0]);
-    Ring<kRawStages> rr;
-    Ring<kPlStages> pr;
-    for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
+    const int u = xw * 32 + lane;
+    const int arow_cta = u >> 2;
+    const int bkrow = (u & 127) >> 3;
+    const uint32_t ready0 = smem_u32(&ready[0]);
+    float* fac = reinterpret_cast<float*>(smem + Y::kFacOff);  // [2][kMaxK]
+    Ring<kStages> rr;
+    // per-tile factors, fetched one tile ahead: this thread's B row scales for k = u and
+    // u + 512 (the tile's table is built from them), its A row's q[row][J]
+    float qbn[2], qan[4], gBn = 0.0f;
+    auto fetch = [&](int64_t tile) {
       int64_t b;
       int prow0, pcol0;
-      grid.at(t, b, prow0, pcol0);
-      const int arow = prow0 + (int)rank * kRowsCta + xw * 8 + ar;   // A row of this lane
+      grid.at(tile, b, prow0, pcol0);
+      const int arow = prow0 + (int)rank * kRowsCta + arow_cta;
       const float* qa = A.q + (b / A.div) * A.sq + (int64_t)arow * nJk;
-      float rho = kNegInf;
-      for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
+#pragma unroll
+      for (int J = 0; J < 4; ++J) qan[J] = J < nJk ? qa[J] : kNegInf;
       const int JB = pcol0 / 256;
       const float* qb = B.q + (b / B.div) * B.sq + JB;
-      const float gB = decode_g(B.G[(b / B.div) * B.sG + JB]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) qbn[h] = u + 512 * h < k ? qb[(int64_t)(u + 512 * h) * nJm] : 0.0f;
+      gBn = decode_g(B.G[(b / B.div) * B.sG + JB]);
+    };
+    if (cluster < grid.tiles) fetch(cluster);
+    int tpar = 0;
+    for (int64_t t = cluster; t < grid.tiles; t += nclusters, tpar ^= 1) {
+      float* ft = fac + tpar * kMaxK;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (u + 512 * h < k) ft[u + 512 * h] = scale_factor(qbn[h], gBn);
+      float qac[4];
+#pragma unroll
+      for (int J = 0; J < 4; ++J) qac[J] = qan[J];
+      const float rho = fmaxf(fmaxf(qac[0], qac[1]), fmaxf(qac[2], qac[3]));
+      asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");  // table complete
+      if (t + nclusters < grid.tiles) fetch(t + nclusters);
       float fa = 0.0f;
       int curJ = -1;
-      float qn[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) qn[j] = qb[(int64_t)(4 * bkq + j) * nJm];
-      for (int kb = 0; kb < nk; ++kb, rr.next(), pr.next()) {
+      for (int kb = 0; kb < nk; ++kb, rr.next()) {
         const int J = (kb * BK) >> 8;
         if (J != curJ) {
-          fa = scale_factor(qa[J], rho);
+          const float qj = J == 0 ? qac[0] : J == 1 ? qac[1] : J == 2 ? qac[2] : qac[3];
+          fa = scale_factor(qj, rho);
           curJ = J;
         }
-        float fb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) fb[j] = scale_factor(qn[j], gB);
-        if (kb + 1 < nk) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) qn[j] = qb[(int64_t)((kb + 1) * BK + 4 * bkq + j) * nJm];
-        }
-        mbar_wait(smem_u32(&raw_full[rr.s]), rr.ph);
-        const uint32_t rb = base + rr.s * kRaw;
-        const float4 va = ld_shared_v4(rb + xw * 512 + lane * 16);
-        float vb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) vb[j] = lds32(rb + kRawA + (4 * bkq + j) * 512 + bn * 4);
-        uint32_t ha[4], la[4], hb[4], lb[4];
-        if (debug & 16) {
-          split_tf32_rn(va.x * fa, ha[0], la[0]);
-          split_tf32_rn(va.y * fa, ha[1], la[1]);
-          split_tf32_rn(va.z * fa, ha[2], la[2]);
-          split_tf32_rn(va.w * fa, ha[3], la[3]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) split_tf32_rn(vb[j] * fb[j], hb[j], lb[j]);
-        } else {
-          split_tf32(va.x * fa, ha[0], la[0]);
-          split_tf32(va.y * fa, ha[1], la[1]);
-          split_tf32(va.z * fa, ha[2], la[2]);
-          split_tf32(va.w * fa, ha[3], la[3]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) split_tf32(vb[j] * fb[j], hb[j], lb[j]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&raw_free[rr.s]));
-        mbar_wait(smem_u32(&pl_free[pr.s]), pr.ph ^ 1u);
-        const uint32_t pb = base + kPlOff + pr.s * kPl;
-        if ((debug & 15) != 1) {
-          const uint32_t ga = pb + xw * kGroupBytes + sw64_off(ar, akq);
-          st_shared_v4(ga, ha[0], ha[1], ha[2], ha[3]);
-          st_shared_v4(ga + 512, la[0], la[1], la[2], la[3]);
-          const uint32_t gb = pb + kPlA + (bn >> 3) * kGroupBytes + sw64_off(bn & 7, bkq);
-          st_shared_v4(gb, hb[0], hb[1], hb[2], hb[3]);
-          st_shared_v4(gb + 512, lb[0], lb[1], lb[2], lb[3]);
+        float fb = ft[kb * BK + bkrow];
+        if (debug & 256) fb = 1.0f, fa = 1.0f;  // layout probe: no factors
+        mbar_wait(smem_u32(&full[rr.s]), rr.ph);
+        const uint32_t sb = base + rr.s * kStage + u * 16;
+        const float4 va = ld_shared_v4(sb);
+        const float4 vb = ld_shared_v4(sb + kOffBb);
+        if (debug & 128) {  // layout probe: all-ones operands
+          const uint32_t one = __float_as_uint(1.0f);
+          st_shared_v4(sb, one, one, one, one);
+          st_shared_v4(sb + kOffAs, 0u, 0u, 0u, 0u);
+          st_shared_v4(sb + kOffBb, one, one, one, one);
+          st_shared_v4(sb + kOffBs, 0u, 0u, 0u, 0u);
+        } else if ((debug & 15) != 1) {
+          uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+          split_tf32(va.x * fa, h0, l0);
+          split_tf32(va.y * fa, h1, l1);
+          split_tf32(va.z * fa, h2, l2);
+          split_tf32(va.w * fa, h3, l3);
+          st_shared_v4(sb, h0, h1, h2, h3);
+          st_shared_v4(sb + kOffAs, l0, l1, l2, l3);
+          split_tf32(vb.x * fb, h0, l0);
+          split_tf32(vb.y * fb, h1, l1);
+          split_tf32(vb.z * fb, h2, l2);
+          split_tf32(vb.w * fb, h3, l3);
+          st_shared_v4(sb + kOffBb, h0, h1, h2, h3);
+          st_shared_v4(sb + kOffBs, l0, l1, l2, l3);
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive_rank(pl_ready0 + pr.s * 8, 0);
+        if (lane == 0) mbar_arrive_rank(ready0 + rr.s * 8, 0);
       }
     }
   } else {
@@ -443,13 +458,13 @@ int ts_debug() {
   return v;
 }
 
-template <int kOut>
+template <int kOut, int S>
 int max_clusters() {
   static int v = [] {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmem;
+    cfg.dynamicSmemBytes = Lay<kOut, S>::kSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -458,7 +473,8 @@ int max_clusters() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, lmme_ts_kernel<kOut>, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, lmme_ts_kernel<kOut, S>, &cfg) != cudaSuccess ||
+        n < 1) {
       cudaGetLastError();
       n = num_sms() / 2;
     }
@@ -467,13 +483,14 @@ int max_clusters() {
   return v;
 }
 
-template <int kOut>
-int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
-           const CUtensorMap& mapOut, cudaStream_t s) {
+template <int kOut, int S>
+int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
+               const CUtensorMap& mapOut, cudaStream_t s) {
+  constexpr int kSmem = Lay<kOut, S>::kSmem;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmem) != cudaSuccess)
+    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut, S>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
       return cuda_fail(cudaGetLastError(), "lmme_ts smem attribute");
     attr_set = true;
   }
@@ -481,7 +498,7 @@ int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
   pg.nct = p.m / kPairN;
   pg.nrt = p.n / 256;
   pg.tiles = p.batch * pg.nct * pg.nrt;
-  const int64_t mc = max_clusters<kOut>();
+  const int64_t mc = max_clusters<kOut, S>();
   const int64_t clusters = pg.tiles < mc ? pg.tiles : mc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
@@ -495,10 +512,31 @@ int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut>, mapA, mapB, mapOut, p.A, p.B, p.T, p.parts, pg,
+  cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S>, mapA, mapB, mapOut, p.A, p.B, p.T, p.parts, pg,
                      p.n, p.k, p.m, ts_debug());
   GOOM_CHECK_LAUNCH("lmme_ts_kernel");
   return GOOM_OK;
+}
+
+// ring depths (raw, plane): GOOM_TS_STAGES=<index> picks a probe configuration
+int stage_cfg() {
+  static int v = [] {
+    const char* e = getenv("GOOM_TS_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int kOut>
+int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
+           const CUtensorMap& mapOut, cudaStream_t s) {
+  if constexpr (kOut == kTsOutDigest) {
+    if (stage_cfg() == 1) return launch_cfg<kOut, 5>(p, mapA, mapB, mapOut, s);
+    return launch_cfg<kOut, 6>(p, mapA, mapB, mapOut, s);
+  } else {
+    if (stage_cfg() == 1) return launch_cfg<kOut, 4>(p, mapA, mapB, mapOut, s);
+    return launch_cfg<kOut, 5>(p, mapA, mapB, mapOut, s);
+  }
 }
 
 inline int64_t mats(int64_t stride, int64_t div, int64_t batch) {
@@ -508,7 +546,8 @@ inline int64_t mats(int64_t stride, int64_t div, int64_t batch) {
 }  // namespace
 
 bool lmme_ts_eligible(int n, int k, int m) {
-  return n > 0 && k > 0 && m > 0 && n % 256 == 0 && k % 256 == 0 && m % 256 == 0;
+  // k <= 1024: the transform keeps a tile's per-K-block factors in two registers per lane
+  return n > 0 && k > 0 && m > 0 && n % 256 == 0 && k % 256 == 0 && m % 256 == 0 && k <= 1024;
 }
 
 int lmme_ts(const TsProblem& p, cudaStream_t s) {
@@ -517,21 +556,24 @@ int lmme_ts(const TsProblem& p, cudaStream_t s) {
   const uintptr_t al = reinterpret_cast<uintptr_t>(p.A.U) | reinterpret_cast<uintptr_t>(p.B.U);
   if ((al & 15) || ((p.A.sU | p.B.sU) & 3)) return fail(GOOM_EINVAL, "lmme_ts: operand alignment");
   alignas(64) CUtensorMap mapA, mapB, mapOut;
-  {  // A fp32 (k, n, matrix), box 16 k x 128 rows
+  {  // A fp32 (k, n, matrix), box 16 k x 128 rows, 64B swizzle: the UMMA K-major SW64 layout
     cuuint64_t dims[3] = {(cuuint64_t)p.k, (cuuint64_t)p.n,
                           (cuuint64_t)mats(p.A.sU, p.A.div, p.batch)};
     cuuint64_t strides[2] = {(cuuint64_t)p.k * 4,
                              (cuuint64_t)(p.A.sU ? p.A.sU : (int64_t)p.n * p.k) * 4};
     cuuint32_t box[3] = {BK, kRowsCta, 1};
-    GOOM_TRY(encode_raw(&mapA, p.A.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box));
+    GOOM_TRY(encode_raw(&mapA, p.A.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box,
+                        CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  {  // B fp32 (m, k, matrix), box 128 cols x 16 k
-    cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.k,
+  {  // B fp32 (32 cols, k, m/32 chunks, matrix), box 32 x 16 k x 4 x 1, 128B/32B-atom
+     // swizzle: [chunk][k][32 cols] = the UMMA MN-major 128B_BASE32B layout (chunks 2 KB apart)
+    cuuint64_t dims[4] = {32, (cuuint64_t)p.k, (cuuint64_t)(p.m / 32),
                           (cuuint64_t)mats(p.B.sU, p.B.div, p.batch)};
-    cuuint64_t strides[2] = {(cuuint64_t)p.m * 4,
+    cuuint64_t strides[3] = {(cuuint64_t)p.m * 4, 128,
                              (cuuint64_t)(p.B.sU ? p.B.sU : (int64_t)p.k * p.m) * 4};
-    cuuint32_t box[3] = {kPairN / 2, BK, 1};
-    GOOM_TRY(encode_raw(&mapB, p.B.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, strides, box));
+    cuuint32_t box[4] = {32, BK, kPairN / 2 / 32, 1};
+    GOOM_TRY(encode_raw(&mapB, p.B.U, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dims, strides, box,
+                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   }
   if (p.kind == kTsOutGoom) {
     if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.strideC & 1))
