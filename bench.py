@@ -43,8 +43,8 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--T", type=int, default=1 << 20)
     p.add_argument("--d", type=int, default=512)
-    p.add_argument("--window", type=int, default=8192)
-    p.add_argument("--block", type=int, default=64)
+    p.add_argument("--window", type=int, default=32768)
+    p.add_argument("--block", type=int, default=128)
     p.add_argument("--seed", type=int, default=2510)
     p.add_argument("--cpu-sample", type=int, default=128, help="leaves in the CPU baseline sample")
     p.add_argument("--e2e-T", type=int, default=2048)
@@ -136,6 +136,30 @@ def measured_peaks():
         return pk, "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def cublas_tf32_tflops(torch, n=8192, reps=10):
+    """In-run cuBLAS TF32 GEMM (fp32 matmul with TF32 tensor cores), best of `reps`: the
+    measured denominator for a kind::tf32 kernel (the driver's peaks are bf16)."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(2):
+            a @ b
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            a @ b
+            e.record()
+            torch.cuda.synchronize()
+            best = min(best, s.elapsed_time(e))
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
 
 
 def reference_arm(args):
@@ -261,6 +285,7 @@ def main():
     lmme_ms = s.elapsed_time(e) / reps
     tflops = 2.0 * d ** 3 * nb / (lmme_ms / 1e3) / 1e12
     peak_3xtf32 = pk["bf16_tflops"] / 2 / 3
+    tf32_cublas = cublas_tf32_tflops(torch)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tf):
@@ -319,7 +344,9 @@ def main():
                          "kernel": f"{kname}, phase-3 shape batch={nb} (carry per {args.block}), "
                                    f"{lmme_ms:.2f} ms/launch; algorithmic 2*d^3 flop/product",
                          "peak_source": f"{src} bf16 {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 "
-                                        "(3xTF32 split)"},
+                                        "(3xTF32 split)",
+                         "tf32_cublas_tflops_in_run": tf32_cublas,
+                         "frac_vs_cublas_tf32_div3": tflops / (tf32_cublas / 3)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * d * d * 8,
                     "d2h_bytes_per_step": ne * 16,
                     "workload": f"T={Te} host (pinned) leaves via harness.run_chain"},

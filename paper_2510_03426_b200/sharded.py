@@ -48,21 +48,40 @@ def exclusive_carry(local_total: torch.Tensor, lmme: Callable, group=None) -> Op
     return fold_carry([torch.view_as_complex(g) for g in gathered], rank, lmme)
 
 
+def shard_total(n: int, d: int, seed: int, t0: int, window: int, block: int) -> torch.Tensor:
+    """A_{t0+n-1} ... A_{t0} of this rank's shard, window by window (complex64 d x d).
+
+    d % 256 == 0: the tile-scaled engine's phases 1 + 2 only (ops.chain_ts with no prefix
+    output: its carry-out is the window total, phase 3 is skipped); otherwise a pairwise
+    tree of batched complex64 LMMEs (harness.chain_total)."""
+    from . import ops
+    from .harness import chain_total, random_chain
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    total = None
+    for w0 in range(0, n, window):
+        m = min(window, n - w0)
+        if ops.ts_eligible(d):
+            _, _, c = ops.chain_ts(ops.ts_random_normal(m, d, seed, t0 + w0, dev), block, None,
+                                   out=False, digests=False, carry_out=True)
+            wt = ops.ts_to_goom(c)[0]
+        else:
+            wt = chain_total(random_chain(m, d, seed, t0 + w0))
+        total = wt if total is None else torch.ops.goom.lmme(wt[None], total[None])[0]
+    return total
+
+
 def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
                       group=None, snapshot_every: int = 0):
     """Rank-local part of a time-sharded chain run; returns (t0, ChainRun)."""
-    from .harness import chain_total, random_chain, run_chain
+    from .harness import run_chain
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     t0, n = shard_range(T, rank, world)
     carry = None
     if world > 1:
-        total = None
-        for w0 in range(0, n, window):
-            m = min(window, n - w0)
-            wt = chain_total(random_chain(m, d, seed, t0 + w0))
-            total = wt if total is None else torch.ops.goom.lmme(wt, total)
+        total = shard_total(n, d, seed, t0, window, block)
         carry = exclusive_carry(total, torch.ops.goom.lmme, group)
     return t0, run_chain(n, d, seed, window, block, t0=t0, carry=carry,
                          snapshot_every=snapshot_every)

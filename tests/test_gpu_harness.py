@@ -73,17 +73,18 @@ def test_growth_rate_matches_lyapunov_theory(h):
     assert abs(rate - expected) < 0.02 * expected
 
 
-def test_chain_total_and_sharded_fold_on_one_gpu(h):
+@pytest.mark.parametrize("d", [128, 256])
+def test_chain_total_and_sharded_fold_on_one_gpu(h, d):
     """The sharded algorithm (totals -> exclusive carries -> local scans), run shard by
-    shard on one GPU, equals the single-GPU chain."""
+    shard on one GPU, equals the single-GPU chain (d = 256: tile-scaled totals and scans)."""
     from paper_2510_03426_b200 import sharded
 
-    T, d, world = 257, 128, 3
+    T, world = 257, 3
     full = h.run_chain(T, d, seed=9, window=128, block=16)
     totals, runs = [], []
     for r in range(world):
         t0, n = sharded.shard_range(T, r, world)
-        totals.append(h.chain_total(h.random_chain(n, d, 9, t0)))
+        totals.append(sharded.shard_total(n, d, 9, t0, 64, 16))
     for r in range(world):
         t0, n = sharded.shard_range(T, r, world)
         carry = sharded.fold_carry(totals, r, torch.ops.goom.lmme)
