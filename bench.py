@@ -288,9 +288,10 @@ def main():
     tf32_cublas = cublas_tf32_tflops(torch)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and ops.ts_eligible(d) and d == 512:
         with open(tf) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            per = json.load(f).get("dram_bytes_per_product")
+        traffic = per * nb if per else None  # ncu capture scaled to this launch's batch
     del L, C
     torch.cuda.empty_cache()
 
