@@ -58,6 +58,7 @@ struct Smem {
   Rt* scal;       // 2d
   double* vec;    // 2d
   double* red;    // 2 * kWarps
+  double* part;   // 4 * kMaxD: per-(row chunk, column) partials of the column-parallel kernels
   int* ints;      // 8
 };
 
@@ -65,7 +66,8 @@ template <class Rt>
 inline size_t smem_bytes(int d) {
   size_t dd = (size_t)d * d;
   return 2 * dd * sizeof(Cx<Rt>) + 2 * dd * sizeof(double) + 2 * d * sizeof(Rt) +
-         2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 8 * sizeof(int) + 64;
+         2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 4 * kMaxD * sizeof(double) +
+         8 * sizeof(int) + 64;
 }
 
 template <class Rt>
@@ -80,7 +82,8 @@ __device__ Smem<Rt> carve(char* base, int d) {
   s.tr = s.tl + dd;
   s.vec = s.W + dd;
   s.red = s.vec + 2 * d;
-  s.scal = reinterpret_cast<Rt*>(s.red + 2 * kWarps);
+  s.part = s.red + 2 * kWarps;
+  s.scal = reinterpret_cast<Rt*>(s.part + 4 * kMaxD);
   s.ints = reinterpret_cast<int*>(s.scal + 2 * d);
   return s;
 }
@@ -158,23 +161,35 @@ __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<R
 }
 
 // Column log-norms nu_j (FP64) into sm.vec[0..d); returns true if a column is all zero.
+// Thread (column cc = tid % 64, row chunk ch = tid / 64) covers rows ch, ch+4, ...: the
+// per-column max and sum of squares are 4-way partials combined through sm.part.
 template <class Rt>
 __device__ bool unit_columns(const Cx<Rt>* X, int d, const Smem<Rt>& sm) {
-  const int tid = threadIdx.x;
+  static_assert(kThreads == 4 * kMaxD, "column-parallel mapping: 4 row chunks x 64 columns");
+  const int tid = threadIdx.x, cc = tid & (kMaxD - 1), ch = tid / kMaxD;
   if (tid == 0) sm.ints[0] = 0;
+  double m = -INFINITY;
+  if (cc < d)
+    for (int r = ch; r < d; r += 4) m = fmax(m, (double)X[r * d + cc].x);
+  sm.part[ch * kMaxD + cc] = m;
   __syncthreads();
-  for (int j = tid; j < d; j += kThreads) {
-    double m = -INFINITY;
-    for (int r = 0; r < d; ++r) m = fmax(m, (double)X[r * d + j].x);
-    if (m == -INFINITY) {
-      sm.ints[0] = 1;
-      sm.vec[j] = -INFINITY;
-      continue;
-    }
-    double dm = (double)m, acc = 0.0;
-    for (int r = 0; r < d; ++r) acc += exp(2.0 * ((double)X[r * d + j].x - dm));
-    sm.vec[j] = dm + 0.5 * log(acc);
+  double cm = -INFINITY;
+  if (cc < d) {
+    cm = fmax(fmax(sm.part[cc], sm.part[kMaxD + cc]),
+              fmax(sm.part[2 * kMaxD + cc], sm.part[3 * kMaxD + cc]));
+    if (cm == -INFINITY && ch == 0) sm.ints[0] = 1;
   }
+  double acc = 0.0;
+  if (cc < d && cm != -INFINITY)
+    for (int r = ch; r < d; r += 4) acc += exp(2.0 * ((double)X[r * d + cc].x - cm));
+  __syncthreads();  // every thread has read its column max before the partials are reused
+  sm.part[ch * kMaxD + cc] = acc;
+  __syncthreads();
+  if (cc < d && ch == 0)
+    sm.vec[cc] = cm == -INFINITY
+                     ? -INFINITY
+                     : cm + 0.5 * log(((sm.part[cc] + sm.part[kMaxD + cc]) +
+                                       sm.part[2 * kMaxD + cc]) + sm.part[3 * kMaxD + cc]);
   __syncthreads();
   bool zero = sm.ints[0] != 0;
   if (!zero) {
@@ -264,6 +279,7 @@ __device__ bool policy_select(const Cx<Rt>* X, int d, const Policy& pol, const S
 template <class Rt>
 __device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;  // column, row chunk (4 x 64 threads)
   double* tau = sm.vec;      // [0, d)
   double* diag = sm.vec + d;  // [d, 2d)
   for (int j = 0; j < d; ++j) {
@@ -290,30 +306,43 @@ __device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm) {
     const double scale = sm.red[0];
     const double tj = tau[j];
     if (tj != 0.0) {
-      for (int r = j + 1 + tid; r < d; r += kThreads) sm.R[r * d + j] *= scale;  // v_r
+      if (tid > j && tid < d) sm.R[tid * d + j] *= scale;  // v_r (v_j = 1 implicit)
       __syncthreads();
-      for (int c = j + 1 + w; c < d; c += kWarps) {
-        double s = lane == 0 ? sm.R[j * d + c] : 0.0;
-        for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.R[r * d + c], s);
-        s = warp_sum_d(s) * tj;
-        if (lane == 0) sm.R[j * d + c] -= s;
-        for (int r = j + 1 + lane; r < d; r += 32) sm.R[r * d + c] -= s * sm.R[r * d + j];
+      // w_c = tau (R_jc + sum_{r>j} v_r R_rc) for c > j: thread (cc, ch) sums rows j+1+ch, +4..
+      double p = 0.0;
+      if (cc > j && cc < d) {
+        if (ch == 0) p = sm.R[j * d + cc];
+        for (int r = j + 1 + ch; r < d; r += 4) p = fma(sm.R[r * d + j], sm.R[r * d + cc], p);
+      }
+      sm.part[ch * kMaxD + cc] = p;
+      __syncthreads();
+      if (cc > j && cc < d) {
+        const double wc = (((sm.part[cc] + sm.part[kMaxD + cc]) + sm.part[2 * kMaxD + cc]) +
+                           sm.part[3 * kMaxD + cc]) * tj;
+        if (ch == 0) sm.R[j * d + cc] -= wc;
+        for (int r = j + 1 + ch; r < d; r += 4) sm.R[r * d + cc] -= wc * sm.R[r * d + j];
       }
     }
     __syncthreads();
   }
-  // Q = H_0 ... H_{d-1} I, accumulated backwards (LAPACK dorg2r order)
+  // Q = H_0 ... H_{d-1} I, accumulated backwards (LAPACK dorg2r order), same mapping
   for (int e = tid; e < d * d; e += kThreads) sm.W[e] = (e / d == e % d) ? 1.0 : 0.0;
   __syncthreads();
   for (int j = d - 1; j >= 0; --j) {
     const double tj = tau[j];
     if (tj == 0.0) continue;
-    for (int c = w; c < d; c += kWarps) {
-      double s = lane == 0 ? sm.W[j * d + c] : 0.0;
-      for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.W[r * d + c], s);
-      s = warp_sum_d(s) * tj;
-      if (lane == 0) sm.W[j * d + c] -= s;
-      for (int r = j + 1 + lane; r < d; r += 32) sm.W[r * d + c] -= s * sm.R[r * d + j];
+    double p = 0.0;
+    if (cc < d) {
+      if (ch == 0) p = sm.W[j * d + cc];
+      for (int r = j + 1 + ch; r < d; r += 4) p = fma(sm.R[r * d + j], sm.W[r * d + cc], p);
+    }
+    sm.part[ch * kMaxD + cc] = p;
+    __syncthreads();
+    if (cc < d) {
+      const double wc = (((sm.part[cc] + sm.part[kMaxD + cc]) + sm.part[2 * kMaxD + cc]) +
+                         sm.part[3 * kMaxD + cc]) * tj;
+      if (ch == 0) sm.W[j * d + cc] -= wc;
+      for (int r = j + 1 + ch; r < d; r += 4) sm.W[r * d + cc] -= wc * sm.R[r * d + j];
     }
     __syncthreads();
   }
