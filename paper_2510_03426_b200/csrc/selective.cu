@@ -105,18 +105,27 @@ __device__ double block_max(double v, double* red) {
 template <class Rt>
 __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<Rt>* out, int d,
                            const Smem<Rt>& sm) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int i = w; i < d; i += kWarps) {
-    Rt m = Rt(-INFINITY);
-    for (int j = lane; j < d; j += 32) m = gmax(m, Lg[i * d + j].x);
-    m = warp_max_t(m);
-    if (lane == 0) sm.scal[i] = gmax(m, Rt(0));
-  }
-  for (int j = tid; j < d; j += kThreads) {
-    Rt m = Rt(-INFINITY);
-    for (int r = 0; r < d; ++r) m = gmax(m, Rs[r * d + j].x);
-    sm.scal[d + j] = gmax(m, Rt(0));
-  }
+  const int tid = threadIdx.x, cc = tid & (kMaxD - 1), ch = tid / kMaxD;
+  // clamped row maxima of Lg and column maxima of Rs: 4 row/column chunks per index
+  Rt mr = Rt(-INFINITY), mc = Rt(-INFINITY);
+  if (cc < d)
+    for (int t = ch; t < d; t += 4) {
+      mr = gmax(mr, Lg[cc * d + t].x);
+      mc = gmax(mc, Rs[t * d + cc].x);
+    }
+  sm.part[ch * kMaxD + cc] = (double)mr;
+  __syncthreads();
+  if (cc < d && ch == 0)
+    sm.scal[cc] = gmax(gmax(gmax((Rt)sm.part[cc], (Rt)sm.part[kMaxD + cc]),
+                            gmax((Rt)sm.part[2 * kMaxD + cc], (Rt)sm.part[3 * kMaxD + cc])),
+                       Rt(0));
+  __syncthreads();
+  sm.part[ch * kMaxD + cc] = (double)mc;
+  __syncthreads();
+  if (cc < d && ch == 0)
+    sm.scal[d + cc] = gmax(gmax(gmax((Rt)sm.part[cc], (Rt)sm.part[kMaxD + cc]),
+                                gmax((Rt)sm.part[2 * kMaxD + cc], (Rt)sm.part[3 * kMaxD + cc])),
+                           Rt(0));
   __syncthreads();
   for (int e = tid; e < d * d; e += kThreads) {
     int i = e / d, j = e % d;
@@ -202,10 +211,13 @@ __device__ bool unit_columns(const Cx<Rt>* X, int d, const Smem<Rt>& sm) {
   return zero;
 }
 
-// slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor
+// slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor.
+// Three barriers per pivot: pivot search (warp 0), row swap, trailing update with the
+// column-parallel mapping (column cc = tid % 64 > c, rows c+1+ch, +4, ...).
 template <class Rt>
 __device__ bool volume_deficient(int d, double log_floor, const Smem<Rt>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;
   for (int e = tid; e < d * d; e += kThreads) sm.W[e] = sm.R[e];
   __syncthreads();
   double logdet = 0.0;
@@ -223,28 +235,26 @@ __device__ bool volume_deficient(int d, double log_floor, const Smem<Rt>& sm) {
         int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
-      if (lane == 0) sm.ints[1] = bi;
+      if (lane == 0) {
+        sm.ints[1] = bi;
+        sm.red[1] = sm.W[bi * d + c];
+      }
     }
     __syncthreads();
     const int piv = sm.ints[1];
-    const double pv = sm.W[piv * d + c];
-    __syncthreads();  // every thread holds pv before the row swap overwrites it
+    const double pv = sm.red[1];
     if (pv == 0.0) return true;  // det_sign == 0
-    if (piv != c)
-      for (int j = tid; j < d; j += kThreads) {
-        double t = sm.W[c * d + j];
-        sm.W[c * d + j] = sm.W[piv * d + j];
-        sm.W[piv * d + j] = t;
-      }
-    __syncthreads();
+    if (piv != c && tid < d && tid >= c) {
+      const double t = sm.W[c * d + tid];
+      sm.W[c * d + tid] = sm.W[piv * d + tid];
+      sm.W[piv * d + tid] = t;
+    }
     logdet += log(fabs(pv));
-    const double inv = 1.0 / pv;
-    for (int r = c + 1 + tid; r < d; r += kThreads) sm.vec[d + r] = sm.W[r * d + c] * inv;
     __syncthreads();
-    const int n = d - c - 1;
-    for (int e = tid; e < n * n; e += kThreads) {
-      int r = c + 1 + e / n, j = c + 1 + e % n;
-      sm.W[r * d + j] -= sm.vec[d + r] * sm.W[c * d + j];
+    const double inv = 1.0 / pv;
+    if (cc > c && cc < d) {
+      const double u = sm.W[c * d + cc];
+      for (int r = c + 1 + ch; r < d; r += 4) sm.W[r * d + cc] -= (sm.W[r * d + c] * inv) * u;
     }
     __syncthreads();
   }
