@@ -38,6 +38,10 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
     """Scan leaves t0 .. t0+T-1 (generated, or the given `leaves` tensor) with an
     optional right carry; returns per-prefix digests, the final prefix, snapshots.
 
+    `leaves` may be complex64 GOOMs on the device, or real float32 matrices — on the
+    device, or in pinned host memory, in which case each window's host->device copy
+    runs on a copy stream overlapped with the previous window's scan (tile-scaled path).
+
     d % 256 == 0 runs on the tile-scaled engine (ops.chain_ts): leaves are generated
     (or imported) tile-scaled, prefixes are digested inside the phase-3 LMME epilogue
     and the carry between windows stays tile-scaled. Other d use the complex64 scan +
@@ -45,6 +49,8 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
     if ops.ts_eligible(d):
         return _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves)
     dev = torch.device("cuda", torch.cuda.current_device())
+    if leaves is not None and leaves.dtype == torch.float32:  # real matrices -> GOOMs
+        leaves = torch.ops.goom.from_real(leaves.to(dev), float("-inf"), False)
     digests = torch.empty((T, 4), dtype=torch.float32, device=dev)
     snaps: Dict[int, torch.Tensor] = {}
     for w0 in range(0, T, window):
@@ -61,21 +67,62 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
     return ChainRun(digests, carry, snaps)
 
 
+_ORDERED_ZERO = -2147483648  # float_to_ordered(0.0f) = 0x80000000 as int32
+
+
+def real_leaves_ts(x: torch.Tensor) -> "ops.TsMats":
+    """Real float32 leaves (device) as tile-scaled matrices without a copy: U = x, q = 0,
+    G = bits(0) (a real matrix is its own tile-scaled form with unit scales)."""
+    T, d = x.shape[0], x.shape[-1]
+    q = torch.zeros((T, d, d // 256), dtype=torch.float32, device=x.device)
+    G = torch.full((T, d // 256), _ORDERED_ZERO, dtype=torch.int32, device=x.device)
+    return ops.TsMats(x, q, G)
+
+
 def _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves) -> ChainRun:
     dev = torch.device("cuda", torch.cuda.current_device())
     digests = torch.empty((T, 4), dtype=torch.float32, device=dev)
     snaps: Dict[int, torch.Tensor] = {}
     c = ops.ts_from_goom(carry.reshape(1, d, d)) if carry is not None else None
-    for w0 in range(0, T, window):
+    streamed = leaves is not None and not leaves.is_cuda
+    if streamed:
+        if leaves.dtype != torch.float32:
+            raise ValueError("host leaves are streamed as real float32 matrices")
+        main = torch.cuda.current_stream()
+        copy = torch.cuda.Stream(device=dev)
+        bufs = [torch.empty((min(window, T), d, d), dtype=torch.float32, device=dev)
+                for _ in range(2)]
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def h2d(i, w0):
+            n = min(window, T - w0)
+            copy.wait_event(free[i % 2])
+            with torch.cuda.stream(copy):
+                bufs[i % 2][:n].copy_(leaves[w0:w0 + n], non_blocking=True)
+                ready[i % 2].record(copy)
+        for e in free:
+            e.record(main)
+        h2d(0, 0)
+    starts = list(range(0, T, window))
+    for i, w0 in enumerate(starts):
         n = min(window, T - w0)
-        if leaves is not None:
-            A = ops.ts_from_goom(leaves[w0:w0 + n])
+        if streamed:
+            main.wait_event(ready[i % 2])
+            if i + 1 < len(starts):
+                h2d(i + 1, starts[i + 1])
+            A = real_leaves_ts(bufs[i % 2][:n])
+        elif leaves is not None:
+            x = leaves[w0:w0 + n]
+            A = real_leaves_ts(x.contiguous()) if x.dtype == torch.float32 else ops.ts_from_goom(x)
         else:
             A = ops.ts_random_normal(n, d, seed, t0 + w0, dev)
         want = bool(snapshot_every) and any((t0 + t) % snapshot_every == 0
                                             for t in range(w0, w0 + n))
         P, dg, c = ops.chain_ts(A, block, c, out=want, digests=True, carry_out=True)
         digests[w0:w0 + n] = dg
+        if streamed:
+            free[i % 2].record(main)
         if want:
             for t in range(w0, w0 + n):
                 if (t0 + t) % snapshot_every == 0:

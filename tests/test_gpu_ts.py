@@ -202,3 +202,19 @@ def test_harness_ts_growth_and_digest_parity(g, ops):
     rate = harness.growth_rate(run.digests)
     psi = math.log(d / 2) - 1 / d - 1 / (12 * (d / 2) ** 2)
     assert abs(rate - 0.5 * (math.log(2) + psi)) < 0.02
+
+
+def test_harness_streams_real_host_leaves(g, ops):
+    """run_chain with real float32 leaves in pinned host memory (copied window by window on a
+    copy stream) equals the run on the same chain generated on the device."""
+    from paper_2510_03426_b200 import harness
+
+    d, T = 256, 96
+    gen = harness.run_chain(T, d, seed=11, window=32, block=8)
+    host = ops.ts_random_normal(T, d, 11, 0, torch.device("cuda")).U.cpu().pin_memory()
+    got = harness.run_chain(T, d, window=32, block=8, leaves=host)
+    assert torch.equal(got.digests, gen.digests)
+    dev_real = harness.run_chain(T, d, window=32, block=8, leaves=host.cuda())
+    assert torch.equal(dev_real.digests, gen.digests)
+    with pytest.raises(ValueError):
+        harness.run_chain(T, d, window=32, block=8, leaves=host.double())
