@@ -197,6 +197,16 @@ int goom_policy_select_c128(const goom_c128* X, int64_t batch, int d,
 int goom_policy_reset_c128(const goom_c128* X, goom_c128* R, int64_t batch, int d,
                            const goom_reset_policy* policy, void* stream);
 
+/* ---- Lyapunov spectrum stages (b)-(d) (lyapunov.py:311-356) ------ */
+/* Batched Householder QR of real d x d matrices (d <= 64) with R's diagonal made
+ * non-negative (qr_factor_batched, lyapunov.py:79-99): Q (batch, d, d) and, if absdiag is
+ * not NULL, |diag R| (batch, d). */
+int goom_qr_batched_f64(const double* M, double* Q, double* absdiag, int64_t batch, int d,
+                        void* stream);
+/* Stage (b): each complex128 state log-unit-normalised per column, exponentiated and
+ * QR-factored for its orthonormal basis Q (real). EINVAL if a state lost a whole column. */
+int goom_unit_qr_batched_c128(const goom_c128* X, double* Q, int64_t batch, int d, void* stream);
+
 /* ---- long-chain harness (SPEC.md:391-455 run_chain) -------- */
 /* n random-normal reals as GOOMs, element i drawn from Philox4x32-10 keyed (seed,
  * offset + i): chain leaf t of a d x d chain uses offset t*d*d on any GPU or shard.

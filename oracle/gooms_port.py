@@ -562,6 +562,75 @@ def scan_selective(st: Stack, policy: Policy, block: Optional[int]):
 
 
 # ---------------------------------------------------------------------------
+# Lyapunov stages (b)-(d) and the largest exponent
+
+
+def qr_factor_batched(ms):
+    """Householder QR over a stack, R diagonal made non-negative.  lyapunov.py:79-99.
+    Reflector v = x + sign(x0) ||x|| e0 (sign(0) = +), beta = 2 / v.v (0 when v = 0),
+    R <- R - beta v (v^T R), Q <- Q - beta (Q v) v^T, then column flips by sign(R_jj)."""
+    r = np.array(ms, dtype=np.float64)
+    N, n, _ = r.shape
+    q = np.broadcast_to(np.eye(n), (N, n, n)).copy()
+    for j in range(n):
+        x = r[:, j:, j]
+        norm_x = np.sqrt(np.einsum("nk,nk->n", x, x))
+        v = x.copy()
+        v[:, 0] += np.where(x[:, 0] >= 0, norm_x, -norm_x)
+        vv = np.einsum("nk,nk->n", v, v)
+        beta = np.where(vv > 0, 2.0 / np.where(vv > 0, vv, 1.0), 0.0)
+        w = np.einsum("nk,nkm->nm", v, r[:, j:, :])
+        r[:, j:, :] -= beta[:, None, None] * v[:, :, None] * w[:, None, :]
+        u = np.einsum("nmk,nk->nm", q[:, :, j:], v)
+        q[:, :, j:] -= beta[:, None, None] * u[:, :, None] * v[:, None, :]
+    flip = np.where(np.diagonal(r, axis1=1, axis2=2) < 0, -1.0, 1.0)
+    r *= flip[:, :, None]
+    q *= flip[:, None, :]
+    return q, r
+
+
+def spectrum_parallel(mats, dt, colinearity_threshold=0.99, check_interval=12, block=256):
+    """Parallel Lyapunov spectrum.  lyapunov.py:311-356: (a) selective colinearity scan of
+    [S0 = I, J_0 .. J_{T-2}], (b) log-unit-normalised states -> batched QR bases,
+    (c) J_t Q_{t-1}, (d) mean log |diag R| of the batched QR of (c), sorted descending."""
+    T, d = mats.shape[0], mats.shape[-1]
+    alog = np.empty((T, d, d))
+    asign = np.empty((T, d, d))
+    alog[0], asign[0] = log_sign(np.eye(d))
+    if T > 1:
+        alog[1:], asign[1:] = log_sign(mats[:T - 1])
+    pol = colinearity_policy(colinearity_threshold, check_interval)
+    V, Vs, sites = selective_chain(alog, asign, pol, block)
+    nu = col_log_norms(V)
+    if (nu == NEG_INF).any():
+        raise ValueError("a scan state lost a whole column; cannot orthonormalize")
+    bases = qr_factor_batched(Vs * np.exp(V - nu))[0]
+    _, r = qr_factor_batched(np.matmul(mats, bases))
+    diag = np.abs(np.diagonal(r, axis1=1, axis2=2))
+    if np.any(diag == 0.0):
+        raise ValueError("degenerate Jacobian chain")
+    return np.sort(np.mean(np.log(diag), axis=0) / dt)[::-1], len(sites)
+
+
+def lle_parallel(mats, u0, dt, block=256):
+    """Largest exponent from one affine scan with a d x 1 bias.  lyapunov.py:403-429."""
+    T, d = mats.shape[0], mats.shape[-1]
+    alog = np.empty((T + 1, d, d))
+    asign = np.empty((T + 1, d, d))
+    alog[0] = NEG_INF
+    asign[0] = 1.0
+    alog[1:], asign[1:] = log_sign(mats)
+    blog = np.full((T + 1, d, 1), NEG_INF)
+    bsign = np.ones((T + 1, d, 1))
+    blog[0], bsign[0] = log_sign(np.asarray(u0, dtype=np.float64).reshape(d, 1))
+    out = scan_affine_blocked(Stack(alog, asign, blog, bsign, np.zeros(T + 1, bool)), block)
+    final = out.blog[-1].ravel()
+    m = final.max()
+    lse = 2.0 * m + math.log(np.sum(np.exp(2.0 * (final - m))))
+    return lse / (2.0 * dt * T)
+
+
+# ---------------------------------------------------------------------------
 # parity metrics (SURVEY §8c)
 
 

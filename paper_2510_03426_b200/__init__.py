@@ -31,7 +31,9 @@ from .core import (  # noqa: F401
     to_real,
     to_real_scaled,
 )
-from .lyapunov import colinearity_policy, colinearity_select, orthonormal_reset  # noqa: F401
+from .lyapunov import (JacobianChain, SpectrumResult, colinearity_policy,  # noqa: F401
+                       colinearity_select, lle_parallel, lle_sequential, orthonormal_reset,
+                       qr_factor_batched, spectrum_parallel, spectrum_sequential)
 from .scan import (  # noqa: F401
     ResetPolicy,
     ScanPair,

@@ -120,6 +120,9 @@ SIGNATURES = {
     "goom_random_normal_c64": (_I, [_P, _I64, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "goom_digest_c64": (_I, [_P, _I64, _I64, _P, _P]),
     "goom_kernel_launches": (ctypes.c_longlong, []),
+    # Lyapunov stages (b)-(d)
+    "goom_qr_batched_f64": (_I, [_P, _P, _P, _I64, _I, _P]),
+    "goom_unit_qr_batched_c128": (_I, [_P, _P, _I64, _I, _P]),
     # tile-scaled fp32 chain engine
     "goom_random_normal_ts": (_I, [_P, _P, _P, _I64, _I, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "goom_ts_from_c64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),

@@ -287,7 +287,8 @@ __device__ bool policy_select(const Cx<Rt>* X, int d, const Policy& pol, const S
 // Householder QR of sm.R in place; Q into sm.W. positive_diag flips Q columns so
 // that diag(R) > 0 (the CGS2 basis). Returns GOOM_ERANK on a rank-deficient state.
 template <class Rt>
-__device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm) {
+__device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm,
+                             bool check_rank = true) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;  // column, row chunk (4 x 64 threads)
   double* tau = sm.vec;      // [0, d)
@@ -359,8 +360,9 @@ __device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm) {
   int rc = GOOM_OK;
   if (positive_diag) {
     const double tiny = 64.0 * 2.220446049250313e-16;
-    for (int j = 0; j < d; ++j)
-      if (fabs(diag[j]) < tiny) rc = GOOM_ERANK;
+    if (check_rank)
+      for (int j = 0; j < d; ++j)
+        if (fabs(diag[j]) < tiny) rc = GOOM_ERANK;
     if (rc == GOOM_OK)
       for (int e = tid; e < d * d; e += kThreads)
         if (diag[e % d] < 0.0) sm.W[e] = -sm.W[e];
@@ -482,6 +484,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   copy_mat(X + blockIdx.x * mat, sm.el, d);
   int rc = policy_reset(sm.el, R + blockIdx.x * mat, d, kind, sm);
   if (rc != GOOM_OK && threadIdx.x == 0) *status = rc;
+}
+
+// Batched Householder QR with R's diagonal made non-negative (qr_factor_batched,
+// lyapunov.py:79-99): one CTA per matrix, the walk's column-parallel Householder.
+// from_goom: the input is a complex128 GOOM state, first log-unit-normalised per column
+// (spectrum_parallel stage (b), lyapunov.py:343-347); an all-zero column sets *status.
+// Outputs Q (real, row-major) and |diag R|.
+__global__ void __launch_bounds__(kThreads, 1)
+    qr_batched_kernel(const double* __restrict__ M, const double2* __restrict__ X,
+                      double* __restrict__ Q, double* __restrict__ absdiag, int d,
+                      int* __restrict__ status) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem<double> sm = carve<double>(smem_raw, d);
+  const int64_t mat = (int64_t)d * d;
+  if (X) {
+    copy_mat(X + blockIdx.x * mat, sm.el, d);
+    if (unit_columns(sm.el, d, sm)) {
+      if (threadIdx.x == 0) *status = GOOM_EINVAL;
+      return;
+    }
+  } else {
+    for (int e = threadIdx.x; e < d * d; e += kThreads) sm.R[e] = M[blockIdx.x * mat + e];
+    __syncthreads();
+  }
+  householder_q(d, /*positive_diag=*/true, sm, /*check_rank=*/false);
+  for (int e = threadIdx.x; e < d * d; e += kThreads) Q[blockIdx.x * mat + e] = sm.W[e];
+  if (absdiag)
+    for (int j = threadIdx.x; j < d; j += kThreads) absdiag[blockIdx.x * d + j] = fabs(sm.vec[d + j]);
 }
 
 inline size_t round_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -718,6 +748,47 @@ int goom_policy_reset_c64(const goom_c64* X, goom_c64* R, int64_t batch, int d,
 int goom_policy_reset_c128(const goom_c128* X, goom_c128* R, int64_t batch, int d,
                            const goom_reset_policy* policy, void* stream) {
   return reset_batch<double>(X, R, batch, d, policy, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int qr_batched_entry(const double* M, const double2* X, double* Q, double* absdiag,
+                     int64_t batch, int d, void* stream) {
+  if (batch < 0) return goom::fail(GOOM_EINVAL, "batch must be >= 0");
+  if (d < 1 || d > goom::kMaxD)
+    return goom::fail(GOOM_EUNSUPPORTED, "batched QR keeps a matrix in one CTA: 1 <= d <= 64");
+  if (batch == 0) return GOOM_OK;
+  if ((!M && !X) || !Q) return goom::fail(GOOM_EINVAL, "null pointer");
+  cudaStream_t st = goom::as_stream(stream);
+  int* status = nullptr;
+  if (cudaMallocAsync(&status, sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
+    return goom::cuda_fail(cudaGetLastError(), "qr status");
+  GOOM_TRY(goom::set_smem<double>((const void*)goom::qr_batched_kernel, d));
+  goom::qr_batched_kernel<<<(unsigned)batch, goom::kThreads, goom::smem_bytes<double>(d), st>>>(
+      M, X, Q, absdiag, d, status);
+  GOOM_CHECK_LAUNCH("qr_batched_kernel");
+  int host_status = 0;
+  cudaMemcpyAsync(&host_status, status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(status, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return goom::cuda_fail(cudaGetLastError(), "qr sync");
+  if (host_status != GOOM_OK)
+    return goom::fail(host_status, "a scan state lost a whole column; cannot orthonormalize");
+  return GOOM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int goom_qr_batched_f64(const double* M, double* Q, double* absdiag, int64_t batch, int d,
+                        void* stream) {
+  return qr_batched_entry(M, nullptr, Q, absdiag, batch, d, stream);
+}
+
+int goom_unit_qr_batched_c128(const goom_c128* X, double* Q, int64_t batch, int d, void* stream) {
+  return qr_batched_entry(nullptr, reinterpret_cast<const double2*>(X), Q, nullptr, batch, d,
+                          stream);
 }
 
 }  // extern "C"

@@ -212,3 +212,29 @@ def test_lorenz96_jacobians_match_reference_machinery():
     f, df, x0, dt = S.lorenz96(16)
     mats = S.integrate_chain(f, df, x0, dt, burn_in=200, T=40, seed=0)
     np.testing.assert_allclose(mats, z["mats"], rtol=1e-12, atol=1e-12)
+
+
+# ---- Lyapunov stages (b)-(d) and the LLE (tests/golden/make_golden_lyap.py) ----------
+
+
+def test_oracle_qr_batched_matches_reference():
+    z = load_golden("qr_batched")
+    q, r = G.qr_factor_batched(z["ms"])
+    np.testing.assert_array_equal(q, z["q"])
+    np.testing.assert_array_equal(r, z["r"])
+
+
+@pytest.mark.parametrize("name,interval", [("spectrum_lorenz", 8), ("spectrum_l96_d16", 12)])
+def test_oracle_spectrum_parallel_matches_reference(name, interval):
+    z = load_golden(name)
+    lam, resets = G.spectrum_parallel(z["mats"], float(z["dt"]), check_interval=interval)
+    assert resets == int(z["resets"])
+    np.testing.assert_allclose(lam, z["lambdas"], rtol=0, atol=1e-12)
+
+
+def test_oracle_lle_parallel_matches_reference():
+    z = load_golden("lle_random")
+    for i in range(len(z["par"])):
+        got = G.lle_parallel(z["mats"][i], z["u0"][i], 0.5)
+        assert abs(got - z["par"][i]) <= 1e-12
+        assert abs(got - z["seq"][i]) <= 1e-8

@@ -51,6 +51,16 @@ def main():
     # every log-magnitude finite or -inf (exact zeros, e.g. the identity leaf's off-diagonal)
     finite = bool((torch.isfinite(V.real) | (V.real == float("-inf"))).all())
 
+    # the full spectrum estimator (stages (a)-(d), lyapunov.py:311-356) on the GPU
+    chain = g.JacobianChain(dt=dt, mats=mats)
+    g.spectrum_parallel(g.JacobianChain(dt=dt, mats=mats[:256]))  # warm-up
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    spec = g.spectrum_parallel(chain)
+    torch.cuda.synchronize()
+    spec_s = time.perf_counter() - t2
+    lam_sum = float(np.sum(spec.lambdas))
+
     # parity + CPU baseline on a prefix
     Tc = min(args.T_cpu, args.T)
     t1 = time.perf_counter()
@@ -65,6 +75,9 @@ def main():
         "config": "lyapunov_lorenz96_selective", "d": args.d, "T": args.T,
         "policy": "colinearity(0.99, interval 12, volume 1e-9), consume_leaf=False",
         "gpu_ms": gpu_ms, "gpu_matrices_per_s": args.T / (gpu_ms / 1e3), "resets": len(sites),
+        "spectrum_parallel_s": spec_s, "spectrum_matrices_per_s": args.T / spec_s,
+        "lambda_max": float(spec.lambdas[0]), "lambda_sum": lam_sum,
+        "spectrum_resets": spec.resets,
         "finite": finite, "input_generation_s": gen_s,
         "cpu_prefix_T": Tc, "cpu_s": cpu_s, "cpu_matrices_per_s": Tc / cpu_s,
         "cpu_cores": os.cpu_count(), "cpu_kind": "port (oracle/gooms_port.selective_chain, float64)",
