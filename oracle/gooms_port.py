@@ -630,6 +630,33 @@ def lle_parallel(mats, u0, dt, block=256):
     return lse / (2.0 * dt * T)
 
 
+def ssm_forward_parallel(A, B, C, D, x0, u, block=256):
+    """Non-diagonal SSM as an affine scan (ssm.py:110-137): leaves (A, B u_t) after the
+    leading (0, x0); states = the prefixes' bias columns; then _finish (ssm.py:84-98):
+    c_t = max log x_t (0 for an all-zero state), y = (s e^{log - c + 2}) C^T + u D^T."""
+    T, d = u.shape
+    a_log, a_sign = log_sign(np.asarray(A, dtype=np.float64))
+    b_log, b_sign = log_sign(np.asarray(B, dtype=np.float64))
+    u_log, u_sign = log_sign(u.reshape(T, d, 1))
+    bu_log, bu_sign = lmme(b_log, b_sign, u_log, u_sign)
+    alog = np.empty((T + 1, d, d))
+    asign = np.ones((T + 1, d, d))
+    alog[0] = NEG_INF
+    alog[1:] = a_log
+    asign[1:] = a_sign
+    blog = np.empty((T + 1, d, 1))
+    bsign = np.empty((T + 1, d, 1))
+    blog[0], bsign[0] = log_sign(np.asarray(x0, dtype=np.float64).reshape(d, 1))
+    blog[1:] = bu_log
+    bsign[1:] = bu_sign
+    out = scan_affine_blocked(Stack(alog, asign, blog, bsign, np.zeros(T + 1, bool)), block)
+    sl, ss = out.blog[1:, :, 0], out.bsign[1:, :, 0]
+    c = sl.max(axis=1)
+    c = np.where(c == NEG_INF, 0.0, c)
+    y = (ss * np.exp(sl - c[:, None] + 2.0)) @ np.asarray(C).T + u @ np.asarray(D).T
+    return sl, ss, c, y
+
+
 # ---------------------------------------------------------------------------
 # parity metrics (SURVEY §8c)
 

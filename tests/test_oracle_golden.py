@@ -238,3 +238,13 @@ def test_oracle_lle_parallel_matches_reference():
         got = G.lle_parallel(z["mats"][i], z["u0"][i], 0.5)
         assert abs(got - z["par"][i]) <= 1e-12
         assert abs(got - z["seq"][i]) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["ssm_random_d4", "ssm_growing_d8", "ssm_explode_d8"])
+def test_oracle_ssm_forward_matches_reference(name):
+    z = load_golden(name)
+    sl, ss, c, y = G.ssm_forward_parallel(z["A"], z["B"], z["C"], z["D"], z["x0"], z["u"])
+    np.testing.assert_array_equal(sl, z["state_log"])
+    np.testing.assert_array_equal(ss, z["state_sign"])
+    np.testing.assert_array_equal(c, z["scales"])
+    np.testing.assert_array_equal(y, z["y"])
