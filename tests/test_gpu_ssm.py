@@ -89,9 +89,26 @@ def test_ssm_batched_equals_per_sequence(s):
                     rng.standard_normal((2 * d, d)), rng.standard_normal((2 * d, d)))
     x0s = rng.standard_normal((S, d))
     us = rng.standard_normal((S, T, d))
-    sl, ss, c, y = s.ssm_forward_batched(p, x0s, us, block_size=32)
+    sl, ss, c, y = (t.cpu().numpy() for t in s.ssm_forward_batched(p, x0s, us, block_size=32,
+                                                                    chunk=0))
+    cl, cs, cc, cy = (t.cpu().numpy() for t in s.ssm_forward_batched(p, x0s, us, chunk=16))
+    assert rel_log(cl, sl) < 1e-10
+    np.testing.assert_array_equal(cs, ss)
+    np.testing.assert_allclose(cy, y, rtol=1e-9, atol=1e-12)
     for i in range(S):
         one = s.ssm_forward_parallel(p, x0s[i], us[i], block_size=32)
         assert rel_log(sl[i], one.state_log) < 1e-10
         np.testing.assert_array_equal(ss[i], one.state_sign)
         np.testing.assert_allclose(y[i], one.y, rtol=1e-9, atol=1e-12)
+
+
+def test_ssm_chunked_matches_reference_growth(s):
+    """The chunked evaluation on the reference's growing-spectral-radius fixture (T = 512
+    not a multiple of the chunk: padded steps)."""
+    z = load_golden("ssm_growing_d8")
+    p = s.SsmParams(z["A"], z["B"], z["C"], z["D"])
+    sl, ss, c, y = (t.cpu().numpy() for t in s.ssm_forward_batched(p, z["x0"][None],
+                                                                    z["u"][None], chunk=48))
+    assert rel_log(sl[0], z["state_log"]) < 1e-10
+    np.testing.assert_array_equal(ss[0], z["state_sign"])
+    np.testing.assert_allclose(y[0], z["y"], rtol=1e-7, atol=1e-9)

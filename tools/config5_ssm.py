@@ -44,13 +44,14 @@ def main():
     finite = True
     for h in range(H):
         sl, ss, c, y = ssm.ssm_forward_batched(params[h], x0[h], u[h])
-        finite &= bool(np.isfinite(sl).all() and np.isfinite(y).all())
+        finite &= bool(torch.isfinite(sl).all() and torch.isfinite(y).all())
     torch.cuda.synchronize()
     gpu_s = time.perf_counter() - t0
     # parity spot check: head 0, sequence 0 vs the oracle port
     osl, oss, oc, oy = G.ssm_forward_parallel(params[0].A, params[0].B, params[0].C, params[0].D,
                                               x0[0, 0], u[0, 0])
-    sl, ss, c, y = ssm.ssm_forward_batched(params[0], x0[0, :1], u[0, :1])
+    sl, ss, c, y = (t.cpu().numpy() for t in ssm.ssm_forward_batched(params[0], x0[0, :1],
+                                                                       u[0, :1]))
     err = float(np.max(np.abs(sl[0] - osl) / np.maximum(1.0, np.abs(osl))))
     t1 = time.perf_counter()
     G.ssm_forward_parallel(params[1].A, params[1].B, params[1].C, params[1].D, x0[1, 0], u[1, 0])
@@ -58,6 +59,7 @@ def main():
     print(json.dumps({
         "config": "ssm_forward", "d": d, "heads": H, "batch": S, "T": T,
         "gpu_s": gpu_s, "gpu_steps_per_s": H * S * T / gpu_s, "finite": finite,
+        "gpu_timing": "host float64 inputs -> device, states + outputs left on the device",
         "parity_rel_log_vs_oracle": err, "sign_mismatch": int(np.sum(ss[0] != oss)),
         "cpu_one_sequence_s": cpu_seq_s, "cpu_extrapolated_s": cpu_seq_s * H * S,
         "cpu_kind": "port (oracle/gooms_port.ssm_forward_parallel, float64, one sequence x 512)",
