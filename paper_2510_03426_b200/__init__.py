@@ -33,7 +33,8 @@ from .core import (  # noqa: F401
 )
 from .lyapunov import (JacobianChain, SpectrumResult, colinearity_policy,  # noqa: F401
                        colinearity_select, lle_parallel, lle_sequential, orthonormal_reset,
-                       qr_factor_batched, spectrum_parallel, spectrum_sequential)
+                       load_jacobian_chain, qr_factor_batched, save_jacobian_chain,
+                       spectrum_parallel, spectrum_sequential)
 from .scan import (  # noqa: F401
     ResetPolicy,
     ScanPair,

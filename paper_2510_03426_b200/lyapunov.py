@@ -220,3 +220,48 @@ def lle_sequential(chain, u0) -> float:
         acc += math.log(ns)
         v = sv / ns
     return acc / (chain.dt * chain.T)
+
+
+# ---------------------------------------------------------------------------
+# goomjac v1: the Jacobian-chain text format (lyapunov.py:433-476; host I/O)
+
+
+def save_jacobian_chain(chain, path):
+    """`goomjac v1 d=<d> T=<T> dt=<repr>` then T*d rows of d repr() floats."""
+    with open(path, "w") as fh:
+        fh.write(f"goomjac v1 d={chain.dim} T={chain.T} dt={float(chain.dt)!r}\n")
+        for mat in chain.mats:
+            for row in mat:
+                fh.write(" ".join(repr(float(v)) for v in row) + "\n")
+
+
+def load_jacobian_chain(path) -> JacobianChain:
+    """Strict parser: bad header / field / row count / width / non-finite -> ValueError."""
+    with open(path) as fh:
+        lines = fh.read().split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        raise ValueError("empty jacobian chain file")
+    head = lines[0].split()
+    if len(head) != 5 or head[:2] != ["goomjac", "v1"]:
+        raise ValueError(f"bad header: {lines[0]!r}")
+    try:
+        kv = dict(item.split("=", 1) for item in head[2:])
+        d, T, dt = int(kv["d"]), int(kv["T"]), float(kv["dt"])
+    except (KeyError, ValueError) as exc:
+        raise ValueError(f"bad header: {lines[0]!r}") from exc
+    if d < 1 or T < 1 or not dt > 0:
+        raise ValueError("header fields out of range")
+    rows = lines[1:]
+    if len(rows) != T * d:
+        raise ValueError(f"expected {T * d} matrix rows, found {len(rows)}")
+    mats = np.empty((T * d, d))
+    for i, line in enumerate(rows):
+        vals = line.split()
+        if len(vals) != d:
+            raise ValueError(f"row {i + 2}: expected {d} values, found {len(vals)}")
+        mats[i] = [float(v) for v in vals]
+    if not np.isfinite(mats).all():
+        raise ValueError("non-finite matrix entries")
+    return JacobianChain(dt=dt, mats=mats.reshape(T, d, d))
