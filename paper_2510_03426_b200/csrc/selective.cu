@@ -60,6 +60,7 @@ struct Smem {
   double* red;    // 2 * kWarps
   double* part;   // 4 * kMaxD: per-(row chunk, column) partials of the column-parallel kernels
   int* ints;      // 8
+  int* iw;        // 8 + 2 * kMaxD: LU pivot partials and row permutations
 };
 
 template <class Rt>
@@ -67,7 +68,7 @@ inline size_t smem_bytes(int d) {
   size_t dd = (size_t)d * d;
   return 2 * dd * sizeof(Cx<Rt>) + 2 * dd * sizeof(double) + 2 * d * sizeof(Rt) +
          2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 4 * kMaxD * sizeof(double) +
-         8 * sizeof(int) + 64;
+         (16 + 2 * kMaxD) * sizeof(int) + 64;
 }
 
 template <class Rt>
@@ -85,6 +86,7 @@ __device__ Smem<Rt> carve(char* base, int d) {
   s.part = s.red + 2 * kWarps;
   s.scal = reinterpret_cast<Rt*>(s.part + 4 * kMaxD);
   s.ints = reinterpret_cast<int*>(s.scal + 2 * d);
+  s.iw = s.ints + 8;
   return s;
 }
 
@@ -212,53 +214,76 @@ __device__ bool unit_columns(const Cx<Rt>* X, int d, const Smem<Rt>& sm) {
 }
 
 // slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor.
-// Three barriers per pivot: pivot search (warp 0), row swap, trailing update with the
-// column-parallel mapping (column cc = tid % 64 > c, rows c+1+ch, +4, ...).
+// One barrier per pivot: rows are never swapped (a double-buffered logical -> physical
+// row map instead), and the threads updating column c+1 also reduce its pivot candidates
+// (4 row-chunk partials, smallest row among equal maxima, as idamax), so the next step
+// starts with its pivot known. Column-parallel mapping: column cc = tid % 64 > c, logical
+// rows c+1+ch, +4, ...
 template <class Rt>
 __device__ bool volume_deficient(int d, double log_floor, const Smem<Rt>& sm) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
   const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;
+  double* pmax = sm.part;     // [2][4]
+  int* pidx = sm.iw;          // [2][4]
+  int* perm = sm.iw + 8;      // [2][kMaxD]
   for (int e = tid; e < d * d; e += kThreads) sm.W[e] = sm.R[e];
+  if (tid < d) perm[tid] = tid;
+  if (cc == 0) {
+    double best = -1.0;
+    int bi = d;
+    for (int r = ch; r < d; r += 4) {
+      const double v = fabs(sm.R[r * d]);
+      if (v > best) { best = v; bi = r; }
+    }
+    pmax[ch] = best;
+    pidx[ch] = bi;
+  }
   __syncthreads();
-  double logdet = 0.0;
+  // log|det| = log(prod |pv|) kept as mantissa * 2^exponent: one log at the end, not per pivot
+  double mant = 1.0;
+  int expo = 0;
   for (int c = 0; c < d; ++c) {
-    if (w == 0) {
-      double best = -1.0;
-      int bi = c;
-      for (int r = c + lane; r < d; r += 32) {
-        double v = fabs(sm.W[r * d + c]);
-        if (v > best) { best = v; bi = r; }
-      }
+    const int cur = c & 1, nxt = cur ^ 1;
+    double best = pmax[cur * 4];
+    int piv = pidx[cur * 4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (lane == 0) {
-        sm.ints[1] = bi;
-        sm.red[1] = sm.W[bi * d + c];
-      }
+    for (int k = 1; k < 4; ++k) {
+      const double v = pmax[cur * 4 + k];
+      const int i = pidx[cur * 4 + k];
+      if (v > best || (v == best && i < piv)) { best = v; piv = i; }
     }
-    __syncthreads();
-    const int piv = sm.ints[1];
-    const double pv = sm.red[1];
-    if (pv == 0.0) return true;  // det_sign == 0
-    if (piv != c && tid < d && tid >= c) {
-      const double t = sm.W[c * d + tid];
-      sm.W[c * d + tid] = sm.W[piv * d + tid];
-      sm.W[piv * d + tid] = t;
-    }
-    logdet += log(fabs(pv));
-    __syncthreads();
+    const int* pc = perm + cur * kMaxD;
+    int* pn = perm + nxt * kMaxD;
+    const int rowc = pc[piv];  // physical pivot row: logical row c from now on
+    const int rowp = pc[c];    // physical row that moves to logical row piv
+    const double pv = sm.W[rowc * d + c];
+    if (pv == 0.0) return true;  // det_sign == 0 (uniform across the CTA)
+    int e;
+    mant = frexp(mant * fabs(pv), &e);
+    expo += e;
     const double inv = 1.0 / pv;
+    if (tid < d) pn[tid] = tid == c ? rowc : (tid == piv ? rowp : pc[tid]);
+    double nb = -1.0;
+    int ni = d;
     if (cc > c && cc < d) {
-      const double u = sm.W[c * d + cc];
-      for (int r = c + 1 + ch; r < d; r += 4) sm.W[r * d + cc] -= (sm.W[r * d + c] * inv) * u;
+      const double u = sm.W[rowc * d + cc];
+      for (int r = c + 1 + ch; r < d; r += 4) {
+        const int pr = r == piv ? rowp : pc[r];
+        const double nv = sm.W[pr * d + cc] - (sm.W[pr * d + c] * inv) * u;
+        sm.W[pr * d + cc] = nv;
+        if (cc == c + 1) {
+          const double a = fabs(nv);
+          if (a > nb) { nb = a; ni = r; }
+        }
+      }
+    }
+    if (cc == c + 1) {
+      pmax[nxt * 4 + ch] = nb;
+      pidx[nxt * 4 + ch] = ni;
     }
     __syncthreads();
   }
-  return logdet < log_floor;
+  return log(mant) + expo * 0.69314718055994530942 < log_floor;
 }
 
 template <class Rt>
