@@ -249,6 +249,17 @@ int goom_chain_ts(const float* U, const float* q, const uint32_t* G, int64_t T, 
                   float* digests4, float* oU, float* oq, uint32_t* oG, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* The same window in two stages, for time-sharded runs (sharded.py): _local runs the
+ * carry-independent phases 1-2 into `ws` and writes the window total (A_{T-1} ... A_0) to
+ * oU/oq/oG; _finish, later and with the same ws, applies a right carry (cU/cq/cG, may be
+ * NULL) to every block carry and runs phase 3 (prefixes / digests / carry-out). */
+int goom_chain_ts_local(const float* U, const float* q, const uint32_t* G, int64_t T, int d,
+                        int block, float* oU, float* oq, uint32_t* oG, void* ws, size_t ws_bytes,
+                        void* stream);
+int goom_chain_ts_finish(int64_t T, int d, int block, const float* cU, const float* cq,
+                         const uint32_t* cG, goom_c64* out, float* digests4, float* oU, float* oq,
+                         uint32_t* oG, void* ws, size_t ws_bytes, void* stream);
+
 /* Kernels libgoom has launched in this process (bench accounting). */
 long long goom_kernel_launches(void);
 

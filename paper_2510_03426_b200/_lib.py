@@ -133,6 +133,11 @@ SIGNATURES = {
          _I, _I, _P],
     ),
     "goom_chain_ts_workspace_size": (_SZ, [_I64, _I, _I]),
+    "goom_chain_ts_local": (_I, [_P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _SZ, _P]),
+    "goom_chain_ts_finish": (
+        _I,
+        [_I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+    ),
     "goom_chain_ts": (
         _I,
         [_P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],

@@ -107,23 +107,37 @@ size_t chain_ts_workspace_bytes(int64_t T, int d, int block, bool leaves_given_t
          1024;
 }
 
-// A (tile-scaled leaves, T of them) -> out (complex64 prefixes) or digests (T float4);
-// carry_in / carry_out tile-scaled (may be null). tree_carries: phase 2 as a Kogge-Stone
-// scan of the block totals (ceil(log2 nb) batched launches, ~nb log2 nb products) instead
-// of the reference's sequential fold (nb dependent single-product launches, each on 8 of
-// the 148 SMs at d = 512); a different but fixed combine tree, deterministic per (T, block).
-int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_in,
-                  float2* out, float4* digests, TsBuf* carry_out, char* ws, size_t ws_bytes,
-                  cudaStream_t st, bool tree_carries) {
-  const int64_t s = block < T ? block : T;
-  const int64_t nb = (T + s - 1) / s;
+struct ChainWs {
+  TsBuf L, Cx, Cy;
+  float2* ident;
+  float4* parts;
+  int64_t s, nb;
+};
+
+// carve the window workspace (the same layout for every stage, so a caller can keep it
+// between chain_local and chain_finish)
+int chain_ws(int64_t T, int d, int block, char* ws, size_t ws_bytes, ChainWs& w) {
+  w.s = block < T ? block : T;
+  w.nb = (T + w.s - 1) / w.s;
   Carve cv{ws};
-  TsBuf L = cv.ts(T, d);
-  TsBuf Cx = cv.ts(nb + 1, d);
-  TsBuf Cy = cv.ts(nb + 1, d);  // Kogge-Stone ping-pong buffer
-  float2* ident = cv.take<float2>((size_t)d * d);
-  float4* parts = cv.take<float4>((size_t)T * (d / 32) * (d / 256));
+  w.L = cv.ts(T, d);
+  w.Cx = cv.ts(w.nb + 1, d);
+  w.Cy = cv.ts(w.nb + 1, d);  // Kogge-Stone ping-pong buffer / carried carries
+  w.ident = cv.take<float2>((size_t)d * d);
+  w.parts = cv.take<float4>((size_t)T * (d / 32) * (d / 256));
   if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "tile-scaled chain workspace too small");
+  return GOOM_OK;
+}
+
+// phases 1 and 2: local products L and the block carries Cx[0..nb] (Cx[0] = carry-in or I,
+// Cx[nb] = the window's last prefix); carry-independent when carry_in is null
+int chain_local(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_in, char* ws,
+                size_t ws_bytes, cudaStream_t st, bool tree_carries) {
+  ChainWs w;
+  GOOM_TRY(chain_ws(T, d, block, ws, ws_bytes, w));
+  const int64_t s = w.s, nb = w.nb;
+  TsBuf &L = w.L, &Cx = w.Cx, &Cy = w.Cy;
+  float2* ident = w.ident;
   const int nJ = d / 256;
   // every G slot that an epilogue max-reduces starts at "unset" (0)
   if (cudaMemsetAsync(L.G, 0, sizeof(uint32_t) * (size_t)T * nJ, st) != cudaSuccess ||
@@ -184,17 +198,46 @@ int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carr
                             Cx.out(kb + 1, 0), nullptr, 1, d, st));
     }
   }
-  // phase 3: P_t = L_t (x) Cx[t / s]
-  if (out)
-    GOOM_TRY(lmme_ts_call(L.in(0, 1), Cx.in(0, 1, s), kTsOutGoom, out, (int64_t)d * d, TsOut{},
-                          nullptr, T, d, st));
-  if (digests) {
-    GOOM_TRY(lmme_ts_call(L.in(0, 1), Cx.in(0, 1, s), kTsOutDigest, nullptr, 0, TsOut{}, parts, T,
-                          d, st));
-    GOOM_TRY(launch_digest_reduce(parts, (d / 32) * nJ, digests, T, st));
-  }
-  if (carry_out) GOOM_TRY(copy_ts(*carry_out, 0, Cx, nb, 1, 1, st));
   return GOOM_OK;
+}
+
+// phase 3 (+ optional right carry applied to every block carry first):
+// P_t = L_t (x) (Cx[t / s] (x) carry); the carry-out is the last prefix
+int chain_finish(int64_t T, int d, int block, const TsBuf* carry, float2* out, float4* digests,
+                 TsBuf* carry_out, char* ws, size_t ws_bytes, cudaStream_t st) {
+  ChainWs w;
+  GOOM_TRY(chain_ws(T, d, block, ws, ws_bytes, w));
+  const int64_t s = w.s, nb = w.nb;
+  const int nJ = d / 256;
+  if (carry) {  // Cx[k] <- Cx[k] (x) carry, one batched launch (Cx[0] = I -> carry)
+    if (cudaMemsetAsync(w.Cy.G, 0, sizeof(uint32_t) * (size_t)(nb + 1) * nJ, st) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "tile-scaled G reset");
+    GOOM_TRY(lmme_ts_call(w.Cx.in(0, 1), carry->in(0, 0), kTsOutTs, nullptr, 0, w.Cy.out(0, 1),
+                          nullptr, nb + 1, d, st));
+    GOOM_TRY(copy_ts(w.Cx, 0, w.Cy, 0, nb + 1, 1, st));
+  }
+  if (out)
+    GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutGoom, out, (int64_t)d * d,
+                          TsOut{}, nullptr, T, d, st));
+  if (digests) {
+    GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutDigest, nullptr, 0, TsOut{},
+                          w.parts, T, d, st));
+    GOOM_TRY(launch_digest_reduce(w.parts, (d / 32) * nJ, digests, T, st));
+  }
+  if (carry_out) GOOM_TRY(copy_ts(*carry_out, 0, w.Cx, nb, 1, 1, st));
+  return GOOM_OK;
+}
+
+// A (tile-scaled leaves, T of them) -> out (complex64 prefixes) or digests (T float4);
+// carry_in / carry_out tile-scaled (may be null). tree_carries: phase 2 as a Kogge-Stone
+// scan of the block totals (ceil(log2 nb) batched launches, ~nb log2 nb products) instead
+// of the reference's sequential fold (nb dependent single-product launches, each on 8 of
+// the 148 SMs at d = 512); a different but fixed combine tree, deterministic per (T, block).
+int chain_scan_ts(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_in,
+                  float2* out, float4* digests, TsBuf* carry_out, char* ws, size_t ws_bytes,
+                  cudaStream_t st, bool tree_carries) {
+  GOOM_TRY(chain_local(A, T, d, block, carry_in, ws, ws_bytes, st, tree_carries));
+  return chain_finish(T, d, block, nullptr, out, digests, carry_out, ws, ws_bytes, st);
 }
 
 // complex64 leaves -> tile-scaled -> chain_scan_ts (the public chain scan for d % 256 == 0)
@@ -255,6 +298,37 @@ int goom_chain_ts(const float* U, const float* q, const uint32_t* G, int64_t T, 
                        reinterpret_cast<float4*>(digests4), oU ? &co : nullptr,
                        reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream),
                        /*tree_carries=*/true);
+}
+
+int goom_chain_ts_local(const float* U, const float* q, const uint32_t* G, int64_t T, int d,
+                        int block, float* oU, float* oq, uint32_t* oG, void* ws, size_t ws_bytes,
+                        void* stream) {
+  if (T < 1 || block < 1) return fail(GOOM_EINVAL, "T and block must be >= 1");
+  if (d < 256 || d % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled chain needs d % 256 == 0");
+  if (!U || !q || !G || !ws) return fail(GOOM_EINVAL, "null pointer");
+  const TsBuf A = ts_of(const_cast<float*>(U), const_cast<float*>(q), const_cast<uint32_t*>(G), d);
+  cudaStream_t st = as_stream(stream);
+  GOOM_TRY(chain_local(A, T, d, block, nullptr, reinterpret_cast<char*>(ws), ws_bytes, st, true));
+  if (oU) {
+    ChainWs w;
+    GOOM_TRY(chain_ws(T, d, block, reinterpret_cast<char*>(ws), ws_bytes, w));
+    TsBuf total = ts_of(oU, oq, oG, d);
+    GOOM_TRY(copy_ts(total, 0, w.Cx, w.nb, 1, 1, st));
+  }
+  return GOOM_OK;
+}
+
+int goom_chain_ts_finish(int64_t T, int d, int block, const float* cU, const float* cq,
+                         const uint32_t* cG, goom_c64* out, float* digests4, float* oU, float* oq,
+                         uint32_t* oG, void* ws, size_t ws_bytes, void* stream) {
+  if (T < 1 || block < 1) return fail(GOOM_EINVAL, "T and block must be >= 1");
+  if (d < 256 || d % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled chain needs d % 256 == 0");
+  if (!ws) return fail(GOOM_EINVAL, "null workspace");
+  TsBuf ci = ts_of(const_cast<float*>(cU), const_cast<float*>(cq), const_cast<uint32_t*>(cG), d);
+  TsBuf co = ts_of(oU, oq, oG, d);
+  return chain_finish(T, d, block, cU ? &ci : nullptr, reinterpret_cast<float2*>(out),
+                      reinterpret_cast<float4*>(digests4), oU ? &co : nullptr,
+                      reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream));
 }
 
 int goom_ts_from_c64(const goom_c64* X, int64_t batch, int rows, int cols, float* U, float* q,

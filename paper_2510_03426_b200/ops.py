@@ -443,3 +443,42 @@ def chain_ts(leaves: TsMats, block: int, carry: Optional[TsMats] = None, out: bo
               p(carry.G if carry else None), p(P), p(dg), p(co.U if co else None),
               p(co.q if co else None), p(co.G if co else None), ws.data_ptr(), nws, _stream())
     return P, dg, co
+
+
+class ChainWindow(NamedTuple):
+    """A window's carry-independent state kept between chain_ts_local and chain_ts_finish."""
+    ws: torch.Tensor
+    nbytes: int
+    T: int
+    d: int
+    block: int
+
+
+def chain_ts_local(leaves: TsMats, block: int):
+    """Phases 1-2 of a window with no carry: returns (ChainWindow, window total TsMats)."""
+    T, d = leaves.U.shape[0], leaves.U.shape[-1]
+    dev = leaves.U.device
+    ws, nws = _ws(int(_lib.load().goom_chain_ts_workspace_size(T, d, int(block))), dev)
+    tot = ts_empty(1, d, dev)
+    _lib.call("goom_chain_ts_local", leaves.U.data_ptr(), leaves.q.data_ptr(),
+              leaves.G.data_ptr(), T, d, int(block), tot.U.data_ptr(), tot.q.data_ptr(),
+              tot.G.data_ptr(), ws.data_ptr(), nws, _stream())
+    return ChainWindow(ws, nws, T, d, int(block)), tot
+
+
+def chain_ts_finish(win: ChainWindow, carry: Optional[TsMats], out: bool = False,
+                    digests: bool = True, carry_out: bool = True):
+    """Phase 3 of a window prepared by chain_ts_local, with a right carry (or none)."""
+    dev = win.ws.device
+    P = torch.empty((win.T, win.d, win.d), dtype=torch.complex64, device=dev) if out else None
+    dg = torch.empty((win.T, 4), dtype=torch.float32, device=dev) if digests else None
+    co = ts_empty(1, win.d, dev) if carry_out else None
+
+    def p(t):
+        return None if t is None else t.data_ptr()
+
+    _lib.call("goom_chain_ts_finish", win.T, win.d, win.block, p(carry.U if carry else None),
+              p(carry.q if carry else None), p(carry.G if carry else None), p(P), p(dg),
+              p(co.U if co else None), p(co.q if co else None), p(co.G if co else None),
+              win.ws.data_ptr(), win.nbytes, _stream())
+    return P, dg, co

@@ -103,3 +103,35 @@ def test_kernel_launch_counter_moves(h):
     n0 = ops.kernel_launches()
     h.random_chain(4, 8)
     assert ops.kernel_launches() > n0
+
+
+def test_resident_shards_equal_the_single_gpu_chain(h):
+    """run_shard_resident (local products kept between the totals pass and phase 3) run
+    shard by shard on one GPU, with the exclusive carries folded from the shard totals
+    exactly as the all-gather would, equals the single-GPU chain."""
+    from paper_2510_03426_b200 import sharded
+
+    T, d, world, window, block = 300, 256, 3, 64, 8
+    full = h.run_chain(T, d, seed=12, window=window, block=block)
+    totals = []
+
+    def record(tot):
+        totals.append(tot)
+        return None
+
+    # pass A: every shard's total (what each rank contributes to the all-gather)
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        sharded.run_shard_resident(n, d, 12, t0, window, block, record)
+    runs = []
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        carry = sharded.fold_carry(totals, r, torch.ops.goom.lmme)
+        runs.append(sharded.run_shard_resident(n, d, 12, t0, window, block, lambda _t: carry))
+    dg = torch.cat([r.digests for r in runs]).double().cpu().numpy()
+    ref = full.digests.double().cpu().numpy()
+    assert np.max(np.abs(dg[:, 1] - ref[:, 1]) / np.maximum(1, np.abs(ref[:, 1]))) < 1e-4
+    assert (dg[:, 2] == 1).all()
+    gl, gs = to_np(runs[-1].final[None])
+    rl, rs = to_np(full.final[None])
+    assert scaled_real_err(gl, gs, rl, rs).max() < 1e-2
