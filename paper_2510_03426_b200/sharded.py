@@ -72,42 +72,59 @@ def shard_total(n: int, d: int, seed: int, t0: int, window: int, block: int) -> 
 
 
 def run_shard_resident(n: int, d: int, seed: int, t0: int, window: int, block: int,
-                       exchange: Callable):
+                       exchange: Callable, max_resident: Optional[int] = None):
     """This rank's shard with its local products kept on the device (d % 256 == 0).
 
     Pass 1 runs the carry-independent phases 1-2 of every window (ops.chain_ts_local) and
-    folds the window totals into the shard total; `exchange(total)` (all-gather + fold, or
-    a test double) returns the shard's exclusive carry; pass 2 runs only phase 3 of each
-    window with its carry (ops.chain_ts_finish). Every local product is computed once, so a
-    rank does ~2 n products instead of ~3 n when the totals are recomputed (shard_total)."""
+    folds the window totals into the shard total, keeping the first `max_resident` windows'
+    local products (default: as many as fit in free device memory); `exchange(total)`
+    (all-gather + fold, or a test double) returns the shard's exclusive carry; pass 2 runs
+    only phase 3 for the resident windows (ops.chain_ts_finish) and the whole window for the
+    others. A fully resident rank does ~2 n products (the single-GPU work); one that keeps
+    nothing does ~3 n (the totals recomputed, as shard_total + run_chain)."""
     from . import ops
     from .harness import ChainRun
 
     dev = torch.device("cuda", torch.cuda.current_device())
+    if max_resident is None:
+        per = min(window, n) * d * d * 4 * 1.08
+        max_resident = max(0, int((0.92 * _free_bytes() - per) // per))
     wins, total = [], None
     for w0 in range(0, n, window):
         m = min(window, n - w0)
         leaves = ops.ts_random_normal(m, d, seed, t0 + w0, dev)
         win, wt = ops.chain_ts_local(leaves, block)
         del leaves
-        wins.append((w0, m, win))
+        keep = sum(1 for x in wins if x[2] is not None) < max_resident
+        wins.append((w0, m, win if keep else None))
+        del win
         total = wt if total is None else ops.lmme_ts(wt, total, 1)  # later windows on the left
     carry = exchange(ops.ts_to_goom(total)[0])
     c = ops.ts_from_goom(carry.reshape(1, d, d)) if carry is not None else None
     digests = torch.empty((n, 4), dtype=torch.float32, device=dev)
     for i, (w0, m, win) in enumerate(wins):
-        _, dg, c = ops.chain_ts_finish(win, c, digests=True, carry_out=True)
+        if win is not None:
+            _, dg, c = ops.chain_ts_finish(win, c, digests=True, carry_out=True)
+        else:
+            _, dg, c = ops.chain_ts(ops.ts_random_normal(m, d, seed, t0 + w0, dev), block, c,
+                                    digests=True, carry_out=True)
         digests[w0:w0 + m] = dg
         wins[i] = None  # release the window's workspace
     return ChainRun(digests, ops.ts_to_goom(c)[0], {})
 
 
+def _free_bytes() -> int:
+    """Device memory available to new tensors: free on the device plus what the caching
+    allocator holds but does not use."""
+    free, _ = torch.cuda.mem_get_info()
+    return free + torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+
+
 def resident_fits(n: int, d: int, window: int) -> bool:
     """Whether every window's local products of an n-leaf shard fit in free device memory
     (tile-scaled: 4 B per element, plus one window of leaves being generated)."""
-    free, _ = torch.cuda.mem_get_info()
     need = (n + min(window, n)) * d * d * 4 * 1.08
-    return need < 0.92 * free
+    return need < 0.92 * _free_bytes()
 
 
 def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
@@ -121,12 +138,12 @@ def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: 
     t0, n = shard_range(T, rank, world)
     if world > 1 and ops.ts_eligible(d) and not snapshot_every:
         w = window
-        while w > 4096 and not resident_fits(n, d, w):
-            w //= 2  # a smaller window leaves room for the resident local products
-        if resident_fits(n, d, w):
-            return t0, run_shard_resident(
-                n, d, seed, t0, w, block,
-                lambda tot: exclusive_carry(tot, torch.ops.goom.lmme, group))
+        while w > 8192 and not resident_fits(n, d, w):
+            w //= 2  # a smaller window leaves room for more resident local products
+        # keeps as many windows' local products as fit; recomputes only the rest
+        return t0, run_shard_resident(
+            n, d, seed, t0, w, block,
+            lambda tot: exclusive_carry(tot, torch.ops.goom.lmme, group))
     carry = None
     if world > 1:
         total = shard_total(n, d, seed, t0, window, block)

@@ -127,7 +127,9 @@ def test_resident_shards_equal_the_single_gpu_chain(h):
     for r in range(world):
         t0, n = sharded.shard_range(T, r, world)
         carry = sharded.fold_carry(totals, r, torch.ops.goom.lmme)
-        runs.append(sharded.run_shard_resident(n, d, 12, t0, window, block, lambda _t: carry))
+        # rank 1 keeps only one window resident: its other windows are recomputed
+        runs.append(sharded.run_shard_resident(n, d, 12, t0, window, block, lambda _t: carry,
+                                               max_resident=1 if r == 1 else None))
     dg = torch.cat([r.digests for r in runs]).double().cpu().numpy()
     ref = full.digests.double().cpu().numpy()
     assert np.max(np.abs(dg[:, 1] - ref[:, 1]) / np.maximum(1, np.abs(ref[:, 1]))) < 1e-4

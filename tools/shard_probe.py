@@ -12,16 +12,13 @@ sys.path.insert(0, ".")
 from paper_2510_03426_b200 import harness, sharded  # noqa: E402
 
 T, d, block = 1 << 20, 512, 128
-for G in (8, 4):
+for G in (8, 4, 2):
     n = T // G
     for mode in ("resident", "recompute"):
         if mode == "resident":
             w = 32768
-            while w > 4096 and not sharded.resident_fits(n, d, w):
+            while w > 8192 and not sharded.resident_fits(n, d, w):
                 w //= 2
-            if not sharded.resident_fits(n, d, w):
-                print(json.dumps({"G": G, "mode": mode, "skipped": "does not fit"}), flush=True)
-                continue
             fn = lambda: sharded.run_shard_resident(n, d, 1, 0, w, block, lambda t: t)  # noqa: E731
         else:
             w = 32768
