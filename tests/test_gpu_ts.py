@@ -43,11 +43,11 @@ def rand_ls(rng, *shape):
     return G.log_sign(rng.standard_normal(shape).astype(np.float32))
 
 
-@pytest.mark.parametrize("d", [256, 512])
-def test_lmme_ts_all_epilogues_match_oracle(g, ops, d):
+@pytest.mark.parametrize("d,batch", [(256, 3), (512, 3), (1024, 1)])
+def test_lmme_ts_all_epilogues_match_oracle(g, ops, d, batch):
     rng = np.random.default_rng(d)
-    al, as_ = rand_ls(rng, 3, d, d)
-    bl, bs = rand_ls(rng, 3, d, d)
+    al, as_ = rand_ls(rng, batch, d, d)
+    bl, bs = rand_ls(rng, batch, d, d)
     ta, tb = ops.ts_from_goom(cz(al, as_)), ops.ts_from_goom(cz(bl, bs))
     for kind in (0, 1):
         out = ops.lmme_ts(ta, tb, kind)
@@ -59,8 +59,8 @@ def test_lmme_ts_all_epilogues_match_oracle(g, ops, d):
     dg = ops.lmme_ts(ta, tb, 2).double().cpu().numpy()
     wl, _ = G.lmme(al.astype(np.float64), as_.astype(np.float64), bl.astype(np.float64),
                    bs.astype(np.float64))
-    top = wl.reshape(3, -1).max(axis=1)
-    lfro = top + 0.5 * np.log(np.exp(2 * (wl.reshape(3, -1) - top[:, None])).sum(axis=1))
+    top = wl.reshape(batch, -1).max(axis=1)
+    lfro = top + 0.5 * np.log(np.exp(2 * (wl.reshape(batch, -1) - top[:, None])).sum(axis=1))
     assert np.abs(dg[:, 0] - top).max() < 1e-4 * max(1, np.abs(top).max())
     assert np.abs(dg[:, 1] - lfro).max() < 1e-4 * max(1, np.abs(lfro).max())
     assert (dg[:, 2] == 1).all()
@@ -127,7 +127,8 @@ def test_lmme_ts_edge_cases(g, ops):
     assert np.all((gs[1] == ss[0]) | (kap < 1e-4))
 
 
-@pytest.mark.parametrize("d,T,block", [(256, 64, 8), (256, 33, 64), (512, 24, 5)])
+@pytest.mark.parametrize("d,T,block", [(256, 64, 8), (256, 33, 64), (512, 24, 5), (1024, 6, 2),
+                                       (256, 1, 4)])
 def test_chain_ts_matches_float64_oracle(g, ops, d, T, block):
     """The public chain scan (tile-scaled engine for d % 256 == 0) vs the float64 oracle,
     calibrated by the reference's own float32 runs (SURVEY §8c chain criterion)."""
