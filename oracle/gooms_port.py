@@ -657,6 +657,81 @@ def ssm_forward_parallel(A, B, C, D, x0, u, block=256):
     return sl, ss, c, y
 
 
+def _signed_lse(logs, signs, axis):
+    """log-domain signed sum along axis: (log|sum|, sign); an all -inf / cancelled sum -> (-inf, +1)."""
+    m = np.max(logs, axis=axis, keepdims=True)
+    mf = np.where(np.isfinite(m), m, 0.0)
+    with np.errstate(under="ignore"):
+        tot = np.sum(signs * np.exp(logs - mf), axis=axis, keepdims=True)
+    with np.errstate(divide="ignore"):
+        out = np.where(tot == 0.0, NEG_INF, np.log(np.abs(tot)) + mf)
+    return np.squeeze(out, axis), np.squeeze(np.where(tot < 0, -1.0, 1.0), axis)
+
+
+def _real_of_log(log, sign):
+    with np.errstate(over="ignore", under="ignore"):
+        return sign * np.exp(log)
+
+
+def ssm_backward(A, B, C, D, x0, u, sl, ss, c, gy):
+    """Gradients of sum(gy * y) for ssm_forward_parallel's outputs (sl, ss, c). The
+    reference has no autodiff; this restates the adjoint of its
+    forward (ssm.py:84-98, 99-137) in the log domain, one reverse step at a time with this
+    module's lmme / gadd, and is pinned against torch float64 autograd on chains without
+    overflow (tests/golden/make_golden_ssm_bwd.py):
+      z_t = s_t e^{l_t - c_t + 2}; gz_t = C^T gy_t; i* = first argmax_i l_t,i;
+      h_t = e^2 gz_t - e_{i*} s_{t,i*} (gz_t . z_t)   (no c-term for an all-zero state);
+      lam_{T-1} = e^{-c} h_{T-1};  lam_t = A^T (x) lam_{t+1} (+) e^{-c_t} h_t (run on
+      lam e^{K}, K = max_t c_t);
+      dA = sum_t lam_t x_{t-1}^T (x_{-1} = x0), dB = sum_t lam_t u_t^T (signed log-sum-exp
+      over t, then exp); du_t = B^T lam_t + D^T gy_t; dx0 = A^T lam_0;
+      dC = sum gy_t z_t^T; dD = sum gy_t u_t^T.  Returns a dict of float64 arrays."""
+    A, B, C, D = (np.asarray(m, dtype=np.float64) for m in (A, B, C, D))
+    x0 = np.asarray(x0, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    gy = np.asarray(gy, dtype=np.float64)
+    T, d = u.shape
+    z = ss * np.exp(sl - c[:, None] + 2.0)
+    gz = gy @ C
+    h = math.exp(2.0) * gz
+    live = np.max(sl, axis=1) != NEG_INF
+    istar = np.argmax(sl, axis=1)
+    dot = np.sum(gz * z, axis=1)
+    rows = np.arange(T)
+    h[rows, istar] -= np.where(live, ss[rows, istar] * dot, 0.0)
+    hl, hs = log_sign(h)
+    # the recurrence runs on lam e^{K}, K = max_t c_t: this module's lmme clamps its scales
+    # at 0 like the reference, so an adjoint below e^{-745} would otherwise vanish
+    K = float(np.max(c))
+    gl = hl + (K - c)[:, None]
+    at_l, at_s = log_sign(A.T.copy())
+    lam_l = np.empty((T, d))
+    lam_s = np.empty((T, d))
+    cur_l, cur_s = gl[T - 1].reshape(d, 1), hs[T - 1].reshape(d, 1)
+    lam_l[T - 1], lam_s[T - 1] = cur_l[:, 0], cur_s[:, 0]
+    for t in range(T - 2, -1, -1):
+        pl, ps = lmme(at_l, at_s, cur_l, cur_s)
+        cur_l, cur_s = gadd(pl, ps, gl[t].reshape(d, 1), hs[t].reshape(d, 1))
+        lam_l[t], lam_s[t] = cur_l[:, 0], cur_s[:, 0]
+    lam_l = lam_l - K
+    x0l, x0s = log_sign(x0)
+    prev_l = np.concatenate([x0l[None], sl[:-1]])
+    prev_s = np.concatenate([x0s[None], ss[:-1]])
+    ul, us = log_sign(u)
+    dA = _real_of_log(*_signed_lse(lam_l[:, :, None] + prev_l[:, None, :],
+                                   lam_s[:, :, None] * prev_s[:, None, :], 0))
+    dB = _real_of_log(*_signed_lse(lam_l[:, :, None] + ul[:, None, :],
+                                   lam_s[:, :, None] * us[:, None, :], 0))
+    bt_l, bt_s = log_sign(B.T.copy())
+    bl, bs = lmme(np.broadcast_to(bt_l, (T, d, d)), np.broadcast_to(bt_s, (T, d, d)),
+                  lam_l[:, :, None], lam_s[:, :, None])
+    du = _real_of_log(bl[:, :, 0], bs[:, :, 0]) + gy @ D
+    xl, xs = lmme(at_l, at_s, lam_l[0].reshape(d, 1), lam_s[0].reshape(d, 1))
+    dx0 = _real_of_log(xl[:, 0], xs[:, 0])
+    return {"A": dA, "B": dB, "C": gy.T @ z, "D": gy.T @ u, "x0": dx0, "u": du,
+            "lam_log": lam_l, "lam_sign": lam_s}
+
+
 # ---------------------------------------------------------------------------
 # parity metrics (SURVEY §8c)
 

@@ -203,6 +203,41 @@ def lmme_gadd(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor) -> torch.Tensor
     return _lmme_impl(a, b, d)
 
 
+def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch: int,
+                 d: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """C[i] = A[i // a_div] (x) B[i // b_div] (+ D[i]) for i < batch, one launch.
+    a (Na, n, k) and b (Nb, k, m) are contiguous stacks (N = 1 broadcasts); d, when given,
+    is (batch, n, m). Shares operands across a batch without materialising the broadcast
+    (e.g. one chunk-entry panel per head against every power of A)."""
+    _need_cuda(a, b, d)
+    _need_goom(a, b, d)
+    if a.dim() != 3 or b.dim() != 3 or a.shape[2] != b.shape[1]:
+        raise ValueError("lmme_indexed takes (N, n, k) and (N, k, m) stacks")
+    n, k, m = a.shape[1], a.shape[2], b.shape[2]
+    for t, div in ((a, a_div), (b, b_div)):
+        if t.shape[0] != 1 and (batch - 1) // div >= t.shape[0]:
+            raise ValueError("operand stack too short for batch / div")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty((batch, n, m), dtype=a.dtype, device=a.device)
+    if batch == 0:
+        return out
+    sa = 0 if a.shape[0] == 1 else n * k
+    sb = 0 if b.shape[0] == 1 else k * m
+    ws, nws = _ws(_size("goom_lmme_workspace_size", a.dtype, batch, n, k, m), a.device)
+    oa = _lib.goom_operand(a.data_ptr(), sa, max(1, a_div))
+    ob = _lib.goom_operand(b.data_ptr(), sb, max(1, b_div))
+    if d is None:
+        _lib.call(_lib.fn("goom_lmme", a.dtype), oa, ob, out.data_ptr(), n * m, batch, n, k, m,
+                  _ptr(ws), nws, _stream())
+    else:
+        if d.shape != (batch, n, m) or d.dtype != a.dtype:
+            raise ValueError("bias must be (batch, n, m) of the operands' dtype")
+        d = d.contiguous()
+        _lib.call(_lib.fn("goom_lmme_gadd", a.dtype), oa, ob, _lib.goom_operand(d.data_ptr(), n * m, 1),
+                  out.data_ptr(), n * m, batch, n, k, m, _ptr(ws), nws, _stream())
+    return out
+
+
 # ---------------------------------------------------------------------------
 # scans
 

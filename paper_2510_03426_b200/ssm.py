@@ -19,6 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import ops
+
 NEG_INF = float("-inf")
 
 
@@ -120,6 +122,16 @@ def _bu(params, u_t: torch.Tensor) -> torch.Tensor:
     return torch.ops.goom.lmme(Bg[None], ug)
 
 
+def _bu_heads(B: torch.Tensor, u: torch.Tensor) -> torch.Tensor:
+    """B_h u_t for every head and step as GOOMs: one LMME of each head's d x d B with its
+    d x (S T) panel of inputs (ssm.py:107-109). B (H, d, d) real, u (H, S, T, d) real ->
+    (H, S, T, d) complex128."""
+    H, S, T, d = u.shape
+    ug = _goom(u.reshape(H, S * T, d).transpose(1, 2))
+    bu = torch.ops.goom.lmme(_goom(B), ug)                               # (H, d, S T)
+    return bu.transpose(1, 2).reshape(H, S, T, d)
+
+
 def _scan_states(params, x0s: np.ndarray, us: np.ndarray, block_size: int) -> torch.Tensor:
     """States of S sequences (x0s (S, d), us (S, T, d)) sharing `params`: one affine scan
     over S (T + 1) leaves; returns complex128 (S, T, d)."""
@@ -166,44 +178,61 @@ def ssm_forward_sequential(params, x0, u) -> SsmRun:
     return SsmRun(x0=x0, u=u, y=y, scales=c, state_log=sl, state_sign=ss)
 
 
-def _chunked_states(params, x0s: np.ndarray, us: np.ndarray, chunk: int) -> torch.Tensor:
-    """States of S sequences sharing A by chunks of L = `chunk` steps with the powers of A
-    shared by every chunk — O(T d^2) matrix-vector work instead of the affine scan's
-    O(T d^3) matrix-matrix work on a constant A slot:
-      local   y_{c,i} = A (x) y_{c,i-1} (+) b_{cL+i}   (L-1 launches, all chunks at once)
-      entry   s_{c+1} = A^L (x) s_c (+) y_{c,L-1}     (nC launches, s_0 = x0)
-      state   x_{cL+i} = A^{i+1} (x) s_c (+) y_{c,i}   (L launches)
-    Every launch is one LMME of a d x d power with a d x (S nC) panel of column vectors.
-    Same states as the reference's scan up to float64 rounding (a different tree)."""
-    dev = _dev()
-    S, T, d = us.shape
+def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: int) -> torch.Tensor:
+    """x_t = A (x) x_{t-1} (+) b_t for H heads x S sequences with the powers of A shared by
+    every chunk of L = `chunk` steps — O(T d^2) matrix-vector work instead of the affine
+    scan's O(T d^3) matrix-matrix work on a constant A slot. Ag (H, d, d), b (H, S, T, d),
+    s0 (H, S, d) complex128 GOOMs -> states (H, S, T, d):
+      local   y_{c,i} = A (x) y_{c,i-1} (+) b_{cL+i}   (L-1 launches, all heads and chunks)
+      powers  P_i = A^{i+1}                            (L-1 launches, all heads)
+      entry   s_{c+1} = A^L (x) s_c (+) y_{c,L-1}     (nC-1 launches, s_0 = the initial state)
+      state   x_{cL+i} = A^{i+1} (x) s_c (+) y_{c,i}   (one launch: every (head, i) pair, the
+                                                      head's entry panel shared via div = L)
+    Every launch is an LMME of d x d matrices with d x (S nC) panels of column vectors.
+    The same states as the reference's scan up to float64 rounding (a different tree)."""
+    H, S, T, d = b.shape
+    dev = b.device
     L = max(1, min(chunk, T))
     nC = (T + L - 1) // L
     Tp = nC * L
-    u_t = torch.zeros((S, Tp, d), dtype=torch.float64, device=dev)
-    u_t[:, :T] = torch.as_tensor(us, dtype=torch.float64, device=dev)
-    b = _bu(params, u_t).reshape(S, nC, L, d)                    # b_t, padded steps = 0 (-inf)
-    Ag = _goom(torch.as_tensor(params.A, device=dev))
-    # panel layout: column index = s * nC + c
-    bi = b.permute(2, 3, 0, 1).reshape(L, d, S * nC)             # [i] -> (d, S nC)
-    Y = torch.empty((L, d, S * nC), dtype=torch.complex128, device=dev)
+    if Tp != T:
+        zero = torch.complex(torch.tensor(NEG_INF, dtype=torch.float64),
+                             torch.tensor(0.0, dtype=torch.float64))
+        bp = torch.full((H, S, Tp, d), zero, dtype=torch.complex128, device=dev)
+        bp[:, :, :T] = b
+        b = bp
+    N = S * nC
+    # panels: column index = s * nC + c; bi[i] (H, d, N)
+    bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).reshape(L, H, d, N)
+    Y = torch.empty((L, H, d, N), dtype=torch.complex128, device=dev)
     Y[0] = bi[0]
     for i in range(1, L):
-        Y[i] = torch.ops.goom.lmme_gadd(Ag[None], Y[i - 1][None], bi[i][None])[0]
-    P = torch.empty((L, d, d), dtype=torch.complex128, device=dev)  # P[i] = A^{i+1}
-    P[0] = Ag
+        Y[i] = torch.ops.goom.lmme_gadd(Ag, Y[i - 1], bi[i])
+    P = torch.empty((H, L, d, d), dtype=torch.complex128, device=dev)  # P[h, i] = A_h^{i+1}
+    P[:, 0] = Ag
     for i in range(1, L):
-        P[i] = torch.ops.goom.lmme(Ag[None], P[i - 1][None])[0]
-    s = torch.empty((nC, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
-    s[0] = _goom(torch.as_tensor(x0s, dtype=torch.float64, device=dev).T.contiguous())
-    Yl = Y[L - 1].reshape(d, S, nC)
+        P[:, i] = torch.ops.goom.lmme(Ag, P[:, i - 1])
+    s = torch.empty((nC, H, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
+    s[0] = s0.transpose(1, 2)
+    Yl = Y[L - 1].reshape(H, d, S, nC)
+    PL = P[:, L - 1].contiguous()
     for c in range(1, nC):
-        s[c] = torch.ops.goom.lmme_gadd(P[L - 1][None], s[c - 1][None],
-                                        Yl[:, :, c - 1].contiguous()[None])[0]
-    S_all = s.permute(1, 2, 0).reshape(d, S * nC)                # (d, S nC) like the panels
-    X = torch.ops.goom.lmme_gadd(P, S_all.expand(L, d, S * nC).contiguous(), Y)  # (L, d, S nC)
-    X = X.reshape(L, d, S, nC).permute(2, 3, 0, 1).reshape(S, Tp, d)
-    return X[:, :T]
+        s[c] = torch.ops.goom.lmme_gadd(PL, s[c - 1], Yl[..., c - 1])
+    S_all = s.permute(1, 2, 3, 0).reshape(H, d, N)                      # (H, d, S nC)
+    Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
+    X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)
+    X = X.reshape(H, L, d, S, nC).permute(0, 3, 4, 1, 2).reshape(H, S, Tp, d)
+    return X[:, :, :T]
+
+
+def _chunked_states(params, x0s: np.ndarray, us: np.ndarray, chunk: int) -> torch.Tensor:
+    """One head (S sequences) through _chunked_scan; returns complex128 (S, T, d)."""
+    dev = _dev()
+    u_t = torch.as_tensor(us, dtype=torch.float64, device=dev)
+    Ag = _goom(torch.as_tensor(params.A, device=dev))[None]
+    bu = _bu_heads(torch.as_tensor(params.B, device=dev)[None], u_t[None])
+    s0 = _goom(torch.as_tensor(x0s, dtype=torch.float64, device=dev))[None]
+    return _chunked_scan(Ag, bu, s0, chunk)[0]
 
 
 def ssm_forward_batched(params, x0s, us, block_size=256, chunk=64):
@@ -221,3 +250,187 @@ def ssm_forward_batched(params, x0s, us, block_size=256, chunk=64):
     else:
         state = _scan_states(params, x0s, us, block_size)
     return _finish(params, x0s, us, state, to_host=False)
+
+
+# ---------------------------------------------------------------------------
+# many heads, forward + backward (config 5: 16 heads x 32 sequences, d = 64, T = 4096)
+
+_E2 = math.exp(2.0)
+
+
+def _heads_args(A, B, C, D, x0s, us):
+    dev = _dev()
+    t = [torch.as_tensor(v, dtype=torch.float64, device=dev) for v in (A, B, C, D, x0s, us)]
+    A, B, C, D, x0s, us = t
+    if A.dim() != 3 or A.shape[1] != A.shape[2]:
+        raise ValueError("A must be (H, d, d)")
+    H, d = A.shape[0], A.shape[1]
+    if B.shape != (H, d, d) or C.shape != (H, 2 * d, d) or D.shape != (H, 2 * d, d):
+        raise ValueError("B (H, d, d), C and D (H, 2d, d) must match A")
+    if us.dim() != 4 or us.shape[0] != H or us.shape[-1] != d or us.shape[2] < 1:
+        raise ValueError("us must be (H, S, T, d) with T >= 1")
+    if x0s.shape != (H, us.shape[1], d):
+        raise ValueError("x0s must be (H, S, d)")
+    for m in (A, B, C, D, x0s, us):
+        if not bool(torch.isfinite(m).all()):
+            raise ValueError("inputs must be finite")
+    return A, B, C, D, x0s, us
+
+
+def _sign_of(z: torch.Tensor) -> torch.Tensor:
+    return torch.where(torch.cos(z.imag) < 0, -1.0, 1.0).to(torch.float64)
+
+
+def _scales(sl: torch.Tensor) -> torch.Tensor:
+    c = sl.max(dim=-1).values
+    return torch.where(c == NEG_INF, torch.zeros_like(c), c)
+
+
+def ssm_forward_heads(A, B, C, D, x0s, us, chunk=64):
+    """H heads, each with its own (A, B, C, D) and S sequences: x0s (H, S, d), us
+    (H, S, T, d) -> (state_log, state_sign, scales, y) float64 CUDA tensors with leading
+    (H, S). Every launch covers all heads (the per-head loop of ssm_forward_batched folded
+    into the LMME batch); the recurrence and output map are ssm.py:84-98, 110-137."""
+    A, B, C, D, x0s, us = _heads_args(A, B, C, D, x0s, us)
+    state = _chunked_scan(_goom(A), _bu_heads(B, us), _goom(x0s), chunk)
+    sl, ss = state.real, _sign_of(state)
+    c = _scales(sl)
+    z = ss * torch.exp(sl - c[..., None] + 2.0)
+    H, S, T, d = us.shape
+    y = (torch.bmm(z.reshape(H, S * T, d), C.transpose(1, 2)) +
+         torch.bmm(us.reshape(H, S * T, d), D.transpose(1, 2))).reshape(H, S, T, 2 * d)
+    return sl, ss, c, y
+
+
+def _scaled_outer(alog, asign, b, heads_shape):
+    """sum over (S, T) of a_t b_t^T with a = asign e^{alog} in float64 without underflow
+    of the common scale: a per-head shift m, e^m (a e^{-m})^T b. alog/asign (H, S, T, d),
+    b (H, S, T, d') real -> (H, d, d')."""
+    H = heads_shape
+    m = alog.reshape(H, -1).max(dim=1).values                          # (H,)
+    mf = torch.where(torch.isfinite(m), m, torch.zeros_like(m))
+    a = asign * torch.exp(alog - mf[:, None, None, None])
+    d, d2 = alog.shape[-1], b.shape[-1]
+    out = torch.bmm(a.reshape(H, -1, d).transpose(1, 2), b.reshape(H, -1, d2))
+    out = out * torch.exp(mf)[:, None, None]
+    return torch.where(torch.isfinite(m)[:, None, None], out, torch.zeros_like(out))
+
+
+def _rowwise(alog, asign, M):
+    """a_t M per step (a = asign e^{alog} (H, S, T, d), M (H, d, d')) with a per-step shift,
+    so a step whose adjoint is below float64 range rounds to zero instead of to garbage."""
+    m = alog.max(dim=-1).values
+    mf = torch.where(torch.isfinite(m), m, torch.zeros_like(m))
+    a = asign * torch.exp(alog - mf[..., None])
+    H, S, T, d = alog.shape
+    out = torch.bmm(a.reshape(H, S * T, d), M).reshape(H, S, T, M.shape[-1])
+    return torch.where(torch.isfinite(m)[..., None], out * torch.exp(mf)[..., None],
+                       torch.zeros_like(out))
+
+
+def ssm_backward_heads(A, B, C, D, x0s, us, state_log, state_sign, scales, gy, chunk=64):
+    """Gradients of sum(gy * y) for ssm_forward_heads: (dA, dB, dC, dD, dx0s, dus), the
+    parameter gradients summed over each head's S sequences. The reference has no autodiff
+    (SURVEY §8d config 5); this is the adjoint recurrence, pinned against torch float64
+    autograd (tests/golden/make_golden_ssm_bwd.py) and the oracle's log-domain restatement
+    (oracle/gooms_port.ssm_backward):
+      z_t = s_t e^{l_t - c_t + 2}, c_t = l_{t,i*} (i* the first argmax; constant for an
+      all-zero state), gz_t = C^T gy_t,
+      dL/dx_t (direct) = e^{-c_t} h_t,  h_t = e^2 gz_t - e_{i*} s_{t,i*} (gz_t . z_t),
+      lam_t = A^T (x) lam_{t+1} (+) e^{-c_t} h_t  — a reverse GOOM scan (_chunked_scan on
+      A^T, run on lam e^{K}, K = max_t c_t), so the adjoint stays exact while e^{-c_t} is far
+      below float64 range,
+      dA = sum lam_t x_{t-1}^T (x_{-1} = x0), dB = sum lam_t u_t^T, du_t = B^T lam_t + D^T gy_t,
+      dx0 = A^T lam_0, dC = sum gy_t z_t^T, dD = sum gy_t u_t^T."""
+    A, B, C, D, x0s, us = _heads_args(A, B, C, D, x0s, us)
+    dev = A.device
+    sl = torch.as_tensor(state_log, dtype=torch.float64, device=dev)
+    ss = torch.as_tensor(state_sign, dtype=torch.float64, device=dev)
+    c = torch.as_tensor(scales, dtype=torch.float64, device=dev)
+    gy = torch.as_tensor(gy, dtype=torch.float64, device=dev)
+    H, S, T, d = us.shape
+    if gy.shape != (H, S, T, 2 * d) or sl.shape != (H, S, T, d) or c.shape != (H, S, T):
+        raise ValueError("forward results / gy shapes do not match the inputs")
+    z = ss * torch.exp(sl - c[..., None] + 2.0)
+    gz = torch.bmm(gy.reshape(H, S * T, 2 * d), C).reshape(H, S, T, d)
+    # direct gradient through z_t = x_t e^{2 - c(x_t)}
+    h = _E2 * gz
+    live = sl.max(dim=-1).values != NEG_INF
+    istar = sl.argmax(dim=-1, keepdim=True)
+    corr = torch.gather(ss, -1, istar) * (gz * z).sum(-1, keepdim=True)
+    h = h.scatter_add(-1, istar, -corr * live[..., None].to(h.dtype))
+    # adjoint: reverse-time scan with A^T from a zero adjoint, run on lam e^{K} with K the
+    # sequence's largest scale: the reference LMME clamps its scales at 0 (core.py:250-251),
+    # so adjoints ~ e^{-c_t} below float64 range would vanish, while lam e^{K} >~ 1
+    K = c.max(dim=-1).values                                           # (H, S)
+    g = _goom(h)
+    g = torch.complex(g.real + (K[..., None] - c)[..., None], g.imag)
+    zero = torch.full((H, S, d), complex(NEG_INF, 0.0), dtype=torch.complex128, device=dev)
+    lam = _chunked_scan(_goom(A.transpose(1, 2).contiguous()), g.flip(2), zero, chunk).flip(2)
+    ll, ls = lam.real - K[..., None, None], _sign_of(lam)
+    # x_{t-1} / e^{c_{t-1}}, with x_{-1} = x0
+    x0g = _goom(x0s)
+    c0 = _scales(x0g.real)
+    prev_l = torch.cat([x0g.real[:, :, None], sl[:, :, :-1]], dim=2)
+    prev_s = torch.cat([_sign_of(x0g)[:, :, None], ss[:, :, :-1]], dim=2)
+    prev_c = torch.cat([c0[:, :, None], c[:, :, :-1]], dim=2)
+    xn = prev_s * torch.exp(prev_l - prev_c[..., None])
+    dA = _scaled_outer(ll + prev_c[..., None], ls, xn, H)
+    dB = _scaled_outer(ll, ls, us, H)
+    dus = _rowwise(ll, ls, B) + torch.bmm(gy.reshape(H, S * T, 2 * d), D).reshape(H, S, T, d)
+    dx0s = _rowwise(ll[:, :, :1], ls[:, :, :1], A)[:, :, 0]
+    dC = torch.bmm(gy.reshape(H, S * T, 2 * d).transpose(1, 2), z.reshape(H, S * T, d))
+    dD = torch.bmm(gy.reshape(H, S * T, 2 * d).transpose(1, 2), us.reshape(H, S * T, d))
+    return dA, dB, dC, dD, dx0s, dus
+
+
+@dataclass(frozen=True)
+class SsmGrads:
+    """Gradients of sum(dy * y) for one sequence (numpy float64)."""
+
+    A: np.ndarray
+    B: np.ndarray
+    C: np.ndarray
+    D: np.ndarray
+    x0: np.ndarray
+    u: np.ndarray
+
+
+def ssm_backward(params, run: SsmRun, dy, chunk=64) -> SsmGrads:
+    """Adjoint of ssm_forward_parallel / ssm_forward_sequential for one sequence: the
+    gradients of sum(dy * run.y) with respect to A, B, C, D, x0 and u (see
+    ssm_backward_heads for the recurrence)."""
+    dy = np.asarray(dy, dtype=np.float64)
+    if dy.shape != run.y.shape:
+        raise ValueError("dy must match the output shape (T, 2d)")
+    p = params
+    r = ssm_backward_heads(p.A[None], p.B[None], p.C[None], p.D[None], run.x0[None, None],
+                           run.u[None, None], run.state_log[None, None],
+                           run.state_sign[None, None], run.scales[None, None], dy[None, None],
+                           chunk)
+    dA, dB, dC, dD, dx0, du = (t.cpu().numpy() for t in r)
+    return SsmGrads(A=dA[0], B=dB[0], C=dC[0], D=dD[0], x0=dx0[0, 0], u=du[0, 0])
+
+
+class SsmFunction(torch.autograd.Function):
+    """y = SSM(A, B, C, D, x0s, us) for H heads x S sequences as a differentiable layer:
+    forward = ssm_forward_heads, backward = ssm_backward_heads (a deep RNN stacks these)."""
+
+    @staticmethod
+    def forward(ctx, A, B, C, D, x0s, us, chunk):
+        sl, ss, c, y = ssm_forward_heads(A, B, C, D, x0s, us, chunk)
+        ctx.save_for_backward(A, B, C, D, x0s, us, sl, ss, c)
+        ctx.chunk = chunk
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        A, B, C, D, x0s, us, sl, ss, c = ctx.saved_tensors
+        grads = ssm_backward_heads(A, B, C, D, x0s, us, sl, ss, c, gy.contiguous(), ctx.chunk)
+        return (*grads, None)
+
+
+def ssm_layer(A, B, C, D, x0s, us, chunk=64):
+    """Differentiable multi-head GOOM SSM (float64 CUDA tensors, shapes as in
+    ssm_forward_heads); returns y (H, S, T, 2d)."""
+    return SsmFunction.apply(A, B, C, D, x0s, us, chunk)

@@ -1,8 +1,11 @@
-"""non-diagonal GOOM recurrence, d_state = 64, 16 heads,
-batch 32, T = 4096 — 512 sequences, each head's 32 sequences one affine scan on the GPU
-(ssm.ssm_forward_batched, complex128). Backward: the reference has no autodiff, so there
-is nothing to be parity-tested against ("parity unpinned"); not measured.
-CPU baseline: the reference algorithm (oracle port, float64) on one sequence, x 512.
+"""non-diagonal GOOM recurrence, d_state = 64, 16 heads, batch 32,
+T = 4096 — 512 sequences, forward + backward (ssm.ssm_forward_heads /
+ssm_backward_heads: every launch covers all 16 heads; complex128 log-domain recurrence,
+the reference's float64). Times are device-resident inputs, CUDA events around
+forward and forward+backward; the host->device upload of the float64 inputs is reported
+separately. Parity: head 0 sequence 0 against the oracle port's forward and its
+log-domain adjoint (oracle/gooms_port.ssm_backward).
+CPU baseline: the oracle port (forward scan + adjoint, float64) on one sequence, x 512.
 Prints one JSON line."""
 
 import argparse
@@ -22,6 +25,8 @@ def main():
     ap.add_argument("--heads", type=int, default=16)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--T", type=int, default=4096)
+    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     import torch
 
@@ -30,40 +35,78 @@ def main():
 
     rng = np.random.default_rng(5)
     d, H, S, T = args.d, args.heads, args.batch, args.T
-    params = []
-    for _ in range(H):
-        a = rng.standard_normal((d, d))
-        a *= rng.uniform(1.0, 1.5) / np.max(np.abs(np.linalg.eigvals(a)))
-        params.append(ssm.SsmParams(a, rng.standard_normal((d, d)), rng.standard_normal((2 * d, d)),
-                                    rng.standard_normal((2 * d, d))))
-    x0 = rng.standard_normal((H, S, d))
-    u = rng.standard_normal((H, S, T, d)).astype(np.float64)
-    ssm.ssm_forward_batched(params[0], x0[0, :2], u[0, :2, :256])  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    finite = True
+    A = rng.standard_normal((H, d, d))
     for h in range(H):
-        sl, ss, c, y = ssm.ssm_forward_batched(params[h], x0[h], u[h])
-        finite &= bool(torch.isfinite(sl).all() and torch.isfinite(y).all())
+        A[h] *= rng.uniform(1.0, 1.5) / np.max(np.abs(np.linalg.eigvals(A[h])))
+    B, C, D = (rng.standard_normal((H, r, d)) for r in (d, 2 * d, 2 * d))
+    x0 = rng.standard_normal((H, S, d))
+    u = rng.standard_normal((H, S, T, d))
+    gy = rng.standard_normal((H, S, T, 2 * d))
+    dev = torch.device("cuda")
+    t0 = time.perf_counter()
+    dA_, dB_, dC_, dD_, dx0_, du_, dgy_ = (torch.as_tensor(v, device=dev) for v in (A, B, C, D, x0, u, gy))
     torch.cuda.synchronize()
-    gpu_s = time.perf_counter() - t0
-    # parity spot check: head 0, sequence 0 vs the oracle port
-    osl, oss, oc, oy = G.ssm_forward_parallel(params[0].A, params[0].B, params[0].C, params[0].D,
-                                              x0[0, 0], u[0, 0])
-    sl, ss, c, y = (t.cpu().numpy() for t in ssm.ssm_forward_batched(params[0], x0[0, :1],
-                                                                       u[0, :1]))
-    err = float(np.max(np.abs(sl[0] - osl) / np.maximum(1.0, np.abs(osl))))
+    upload_s = time.perf_counter() - t0
+
+    def fwd():
+        return ssm.ssm_forward_heads(dA_, dB_, dC_, dD_, dx0_, du_, chunk=args.chunk)
+
+    def fwd_bwd():
+        sl, ss, c, y = fwd()
+        return (sl, ss, c, y), ssm.ssm_backward_heads(dA_, dB_, dC_, dD_, dx0_, du_, sl, ss, c,
+                                                      dgy_, chunk=args.chunk)
+
+    # warm-up on a slice
+    ssm.ssm_forward_heads(dA_, dB_, dC_, dD_, dx0_[:, :2], du_[:, :2, :256], chunk=args.chunk)
+    fwd_bwd()
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        ts = []
+        for _ in range(args.reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            r = fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        return float(np.median(ts)), r
+
+    f_s, (sl, ss, c, y) = timed(fwd)
+    fb_s, (_, grads) = timed(fwd_bwd)
+    finite = bool(torch.isfinite(sl).all() and torch.isfinite(y).all() and
+                  all(bool(torch.isfinite(g).all()) for g in grads))
+    # parity: head 0, sequence 0 vs the oracle
+    osl, oss, oc, oy = G.ssm_forward_parallel(A[0], B[0], C[0], D[0], x0[0, 0], u[0, 0])
+    sl0 = sl[0, 0].cpu().numpy()
+    err = float(np.max(np.abs(sl0 - osl) / np.maximum(1.0, np.abs(osl))))
     t1 = time.perf_counter()
-    G.ssm_forward_parallel(params[1].A, params[1].B, params[1].C, params[1].D, x0[1, 0], u[1, 0])
-    cpu_seq_s = time.perf_counter() - t1
+    ob = G.ssm_backward(A[0], B[0], C[0], D[0], x0[0, 0], u[0, 0], osl, oss, oc, gy[0, 0])
+    cpu_bwd_s = time.perf_counter() - t1
+    one = ssm.ssm_backward_heads(dA_[:1], dB_[:1], dC_[:1], dD_[:1], dx0_[:1, :1], du_[:1, :1],
+                                 sl[:1, :1], ss[:1, :1], c[:1, :1], dgy_[:1, :1], chunk=args.chunk)
+    gerr = {k: float(np.max(np.abs(g[0].cpu().numpy() - ob[k])) / np.max(np.abs(ob[k])))
+            for k, g in zip(("A", "B", "C", "D"), one[:4])}
+    gerr["u"] = float(np.max(np.abs(one[5][0, 0].cpu().numpy() - ob["u"])) / np.max(np.abs(ob["u"])))
+    t1 = time.perf_counter()
+    G.ssm_forward_parallel(A[1], B[1], C[1], D[1], x0[1, 0], u[1, 0])
+    cpu_fwd_s = time.perf_counter() - t1
+    steps = H * S * T
     print(json.dumps({
-        "config": "ssm_forward", "d": d, "heads": H, "batch": S, "T": T,
-        "gpu_s": gpu_s, "gpu_steps_per_s": H * S * T / gpu_s, "finite": finite,
-        "gpu_timing": "host float64 inputs -> device, states + outputs left on the device",
-        "parity_rel_log_vs_oracle": err, "sign_mismatch": int(np.sum(ss[0] != oss)),
-        "cpu_one_sequence_s": cpu_seq_s, "cpu_extrapolated_s": cpu_seq_s * H * S,
-        "cpu_kind": "port (oracle/gooms_port.ssm_forward_parallel, float64, one sequence x 512)",
-        "cpu_cores": os.cpu_count(), "backward": "not measured (no reference autodiff)",
+        "config": "ssm_forward_backward", "d": d, "heads": H, "batch": S, "T": T,
+        "chunk": args.chunk, "gpu_forward_s": f_s, "gpu_forward_backward_s": fb_s,
+        "gpu_steps_per_s_fwd": steps / f_s, "gpu_steps_per_s_fwd_bwd": steps / fb_s,
+        "upload_s": upload_s, "finite": finite, "max_scale": float(c.max()),
+        "gpu_timing": "CUDA events, float64 inputs resident on the device; outputs and "
+                      "gradients left on the device",
+        "parity_fwd_rel_log_vs_oracle": err,
+        "sign_mismatch": int(np.sum(ss[0, 0].cpu().numpy() != oss)),
+        "parity_bwd_rel_vs_oracle": gerr,
+        "cpu_one_sequence_fwd_s": cpu_fwd_s, "cpu_one_sequence_bwd_s": cpu_bwd_s,
+        "cpu_extrapolated_fwd_bwd_s": (cpu_fwd_s + cpu_bwd_s) * H * S,
+        "cpu_kind": "port (oracle/gooms_port.ssm_forward_parallel + ssm_backward, float64, "
+                    "one sequence x 512)", "cpu_cores": 1,
     }), flush=True)
 
 
