@@ -28,6 +28,9 @@
 //     pkg/tests/test_scan.py:60-75).
 #include <vector>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "goom_internal.cuh"
 
 namespace goom {
@@ -38,12 +41,26 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxD = 64;
 
+// Walk phase clocks (thread 0 of the single walk CTA), read back by the host when
+// GOOM_WALK_TIMING is set: [0] tile LMME / copy, [1] carry store, [2] column norms,
+// [3] Gram, [4] LU volume test, [5] reset (norms + QR + Q), [6] reset log export,
+// [7] carry copy, [8] tiles, [9] fires.
+__device__ unsigned long long g_walk_prof[16];
+__device__ __forceinline__ void prof_add(bool on, int slot, long long& t0) {
+  if (on && threadIdx.x == 0) {
+    const long long t = clock64();
+    g_walk_prof[slot] += (unsigned long long)(t - t0);
+    t0 = t;
+  }
+}
+
 struct Policy {
   int kind;
   int interval;
   int consume;
   double threshold;
   double log_floor;
+  int timing;
 };
 
 // Shared-memory carve-up of the walk CTA; Rt is the chain's backing precision.
@@ -171,243 +188,303 @@ __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<R
   __syncthreads();
 }
 
-// Column log-norms nu_j (FP64) into sm.vec[0..d); returns true if a column is all zero.
-// Thread (column cc = tid % 64, row chunk ch = tid / 64) covers rows ch, ch+4, ...: the
-// per-column max and sum of squares are 4-way partials combined through sm.part.
+// ---- register-resident column kernels (d <= 64, 256 threads) -------------------------
+// Warp w owns columns 8w .. 8w+7; lane l holds column c = 8w + l/4, rows r = l%4 + 4i
+// (i < 16) in registers. Column reductions are 4-lane shuffles, so the column norms, the
+// Householder updates and the Q accumulation need no CTA barrier; the QR's only barrier
+// per column publishes the reflector.
+struct ColLane {
+  int c, rc;
+};
+__device__ __forceinline__ ColLane col_lane() {
+  return ColLane{(int)(threadIdx.x >> 5) * 8 + (int)((threadIdx.x & 31) >> 2), (int)(threadIdx.x & 3)};
+}
+__device__ __forceinline__ double quad_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+__device__ __forceinline__ double quad_max(double v) {
+  v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  return fmax(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+
+// Log-unit-normalised columns (lyapunov.py:255-263) of X (smem GOOMs, d x d): this
+// thread's column into x, the whole matrix into sm.R (row-major, for the Gram) and the
+// column log-norms nu_c = m + 1/2 log sum e^{2(L - m)} into sm.vec[0, d). Returns true
+// (CTA-uniform) when some column is all zero.
 template <class Rt>
-__device__ bool unit_columns(const Cx<Rt>* X, int d, const Smem<Rt>& sm) {
-  static_assert(kThreads == 4 * kMaxD, "column-parallel mapping: 4 row chunks x 64 columns");
-  const int tid = threadIdx.x, cc = tid & (kMaxD - 1), ch = tid / kMaxD;
-  if (tid == 0) sm.ints[0] = 0;
+__device__ bool unit_columns_regs(const Cx<Rt>* X, int d, double (&x)[16], const Smem<Rt>& sm) {
+  const ColLane L = col_lane();
+  const bool live = L.c < d;
+  double lg[16];
   double m = -INFINITY;
-  if (cc < d)
-    for (int r = ch; r < d; r += 4) m = fmax(m, (double)X[r * d + cc].x);
-  sm.part[ch * kMaxD + cc] = m;
-  __syncthreads();
-  double cm = -INFINITY;
-  if (cc < d) {
-    cm = fmax(fmax(sm.part[cc], sm.part[kMaxD + cc]),
-              fmax(sm.part[2 * kMaxD + cc], sm.part[3 * kMaxD + cc]));
-    if (cm == -INFINITY && ch == 0) sm.ints[0] = 1;
-  }
-  double acc = 0.0;
-  if (cc < d && cm != -INFINITY)
-    for (int r = ch; r < d; r += 4) acc += exp(2.0 * ((double)X[r * d + cc].x - cm));
-  __syncthreads();  // every thread has read its column max before the partials are reused
-  sm.part[ch * kMaxD + cc] = acc;
-  __syncthreads();
-  if (cc < d && ch == 0)
-    sm.vec[cc] = cm == -INFINITY
-                     ? -INFINITY
-                     : cm + 0.5 * log(((sm.part[cc] + sm.part[kMaxD + cc]) +
-                                       sm.part[2 * kMaxD + cc]) + sm.part[3 * kMaxD + cc]);
-  __syncthreads();
-  bool zero = sm.ints[0] != 0;
-  if (!zero) {
-    for (int e = tid; e < d * d; e += kThreads) {
-      Cx<Rt> z = X[e];
-      sm.R[e] = (double)goom_sign_t<Rt>(z.y) * exp((double)z.x - sm.vec[e % d]);
-    }
-  }
-  __syncthreads();
-  return zero;
-}
-
-// slogdet(R) via LU with partial pivoting on W; returns (det == 0) || logdet < floor.
-// One barrier per pivot: rows are never swapped (a double-buffered logical -> physical
-// row map instead), and the threads updating column c+1 also reduce its pivot candidates
-// (4 row-chunk partials, smallest row among equal maxima, as idamax), so the next step
-// starts with its pivot known. Column-parallel mapping: column cc = tid % 64 > c, logical
-// rows c+1+ch, +4, ...
-template <class Rt>
-__device__ bool volume_deficient(int d, double log_floor, const Smem<Rt>& sm) {
-  const int tid = threadIdx.x;
-  const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;
-  double* pmax = sm.part;     // [2][4]
-  int* pidx = sm.iw;          // [2][4]
-  int* perm = sm.iw + 8;      // [2][kMaxD]
-  for (int e = tid; e < d * d; e += kThreads) sm.W[e] = sm.R[e];
-  if (tid < d) perm[tid] = tid;
-  if (cc == 0) {
-    double best = -1.0;
-    int bi = d;
-    for (int r = ch; r < d; r += 4) {
-      const double v = fabs(sm.R[r * d]);
-      if (v > best) { best = v; bi = r; }
-    }
-    pmax[ch] = best;
-    pidx[ch] = bi;
-  }
-  __syncthreads();
-  // log|det| = log(prod |pv|) kept as mantissa * 2^exponent: one log at the end, not per pivot
-  double mant = 1.0;
-  int expo = 0;
-  for (int c = 0; c < d; ++c) {
-    const int cur = c & 1, nxt = cur ^ 1;
-    double best = pmax[cur * 4];
-    int piv = pidx[cur * 4];
 #pragma unroll
-    for (int k = 1; k < 4; ++k) {
-      const double v = pmax[cur * 4 + k];
-      const int i = pidx[cur * 4 + k];
-      if (v > best || (v == best && i < piv)) { best = v; piv = i; }
+  for (int i = 0; i < 16; ++i) {
+    const int r = L.rc + 4 * i;
+    lg[i] = -INFINITY;
+    x[i] = 1.0;
+    if (live && r < d) {
+      const Cx<Rt> z = X[r * d + L.c];
+      lg[i] = (double)z.x;
+      x[i] = (double)goom_sign_t<Rt>(z.y);
     }
-    const int* pc = perm + cur * kMaxD;
-    int* pn = perm + nxt * kMaxD;
-    const int rowc = pc[piv];  // physical pivot row: logical row c from now on
-    const int rowp = pc[c];    // physical row that moves to logical row piv
-    const double pv = sm.W[rowc * d + c];
-    if (pv == 0.0) return true;  // det_sign == 0 (uniform across the CTA)
-    int e;
-    mant = frexp(mant * fabs(pv), &e);
-    expo += e;
-    const double inv = 1.0 / pv;
-    if (tid < d) pn[tid] = tid == c ? rowc : (tid == piv ? rowp : pc[tid]);
-    double nb = -1.0;
-    int ni = d;
-    if (cc > c && cc < d) {
-      const double u = sm.W[rowc * d + cc];
-      for (int r = c + 1 + ch; r < d; r += 4) {
-        const int pr = r == piv ? rowp : pc[r];
-        const double nv = sm.W[pr * d + cc] - (sm.W[pr * d + c] * inv) * u;
-        sm.W[pr * d + cc] = nv;
-        if (cc == c + 1) {
-          const double a = fabs(nv);
-          if (a > nb) { nb = a; ni = r; }
-        }
-      }
-    }
-    if (cc == c + 1) {
-      pmax[nxt * 4 + ch] = nb;
-      pidx[nxt * 4 + ch] = ni;
-    }
-    __syncthreads();
+    m = fmax(m, lg[i]);
   }
-  return log(mant) + expo * 0.69314718055994530942 < log_floor;
+  m = quad_max(m);
+  const bool zero = live && m == -INFINITY;
+  double s0 = 0.0, s1 = 0.0;
+  if (m != -INFINITY) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      s0 += exp(2.0 * (lg[i] - m));
+      s1 += exp(2.0 * (lg[i + 1] - m));
+    }
+  }
+  const double ss = quad_sum(s0 + s1);  // every lane: full-warp shuffle
+  const double nu = m == -INFINITY ? -INFINITY : m + 0.5 * log(ss);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = L.rc + 4 * i;
+    x[i] = (live && r < d && !zero) ? x[i] * exp(lg[i] - nu) : 0.0;
+    if (live && r < d) sm.R[r * d + L.c] = x[i];
+  }
+  if (live && L.rc == 0) sm.vec[L.c] = nu;
+  return __syncthreads_or(zero) != 0;
 }
 
+// max_{i<j} |G_ij|, G = R^T R of sm.R (the unit-column Gram, lyapunov.py:146-155):
+// 4 x 4 register tiles, one pass over the rows.
 template <class Rt>
-__device__ bool policy_select(const Cx<Rt>* X, int d, const Policy& pol, const Smem<Rt>& sm) {
-  if (pol.kind == GOOM_POLICY_NEVER) return false;
-  bool zero = unit_columns(X, d, sm);
-  if (pol.kind == GOOM_POLICY_NORM_THRESHOLD) {
-    double m = -INFINITY;
-    for (int j = threadIdx.x; j < d; j += kThreads) m = fmax(m, sm.vec[j]);
-    return block_max(m, sm.red) > pol.threshold;
+__device__ double gram_offdiag_max(int d, const Smem<Rt>& sm) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int r = 0; r < d; ++r) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ty + 16 * a, j = tx + 16 * a;
+      av[a] = i < d ? sm.R[r * d + i] : 0.0;
+      bv[a] = j < d ? sm.R[r * d + j] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
   }
-  if (zero) return true;
   double g = 0.0;
-  for (int e = threadIdx.x; e < d * d; e += kThreads) {
-    int i = e / d, j = e % d;
-    if (i >= j) continue;
-    double acc = 0.0;
-    for (int r = 0; r < d; ++r) acc = fma(sm.R[r * d + i], sm.R[r * d + j], acc);
-    g = fmax(g, fabs(acc));
-  }
-  if (block_max(g, sm.red) > pol.threshold) return true;
-  if (pol.log_floor == -INFINITY) return false;
-  return volume_deficient(d, pol.log_floor, sm);
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      if (i < j && j < d) g = fmax(g, fabs(acc[a][b]));
+    }
+  return block_max(g, sm.red);
 }
 
-// Householder QR of sm.R in place; Q into sm.W. positive_diag flips Q columns so
-// that diag(R) > 0 (the CGS2 basis). Returns GOOM_ERANK on a rank-deficient state.
+// Householder QR (LAPACK dgeqr2 / dlarfg arithmetic) of the register-resident matrix.
+// Reflector j goes to sm.W as row j of V^T (v_j[j] = 1, zero above), tau_j to
+// sm.vec[0, d), R_jj to sm.vec[d, 2d). x is consumed. One CTA barrier per column.
 template <class Rt>
-__device__ int householder_q(int d, bool positive_diag, const Smem<Rt>& sm,
-                             bool check_rank = true) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int cc = tid & (kMaxD - 1), ch = tid / kMaxD;  // column, row chunk (4 x 64 threads)
-  double* tau = sm.vec;      // [0, d)
-  double* diag = sm.vec + d;  // [d, 2d)
+__device__ void qr_regs(double (&x)[16], int d, const Smem<Rt>& sm) {
+  const ColLane L = col_lane();
+  const int warp = threadIdx.x >> 5, qbase = threadIdx.x & 28;
+  double* Vt = sm.W;
+  double* tau = sm.vec;
+  double* diag = sm.vec + d;
   for (int j = 0; j < d; ++j) {
-    if (w == 0) {
-      double s = 0.0;
-      for (int r = j + 1 + lane; r < d; r += 32) s = fma(sm.R[r * d + j], sm.R[r * d + j], s);
-      s = warp_sum_d(s);
-      if (lane == 0) {
-        double alpha = sm.R[j * d + j];
-        if (s == 0.0) {
-          tau[j] = 0.0;
-          diag[j] = alpha;
-          sm.red[0] = 0.0;
-        } else {
-          double beta = -copysign(sqrt(fma(alpha, alpha, s)), alpha);
-          tau[j] = (beta - alpha) / beta;
+    if (warp < (j >> 3)) break;   // every column of this warp is final; the warps still
+                                  // active sync on a named barrier sized to them
+    if (warp == (j >> 3)) {       // the warp owning column j builds the reflector; full-warp
+                                  // shuffles, only the quad of column j keeps its values
+      double s0 = 0.0, s1 = 0.0, alpha = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = L.rc + 4 * i;
+        if (r > j && r < d) {
+          if (i & 1) s1 = fma(x[i], x[i], s1);
+          else s0 = fma(x[i], x[i], s0);
+        }
+        if (r == j) alpha = x[i];
+      }
+      const double s = quad_sum(s0 + s1);
+      alpha = __shfl_sync(0xffffffffu, alpha, qbase | (j & 3));
+      if (L.c == j) {
+        // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta,
+        // v = x / (alpha - beta); one rsqrt and one reciprocal instead of sqrt + 2 divisions
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+          const double n2 = fma(alpha, alpha, s);
+          const double rn = rsqrt(n2);
+          const double nrm = n2 * rn;
+          beta = -copysign(nrm, alpha);
+          t = fma(fabs(alpha), rn, 1.0);                 // (beta - alpha) / beta
+          scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);  // 1 / (alpha - beta)
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = L.rc + 4 * i;
+          if (r < d) Vt[j * d + r] = r > j ? x[i] * scale : (r == j ? 1.0 : 0.0);
+        }
+        if (L.rc == 0) {
+          tau[j] = t;
           diag[j] = beta;
-          sm.red[0] = 1.0 / (alpha - beta);
-          sm.R[j * d + j] = beta;
         }
       }
     }
-    __syncthreads();
-    const double scale = sm.red[0];
-    const double tj = tau[j];
-    if (tj != 0.0) {
-      if (tid > j && tid < d) sm.R[tid * d + j] *= scale;  // v_r (v_j = 1 implicit)
-      __syncthreads();
-      // w_c = tau (R_jc + sum_{r>j} v_r R_rc) for c > j: thread (cc, ch) sums rows j+1+ch, +4..
-      double p = 0.0;
-      if (cc > j && cc < d) {
-        if (ch == 0) p = sm.R[j * d + cc];
-        for (int r = j + 1 + ch; r < d; r += 4) p = fma(sm.R[r * d + j], sm.R[r * d + cc], p);
+    asm volatile("bar.sync 1, %0;" ::"r"((kWarps - (j >> 3)) * 32) : "memory");
+    const double t = tau[j];
+    if (t != 0.0) {
+      double p0 = 0.0, p1 = 0.0, v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = L.rc + 4 * i;
+        v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
+        if (i & 1) p1 = fma(v[i], x[i], p1);
+        else p0 = fma(v[i], x[i], p0);
       }
-      sm.part[ch * kMaxD + cc] = p;
-      __syncthreads();
-      if (cc > j && cc < d) {
-        const double wc = (((sm.part[cc] + sm.part[kMaxD + cc]) + sm.part[2 * kMaxD + cc]) +
-                           sm.part[3 * kMaxD + cc]) * tj;
-        if (ch == 0) sm.R[j * d + cc] -= wc;
-        for (int r = j + 1 + ch; r < d; r += 4) sm.R[r * d + cc] -= wc * sm.R[r * d + j];
+      const double w = t * quad_sum(p0 + p1);
+      if (L.c > j && L.c < d) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = fma(-w, v[i], x[i]);
       }
     }
-    __syncthreads();
-  }
-  // Q = H_0 ... H_{d-1} I, accumulated backwards (LAPACK dorg2r order), same mapping
-  for (int e = tid; e < d * d; e += kThreads) sm.W[e] = (e / d == e % d) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int j = d - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    double p = 0.0;
-    if (cc < d) {
-      if (ch == 0) p = sm.W[j * d + cc];
-      for (int r = j + 1 + ch; r < d; r += 4) p = fma(sm.R[r * d + j], sm.W[r * d + cc], p);
-    }
-    sm.part[ch * kMaxD + cc] = p;
-    __syncthreads();
-    if (cc < d) {
-      const double wc = (((sm.part[cc] + sm.part[kMaxD + cc]) + sm.part[2 * kMaxD + cc]) +
-                         sm.part[3 * kMaxD + cc]) * tj;
-      if (ch == 0) sm.W[j * d + cc] -= wc;
-      for (int r = j + 1 + ch; r < d; r += 4) sm.W[r * d + cc] -= wc * sm.R[r * d + j];
-    }
-    __syncthreads();
-  }
-  int rc = GOOM_OK;
-  if (positive_diag) {
-    const double tiny = 64.0 * 2.220446049250313e-16;
-    if (check_rank)
-      for (int j = 0; j < d; ++j)
-        if (fabs(diag[j]) < tiny) rc = GOOM_ERANK;
-    if (rc == GOOM_OK)
-      for (int e = tid; e < d * d; e += kThreads)
-        if (diag[e % d] < 0.0) sm.W[e] = -sm.W[e];
   }
   __syncthreads();
-  return rc;
 }
 
-// reset(X) -> out (smem or global), canonical GOOMs. Returns a goom_status.
+// Q = H_0 ... H_{d-1} I (LAPACK dorg2r order) from qr_regs' reflectors into q, this
+// thread's column; no barriers (every warp applies all reflectors to its own columns).
+// positive_diag flips columns so that diag(R) > 0 (the CGS2 basis, lyapunov.py:175-194).
 template <class Rt>
-__device__ int policy_reset(const Cx<Rt>* X, Cx<Rt>* out, int d, int kind, const Smem<Rt>& sm) {
-  bool zero = unit_columns(X, d, sm);
-  if (zero) return GOOM_ERANK;
-  int rc = householder_q(d, kind == GOOM_POLICY_COLINEARITY, sm);
-  if (rc != GOOM_OK) return rc;
-  for (int e = threadIdx.x; e < d * d; e += kThreads) {
-    double q = sm.W[e];
-    out[e] = cx<Rt>((Rt)log(fabs(q)), q < 0.0 ? pi_of<Rt>() : Rt(0));
+__device__ void q_regs(double (&q)[16], int d, bool positive_diag, const Smem<Rt>& sm) {
+  const ColLane L = col_lane();
+  const double* Vt = sm.W;
+  const double* tau = sm.vec;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) q[i] = (L.rc + 4 * i == L.c) ? 1.0 : 0.0;
+  for (int j = d - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    double p0 = 0.0, p1 = 0.0, v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = L.rc + 4 * i;
+      v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
+      if (i & 1) p1 = fma(v[i], q[i], p1);
+      else p0 = fma(v[i], q[i], p0);
+    }
+    const double w = t * quad_sum(p0 + p1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) q[i] = fma(-w, v[i], q[i]);
+  }
+  if (positive_diag && L.c < d && sm.vec[d + L.c] < 0.0)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) q[i] = -q[i];
+}
+
+// log|det| of the factored matrix from R's diagonal (= the LU slogdet of the reference,
+// np.linalg.slogdet, up to rounding): true on det == 0 or log|det| < floor.
+template <class Rt>
+__device__ bool volume_deficient_qr(int d, double log_floor, const Smem<Rt>& sm) {
+  if (threadIdx.x < 32) {
+    double l = 0.0;
+    for (int j = threadIdx.x; j < d; j += 32) l += log(fabs(sm.vec[d + j]));
+    l = warp_sum_d(l);
+    if (threadIdx.x == 0) sm.red[2 * kWarps - 1] = l;
   }
   __syncthreads();
+  return sm.red[2 * kWarps - 1] < log_floor;
+}
+
+// sum_j nu_j of the column log-norms unit_columns_regs left in sm.vec[0, d)
+template <class Rt>
+__device__ double col_lognorm_sum(int d, const Smem<Rt>& sm) {
+  if (threadIdx.x < 32) {
+    double l = 0.0;
+    for (int j = threadIdx.x; j < d; j += 32) l += sm.vec[j];
+    l = warp_sum_d(l);
+    if (threadIdx.x == 0) sm.red[2 * kWarps - 2] = l;
+  }
+  __syncthreads();
+  return sm.red[2 * kWarps - 2];
+}
+
+// rank-deficiency floor of the CGS2 reset (lyapunov.py:191-192): |R_jj| < 64 eps
+template <class Rt>
+__device__ bool rank_deficient(int d, const Smem<Rt>& sm) {
+  const double tiny = 64.0 * 2.220446049250313e-16;
+  bool bad = false;
+  for (int j = threadIdx.x; j < d; j += kThreads) bad |= fabs(sm.vec[d + j]) < tiny;
+  return __syncthreads_or(bad) != 0;
+}
+
+// the register column q (rows rc + 4i of column c) -> canonical GOOMs in out (d x d)
+template <class Rt>
+__device__ void export_goom(const double (&q)[16], Cx<Rt>* out, int d) {
+  const ColLane L = col_lane();
+  if (L.c < d)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = L.rc + 4 * i;
+      if (r < d) out[r * d + L.c] = cx<Rt>((Rt)log(fabs(q[i])), q[i] < 0.0 ? pi_of<Rt>() : Rt(0));
+    }
+}
+
+// The policy on one state X (smem): predicate, and on a fire the reset value into out.
+// Returns a goom_status (GOOM_ERANK: the reset of a zero / rank-deficient state); *fire
+// says whether the predicate fired. select_only: predicate only (policy_select).
+template <class Rt>
+__device__ int apply_policy(const Cx<Rt>* X, Cx<Rt>* out, int d, const Policy& pol,
+                            const Smem<Rt>& sm, bool select_only, bool force_fire, bool* fire,
+                            double ldet_x = NAN) {
+  *fire = false;
+  if (pol.kind == GOOM_POLICY_NEVER && !force_fire) return GOOM_OK;
+  long long t0 = clock64();
+  double x[16];
+  const bool zero = unit_columns_regs(X, d, x, sm);
+  prof_add(pol.timing, 2, t0);
+  bool f = force_fire, factored = false;
+  if (pol.kind == GOOM_POLICY_NORM_THRESHOLD) {
+    if (!f) {
+      double m = -INFINITY;
+      for (int j = threadIdx.x; j < d; j += kThreads) m = fmax(m, sm.vec[j]);
+      f = block_max(m, sm.red) > pol.threshold;
+    }
+  } else if (pol.kind == GOOM_POLICY_COLINEARITY || force_fire) {
+    f = f || zero;
+    if (!f && !zero) {
+      f = gram_offdiag_max(d, sm) > pol.threshold;
+      prof_add(pol.timing, 3, t0);
+    }
+    if (!zero && !f && pol.log_floor != -INFINITY) {
+      if (!isnan(ldet_x)) {
+        // log|det| of the unit-column matrix = log|det X| - sum_j nu_j, with log|det X|
+        // known from the walk (det is multiplicative): no factorisation on this path
+        f = ldet_x - col_lognorm_sum(d, sm) < pol.log_floor;
+      } else {
+        qr_regs(x, d, sm);
+        factored = true;
+        f = volume_deficient_qr(d, pol.log_floor, sm);
+      }
+      prof_add(pol.timing, 4, t0);
+    }
+  }
+  *fire = f;
+  if (!f || select_only) return GOOM_OK;
+  if (zero) return GOOM_ERANK;
+  if (!factored) qr_regs(x, d, sm);
+  const bool colin = pol.kind == GOOM_POLICY_COLINEARITY;
+  if (colin && rank_deficient(d, sm)) return GOOM_ERANK;
+  q_regs(x, d, colin, sm);
+  prof_add(pol.timing, 5, t0);
+  export_goom<Rt>(x, out, d);
+  __syncthreads();
+  prof_add(pol.timing, 6, t0);
   return GOOM_OK;
 }
 
@@ -423,17 +500,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     selective_walk_kernel(const Cx<Rt>* __restrict__ loc0, const Cx<Rt>* __restrict__ loc1,
                           Cx<Rt>* __restrict__ carries, int8_t* __restrict__ modes,
                           int64_t* __restrict__ sites, int64_t* __restrict__ n_sites,
-                          int* __restrict__ status, int64_t T, int d, int s, Policy pol) {
+                          int* __restrict__ status, int64_t T, int d, int s, Policy pol,
+                          const double* __restrict__ ldet0, const double* __restrict__ ldet1) {
   extern __shared__ __align__(16) char smem_raw[];
   Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   const int64_t ntiles = (T + s - 1) / s;
   int64_t nsite = 0;
   bool have_carry = false, consumed = false;
+  // log|det| of the carry (colinearity volume test): el = loc (x) carry, so
+  // log|det el| = log|det loc| (batched pre-pass) + log|det carry|; a reset carry is
+  // orthonormal (log|det| = 0), a kept carry is the previous el
+  double ldc = 0.0;
+  const bool tm = pol.timing != 0;
+  long long t0 = clock64();
   for (int64_t k = 0; k < ntiles; ++k) {
     const int64_t lo = k * s;
     const int64_t p = (lo + s < T ? lo + s : T) - 1;
     int8_t mode;
+    if (tm && threadIdx.x == 0) g_walk_prof[8] += 1;
+    prof_add(tm, 7, t0);
     if (!have_carry) {
       mode = 0;
       copy_mat(loc0 + p * mat, sm.el, d);
@@ -445,14 +531,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       mode = 1;
       block_lmme(loc0 + p * mat, sm.carry, sm.el, d, sm);
     }
+    prof_add(tm, 0, t0);
     if (mode > 0)
       for (int e = threadIdx.x; e < d * d; e += kThreads) carries[k * mat + e] = sm.carry[e];
     if (threadIdx.x == 0) modes[k] = mode;
+    prof_add(tm, 1, t0);
     consumed = false;
     bool fire = false;
-    if ((p % s) == s - 1 && p <= T - 2) fire = policy_select(sm.el, d, pol, sm);
+    double ldel = NAN;
+    if (ldet0) ldel = mode == 0 ? ldet0[k] : mode == 1 ? ldet0[k] + ldc : (p == lo ? ldc : ldet1[k] + ldc);
+    int rc = GOOM_OK;
+    if ((p % s) == s - 1 && p <= T - 2)
+      rc = apply_policy(sm.el, sm.carry, d, pol, sm, /*select_only=*/false, false, &fire, ldel);
+    ldc = fire ? 0.0 : ldel;
+    if (tm) t0 = clock64();
     if (fire) {
-      int rc = policy_reset(sm.el, sm.carry, d, pol.kind, sm);
+      if (tm && threadIdx.x == 0) g_walk_prof[9] += 1;
       if (rc != GOOM_OK) {
         if (threadIdx.x == 0) *status = rc;
         break;
@@ -496,7 +590,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   copy_mat(X + blockIdx.x * mat, sm.el, d);
-  bool f = policy_select(sm.el, d, pol, sm);
+  bool f = false;
+  apply_policy(sm.el, sm.el, d, pol, sm, /*select_only=*/true, false, &f);
   if (threadIdx.x == 0) fire[blockIdx.x] = f ? 1 : 0;
 }
 
@@ -507,8 +602,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   copy_mat(X + blockIdx.x * mat, sm.el, d);
-  int rc = policy_reset(sm.el, R + blockIdx.x * mat, d, kind, sm);
+  Policy pol{kind, 1, 0, 0.0, -INFINITY, 0};
+  bool f = false;
+  int rc = apply_policy(sm.el, R + blockIdx.x * mat, d, pol, sm, false, /*force_fire=*/true, &f);
   if (rc != GOOM_OK && threadIdx.x == 0) *status = rc;
+}
+
+// log|det| of the tiles' local products (the walk's volume test): CTA k takes the
+// matrix at position min(k s + s, T) - 1 of loc; log|det| = log|det U| + sum_j nu_j with
+// U the unit-column matrix (QR diagonal); -inf for a zero column.
+template <class Rt>
+__global__ void __launch_bounds__(kThreads, 1)
+    tile_logdet_kernel(const Cx<Rt>* __restrict__ loc, int64_t T, int d, int s,
+                       double* __restrict__ out) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem<Rt> sm = carve<Rt>(smem_raw, d);
+  const int64_t mat = (int64_t)d * d;
+  const int64_t lo = (int64_t)blockIdx.x * s;
+  const int64_t p = (lo + s < T ? lo + s : T) - 1;
+  copy_mat(loc + p * mat, sm.el, d);
+  double x[16];
+  if (unit_columns_regs(sm.el, d, x, sm)) {
+    if (threadIdx.x == 0) out[blockIdx.x] = -INFINITY;
+    return;
+  }
+  const double nus = col_lognorm_sum(d, sm);
+  qr_regs(x, d, sm);
+  if (threadIdx.x < 32) {
+    double l = 0.0;
+    for (int j = threadIdx.x; j < d; j += 32) l += log(fabs(sm.vec[d + j]));
+    l = warp_sum_d(l);
+    if (threadIdx.x == 0) out[blockIdx.x] = l + nus;
+  }
 }
 
 // Batched Householder QR with R's diagonal made non-negative (qr_factor_batched,
@@ -523,18 +648,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) char smem_raw[];
   Smem<double> sm = carve<double>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
+  const ColLane L = col_lane();
+  double x[16];
   if (X) {
     copy_mat(X + blockIdx.x * mat, sm.el, d);
-    if (unit_columns(sm.el, d, sm)) {
+    if (unit_columns_regs(sm.el, d, x, sm)) {
       if (threadIdx.x == 0) *status = GOOM_EINVAL;
       return;
     }
   } else {
-    for (int e = threadIdx.x; e < d * d; e += kThreads) sm.R[e] = M[blockIdx.x * mat + e];
-    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = L.rc + 4 * i;
+      x[i] = (L.c < d && r < d) ? M[blockIdx.x * mat + r * d + L.c] : 0.0;
+    }
   }
-  householder_q(d, /*positive_diag=*/true, sm, /*check_rank=*/false);
-  for (int e = threadIdx.x; e < d * d; e += kThreads) Q[blockIdx.x * mat + e] = sm.W[e];
+  qr_regs(x, d, sm);
+  q_regs(x, d, /*positive_diag=*/true, sm);
+  if (L.c < d)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = L.rc + 4 * i;
+      if (r < d) Q[blockIdx.x * mat + r * d + L.c] = x[i];
+    }
   if (absdiag)
     for (int j = threadIdx.x; j < d; j += kThreads) absdiag[blockIdx.x * d + j] = fabs(sm.vec[d + j]);
 }
@@ -552,7 +688,9 @@ int check_policy(const goom_reset_policy* p, int d) {
 }
 
 Policy to_policy(const goom_reset_policy* p) {
-  return Policy{p->kind, p->check_interval, p->consume_leaf, p->threshold, p->log_volume_floor};
+  static const bool timing = std::getenv("GOOM_WALK_TIMING") != nullptr;
+  return Policy{p->kind, p->check_interval, p->consume_leaf, p->threshold, p->log_volume_floor,
+                timing ? 1 : 0};
 }
 
 template <class Rt>
@@ -602,6 +740,7 @@ size_t workspace_bytes(int64_t T, int d, const goom_reset_policy* policy) {
   size_t b = round_up(mat * T);                               // loc0
   if (policy->consume_leaf && s > 1) b += round_up(mat * T);  // loc1
   b += round_up(mat * nt) + round_up(nt) + round_up(sizeof(int) * 4);
+  b += 2 * round_up(sizeof(double) * (size_t)nt);             // tile log-determinants
   b += 2 * round_up(sizeof(Rt) * (size_t)T * d) + 256;        // LMME scale scratch + flag
   return b;
 }
@@ -638,6 +777,10 @@ int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_res
   off += round_up(nt);
   int* status = reinterpret_cast<int*>(base + off);
   off += round_up(sizeof(int) * 4);
+  double* ldet0 = reinterpret_cast<double*>(base + off);
+  off += round_up(sizeof(double) * (size_t)nt);
+  double* ldet1 = reinterpret_cast<double*>(base + off);
+  off += round_up(sizeof(double) * (size_t)nt);
   void* lws = base + off;
   size_t lws_bytes = ws_bytes - off;
 
@@ -648,10 +791,41 @@ int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_res
   if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
     return cuda_fail(cudaGetLastError(), "status reset");
   GOOM_TRY(set_smem<Rt>((const void*)selective_walk_kernel<Rt>, d));
+  const Policy pol = to_policy(policy);
+  // the volume test's log|det| of every tile's local product, batched off the walk
+  static const bool direct_volume = std::getenv("GOOM_WALK_DIRECT_VOLUME") != nullptr;
+  const bool track_det = pol.kind == GOOM_POLICY_COLINEARITY && pol.log_floor != -INFINITY &&
+                         !direct_volume;
+  if (track_det) {
+    GOOM_TRY(set_smem<Rt>((const void*)tile_logdet_kernel<Rt>, d));
+    tile_logdet_kernel<Rt><<<(unsigned)nt, kThreads, smem_bytes<Rt>(d), st>>>(loc0, T, d, (int)s,
+                                                                             ldet0);
+    GOOM_CHECK_LAUNCH("tile_logdet_kernel");
+    if (need_loc1) {
+      tile_logdet_kernel<Rt><<<(unsigned)nt, kThreads, smem_bytes<Rt>(d), st>>>(loc1, T, d,
+                                                                               (int)s, ldet1);
+      GOOM_CHECK_LAUNCH("tile_logdet_kernel");
+    }
+  }
+  if (pol.timing) {
+    unsigned long long zero[16] = {};
+    cudaMemcpyToSymbolAsync(g_walk_prof, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+  }
   selective_walk_kernel<Rt><<<1, kThreads, smem_bytes<Rt>(d), st>>>(
-      loc0, loc1 ? loc1 : loc0, carries, modes, sites, n_sites, status, T, d, (int)s,
-      to_policy(policy));
+      loc0, loc1 ? loc1 : loc0, carries, modes, sites, n_sites, status, T, d, (int)s, pol,
+      track_det ? ldet0 : nullptr, need_loc1 ? ldet1 : ldet0);
   GOOM_CHECK_LAUNCH("selective_walk_kernel");
+  if (pol.timing) {  // debug aid: per-phase clocks of the walk (synchronises the stream)
+    unsigned long long c[16];
+    cudaMemcpyFromSymbolAsync(c, g_walk_prof, sizeof(c), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const char* names[10] = {"tile lmme", "carry store", "col norms", "gram", "lu volume",
+                             "reset qr", "reset export", "carry copy", "tiles", "fires"};
+    std::fprintf(stderr, "[walk timing] tiles %llu fires %llu:", c[8], c[9]);
+    for (int i = 0; i < 8; ++i)
+      std::fprintf(stderr, " %s %.1f us/tile;", names[i], c[8] ? c[i] / 1.9e3 / c[8] : 0.0);
+    std::fprintf(stderr, " (clock64 cycles / 1.9 GHz)\n");
+  }
   // 3. materialise: tile 0 = loc0; tile k>0: loc[t] (x) carry[k]
   if (need_loc1) {
     adopt_loc1_kernel<C><<<(unsigned)nt, 256, 0, st>>>(loc0, loc1, modes, T, d, (int)s);

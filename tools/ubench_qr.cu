@@ -1,0 +1,162 @@
+// Micro-benchmark (profiling aid, not product): latency of the selective walk's 64 x 64
+// FP64 Householder QR (selective.cu qr_regs) in one CTA, with a per-phase clock64 split
+// of an instrumented copy. Built against the library's objects:
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
+//        -Ipaper_2510_03426_b200/csrc -o tools/bin/ubench_qr tools/ubench_qr.cu \
+//        $(ls paper_2510_03426_b200/csrc/build/*.o | grep -v selective.o)
+#include "../paper_2510_03426_b200/csrc/selective.cu"
+
+namespace goom {
+namespace {
+
+__device__ long long g_ph[8];
+
+// current qr_regs with phase clocks, summed over columns by the owner lane (rc == 0) of
+// each column: [0] norm + quad shuffles, [1] reflector scalars, [2] V stores, [3] barrier,
+// [4] dot + update (as seen by the owner of column j+1)
+template <class Rt>
+__device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
+  const ColLane L = col_lane();
+  const int warp = threadIdx.x >> 5, qbase = threadIdx.x & 28;
+  double* Vt = sm.W;
+  double* tau = sm.vec;
+  double* diag = sm.vec + d;
+  for (int j = 0; j < d; ++j) {
+    if (warp < (j >> 3)) break;
+    const bool me = L.c == j && L.rc == 0;
+    long long a = clock64(), b;
+    if (warp == (j >> 3)) {
+      double s0 = 0.0, s1 = 0.0, alpha = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = L.rc + 4 * i;
+        if (r > j && r < d) {
+          if (i & 1) s1 = fma(x[i], x[i], s1);
+          else s0 = fma(x[i], x[i], s0);
+        }
+        if (r == j) alpha = x[i];
+      }
+      const double s = quad_sum(s0 + s1);
+      alpha = __shfl_sync(0xffffffffu, alpha, qbase | (j & 3));
+      b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[0], b - a); a = b;
+      if (L.c == j) {
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+          const double n2 = fma(alpha, alpha, s);
+          const double rn = rsqrt(n2);
+          const double nrm = n2 * rn;
+          beta = -copysign(nrm, alpha);
+          t = fma(fabs(alpha), rn, 1.0);
+          scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+        }
+        b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[1], b - a); a = b;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = L.rc + 4 * i;
+          if (r < d) Vt[j * d + r] = r > j ? x[i] * scale : (r == j ? 1.0 : 0.0);
+        }
+        if (L.rc == 0) {
+          tau[j] = t;
+          diag[j] = beta;
+        }
+        b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[2], b - a); a = b;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"((kWarps - (j >> 3)) * 32) : "memory");
+    const bool next = L.c == j + 1 && L.rc == 0;
+    b = clock64(); if (next) atomicAdd((unsigned long long*)&g_ph[3], b - a); a = b;
+    const double t = tau[j];
+    if (t != 0.0) {
+      double p0 = 0.0, p1 = 0.0, v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = L.rc + 4 * i;
+        v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
+        if (i & 1) p1 = fma(v[i], x[i], p1);
+        else p0 = fma(v[i], x[i], p0);
+      }
+      const double w = t * quad_sum(p0 + p1);
+      if (L.c > j && L.c < d) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = fma(-w, v[i], x[i]);
+      }
+    }
+    b = clock64(); if (next) atomicAdd((unsigned long long*)&g_ph[4], b - a);
+  }
+  __syncthreads();
+}
+
+template <int V>
+__global__ void __launch_bounds__(kThreads, 1) qr_bench(const double* M, int d, int reps, int t_obs,
+                                                         long long* cyc, double* diag_out) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem<double> sm = carve<double>(smem_raw, d);
+  const ColLane L = col_lane();
+  long long total = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int r = L.rc + 4 * i;
+      x[i] = (L.c < d && r < d) ? M[r * d + L.c] : 0.0;
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    if (V == 0) qr_regs(x, d, sm);
+    if (V == 1) qr_regs_timed(x, d, sm, t_obs);
+    if (V == 2) q_regs(x, d, true, sm);
+    __syncthreads();
+    total += clock64() - t0;
+  }
+  if (threadIdx.x == 0) {
+    cyc[0] = total / reps;
+    for (int i = 0; i < 5; ++i) cyc[1 + i] = g_ph[i] / reps;
+  }
+  for (int j = threadIdx.x; j < d; j += kThreads) diag_out[j] = sm.vec[d + j];
+}
+
+}  // namespace
+}  // namespace goom
+
+int main(int argc, char** argv) {
+  using namespace goom;
+  const int d = argc > 1 ? atoi(argv[1]) : 64, reps = 20;
+  static double h[64 * 64];
+  unsigned s = 12345;
+  for (int i = 0; i < d * d; ++i) {
+    s = s * 1664525u + 1013904223u;
+    h[i] = (s >> 8) * (1.0 / 16777216.0) - 0.5;
+  }
+  double *M, *diag;
+  long long* cyc;
+  cudaMalloc(&M, sizeof(double) * d * d);
+  cudaMalloc(&diag, d * sizeof(double));
+  cudaMalloc(&cyc, 8 * sizeof(long long));
+  cudaMemcpy(M, h, sizeof(double) * d * d, cudaMemcpyHostToDevice);
+  const size_t sb = smem_bytes<double>(d);
+  cudaFuncSetAttribute(qr_bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  cudaFuncSetAttribute(qr_bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  cudaFuncSetAttribute(qr_bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  long long hc[8];
+  qr_bench<0><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
+  qr_bench<0><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
+  cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+  printf("qr_regs d=%d: %lld cycles (%.1f per column) [%s]\n", d, hc[0], hc[0] / (double)d,
+         cudaGetErrorString(cudaDeviceSynchronize()));
+  if (argc > 2) return 0;
+  {
+    void* zero;
+    cudaGetSymbolAddress(&zero, g_ph);
+    cudaMemset(zero, 0, 8 * sizeof(long long));
+    qr_bench<1><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
+    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    printf("timed: total %lld; per column: norm %.0f, scalars %.0f, V stores %.0f, barrier(next owner) %.0f, update(next owner) %.0f\n",
+           hc[0], hc[1] / 64.0, hc[2] / 64.0, hc[3] / 64.0, hc[4] / 64.0, hc[5] / 64.0);
+  }
+  qr_bench<2><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
+  cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+  printf("q_regs d=64: %lld cycles\n", hc[0]);
+  printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  return 0;
+}
