@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "goom_internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace goom {
 
@@ -76,8 +77,8 @@ struct Smem {
   double* vec;    // 2d
   double* red;    // 2 * kWarps
   double* part;   // 4 * kMaxD: per-(row chunk, column) partials of the column-parallel kernels
+  uint64_t* mbar;  // 1: the walk's operand prefetch barrier
   int* ints;      // 8
-  int* iw;        // 8 + 2 * kMaxD: LU pivot partials and row permutations
 };
 
 template <class Rt>
@@ -85,7 +86,7 @@ inline size_t smem_bytes(int d) {
   size_t dd = (size_t)d * d;
   return 2 * dd * sizeof(Cx<Rt>) + 2 * dd * sizeof(double) + 2 * d * sizeof(Rt) +
          2 * d * sizeof(double) + 2 * kWarps * sizeof(double) + 4 * kMaxD * sizeof(double) +
-         (16 + 2 * kMaxD) * sizeof(int) + 64;
+         16 + 16 * sizeof(int) + 64;
 }
 
 template <class Rt>
@@ -101,9 +102,9 @@ __device__ Smem<Rt> carve(char* base, int d) {
   s.vec = s.W + dd;
   s.red = s.vec + 2 * d;
   s.part = s.red + 2 * kWarps;
-  s.scal = reinterpret_cast<Rt*>(s.part + 4 * kMaxD);
+  s.mbar = reinterpret_cast<uint64_t*>(s.part + 4 * kMaxD);
+  s.scal = reinterpret_cast<Rt*>(s.mbar + 2);
   s.ints = reinterpret_cast<int*>(s.scal + 2 * d);
-  s.iw = s.ints + 8;
   return s;
 }
 
@@ -119,26 +120,42 @@ __device__ double block_max(double v, double* red) {
   return r;
 }
 
-// out (smem) = Lg (global, d x d) (x) Rs (smem, d x d); Eq. 10-12 at the chain's precision,
-// same per-output FMA order as the SIMT kernels (bitwise-identical products).
+// Eq. 10-12 at the chain's precision in one CTA, split so that the left operand's half
+// (clamped row maxima, scaled exponentials) can be produced ahead of time:
+//   lmme_left   sm.scal[0, d) = max(row max of Lg, 0); sm.tl[k d + i] = s e^{Lg_ik - scal_i}
+//   lmme_right  out (smem) = (tl) (x) Rs with Rs's clamped column maxima, the GEMM and
+//               the log / max-add-back epilogue
+// Same per-output FMA order as the SIMT kernels (bitwise-identical products).
 template <class Rt>
-__device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<Rt>* out, int d,
-                           const Smem<Rt>& sm) {
+__device__ void lmme_left(const Cx<Rt>* __restrict__ Lg, int d, Rt* scal, Rt* tl,
+                          const Smem<Rt>& sm) {
   const int tid = threadIdx.x, cc = tid & (kMaxD - 1), ch = tid / kMaxD;
-  // clamped row maxima of Lg and column maxima of Rs: 4 row/column chunks per index
-  Rt mr = Rt(-INFINITY), mc = Rt(-INFINITY);
+  Rt mr = Rt(-INFINITY);
   if (cc < d)
-    for (int t = ch; t < d; t += 4) {
-      mr = gmax(mr, Lg[cc * d + t].x);
-      mc = gmax(mc, Rs[t * d + cc].x);
-    }
+    for (int t = ch; t < d; t += 4) mr = gmax(mr, Lg[cc * d + t].x);
   sm.part[ch * kMaxD + cc] = (double)mr;
   __syncthreads();
   if (cc < d && ch == 0)
-    sm.scal[cc] = gmax(gmax(gmax((Rt)sm.part[cc], (Rt)sm.part[kMaxD + cc]),
-                            gmax((Rt)sm.part[2 * kMaxD + cc], (Rt)sm.part[3 * kMaxD + cc])),
-                       Rt(0));
+    scal[cc] = gmax(gmax(gmax((Rt)sm.part[cc], (Rt)sm.part[kMaxD + cc]),
+                         gmax((Rt)sm.part[2 * kMaxD + cc], (Rt)sm.part[3 * kMaxD + cc])),
+                    Rt(0));
   __syncthreads();
+  for (int e = tid; e < d * d; e += kThreads) {
+    const int i = e / d, j = e % d;
+    const Cx<Rt> z = Lg[e];  // row i, column j (= k index)
+    tl[j * d + i] = goom_sign_t<Rt>(z.y) * gexp(z.x - scal[i]);
+  }
+  __syncthreads();
+}
+
+template <class Rt>
+__device__ void lmme_right(const Cx<Rt>* Rs, Cx<Rt>* out, int d, const Smem<Rt>& sm,
+                           bool tm = false) {
+  const int tid = threadIdx.x, cc = tid & (kMaxD - 1), ch = tid / kMaxD;
+  long long t0 = clock64();
+  Rt mc = Rt(-INFINITY);
+  if (cc < d)
+    for (int t = ch; t < d; t += 4) mc = gmax(mc, Rs[t * d + cc].x);
   sm.part[ch * kMaxD + cc] = (double)mc;
   __syncthreads();
   if (cc < d && ch == 0)
@@ -147,13 +164,11 @@ __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<R
                            Rt(0));
   __syncthreads();
   for (int e = tid; e < d * d; e += kThreads) {
-    int i = e / d, j = e % d;
-    Cx<Rt> z = Lg[e];  // left operand, row i, column j (= k index)
-    sm.tl[j * d + i] = goom_sign_t<Rt>(z.y) * gexp(z.x - sm.scal[i]);
-    Cx<Rt> q = Rs[e];  // right operand, row i (= k index), column j
-    sm.tr[e] = goom_sign_t<Rt>(q.y) * gexp(q.x - sm.scal[d + j]);
+    const Cx<Rt> q = Rs[e];  // row (= k index), column j
+    sm.tr[e] = goom_sign_t<Rt>(q.y) * gexp(q.x - sm.scal[d + e % d]);
   }
   __syncthreads();
+  prof_add(tm, 10, t0);
   const int ty = tid >> 4, tx = tid & 15;
   Rt acc[4][4];
 #pragma unroll
@@ -174,6 +189,8 @@ __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<R
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = gfma(av[r], bv[c], acc[r][c]);
   }
+  if (tm) __syncthreads();
+  prof_add(tm, 11, t0);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     int i = ty + 16 * r;
@@ -186,6 +203,34 @@ __device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<R
     }
   }
   __syncthreads();
+  prof_add(tm, 12, t0);
+}
+
+// out (smem) = Lg (global) (x) Rs (smem)
+template <class Rt>
+__device__ void block_lmme(const Cx<Rt>* __restrict__ Lg, const Cx<Rt>* Rs, Cx<Rt>* out, int d,
+                           const Smem<Rt>& sm) {
+  lmme_left(Lg, d, sm.scal, sm.tl, sm);
+  lmme_right(Rs, out, d, sm);
+}
+
+// The walk's left operands ahead of time, batched over tiles: CTA k writes tile k's
+// (position min(k s + s, T) - 1 of loc) clamped row maxima to rs[k d ..] and its scaled
+// exponentials, in the walk's sm.tl layout, to P[k d^2 ..] — the walk then streams
+// them into shared memory with one bulk copy instead of reading and exponentiating the
+// GOOM matrix on its sequential path.
+template <class Rt>
+__global__ void __launch_bounds__(kThreads, 1)
+    tile_operand_kernel(const Cx<Rt>* __restrict__ loc, int64_t T, int d, int s,
+                        Rt* __restrict__ P, Rt* __restrict__ rs) {
+  extern __shared__ __align__(16) char smem_raw[];
+  Smem<Rt> sm = carve<Rt>(smem_raw, d);
+  const int64_t dd = (int64_t)d * d;
+  const int64_t lo = (int64_t)blockIdx.x * s;
+  const int64_t p = (lo + s < T ? lo + s : T) - 1;
+  lmme_left(loc + p * dd, d, sm.scal, sm.tl, sm);
+  for (int64_t e = threadIdx.x; e < dd; e += kThreads) P[blockIdx.x * dd + e] = sm.tl[e];
+  for (int i = threadIdx.x; i < d; i += kThreads) rs[blockIdx.x * d + i] = sm.scal[i];
 }
 
 // ---- register-resident column kernels (d <= 64, 256 threads) -------------------------
@@ -206,6 +251,14 @@ __device__ __forceinline__ double quad_sum(double v) {
 __device__ __forceinline__ double quad_max(double v) {
   v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 1));
   return fmax(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+
+__device__ __forceinline__ double tree_sum16(double (&a)[16]) {
+#pragma unroll
+  for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) a[i] += a[i + w];
+  return a[0];
 }
 
 // Log-unit-normalised columns (lyapunov.py:255-263) of X (smem GOOMs, d x d): this
@@ -301,17 +354,14 @@ __device__ void qr_regs(double (&x)[16], int d, const Smem<Rt>& sm) {
                                   // active sync on a named barrier sized to them
     if (warp == (j >> 3)) {       // the warp owning column j builds the reflector; full-warp
                                   // shuffles, only the quad of column j keeps its values
-      double s0 = 0.0, s1 = 0.0, alpha = 0.0;
+      double sq[16], alpha = 0.0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int r = L.rc + 4 * i;
-        if (r > j && r < d) {
-          if (i & 1) s1 = fma(x[i], x[i], s1);
-          else s0 = fma(x[i], x[i], s0);
-        }
+        sq[i] = (r > j && r < d) ? x[i] * x[i] : 0.0;  // independent products, tree sum
         if (r == j) alpha = x[i];
       }
-      const double s = quad_sum(s0 + s1);
+      const double s = quad_sum(tree_sum16(sq));
       alpha = __shfl_sync(0xffffffffu, alpha, qbase | (j & 3));
       if (L.c == j) {
         // dlarfg: beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha) / beta,
@@ -339,15 +389,14 @@ __device__ void qr_regs(double (&x)[16], int d, const Smem<Rt>& sm) {
     asm volatile("bar.sync 1, %0;" ::"r"((kWarps - (j >> 3)) * 32) : "memory");
     const double t = tau[j];
     if (t != 0.0) {
-      double p0 = 0.0, p1 = 0.0, v[16];
+      double pr[16], v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int r = L.rc + 4 * i;
         v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
-        if (i & 1) p1 = fma(v[i], x[i], p1);
-        else p0 = fma(v[i], x[i], p0);
+        pr[i] = v[i] * x[i];
       }
-      const double w = t * quad_sum(p0 + p1);
+      const double w = t * quad_sum(tree_sum16(pr));
       if (L.c > j && L.c < d) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[i] = fma(-w, v[i], x[i]);
@@ -435,20 +484,25 @@ __device__ void export_goom(const double (&q)[16], Cx<Rt>* out, int d) {
     }
 }
 
-// The policy on one state X (smem): predicate, and on a fire the reset value into out.
-// Returns a goom_status (GOOM_ERANK: the reset of a zero / rank-deficient state); *fire
-// says whether the predicate fired. select_only: predicate only (policy_select).
-template <class Rt>
-__device__ int apply_policy(const Cx<Rt>* X, Cx<Rt>* out, int d, const Policy& pol,
-                            const Smem<Rt>& sm, bool select_only, bool force_fire, bool* fire,
-                            double ldet_x = NAN) {
-  *fire = false;
-  if (pol.kind == GOOM_POLICY_NEVER && !force_fire) return GOOM_OK;
-  long long t0 = clock64();
+// The policy on one state X (smem) in two halves. policy_predicate: the column norms (and
+// for colinearity the Gram and the volume test) -> fire; policy_reset_value: on a fire,
+// the reset value into out. The state between them (this thread's unit column, whether
+// it is already factored) stays in registers. ldet_x: log|det X| when the caller tracks
+// it (the walk), NaN to factor X for the volume test.
+struct PolicyRun {
   double x[16];
-  const bool zero = unit_columns_regs(X, d, x, sm);
+  bool zero, factored;
+};
+
+template <class Rt>
+__device__ bool policy_predicate(const Cx<Rt>* X, int d, const Policy& pol, const Smem<Rt>& sm,
+                                 bool force_fire, double ldet_x, PolicyRun& st) {
+  st.zero = st.factored = false;
+  if (pol.kind == GOOM_POLICY_NEVER && !force_fire) return false;
+  long long t0 = clock64();
+  st.zero = unit_columns_regs(X, d, st.x, sm);
   prof_add(pol.timing, 2, t0);
-  bool f = force_fire, factored = false;
+  bool f = force_fire;
   if (pol.kind == GOOM_POLICY_NORM_THRESHOLD) {
     if (!f) {
       double m = -INFINITY;
@@ -456,36 +510,51 @@ __device__ int apply_policy(const Cx<Rt>* X, Cx<Rt>* out, int d, const Policy& p
       f = block_max(m, sm.red) > pol.threshold;
     }
   } else if (pol.kind == GOOM_POLICY_COLINEARITY || force_fire) {
-    f = f || zero;
-    if (!f && !zero) {
+    f = f || st.zero;
+    if (!f) {
       f = gram_offdiag_max(d, sm) > pol.threshold;
       prof_add(pol.timing, 3, t0);
     }
-    if (!zero && !f && pol.log_floor != -INFINITY) {
+    if (!f && pol.log_floor != -INFINITY) {
       if (!isnan(ldet_x)) {
         // log|det| of the unit-column matrix = log|det X| - sum_j nu_j, with log|det X|
         // known from the walk (det is multiplicative): no factorisation on this path
         f = ldet_x - col_lognorm_sum(d, sm) < pol.log_floor;
       } else {
-        qr_regs(x, d, sm);
-        factored = true;
+        qr_regs(st.x, d, sm);
+        st.factored = true;
         f = volume_deficient_qr(d, pol.log_floor, sm);
       }
       prof_add(pol.timing, 4, t0);
     }
   }
-  *fire = f;
-  if (!f || select_only) return GOOM_OK;
-  if (zero) return GOOM_ERANK;
-  if (!factored) qr_regs(x, d, sm);
+  return f;
+}
+
+template <class Rt>
+__device__ int policy_reset_value(Cx<Rt>* out, int d, const Policy& pol, const Smem<Rt>& sm,
+                                  PolicyRun& st) {
+  if (st.zero) return GOOM_ERANK;
+  long long t0 = clock64();
+  if (!st.factored) qr_regs(st.x, d, sm);
   const bool colin = pol.kind == GOOM_POLICY_COLINEARITY;
   if (colin && rank_deficient(d, sm)) return GOOM_ERANK;
-  q_regs(x, d, colin, sm);
+  q_regs(st.x, d, colin, sm);
   prof_add(pol.timing, 5, t0);
-  export_goom<Rt>(x, out, d);
+  export_goom<Rt>(st.x, out, d);
   __syncthreads();
   prof_add(pol.timing, 6, t0);
   return GOOM_OK;
+}
+
+// both halves (the batch select / reset kernels)
+template <class Rt>
+__device__ int apply_policy(const Cx<Rt>* X, Cx<Rt>* out, int d, const Policy& pol,
+                            const Smem<Rt>& sm, bool select_only, bool force_fire, bool* fire) {
+  PolicyRun st;
+  *fire = policy_predicate(X, d, pol, sm, force_fire, NAN, st);
+  if (!*fire || select_only) return GOOM_OK;
+  return policy_reset_value(out, d, pol, sm, st);
 }
 
 template <class C>
@@ -501,7 +570,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           Cx<Rt>* __restrict__ carries, int8_t* __restrict__ modes,
                           int64_t* __restrict__ sites, int64_t* __restrict__ n_sites,
                           int* __restrict__ status, int64_t T, int d, int s, Policy pol,
-                          const double* __restrict__ ldet0, const double* __restrict__ ldet1) {
+                          const double* __restrict__ ldet0, const double* __restrict__ ldet1,
+                          const Rt* __restrict__ P0, const Rt* __restrict__ rs0,
+                          const Rt* __restrict__ P1, const Rt* __restrict__ rs1) {
   extern __shared__ __align__(16) char smem_raw[];
   Smem<Rt> sm = carve<Rt>(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
@@ -512,6 +583,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   // log|det el| = log|det loc| (batched pre-pass) + log|det carry|; a reset carry is
   // orthonormal (log|det| = 0), a kept carry is the previous el
   double ldc = 0.0;
+  // left operands (tile_operand_kernel) stream into sm.tl with one bulk copy per tile,
+  // issued as soon as the previous tile's predicate has released sm.R (= sm.tl)
+  const uint32_t op_bytes = (uint32_t)(mat * sizeof(Rt));
+  const bool bulk = P0 != nullptr && op_bytes % 16 == 0;
+  const uint32_t bar = tc::smem_u32(sm.mbar);
+  if (bulk && threadIdx.x == 0) {
+    tc::mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  bool pending = false;
   const bool tm = pol.timing != 0;
   long long t0 = clock64();
   for (int64_t k = 0; k < ntiles; ++k) {
@@ -523,40 +606,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!have_carry) {
       mode = 0;
       copy_mat(loc0 + p * mat, sm.el, d);
-    } else if (consumed) {
+    } else if (consumed && p == lo) {
       mode = 2;
-      if (p == lo) copy_mat(sm.carry, sm.el, d);
-      else block_lmme(loc1 + p * mat, sm.carry, sm.el, d, sm);
+      copy_mat(sm.carry, sm.el, d);
     } else {
-      mode = 1;
-      block_lmme(loc0 + p * mat, sm.carry, sm.el, d, sm);
+      mode = consumed ? 2 : 1;
+      if (P0) {
+        const Rt* P = mode == 2 ? P1 : P0;
+        const Rt* rs = mode == 2 ? rs1 : rs0;
+        if (pending) {
+          tc::mbar_wait(bar, phase);
+          phase ^= 1;
+          pending = false;
+        } else {
+          for (int64_t e = threadIdx.x; e < mat; e += kThreads) sm.tl[e] = P[k * mat + e];
+        }
+        for (int i = threadIdx.x; i < d; i += kThreads) sm.scal[i] = rs[k * d + i];
+        prof_add(tm, 13, t0);
+        lmme_right(sm.carry, sm.el, d, sm, tm);
+      } else {
+        block_lmme((mode == 2 ? loc1 : loc0) + p * mat, sm.carry, sm.el, d, sm);
+      }
     }
     prof_add(tm, 0, t0);
     if (mode > 0)
       for (int e = threadIdx.x; e < d * d; e += kThreads) carries[k * mat + e] = sm.carry[e];
     if (threadIdx.x == 0) modes[k] = mode;
     prof_add(tm, 1, t0);
-    consumed = false;
     bool fire = false;
     double ldel = NAN;
     if (ldet0) ldel = mode == 0 ? ldet0[k] : mode == 1 ? ldet0[k] + ldc : (p == lo ? ldc : ldet1[k] + ldc);
-    int rc = GOOM_OK;
-    if ((p % s) == s - 1 && p <= T - 2)
-      rc = apply_policy(sm.el, sm.carry, d, pol, sm, /*select_only=*/false, false, &fire, ldel);
+    PolicyRun st;
+    if ((p % s) == s - 1 && p <= T - 2) fire = policy_predicate(sm.el, d, pol, sm, false, ldel, st);
     ldc = fire ? 0.0 : ldel;
+    const bool next_consumed = fire && pol.consume != 0;
+    // prefetch the next tile's left operand (sm.R is free once the predicate is done)
+    if (bulk && k + 1 < ntiles) {
+      const int64_t nlo = lo + s;
+      const bool needs = !(next_consumed && nlo == ((nlo + s < T ? nlo + s : T) - 1));
+      if (needs) {
+        if (threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc::mbar_expect_tx(bar, op_bytes);
+          tc::bulk_g2s(tc::smem_u32(sm.tl), (next_consumed ? P1 : P0) + (k + 1) * mat, op_bytes, bar);
+        }
+        pending = true;
+      }
+    }
     if (tm) t0 = clock64();
     if (fire) {
       if (tm && threadIdx.x == 0) g_walk_prof[9] += 1;
+      const int rc = policy_reset_value(sm.carry, d, pol, sm, st);
       if (rc != GOOM_OK) {
         if (threadIdx.x == 0) *status = rc;
+        if (pending) tc::mbar_wait(bar, phase);  // no bulk copy may outlive the CTA
         break;
       }
       if (threadIdx.x == 0) sites[nsite] = p + 1;
       ++nsite;
-      consumed = pol.consume != 0;
     } else {
-      copy_mat(sm.el, sm.carry, d);
+      Cx<Rt>* t = sm.carry;  // the kept state becomes the carry: swap buffers
+      sm.carry = sm.el;
+      sm.el = t;
     }
+    consumed = next_consumed;
     have_carry = true;
   }
   if (threadIdx.x == 0) *n_sites = nsite;
@@ -741,6 +854,8 @@ size_t workspace_bytes(int64_t T, int d, const goom_reset_policy* policy) {
   if (policy->consume_leaf && s > 1) b += round_up(mat * T);  // loc1
   b += round_up(mat * nt) + round_up(nt) + round_up(sizeof(int) * 4);
   b += 2 * round_up(sizeof(double) * (size_t)nt);             // tile log-determinants
+  const int nops = policy->consume_leaf && s > 1 ? 2 : 1;     // walk left operands + scales
+  b += nops * (round_up(sizeof(Rt) * (size_t)d * d * nt) + round_up(sizeof(Rt) * (size_t)d * nt));
   b += 2 * round_up(sizeof(Rt) * (size_t)T * d) + 256;        // LMME scale scratch + flag
   return b;
 }
@@ -781,6 +896,18 @@ int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_res
   off += round_up(sizeof(double) * (size_t)nt);
   double* ldet1 = reinterpret_cast<double*>(base + off);
   off += round_up(sizeof(double) * (size_t)nt);
+  Rt* P0 = reinterpret_cast<Rt*>(base + off);
+  off += round_up(sizeof(Rt) * (size_t)mat * nt);
+  Rt* rs0 = reinterpret_cast<Rt*>(base + off);
+  off += round_up(sizeof(Rt) * (size_t)d * nt);
+  Rt* P1 = nullptr;
+  Rt* rs1 = nullptr;
+  if (need_loc1) {
+    P1 = reinterpret_cast<Rt*>(base + off);
+    off += round_up(sizeof(Rt) * (size_t)mat * nt);
+    rs1 = reinterpret_cast<Rt*>(base + off);
+    off += round_up(sizeof(Rt) * (size_t)d * nt);
+  }
   void* lws = base + off;
   size_t lws_bytes = ws_bytes - off;
 
@@ -807,13 +934,23 @@ int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_res
       GOOM_CHECK_LAUNCH("tile_logdet_kernel");
     }
   }
+  GOOM_TRY(set_smem<Rt>((const void*)tile_operand_kernel<Rt>, d));
+  tile_operand_kernel<Rt><<<(unsigned)nt, kThreads, smem_bytes<Rt>(d), st>>>(loc0, T, d, (int)s,
+                                                                             P0, rs0);
+  GOOM_CHECK_LAUNCH("tile_operand_kernel");
+  if (need_loc1) {
+    tile_operand_kernel<Rt><<<(unsigned)nt, kThreads, smem_bytes<Rt>(d), st>>>(loc1, T, d,
+                                                                               (int)s, P1, rs1);
+    GOOM_CHECK_LAUNCH("tile_operand_kernel");
+  }
   if (pol.timing) {
     unsigned long long zero[16] = {};
     cudaMemcpyToSymbolAsync(g_walk_prof, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
   }
   selective_walk_kernel<Rt><<<1, kThreads, smem_bytes<Rt>(d), st>>>(
       loc0, loc1 ? loc1 : loc0, carries, modes, sites, n_sites, status, T, d, (int)s, pol,
-      track_det ? ldet0 : nullptr, need_loc1 ? ldet1 : ldet0);
+      track_det ? ldet0 : nullptr, need_loc1 ? ldet1 : ldet0, P0, rs0, need_loc1 ? P1 : P0,
+      need_loc1 ? rs1 : rs0);
   GOOM_CHECK_LAUNCH("selective_walk_kernel");
   if (pol.timing) {  // debug aid: per-phase clocks of the walk (synchronises the stream)
     unsigned long long c[16];
@@ -824,6 +961,9 @@ int selective_chain(const Cx<Rt>* A, Cx<Rt>* V, int64_t T, int d, const goom_res
     std::fprintf(stderr, "[walk timing] tiles %llu fires %llu:", c[8], c[9]);
     for (int i = 0; i < 8; ++i)
       std::fprintf(stderr, " %s %.1f us/tile;", names[i], c[8] ? c[i] / 1.9e3 / c[8] : 0.0);
+    std::fprintf(stderr, " [lmme: operand wait %.1f, col scales + exp %.1f, gemm %.1f, log out %.1f]",
+                 c[8] ? c[13] / 1.9e3 / c[8] : 0.0, c[8] ? c[10] / 1.9e3 / c[8] : 0.0,
+                 c[8] ? c[11] / 1.9e3 / c[8] : 0.0, c[8] ? c[12] / 1.9e3 / c[8] : 0.0);
     std::fprintf(stderr, " (clock64 cycles / 1.9 GHz)\n");
   }
   // 3. materialise: tile 0 = loc0; tile k>0: loc[t] (x) carry[k]

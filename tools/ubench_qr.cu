@@ -12,9 +12,9 @@ namespace {
 
 __device__ long long g_ph[8];
 
-// current qr_regs with phase clocks, summed over columns by the owner lane (rc == 0) of
-// each column: [0] norm + quad shuffles, [1] reflector scalars, [2] V stores, [3] barrier,
-// [4] dot + update (as seen by the owner of column j+1)
+// current qr_regs (tree sums) with a timestamp trace: g_tr[tid][j][pt] for j < 24,
+// pt: 0 loop top, 1 after norm, 2 after scalars, 3 after V stores, 4 after barrier, 5 end
+__device__ long long g_tr[256][24][6];
 template <class Rt>
 __device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
   const ColLane L = col_lane();
@@ -24,22 +24,19 @@ __device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
   double* diag = sm.vec + d;
   for (int j = 0; j < d; ++j) {
     if (warp < (j >> 3)) break;
-    const bool me = L.c == j && L.rc == 0;
-    long long a = clock64(), b;
+    const bool rec = j < 24;
+    if (rec) g_tr[threadIdx.x][j][0] = clock64();
     if (warp == (j >> 3)) {
-      double s0 = 0.0, s1 = 0.0, alpha = 0.0;
+      double sq[16], alpha = 0.0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int r = L.rc + 4 * i;
-        if (r > j && r < d) {
-          if (i & 1) s1 = fma(x[i], x[i], s1);
-          else s0 = fma(x[i], x[i], s0);
-        }
+        sq[i] = (r > j && r < d) ? x[i] * x[i] : 0.0;
         if (r == j) alpha = x[i];
       }
-      const double s = quad_sum(s0 + s1);
+      const double s = quad_sum(tree_sum16(sq));
       alpha = __shfl_sync(0xffffffffu, alpha, qbase | (j & 3));
-      b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[0], b - a); a = b;
+      if (rec) g_tr[threadIdx.x][j][1] = clock64();
       if (L.c == j) {
         double t = 0.0, beta = alpha, scale = 0.0;
         if (s != 0.0) {
@@ -50,7 +47,7 @@ __device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
           t = fma(fabs(alpha), rn, 1.0);
           scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
         }
-        b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[1], b - a); a = b;
+        if (rec) g_tr[threadIdx.x][j][2] = clock64();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int r = L.rc + 4 * i;
@@ -60,29 +57,27 @@ __device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
           tau[j] = t;
           diag[j] = beta;
         }
-        b = clock64(); if (me) atomicAdd((unsigned long long*)&g_ph[2], b - a); a = b;
+        if (rec) g_tr[threadIdx.x][j][3] = clock64();
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"((kWarps - (j >> 3)) * 32) : "memory");
-    const bool next = L.c == j + 1 && L.rc == 0;
-    b = clock64(); if (next) atomicAdd((unsigned long long*)&g_ph[3], b - a); a = b;
+    if (rec) g_tr[threadIdx.x][j][4] = clock64();
     const double t = tau[j];
     if (t != 0.0) {
-      double p0 = 0.0, p1 = 0.0, v[16];
+      double pr[16], v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int r = L.rc + 4 * i;
         v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
-        if (i & 1) p1 = fma(v[i], x[i], p1);
-        else p0 = fma(v[i], x[i], p0);
+        pr[i] = v[i] * x[i];
       }
-      const double w = t * quad_sum(p0 + p1);
+      const double w = t * quad_sum(tree_sum16(pr));
       if (L.c > j && L.c < d) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[i] = fma(-w, v[i], x[i]);
       }
     }
-    b = clock64(); if (next) atomicAdd((unsigned long long*)&g_ph[4], b - a);
+    if (rec) g_tr[threadIdx.x][j][5] = clock64();
   }
   __syncthreads();
 }
@@ -146,13 +141,19 @@ int main(int argc, char** argv) {
          cudaGetErrorString(cudaDeviceSynchronize()));
   if (argc > 2) return 0;
   {
-    void* zero;
-    cudaGetSymbolAddress(&zero, g_ph);
-    cudaMemset(zero, 0, 8 * sizeof(long long));
-    qr_bench<1><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
-    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
-    printf("timed: total %lld; per column: norm %.0f, scalars %.0f, V stores %.0f, barrier(next owner) %.0f, update(next owner) %.0f\n",
-           hc[0], hc[1] / 64.0, hc[2] / 64.0, hc[3] / 64.0, hc[4] / 64.0, hc[5] / 64.0);
+    qr_bench<1><<<1, kThreads, sb>>>(M, d, 1, 0, cyc, diag);
+    cudaDeviceSynchronize();
+    static long long tr[256][24][6];
+    cudaMemcpyFromSymbol(tr, g_tr, sizeof(tr));
+    for (int j : {16, 17, 18, 20}) {
+      const long long base = tr[0 + 64][j][0];  // warp 2 (owner of 16..23), lane 0
+      printf("column %d (owner warp 2):\n", j);
+      for (int t : {64 + 4 * (j - 16), 64, 96, 128, 255}) {
+        printf("  tid %3d:", t);
+        for (int pt = 0; pt < 6; ++pt) printf(" %6lld", tr[t][j][pt] ? tr[t][j][pt] - base : -1);
+        printf("\n");
+      }
+    }
   }
   qr_bench<2><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
   cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
