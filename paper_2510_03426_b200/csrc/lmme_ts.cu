@@ -55,7 +55,6 @@ constexpr int kMaxK = 1024;
 // per-tile right-operand row factors (2 x kMaxK floats) | barriers
 template <int kOut, int S>
 struct Lay {
-  static constexpr int kStages = S;
   static constexpr int kOutBytes = kOut == kTsOutDigest ? 0 : kEpiWarps * 2 * kOutStage;
   static constexpr int kOutOff = S * kStage;
   static constexpr int kFacOff = kOutOff + kOutBytes;
@@ -90,12 +89,6 @@ struct Ring {
     }
   }
 };
-
-__device__ __forceinline__ float lds32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
-}
 
 // exp(q - ref) for q <= ref; exact zero for an all-zero row / block (q = -inf)
 __device__ __forceinline__ float scale_factor(float q, float ref) {

@@ -200,7 +200,6 @@ bool fused_scale_path(const float2* A, const float2* carry_in, int d) {
   return lmme_backend() != 1 && lmme_tc_eligible(d, d, d) &&
          ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(carry_in)) & 15) == 0;
 }
-bool fused_scale_path(const double2*, const double2*, int) { return false; }
 
 }  // namespace
 
@@ -230,7 +229,8 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
   // phase 1: L[k*s] = A[k*s]; L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]
   GOOM_TRY(copy_strided(L, A, mat, mat * s, nb, st, "chain phase-1 copy"));
   if constexpr (sizeof(R) == 4) {
-    if (fused_scale_path(A, carry_in, d))
+    if (fused_scale_path(reinterpret_cast<const float2*>(A),
+                         reinterpret_cast<const float2*>(carry_in), d))
       return chain_scan_tc(A, out, T, d, s, nb, carry_in, L, Cx_, reinterpret_cast<char*>(lws),
                            lws_bytes, st);
   }
