@@ -10,6 +10,8 @@
 //            harness: 2 TiB of d = 512 prefixes are never stored).
 // Cx[nb] = P_{T-1} is the carry-out of a window. Between phases every matrix stays
 // tile-scaled: no exp/log per element except the leaf import and the final export.
+#include <cstdlib>
+
 #include "goom_internal.cuh"
 
 namespace goom {
@@ -104,6 +106,7 @@ size_t chain_ts_workspace_bytes(int64_t T, int d, int block, bool leaves_given_t
   return (leaves_given_ts ? 0 : ts_bytes(T, d)) + ts_bytes(T, d) + 2 * ts_bytes(nb + 1, d) +
          rup(sizeof(float2) * (size_t)d * d) +                       // identity (complex64)
          rup(sizeof(float4) * (size_t)T * (d / 32) * (d / 256)) +    // digest partials
+         rup(sizeof(uint32_t) * (size_t)nb * (d / 256)) +            // phase-1 counters
          1024;
 }
 
@@ -111,8 +114,21 @@ struct ChainWs {
   TsBuf L, Cx, Cy;
   float2* ident;
   float4* parts;
+  uint32_t* done;  // chained phase-1 counters, nb x d / 256
   int64_t s, nb;
 };
+
+// GOOM_CHAIN_PERSISTENT=1 runs phase 1 as ONE persistent launch (lmme_ts chained mode)
+// instead of s - 1 batched launches. Off by default: under the B200's power cap the
+// launches' fill / drain bubbles cost no throughput (the clock rises in them) and the
+// persistent form measured 1-3% slower on phase 1 (profiles/r1_chain_persistent_ab.txt).
+bool chain_persistent() {
+  static const bool v = [] {
+    const char* e = std::getenv("GOOM_CHAIN_PERSISTENT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 // carve the window workspace (the same layout for every stage, so a caller can keep it
 // between chain_local and chain_finish)
@@ -125,6 +141,7 @@ int chain_ws(int64_t T, int d, int block, char* ws, size_t ws_bytes, ChainWs& w)
   w.Cy = cv.ts(w.nb + 1, d);  // Kogge-Stone ping-pong buffer / carried carries
   w.ident = cv.take<float2>((size_t)d * d);
   w.parts = cv.take<float4>((size_t)T * (d / 32) * (d / 256));
+  w.done = cv.take<uint32_t>((size_t)w.nb * (d / 256));
   if (cv.off > ws_bytes) return fail(GOOM_EWORKSPACE, "tile-scaled chain workspace too small");
   return GOOM_OK;
 }
@@ -152,6 +169,24 @@ int chain_local(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_
   }
   // phase 1
   GOOM_TRY(copy_ts(L, 0, A, 0, nb, s, st));  // L[ks] = A[ks]
+  if (s > 1 && T % s == 0 && chain_persistent()) {
+    // every step of every block chain in ONE persistent launch: tiles run step-major and
+    // wait on per-(block, column tile) completion counters instead of kernel boundaries
+    uint32_t* done = w.done;
+    if (cudaMemsetAsync(done, 0, sizeof(uint32_t) * (size_t)nb * nJ, st) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "chain counters reset");
+    TsProblem p{};
+    p.A = A.in(0, 1);
+    p.B = L.in(0, 1);
+    p.kind = kTsOutTs;
+    p.T = L.out(0, 1);
+    p.batch = nb;
+    p.n = p.k = p.m = d;
+    p.chain_s = (int)s;
+    p.chain_T = T;
+    p.chain_done = done;
+    GOOM_TRY(lmme_ts(p, st));
+  } else
   for (int64_t i = 1; i < s; ++i) {
     const int64_t cnt = (T - i + s - 1) / s;
     if (cnt <= 0) break;

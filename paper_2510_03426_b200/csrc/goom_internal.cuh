@@ -92,6 +92,13 @@ struct TsProblem {
   float4* parts;      // kTsOutDigest: [batch][n / 32][m / 256] (max log, lfro top, sum, bad)
   int64_t batch;
   int n, k, m;
+  // chained phase 1 (kTsOutTs only): chain_s > 0 runs L[b s + i] = A[b s + i] (x) L[b s + i - 1]
+  // for i = 1 .. chain_s - 1 and every block b < batch in ONE persistent launch; A, B = T = L
+  // index chain_T matrices with a one-matrix stride; chain_done: batch x (m / 256) counters,
+  // zeroed, completed (row block, CTA) tiles per (block, column tile)
+  int chain_s = 0;
+  int64_t chain_T = 0;
+  uint32_t* chain_done = nullptr;
 };
 bool lmme_ts_eligible(int n, int k, int m);
 int lmme_ts(const TsProblem& p, cudaStream_t s);

@@ -118,11 +118,25 @@ struct PairGrid {
   }
 };
 
+// chained phase 1 (TsProblem::chain_s): tile t is step t / tps + 1 of the block chains
+struct ChainArgs {
+  uint32_t* done;
+  int s;
+  int64_t tps;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int kOut, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
-                   float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug) {
+                   float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug,
+                   ChainArgs ch) {
   using Y = Lay<kOut, S>;
   constexpr int kStages = S, kOutOff = Y::kOutOff;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -166,6 +180,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t base = smem_u32(smem);
+  // tile -> (matrix pair b, row / column offsets, chain step); matrix indices of the
+  // operands and the output: b / div (plain batch) or b s + step (chained phase 1)
+  auto decode = [&](int64_t t, int64_t& b, int& prow0, int& pcol0, int& step) {
+    if (ch.s) {
+      step = (int)(t / ch.tps) + 1;
+      grid.at(t % ch.tps, b, prow0, pcol0);
+    } else {
+      step = 0;
+      grid.at(t, b, prow0, pcol0);
+    }
+  };
+  auto idx_a = [&](int64_t b, int step) -> int64_t {
+    return ch.s ? b * ch.s + step : (A.sU == 0 ? 0 : b / A.div);
+  };
+  auto idx_b = [&](int64_t b, int step) -> int64_t {
+    return ch.s ? b * ch.s + step - 1 : (B.sU == 0 ? 0 : b / B.div);
+  };
+  auto idx_o = [&](int64_t b, int step) -> int64_t { return ch.s ? b * ch.s + step : b; };
+  // a chained step reads the previous step's output: column tile JB of block b is complete
+  // once all (n / 256) row pairs x 2 CTAs of every earlier step have signalled
+  // (warp-collective: lane 0 acquires, __syncwarp orders the other lanes' loads after it)
+  auto dep_ready = [&](int64_t b, int JB, int step) -> bool {
+    if (!ch.s || step < 2) return true;
+    int ok = 0;
+    if (lane == 0)
+      ok = ld_acquire_u32(ch.done + b * nJm + JB) >= (uint32_t)(2 * (n / 256) * (step - 1));
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    __syncwarp();
+    return ok != 0;
+  };
+  auto dep_wait = [&](int64_t b, int JB, int step) {
+    while (!dep_ready(b, JB, step)) __nanosleep(64);
+  };
 
   if (warp == 0) {
     // ------------------------------ TMA loader ------------------------------
@@ -173,12 +220,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       Ring<kStages> rr;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
         int64_t b;
-        int prow0, pcol0;
-        grid.at(t, b, prow0, pcol0);
+        int prow0, pcol0, step;
+        decode(t, b, prow0, pcol0, step);
         const int row0 = prow0 + (int)rank * kRowsCta;
         const int col0 = pcol0 + (int)rank * (kPairN / 2);
-        const int ma = A.sU == 0 ? 0 : (int)(b / A.div);
-        const int mb = B.sU == 0 ? 0 : (int)(b / B.div);
+        const int ma = (int)idx_a(b, step);
+        const int mb = (int)idx_b(b, step);
+        if (ch.s && step >= 2) {
+          const uint32_t need = (uint32_t)(2 * (n / 256) * (step - 1));
+          while (ld_acquire_u32(ch.done + b * nJm + pcol0 / 256) < need) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // acquire before TMA reads
+        }
         for (int kb = 0; kb < nk; ++kb, rr.next()) {
           mbar_wait(smem_u32(&freed[rr.s]), rr.ph ^ 1u);
           const uint32_t bar = smem_u32(&full[rr.s]);
@@ -239,23 +291,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per-tile factors, fetched one tile ahead: this thread's B row scales for k = u and
     // u + 512 (the tile's table is built from them), its A row's q[row][J]
     float qbn[2], qan[4], gBn = 0.0f;
-    auto fetch = [&](int64_t tile) {
+    // fetch(tile, block): false (nothing read) when block is false and a chained tile's
+    // inputs are not complete yet — the look-ahead never waits on a later step
+    auto fetch = [&](int64_t tile, bool block) -> bool {
       int64_t b;
-      int prow0, pcol0;
-      grid.at(tile, b, prow0, pcol0);
+      int prow0, pcol0, step;
+      decode(tile, b, prow0, pcol0, step);
+      const int JB = pcol0 / 256;
+      if (ch.s) {
+        if (!block && !dep_ready(b, JB, step)) return false;
+        dep_wait(b, JB, step);
+      }
       const int arow = prow0 + (int)rank * kRowsCta + arow_cta;
-      const float* qa = A.q + (b / A.div) * A.sq + (int64_t)arow * nJk;
+      const float* qa = A.q + (ch.s ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)arow * nJk;
 #pragma unroll
       for (int J = 0; J < 4; ++J) qan[J] = J < nJk ? qa[J] : kNegInf;
-      const int JB = pcol0 / 256;
-      const float* qb = B.q + (b / B.div) * B.sq + JB;
+      const int64_t ib = ch.s ? idx_b(b, step) : b / B.div;
+      const float* qb = B.q + ib * B.sq + JB;
 #pragma unroll
       for (int h = 0; h < 2; ++h) qbn[h] = u + 512 * h < k ? qb[(int64_t)(u + 512 * h) * nJm] : 0.0f;
-      gBn = decode_g(B.G[(b / B.div) * B.sG + JB]);
+      gBn = decode_g(B.G[ib * B.sG + JB]);
+      return true;
     };
-    if (cluster < grid.tiles) fetch(cluster);
+    bool fetched = cluster < grid.tiles && fetch(cluster, true);
     int tpar = 0;
     for (int64_t t = cluster; t < grid.tiles; t += nclusters, tpar ^= 1) {
+      if (!fetched) fetch(t, true);
       float* ft = fac + tpar * kMaxK;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
@@ -265,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int J = 0; J < 4; ++J) qac[J] = qan[J];
       const float rho = fmaxf(fmaxf(qac[0], qac[1]), fmaxf(qac[2], qac[3]));
       asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");  // table complete
-      if (t + nclusters < grid.tiles) fetch(t + nclusters);
+      fetched = t + nclusters < grid.tiles && fetch(t + nclusters, false);
       float fa = 0.0f;
       int curJ = -1;
       for (int kb = 0; kb < nk; ++kb, rr.next()) {
@@ -316,17 +377,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lt = 0;
     for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
       int64_t b;
-      int prow0, pcol0;
-      grid.at(t, b, prow0, pcol0);
+      int prow0, pcol0, step;
+      decode(t, b, prow0, pcol0, step);
       const int buf = lt & 1;
       const int grow = prow0 + (int)rank * kRowsCta + row;
       const int wrow0 = prow0 + (int)rank * kRowsCta + quad * 32;
       const int JB = pcol0 / 256;
+      const int64_t io = idx_o(b, step);
+      if (ch.s) dep_wait(b, JB, step);
       // product scales: rowmax q of the left operand's row, G of the right operand's block
-      const float* qa = A.q + (b / A.div) * A.sq + (int64_t)grow * nJk;
+      const float* qa = A.q + (ch.s ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)grow * nJk;
       float rho = kNegInf;
       for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
-      const float gB = decode_g(B.G[(b / B.div) * B.sG + JB]);
+      const float gB = decode_g(B.G[(ch.s ? idx_b(b, step) : b / B.div) * B.sG + JB]);
       mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
       tc_fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * kPairN);
@@ -396,12 +459,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                            __float_as_uint(__uint_as_float(v[j + 3]) * sc));
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) tma_store_3d(&mapOut, sbuf, pcol0 + col, wrow0, (int)b);
+            if (lane == 0) tma_store_3d(&mapOut, sbuf, pcol0 + col, wrow0, (int)io);
           }
-          T.q[b * T.sq + (int64_t)grow * nJm + JB] = qrow;
+          T.q[io * T.sq + (int64_t)grow * nJm + JB] = qrow;
           const float gmax = warp_max(qrow);
           if (lane == 0 && gmax != kNegInf)
-            atomicMax(&T.G[b * T.sG + JB], float_to_ordered(gmax));
+            atomicMax(&T.G[io * T.sG + JB], float_to_ordered(gmax));
         } else {
           // digest: this row's max log and log Frobenius norm, reduced over the warp's 32 rows
           float ss = 0.0f;
@@ -430,6 +493,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_rank(acc_empty0 + buf * 8, 0);
+      if (ch.s) {  // publish this CTA's part of the output tile (U, q, G) to the next step
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (warp == 2 + kXformWarps && lane == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ch.done + b * nJm + JB)
+                       : "memory");
+      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -491,6 +564,8 @@ int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& m
   pg.nct = p.m / kPairN;
   pg.nrt = p.n / 256;
   pg.tiles = p.batch * pg.nct * pg.nrt;
+  ChainArgs ch{p.chain_done, p.chain_s, pg.tiles};
+  if (p.chain_s) pg.tiles *= p.chain_s - 1;  // every step of the block chains, step-major
   const int64_t mc = max_clusters<kOut, S>();
   const int64_t clusters = pg.tiles < mc ? pg.tiles : mc;
   cudaLaunchConfig_t cfg = {};
@@ -506,7 +581,7 @@ int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& m
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S>, mapA, mapB, mapOut, p.A, p.B, p.T, p.parts, pg,
-                     p.n, p.k, p.m, ts_debug());
+                     p.n, p.k, p.m, ts_debug(), ch);
   GOOM_CHECK_LAUNCH("lmme_ts_kernel");
   return GOOM_OK;
 }
@@ -546,12 +621,17 @@ bool lmme_ts_eligible(int n, int k, int m) {
 int lmme_ts(const TsProblem& p, cudaStream_t s) {
   if (!lmme_ts_eligible(p.n, p.k, p.m)) return fail(GOOM_EUNSUPPORTED, "lmme_ts: n, k, m % 256");
   if (p.batch == 0) return GOOM_OK;
+  if (p.chain_s && (p.kind != kTsOutTs || p.n != p.k || !p.chain_done || p.chain_s < 2 ||
+                    p.chain_T < p.batch * p.chain_s))
+    return fail(GOOM_EINVAL, "lmme_ts: chained phase 1 needs a square tile-scaled output");
+  // matrices each map spans: a chained launch addresses every matrix of its buffers
+  const int64_t nA = p.chain_s ? p.chain_T : mats(p.A.sU, p.A.div, p.batch);
+  const int64_t nB = p.chain_s ? p.chain_T : mats(p.B.sU, p.B.div, p.batch);
   const uintptr_t al = reinterpret_cast<uintptr_t>(p.A.U) | reinterpret_cast<uintptr_t>(p.B.U);
   if ((al & 15) || ((p.A.sU | p.B.sU) & 3)) return fail(GOOM_EINVAL, "lmme_ts: operand alignment");
   alignas(64) CUtensorMap mapA, mapB, mapOut;
   {  // A fp32 (k, n, matrix), box 16 k x 128 rows, 64B swizzle: the UMMA K-major SW64 layout
-    cuuint64_t dims[3] = {(cuuint64_t)p.k, (cuuint64_t)p.n,
-                          (cuuint64_t)mats(p.A.sU, p.A.div, p.batch)};
+    cuuint64_t dims[3] = {(cuuint64_t)p.k, (cuuint64_t)p.n, (cuuint64_t)nA};
     cuuint64_t strides[2] = {(cuuint64_t)p.k * 4,
                              (cuuint64_t)(p.A.sU ? p.A.sU : (int64_t)p.n * p.k) * 4};
     cuuint32_t box[3] = {BK, kRowsCta, 1};
@@ -560,8 +640,7 @@ int lmme_ts(const TsProblem& p, cudaStream_t s) {
   }
   {  // B fp32 (32 cols, k, m/32 chunks, matrix), box 32 x 16 k x 4 x 1, 128B/32B-atom
      // swizzle: [chunk][k][32 cols] = the UMMA MN-major 128B_BASE32B layout (chunks 2 KB apart)
-    cuuint64_t dims[4] = {32, (cuuint64_t)p.k, (cuuint64_t)(p.m / 32),
-                          (cuuint64_t)mats(p.B.sU, p.B.div, p.batch)};
+    cuuint64_t dims[4] = {32, (cuuint64_t)p.k, (cuuint64_t)(p.m / 32), (cuuint64_t)nB};
     cuuint64_t strides[3] = {(cuuint64_t)p.m * 4, 128,
                              (cuuint64_t)(p.B.sU ? p.B.sU : (int64_t)p.k * p.m) * 4};
     cuuint32_t box[4] = {32, BK, kPairN / 2 / 32, 1};
@@ -583,7 +662,7 @@ int lmme_ts(const TsProblem& p, cudaStream_t s) {
   if (p.kind == kTsOutTs) {
     if ((reinterpret_cast<uintptr_t>(p.T.U) & 15) || (p.T.sU & 3))
       return fail(GOOM_EINVAL, "lmme_ts: output alignment");
-    const int64_t cb = p.T.sU == 0 ? 1 : p.batch;
+    const int64_t cb = p.chain_s ? p.chain_T : (p.T.sU == 0 ? 1 : p.batch);
     const int64_t cs = p.T.sU == 0 ? (int64_t)p.n * p.m : p.T.sU;
     cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.n, (cuuint64_t)cb};
     cuuint64_t strides[2] = {(cuuint64_t)p.m * 4, (cuuint64_t)cs * 4};

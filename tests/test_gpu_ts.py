@@ -219,3 +219,31 @@ def test_harness_streams_real_host_leaves(g, ops):
     assert torch.equal(dev_real.digests, gen.digests)
     with pytest.raises(ValueError):
         harness.run_chain(T, d, window=32, block=8, leaves=host.double())
+
+
+def test_chain_ts_persistent_phase1_matches_launches(g, ops):
+    """The opt-in persistent phase 1 (GOOM_CHAIN_PERSISTENT=1: one launch, step-major tiles,
+    release / acquire counters) gives the same digests as the per-step launches: same
+    products in the same order, so bitwise-equal."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, torch; sys.path.insert(0, '.');"
+        "from paper_2510_03426_b200 import ops;"
+        "L = ops.ts_random_normal(4096, 512, 7, 0, torch.device('cuda'));"
+        "_, dg, c = ops.chain_ts(L, 64, None, digests=True, carry_out=True);"
+        "torch.save((dg.cpu(), ops.ts_to_goom(c).cpu()), sys.argv[1])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("0", "1"):
+        path = os.path.join(root, "gpurun_out", f"_persist_{flag}.pt")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, GOOM_CHAIN_PERSISTENT=flag)
+        subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True,
+                       timeout=300)
+        outs.append(torch.load(path))
+        os.remove(path)
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
