@@ -139,6 +139,8 @@ int lmme_backend();
 // SIMT kernels (lmme_simt.cu)
 template <class R> int lmme_simt_small(const LmmeProblemT<R>& p, cudaStream_t s);
 template <class R> int lmme_simt_tiled(const LmmeProblemT<R>& p, cudaStream_t s);
+// n, k, m <= 64: one CTA per product, row / column scales fused (no pre-pass)
+template <class R> int lmme_simt_whole(const LmmeProblemT<R>& p, cudaStream_t s);
 // tcgen05 3xTF32 (lmme_tc.cu), complex64 only; GOOM_EUNSUPPORTED if not tileable
 int lmme_tc(const LmmeProblem& p, cudaStream_t s);
 bool lmme_tc_eligible(int n, int k, int m);

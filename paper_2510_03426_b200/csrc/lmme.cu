@@ -20,6 +20,7 @@ template <class R>
 bool small_shape(int n, int k, int m) {
   return n <= 32 && k <= 32 && m <= 32;
 }
+bool whole_shape(int n, int k, int m) { return n <= 64 && k <= 64 && m <= 64; }
 }  // namespace
 
 int lmme_backend() { return g_backend.load(); }
@@ -27,7 +28,7 @@ int lmme_backend() { return g_backend.load(); }
 template <class R>
 size_t lmme_workspace_bytes(int64_t batch, int n, int k, int m, int64_t strideA, int64_t divA,
                             int64_t strideB, int64_t divB) {
-  if (small_shape<R>(n, k, m)) return 0;  // small kernel: scales in-kernel
+  if (small_shape<R>(n, k, m) || whole_shape(n, k, m)) return 0;  // scales in-kernel
   return round_up(sizeof(R) * (size_t)distinct(strideA, divA, batch) * n) +
          round_up(sizeof(R) * (size_t)distinct(strideB, divB, batch) * m) + 256 /*phase flag*/;
 }
@@ -38,6 +39,10 @@ int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int backend = g_backend.load();
   const bool small = small_shape<R>(p.n, p.k, p.m);
   if (small && !p.rowA.ptr) return lmme_simt_small<R>(p, s);
+  // n, k, m <= 64 (and not a tcgen05 shape): one CTA per product, scales fused
+  if (whole_shape(p.n, p.k, p.m) && !p.rowA.ptr &&
+      !(sizeof(R) == 4 && backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)))
+    return lmme_simt_whole<R>(p, s);
   if (!p.rowA.ptr || !p.colB.ptr) {
     size_t need = lmme_workspace_bytes<R>(p.batch, p.n, p.k, p.m, p.A.stride, p.A.div,
                                           p.B.stride, p.B.div);

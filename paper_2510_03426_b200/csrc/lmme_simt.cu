@@ -174,7 +174,124 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------------------------
+// lmme_whole: one CTA per product for n, k, m <= 64 with the scales fused: the CTA reads
+// A and B once (coalesced) into shared memory as log-magnitude and sign planes, reduces
+// the clamped row / column maxima there, exponentiates in place into the tiled kernel's
+// [kk][row] / [kk][col] layout and runs the same 4 x 4-per-thread GEMM (ascending kk, one
+// FMA per term) and epilogue — bitwise equal to scale pre-pass + lmme_tiled, with one
+// HBM pass (24 B per element for complex64) instead of three reads.
+constexpr int kWholePitch = 64 + TPAD;
+
+template <class R>
+__global__ void __launch_bounds__(256)
+    lmme_whole_kernel(OperandT<Cx<R>> A, OperandT<Cx<R>> B, OperandT<Cx<R>> D,
+                      Cx<R>* __restrict__ C, int64_t strideC, int64_t b_base, int n, int k,
+                      int m) {
+  extern __shared__ __align__(16) unsigned char whole_smem[];
+  R* sA = reinterpret_cast<R*>(whole_smem);   // [kk][row]: log, then sign * exp(log - a)
+  R* sB = sA + 64 * kWholePitch;              // [kk][col]
+  R* gA = sB + 64 * kWholePitch;              // signs, same layouts
+  R* gB = gA + 64 * kWholePitch;
+  R* sc = gB + 64 * kWholePitch;              // [0, 64) a_i, [64, 128) b_j
+  const int64_t b = b_base + blockIdx.x;
+  const Cx<R>* a = A.at(b);
+  const Cx<R>* bm = B.at(b);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * k; e += 256) {  // coalesced over A's row-major storage
+    const int i = e / k, kk = e % k;
+    const Cx<R> z = a[e];
+    sA[kk * kWholePitch + i] = z.x;
+    gA[kk * kWholePitch + i] = goom_sign_t<R>(z.y);
+  }
+  for (int e = tid; e < k * m; e += 256) {
+    const int kk = e / m, j = e % m;
+    const Cx<R> z = bm[e];
+    sB[kk * kWholePitch + j] = z.x;
+    gB[kk * kWholePitch + j] = goom_sign_t<R>(z.y);
+  }
+  __syncthreads();
+  if (tid < 64) {  // clamped row maxima of A (max is exact: any order)
+    R v = R(-INFINITY);
+    if (tid < n)
+      for (int kk = 0; kk < k; ++kk) v = gmax(v, sA[kk * kWholePitch + tid]);
+    sc[tid] = gmax(v, R(0));
+  } else if (tid < 128) {  // clamped column maxima of B
+    const int j = tid - 64;
+    R v = R(-INFINITY);
+    if (j < m)
+      for (int kk = 0; kk < k; ++kk) v = gmax(v, sB[kk * kWholePitch + j]);
+    sc[tid] = gmax(v, R(0));
+  }
+  __syncthreads();
+  for (int e = tid; e < 64 * k; e += 256) {
+    const int kk = e >> 6, c = e & 63;
+    const int o = kk * kWholePitch + c;
+    sA[o] = c < n ? gA[o] * gexp(sA[o] - sc[c]) : R(0);
+    sB[o] = c < m ? gB[o] * gexp(sB[o] - sc[64 + c]) : R(0);
+  }
+  __syncthreads();
+  const int tx = tid & 15, ty = tid >> 4;
+  R acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = R(0);
+  for (int kk = 0; kk < k; ++kk) {
+    R ar[4], br[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ar[i] = sA[kk * kWholePitch + ty * 4 + i];
+      br[i] = sB[kk * kWholePitch + tx * 4 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = gfma(ar[i], br[j], acc[i][j]);
+  }
+  Cx<R>* c = C + b * strideC;
+  const Cx<R>* dd = D.ptr ? D.at(b) : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = tx * 4 + j;
+      if (cc >= m) continue;
+      Cx<R> o = lmme_out<R>(acc[i][j], sc[r], sc[64 + cc]);
+      if (dd) o = gadd_elem_t<R>(o, dd[(int64_t)r * m + cc]);
+      c[(int64_t)r * m + cc] = o;
+    }
+  }
+}
+
 }  // namespace
+
+template <class R>
+size_t lmme_whole_smem() {
+  return (size_t)(4 * 64 * kWholePitch + 128) * sizeof(R);
+}
+
+template <class R>
+int lmme_simt_whole(const LmmeProblemT<R>& p, cudaStream_t s) {
+  const size_t smem = lmme_whole_smem<R>();
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(lmme_whole_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "lmme_whole smem attribute");
+    attr = true;
+  }
+  const int64_t gmax_ = 2147483647;
+  for (int64_t b0 = 0; b0 < p.batch; b0 += gmax_) {
+    const int64_t nb = p.batch - b0 < gmax_ ? p.batch - b0 : gmax_;
+    lmme_whole_kernel<R><<<(unsigned)nb, 256, smem, s>>>(p.A, p.B, p.D, p.C, p.strideC, b0, p.n,
+                                                         p.k, p.m);
+    GOOM_CHECK_LAUNCH("lmme_whole_kernel");
+  }
+  return GOOM_OK;
+}
 
 template <class R>
 int lmme_simt_small(const LmmeProblemT<R>& p, cudaStream_t s) {
@@ -202,6 +319,8 @@ int lmme_simt_tiled(const LmmeProblemT<R>& p, cudaStream_t s) {
 
 template int lmme_simt_small<float>(const LmmeProblemT<float>&, cudaStream_t);
 template int lmme_simt_small<double>(const LmmeProblemT<double>&, cudaStream_t);
+template int lmme_simt_whole<float>(const LmmeProblemT<float>&, cudaStream_t);
+template int lmme_simt_whole<double>(const LmmeProblemT<double>&, cudaStream_t);
 template int lmme_simt_tiled<float>(const LmmeProblemT<float>&, cudaStream_t);
 template int lmme_simt_tiled<double>(const LmmeProblemT<double>&, cudaStream_t);
 

@@ -366,3 +366,28 @@ def test_lmme_tcgen05_fused_gadd_and_broadcast(g):
             assert err < 1e-4 and flips == 0
     finally:
         g._lib.set_backend(prev)
+
+
+@pytest.mark.parametrize("n,k,m", [(64, 64, 64), (48, 40, 56), (33, 64, 7)])
+def test_lmme_whole_kernel_bitwise_equals_prepass_path(g, n, k, m):
+    """n, k, m <= 64 take the one-CTA-per-product kernel with the row / column maxima fused;
+    it must be bitwise equal to the pre-pass + tiled path (goom_lmme_scaled_c64 with the
+    clamped maxima computed here), which the golden tests pin against the reference."""
+    import ctypes
+
+    torch.manual_seed(n * 10000 + k * 100 + m)
+    batch = 37
+    A = torch.ops.goom.from_real(torch.randn(batch, n, k, device="cuda") * 3, float("-inf"), False)
+    B = torch.ops.goom.from_real(torch.randn(batch, k, m, device="cuda") * 3, float("-inf"), False)
+    A[0, 1, :] = torch.complex(torch.tensor(float("-inf")), torch.tensor(0.0))  # a zero row
+    got = torch.ops.goom.lmme(A, B)
+    ra = A.real.amax(dim=2).clamp_min(0).contiguous()
+    cb = B.real.amax(dim=1).clamp_min(0).contiguous()
+    ref = torch.empty_like(got)
+    lib = g._lib.load()
+    g._lib.check(lib.goom_lmme_scaled_c64(
+        g._lib.goom_operand(A.data_ptr(), n * k, 1), ra.data_ptr(), n,
+        g._lib.goom_operand(B.data_ptr(), k * m, 1), cb.data_ptr(), m, ref.data_ptr(), n * m,
+        batch, n, k, m, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
