@@ -131,7 +131,7 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
-template <int kOut, int S>
+template <int kOut, int S, bool kChain>
 __global__ void __launch_bounds__(kThreads, 1)
     lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // tile -> (matrix pair b, row / column offsets, chain step); matrix indices of the
   // operands and the output: b / div (plain batch) or b s + step (chained phase 1)
   auto decode = [&](int64_t t, int64_t& b, int& prow0, int& pcol0, int& step) {
-    if (ch.s) {
+    if constexpr (kChain) {
       step = (int)(t / ch.tps) + 1;
       grid.at(t % ch.tps, b, prow0, pcol0);
     } else {
@@ -192,17 +192,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   auto idx_a = [&](int64_t b, int step) -> int64_t {
-    return ch.s ? b * ch.s + step : (A.sU == 0 ? 0 : b / A.div);
+    if constexpr (kChain) return b * ch.s + step;
+    return A.sU == 0 ? 0 : b / A.div;
   };
   auto idx_b = [&](int64_t b, int step) -> int64_t {
-    return ch.s ? b * ch.s + step - 1 : (B.sU == 0 ? 0 : b / B.div);
+    if constexpr (kChain) return b * ch.s + step - 1;
+    return B.sU == 0 ? 0 : b / B.div;
   };
-  auto idx_o = [&](int64_t b, int step) -> int64_t { return ch.s ? b * ch.s + step : b; };
+  auto idx_o = [&](int64_t b, int step) -> int64_t {
+    if constexpr (kChain) return b * ch.s + step;
+    return b;
+  };
   // a chained step reads the previous step's output: column tile JB of block b is complete
   // once all (n / 256) row pairs x 2 CTAs of every earlier step have signalled
   // (warp-collective: lane 0 acquires, __syncwarp orders the other lanes' loads after it)
   auto dep_ready = [&](int64_t b, int JB, int step) -> bool {
-    if (!ch.s || step < 2) return true;
+    if (!kChain || step < 2) return true;
     int ok = 0;
     if (lane == 0)
       ok = ld_acquire_u32(ch.done + b * nJm + JB) >= (uint32_t)(2 * (n / 256) * (step - 1));
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col0 = pcol0 + (int)rank * (kPairN / 2);
         const int ma = (int)idx_a(b, step);
         const int mb = (int)idx_b(b, step);
-        if (ch.s && step >= 2) {
+        if (kChain && step >= 2) {
           const uint32_t need = (uint32_t)(2 * (n / 256) * (step - 1));
           while (ld_acquire_u32(ch.done + b * nJm + pcol0 / 256) < need) __nanosleep(64);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // acquire before TMA reads
@@ -298,15 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int prow0, pcol0, step;
       decode(tile, b, prow0, pcol0, step);
       const int JB = pcol0 / 256;
-      if (ch.s) {
+      if constexpr (kChain) {
         if (!block && !dep_ready(b, JB, step)) return false;
         dep_wait(b, JB, step);
       }
       const int arow = prow0 + (int)rank * kRowsCta + arow_cta;
-      const float* qa = A.q + (ch.s ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)arow * nJk;
+      const float* qa = A.q + (kChain ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)arow * nJk;
 #pragma unroll
       for (int J = 0; J < 4; ++J) qan[J] = J < nJk ? qa[J] : kNegInf;
-      const int64_t ib = ch.s ? idx_b(b, step) : b / B.div;
+      const int64_t ib = kChain ? idx_b(b, step) : b / B.div;
       const float* qb = B.q + ib * B.sq + JB;
 #pragma unroll
       for (int h = 0; h < 2; ++h) qbn[h] = u + 512 * h < k ? qb[(int64_t)(u + 512 * h) * nJm] : 0.0f;
@@ -384,12 +389,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int wrow0 = prow0 + (int)rank * kRowsCta + quad * 32;
       const int JB = pcol0 / 256;
       const int64_t io = idx_o(b, step);
-      if (ch.s) dep_wait(b, JB, step);
+      if constexpr (kChain) dep_wait(b, JB, step);
       // product scales: rowmax q of the left operand's row, G of the right operand's block
-      const float* qa = A.q + (ch.s ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)grow * nJk;
+      const float* qa = A.q + (kChain ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)grow * nJk;
       float rho = kNegInf;
       for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
-      const float gB = decode_g(B.G[(ch.s ? idx_b(b, step) : b / B.div) * B.sG + JB]);
+      const float gB = decode_g(B.G[(kChain ? idx_b(b, step) : b / B.div) * B.sG + JB]);
       mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
       tc_fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * kPairN);
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_rank(acc_empty0 + buf * 8, 0);
-      if (ch.s) {  // publish this CTA's part of the output tile (U, q, G) to the next step
+      if constexpr (kChain) {  // publish this CTA's part of the output tile (U, q, G) to the next step
         if (lane == 0) {
           asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
           asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -539,7 +544,7 @@ int max_clusters() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, lmme_ts_kernel<kOut, S>, &cfg) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveClusters(&n, lmme_ts_kernel<kOut, S, false>, &cfg) != cudaSuccess ||
         n < 1) {
       cudaGetLastError();
       n = num_sms() / 2;
@@ -549,13 +554,13 @@ int max_clusters() {
   return v;
 }
 
-template <int kOut, int S>
+template <int kOut, int S, bool kChain = false>
 int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
                const CUtensorMap& mapOut, cudaStream_t s) {
   constexpr int kSmem = Lay<kOut, S>::kSmem;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut, S>,
+    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut, S, kChain>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
       return cuda_fail(cudaGetLastError(), "lmme_ts smem attribute");
     attr_set = true;
@@ -580,7 +585,8 @@ int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& m
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S>, mapA, mapB, mapOut, p.A, p.B, p.T, p.parts, pg,
+  cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S, kChain>, mapA, mapB, mapOut, p.A, p.B, p.T,
+                     p.parts, pg,
                      p.n, p.k, p.m, ts_debug(), ch);
   GOOM_CHECK_LAUNCH("lmme_ts_kernel");
   return GOOM_OK;
@@ -602,6 +608,8 @@ int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
     if (stage_cfg() == 1) return launch_cfg<kOut, 5>(p, mapA, mapB, mapOut, s);
     return launch_cfg<kOut, 6>(p, mapA, mapB, mapOut, s);
   } else {
+    if constexpr (kOut == kTsOutTs)
+      if (p.chain_s) return launch_cfg<kOut, 5, true>(p, mapA, mapB, mapOut, s);
     if (stage_cfg() == 1) return launch_cfg<kOut, 4>(p, mapA, mapB, mapOut, s);
     return launch_cfg<kOut, 5>(p, mapA, mapB, mapOut, s);
   }
