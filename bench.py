@@ -201,9 +201,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GOOM_BENCH_SHARE_GPU=1 (test aid): ranks share the visible GPUs round-robin and talk
+    # over gloo, so the N > 1 path (all-gather of the shard totals, max-over-ranks timing)
+    # can be exercised on a one-GPU box; numbers from such a run are not bench values
+    share = os.environ.get("GOOM_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2510_03426_b200 as goom
     from paper_2510_03426_b200 import harness, ops, sharded

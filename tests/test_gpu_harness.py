@@ -137,3 +137,28 @@ def test_resident_shards_equal_the_single_gpu_chain(h):
     gl, gs = to_np(runs[-1].final[None])
     rl, rs = to_np(full.final[None])
     assert scaled_real_err(gl, gs, rl, rs).max() < 1e-2
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N > 1 path end to end (torchrun, shard totals all-gathered, exclusive
+    carries, max-over-ranks timing, one JSON line from rank 0), with both ranks sharing the
+    box's GPU over gloo (GOOM_BENCH_SHARE_GPU=1)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GOOM_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29547", "bench.py", "--gpus", "2",
+           "--steps", "1", "--warmup", "1", "--T", "4096", "--window", "1024", "--block", "64",
+           "--no-cpu-baseline", "--e2e-T", "256"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    r = json.loads(lines[0])
+    assert r["n_gpus"] == 2 and r["config"]["parallelism"] == "time-sharded x2"
+    assert r["check"]["finite"]
+    assert abs(r["check"]["growth_per_step"] - r["check"]["expected_growth"]) < 0.05
