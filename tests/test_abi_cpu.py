@@ -80,7 +80,8 @@ def test_workspace_queries(lib):
     pol = _lib.goom_reset_policy(1, 12, 0, 0, 0.99, -20.7)
     assert L.goom_scan_selective_chain_workspace_size(1000, 64, ctypes.byref(pol), 256) > 0
     assert L.goom_lmme_workspace_size(16, 8, 8, 8) == 0  # small kernel: in-kernel scales
-    assert L.goom_lmme_workspace_size(16, 64, 64, 64) >= 2 * 16 * 64 * 4
+    assert L.goom_lmme_workspace_size(16, 64, 64, 64) == 0  # one CTA per product, fused scales
+    assert L.goom_lmme_workspace_size(16, 128, 128, 128) >= 2 * 16 * 128 * 4
 
 
 def test_public_api_names():
