@@ -203,7 +203,7 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         b = bp
     N = S * nC
     # panels: column index = s * nC + c; bi[i] (H, d, N)
-    bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).reshape(L, H, d, N)
+    bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).contiguous().reshape(L, H, d, N)
     Y = torch.empty((L, H, d, N), dtype=torch.complex128, device=dev)
     Y[0] = bi[0]
     for i in range(1, L):
@@ -214,10 +214,10 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         P[:, i] = torch.ops.goom.lmme(Ag, P[:, i - 1])
     s = torch.empty((nC, H, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
     s[0] = s0.transpose(1, 2)
-    Yl = Y[L - 1].reshape(H, d, S, nC)
+    Yl = Y[L - 1].reshape(H, d, S, nC).permute(3, 0, 1, 2).contiguous()  # (nC, H, d, S)
     PL = P[:, L - 1].contiguous()
     for c in range(1, nC):
-        s[c] = torch.ops.goom.lmme_gadd(PL, s[c - 1], Yl[..., c - 1])
+        s[c] = torch.ops.goom.lmme_gadd(PL, s[c - 1], Yl[c - 1])
     S_all = s.permute(1, 2, 3, 0).reshape(H, d, N)                      # (H, d, S nC)
     Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
     X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)
