@@ -260,6 +260,18 @@ int goom_chain_ts_finish(int64_t T, int d, int block, const float* cU, const flo
                          const uint32_t* cG, goom_c64* out, float* digests4, float* oU, float* oq,
                          uint32_t* oG, void* ws, size_t ws_bytes, void* stream);
 
+/* Time-sharded chain scan over an NCCL communicator (replaces the reference's
+ * _scan_affine_stack A slot, scan.py:181-214, for a chain split across the GPUs of a node;
+ * SURVEY §8b / §8e). Every rank passes its contiguous chunk A (T_local leaves, rank order =
+ * chain order) and gets the GLOBAL prefixes of those leaves in `out`: local scan, one
+ * ncclAllGather of the d x d chunk totals, the exclusive carry folded on the right, one
+ * batched LMME applying it. nccl_comm is an ncclComm_t (libnccl.so.2 is resolved from the
+ * process at run time); stream-ordered on `stream`. */
+size_t goom_scan_chain_sharded_workspace_size(int64_t T_local, int d, int block, int nranks);
+int goom_scan_chain_sharded_c64(const goom_c64* A, goom_c64* out, int64_t T_local, int d,
+                                int block, void* nccl_comm, void* ws, size_t ws_bytes,
+                                void* stream);
+
 /* Kernels libgoom has launched in this process (bench accounting). */
 long long goom_kernel_launches(void);
 

@@ -150,3 +150,32 @@ def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: 
         carry = exclusive_carry(total, torch.ops.goom.lmme, group)
     return t0, run_chain(n, d, seed, window, block, t0=t0, carry=carry,
                          snapshot_every=snapshot_every)
+
+
+def scan_chain_nccl(A_local: torch.Tensor, block: int = 64, group=None,
+                    comm: Optional[int] = None) -> torch.Tensor:
+    """Global prefixes of this rank's contiguous chunk of a chain split across ranks, in ONE
+    C-ABI call (goom_scan_chain_sharded_c64: local scan, ncclAllGather of the chunk totals,
+    exclusive carry, one batched LMME). A_local: complex64 (T_local, d, d) on this rank's
+    GPU; ranks hold consecutive chunks in rank order. `comm` is a raw ncclComm_t; by default
+    the NCCL communicator of `group` (torch's ProcessGroupNCCL)."""
+    import ctypes
+
+    from . import _lib
+
+    if A_local.dtype != torch.complex64 or not A_local.is_cuda or A_local.dim() != 3:
+        raise ValueError("A_local must be a complex64 CUDA tensor (T_local, d, d)")
+    if comm is None:
+        pg = group if group is not None else dist.distributed_c10d._get_default_group()
+        comm = pg._get_backend(A_local.device)._comm_ptr()
+    A_local = A_local.contiguous()
+    T, d = A_local.shape[0], A_local.shape[1]
+    lib = _lib.load()
+    nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+    nws = int(lib.goom_scan_chain_sharded_workspace_size(T, d, int(block), nranks))
+    ws = torch.empty(nws, dtype=torch.uint8, device=A_local.device)
+    out = torch.empty_like(A_local)
+    _lib.call("goom_scan_chain_sharded_c64", A_local.data_ptr(), out.data_ptr(), T, d, int(block),
+              ctypes.c_void_p(comm), ws.data_ptr(), nws,
+              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    return out

@@ -162,3 +162,63 @@ def test_bench_two_ranks_on_one_gpu():
     assert r["n_gpus"] == 2 and r["config"]["parallelism"] == "time-sharded x2"
     assert r["check"]["finite"]
     assert abs(r["check"]["growth_per_step"] - r["check"]["expected_growth"]) < 0.05
+
+
+def _nccl_single_rank_comm():
+    """A 1-rank NCCL communicator on the current GPU, straight from libnccl.so.2 (torch's)."""
+    import ctypes
+
+    import torch  # noqa: F401  (loads libnccl.so.2)
+
+    lib = ctypes.CDLL("libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert lib.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    assert lib.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    return lib, comm
+
+
+def test_scan_chain_sharded_c_abi_single_rank(h):
+    """goom_scan_chain_sharded_c64 over a real NCCL communicator (1 rank: the all-gather is
+    a copy and the carry is empty): equals goom_scan_chain_c64 bitwise."""
+    from paper_2510_03426_b200 import sharded
+
+    lib, comm = _nccl_single_rank_comm()
+    try:
+        for d, T in ((8, 100), (256, 40)):
+            A = h.random_chain(T, d, seed=3)
+            got = sharded.scan_chain_nccl(A, block=16, comm=comm.value)
+            want = torch.ops.goom.scan_chain(A, 16, None)
+            torch.cuda.synchronize()
+            assert torch.equal(torch.view_as_real(got), torch.view_as_real(want))
+    finally:
+        lib.ncclCommDestroy(comm)
+
+
+def test_scan_chain_sharded_c_abi_fold_matches_python(h):
+    """The C-ABI's exclusive-carry apply (steps 3-4) is the Python sharded fold: the chunks'
+    prefixes times the folded totals of the chunks before, checked against the one-GPU
+    chain; the NCCL all-gather itself is covered by the single-rank test above and the gloo
+    multi-process tests."""
+    from paper_2510_03426_b200 import sharded
+
+    T, d, world = 96, 8, 3
+    A = h.random_chain(T, d, seed=4)
+    full = torch.ops.goom.scan_chain(A, 16, None)
+    totals, chunks = [], []
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        loc = torch.ops.goom.scan_chain(A[t0:t0 + n].contiguous(), 16, None)
+        totals.append(loc[-1])
+        chunks.append(loc)
+    for r in range(world):
+        t0, n = sharded.shard_range(T, r, world)
+        carry = sharded.fold_carry(totals, r, torch.ops.goom.lmme)
+        got = chunks[r] if carry is None else torch.ops.goom.lmme(chunks[r], carry[None])
+        gl, gs = to_np(got)
+        wl, ws = to_np(full[t0:t0 + n])
+        assert scaled_real_err(gl, gs, wl, ws).max() < 1e-3
