@@ -17,7 +17,7 @@ complex64, flags: (T,) bool). The engines run in libgoom:
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional
+from typing import Callable, Optional
 
 import numpy as np
 import torch
