@@ -85,6 +85,17 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// four consecutive values from 16-byte aligned shared memory in one or two vector loads
+__device__ __forceinline__ void lds4(const float* p, float (&v)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+__device__ __forceinline__ void lds4(const double* p, double (&v)[4]) {
+  const double2 x = *reinterpret_cast<const double2*>(p);
+  const double2 y = *reinterpret_cast<const double2*>(p + 2);
+  v[0] = x.x, v[1] = x.y, v[2] = y.x, v[3] = y.y;
+}
+
 // ------------------------------------------------------------------------------
 constexpr int TM = 64, TN = 64, TK = 16, TPAD = 4;
 
@@ -143,11 +154,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
       R ar[4], br[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        ar[i] = sA[kk][ty * 4 + i];
-        br[i] = sB[kk][tx * 4 + i];
-      }
+      lds4(&sA[kk][ty * 4], ar);
+      lds4(&sB[kk][tx * 4], br);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -239,11 +247,8 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < 4; ++j) acc[i][j] = R(0);
   for (int kk = 0; kk < k; ++kk) {
     R ar[4], br[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ar[i] = sA[kk * kWholePitch + ty * 4 + i];
-      br[i] = sB[kk * kWholePitch + tx * 4 + i];
-    }
+    lds4(&sA[kk * kWholePitch + ty * 4], ar);
+    lds4(&sB[kk * kWholePitch + tx * 4], br);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
