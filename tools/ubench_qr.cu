@@ -82,6 +82,71 @@ __device__ void qr_regs_timed(double (&x)[16], int d, const Smem<Rt>& sm, int) {
   __syncthreads();
 }
 
+
+// ablations of the column loop (V = 3: named barrier only; 4: barrier + trailing update;
+// 5: owner reflector + barrier, no update)
+template <int V>
+__device__ void qr_ablate(double (&x)[16], int d, const Smem<double>& sm) {
+  const ColLane L = col_lane();
+  const int warp = threadIdx.x >> 5, qbase = threadIdx.x & 28;
+  double* Vt = sm.W;
+  double* tau = sm.vec;
+  double* diag = sm.vec + d;
+  for (int j = 0; j < d; ++j) {
+    if (warp < (j >> 3)) break;
+    if (V == 5 && warp == (j >> 3)) {
+      double sq[16], alpha = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int r = L.rc + 4 * i;
+        sq[i] = (r > j && r < d) ? x[i] * x[i] : 0.0;
+        if (r == j) alpha = x[i];
+      }
+      const double s = quad_sum(tree_sum16(sq));
+      alpha = __shfl_sync(0xffffffffu, alpha, qbase | (j & 3));
+      if (L.c == j) {
+        double t = 0.0, beta = alpha, scale = 0.0;
+        if (s != 0.0) {
+          const double n2 = fma(alpha, alpha, s);
+          const double rn = rsqrt(n2);
+          const double nrm = n2 * rn;
+          beta = -copysign(nrm, alpha);
+          t = fma(fabs(alpha), rn, 1.0);
+          scale = copysign(__drcp_rn(fabs(alpha) + nrm), alpha);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = L.rc + 4 * i;
+          if (r < d) Vt[j * d + r] = r > j ? x[i] * scale : (r == j ? 1.0 : 0.0);
+        }
+        if (L.rc == 0) {
+          tau[j] = t;
+          diag[j] = beta;
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"((kWarps - (j >> 3)) * 32) : "memory");
+    if (V == 4) {
+      const double t = tau[j];
+      if (t != 0.0) {
+        double pr[16], v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = L.rc + 4 * i;
+          v[i] = (r >= j && r < d) ? Vt[j * d + r] : 0.0;
+          pr[i] = v[i] * x[i];
+        }
+        const double w = t * quad_sum(tree_sum16(pr));
+        if (L.c > j && L.c < d) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) x[i] = fma(-w, v[i], x[i]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 template <int V>
 __global__ void __launch_bounds__(kThreads, 1) qr_bench(const double* M, int d, int reps, int t_obs,
                                                          long long* cyc, double* diag_out) {
@@ -101,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) qr_bench(const double* M, int d, 
     if (V == 0) qr_regs(x, d, sm);
     if (V == 1) qr_regs_timed(x, d, sm, t_obs);
     if (V == 2) q_regs(x, d, true, sm);
+    if (V >= 3) qr_ablate<V>(x, d, sm);
     __syncthreads();
     total += clock64() - t0;
   }
@@ -154,6 +220,14 @@ int main(int argc, char** argv) {
         printf("\n");
       }
     }
+  }
+  for (int v = 3; v <= 5; ++v) {
+    if (v == 3) { cudaFuncSetAttribute(qr_bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb); qr_bench<3><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag); }
+    if (v == 4) { cudaFuncSetAttribute(qr_bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb); qr_bench<4><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag); }
+    if (v == 5) { cudaFuncSetAttribute(qr_bench<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb); qr_bench<5><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag); }
+    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    printf("ablation %d (%s): %lld cycles (%.1f per column)\n", v,
+           v == 3 ? "barrier only" : v == 4 ? "barrier + update" : "owner + barrier", hc[0], hc[0] / 64.0);
   }
   qr_bench<2><<<1, kThreads, sb>>>(M, d, reps, 0, cyc, diag);
   cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
