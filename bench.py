@@ -345,6 +345,18 @@ def main():
             e2e_times.append(ms)
         del r, out
     e2e_value = Te / (statistics.median(e2e_times) / 1e3)
+    # the link's own ceiling in this run: a plain pinned H2D copy of the same leaves
+    dcopy = torch.empty(host.shape, dtype=host.dtype, device=dev)
+    h2d_ms = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        dcopy.copy_(host, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        h2d_ms.append(s.elapsed_time(e))
+    h2d_gbs = host.numel() * host.element_size() / (min(h2d_ms) / 1e3) / 1e9
+    del dcopy
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -373,6 +385,8 @@ def main():
                          "frac_vs_cublas_tf32_div3": tflops / (tf32_cublas / 3)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * d * d * 4,
                     "d2h_bytes_per_step": ne * 16,
+                    "h2d_gbs_per_gpu": ne * d * d * 4 / (statistics.median(e2e_times) / 1e3) / 1e9,
+                    "h2d_gbs_plain_copy_in_run": h2d_gbs,
                     "workload": f"T={Te} real float32 leaves in pinned host memory -> "
                                 f"harness.run_chain (window {we}, H2D overlapped), digests D2H"},
             "gpu_launches": launches // max(args.steps, 1),
