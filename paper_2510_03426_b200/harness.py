@@ -150,3 +150,91 @@ def growth_rate(digests: torch.Tensor) -> float:
         return float("nan")
     h = T // 2
     return float((lf[-1] - lf[h]) / (T - 1 - h))
+
+
+# ---------------------------------------------------------------------------
+# the chain-survival experiment (SPEC.md:391-455 run_chain; paper Fig. 1, Eq. 13-14)
+
+BACKENDS = ("real64", "real32", "goom64", "goom32")
+
+
+@dataclass(frozen=True)
+class ChainConfig:
+    """d x d random-normal chains of up to T_max steps, `trials` of them (SPEC ChainConfig)."""
+
+    d: int
+    T_max: int
+    backend: str
+    seed: int = 0
+    trials: int = 1
+
+    def __post_init__(self):
+        if self.d < 1 or self.T_max < 1 or self.trials < 1:
+            raise ValueError("d, T_max and trials must be >= 1")
+        if self.backend not in BACKENDS:
+            raise ValueError(f"backend must be one of {BACKENDS}")
+
+
+@dataclass
+class ChainResult:
+    """Per trial: steps survived (<= T_max), whether the chain completed, and the first
+    failure ('overflow', 'underflow', 'nan' or None)."""
+
+    survived_steps: list
+    completed: list
+    failure_mode: list
+
+
+def _first_failure(bad: torch.Tensor):
+    """Index of the first True along dim 0 per column (T_max when none)."""
+    T = bad.shape[0]
+    idx = torch.arange(T, device=bad.device)[:, None].expand_as(bad)
+    return torch.where(bad, idx, torch.full_like(idx, T)).min(dim=0).values
+
+
+def chain_survival(cfg: ChainConfig) -> ChainResult:
+    """Iterate S_t = A_t S_{t-1} (S_0 = A_0) over random-normal leaves (device RNG keyed by
+    (seed + trial, t)) until T_max or the first non-finite state. Real backends multiply
+    plainly in float64 / float32 (torch on the GPU, one batched product per step over the
+    trials); GOOM backends run the chain scan on complex128 / complex64 GOOMs, all T_max
+    prefixes, and a state fails when any log-magnitude is non-finite (NaN or +inf) — which
+    for GOOMs is the representable range of the float64 / float32 log itself."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d, T, n = cfg.d, cfg.T_max, cfg.trials
+    leaves = [random_chain(T, d, cfg.seed + i, 0, dev) for i in range(n)]
+    steps, modes = [], []
+    if cfg.backend.startswith("real"):
+        rt = torch.float64 if cfg.backend == "real64" else torch.float32
+        A = torch.stack([torch.ops.goom.to_real(L, True) for L in leaves], dim=1).to(rt)  # (T, n, d, d)
+        S = A[0].clone()
+        alive = torch.ones(n, dtype=torch.bool, device=dev)
+        surv = torch.full((n,), T, dtype=torch.int64, device=dev)
+        mode = torch.zeros(n, dtype=torch.int8, device=dev)  # 0 none, 1 overflow, 2 underflow, 3 nan
+        for t in range(T):
+            if t:
+                S = torch.bmm(A[t], S)
+            flat = S.reshape(n, -1)
+            nan = torch.isnan(flat).any(dim=1)
+            inf = torch.isinf(flat).any(dim=1)
+            zero = (flat == 0).all(dim=1)
+            fail = alive & (nan | inf | zero)
+            surv = torch.where(fail, torch.full_like(surv, t), surv)
+            mode = torch.where(fail, torch.where(nan, 3, torch.where(inf, 1, 2)).to(torch.int8), mode)
+            alive &= ~fail
+            if t % 256 == 255 and not bool(alive.any()):
+                break
+        steps = surv.tolist()
+        names = {0: None, 1: "overflow", 2: "underflow", 3: "nan"}
+        modes = [names[int(m)] for m in mode.tolist()]
+    else:
+        ct = torch.complex128 if cfg.backend == "goom64" else torch.complex64
+        for L in leaves:
+            P = torch.ops.goom.scan_chain(L.to(ct), 64, None)
+            lg = P.real.reshape(T, -1)
+            bad = torch.isnan(lg).any(dim=1) | torch.isposinf(lg).any(dim=1)
+            first = int(_first_failure(bad[:, None])[0])
+            steps.append(first)
+            modes.append(None if first == T else
+                         ("nan" if bool(torch.isnan(lg[first]).any()) else "overflow"))
+    return ChainResult(survived_steps=steps, completed=[s == T for s in steps],
+                       failure_mode=modes)

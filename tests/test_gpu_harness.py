@@ -222,3 +222,21 @@ def test_scan_chain_sharded_c_abi_fold_matches_python(h):
         gl, gs = to_np(got)
         wl, ws = to_np(full[t0:t0 + n])
         assert scaled_real_err(gl, gs, wl, ws).max() < 1e-3
+
+
+def test_chain_survival_real_overflows_goom_completes(h):
+    """SPEC run_chain (paper Fig. 1): float64 products of 8x8 N(0,1) matrices overflow
+    within ~700 steps (log-growth ~1.04/step vs the float64 limit ~709.8), float32 within
+    ~90; complex64 / complex128 GOOM chains complete the whole length."""
+    T = 2000
+    r64 = h.chain_survival(h.ChainConfig(d=8, T_max=T, backend="real64", seed=1, trials=3))
+    r32 = h.chain_survival(h.ChainConfig(d=8, T_max=T, backend="real32", seed=1, trials=3))
+    assert all(not c for c in r64.completed) and all(m == "overflow" for m in r64.failure_mode)
+    assert all(500 < s < 1000 for s in r64.survived_steps), r64.survived_steps
+    assert all(40 < s < 150 for s in r32.survived_steps), r32.survived_steps
+    for be in ("goom64", "goom32"):
+        r = h.chain_survival(h.ChainConfig(d=8, T_max=T, backend=be, seed=1, trials=2))
+        assert all(r.completed) and r.survived_steps == [T, T] and r.failure_mode == [None, None]
+    # d = 1, A = [[1]] never fails: not expressible with random leaves; the config validates
+    with pytest.raises(ValueError):
+        h.ChainConfig(d=8, T_max=10, backend="real16")
