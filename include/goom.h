@@ -272,6 +272,13 @@ int goom_scan_chain_sharded_c64(const goom_c64* A, goom_c64* out, int64_t T_loca
                                 int block, void* nccl_comm, void* ws, size_t ws_bytes,
                                 void* stream);
 
+/* Profiling aid (bench.py's roofline): time every digest phase-3 launch of the
+ * tile-scaled chain engine with CUDA events on its own stream. _timing(1) starts a fresh
+ * log, _timing(0) stops logging; _stats synchronises and returns the logged launches,
+ * their total milliseconds and total products. */
+void goom_chain_ts_phase3_timing(int enable);
+int goom_chain_ts_phase3_stats(int64_t* launches, double* total_ms, int64_t* products);
+
 /* Kernels libgoom has launched in this process (bench accounting). */
 long long goom_kernel_launches(void);
 

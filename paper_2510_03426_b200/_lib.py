@@ -138,6 +138,8 @@ SIGNATURES = {
         _I,
         [_I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
     ),
+    "goom_chain_ts_phase3_timing": (None, [_I]),
+    "goom_chain_ts_phase3_stats": (_I, [_P, _P, _P]),
     "goom_scan_chain_sharded_workspace_size": (_SZ, [_I64, _I, _I, _I]),
     "goom_scan_chain_sharded_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
     "goom_chain_ts": (

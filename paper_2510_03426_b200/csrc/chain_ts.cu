@@ -11,6 +11,9 @@
 // Cx[nb] = P_{T-1} is the carry-out of a window. Between phases every matrix stays
 // tile-scaled: no exp/log per element except the leaf import and the final export.
 #include <cstdlib>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "goom_internal.cuh"
 
@@ -97,6 +100,41 @@ int lmme_ts_call(TsIn a, TsIn b, int kind, float2* C, int64_t strideC, TsOut T, 
   p.n = p.k = p.m = d;
   return lmme_ts(p, st);
 }
+
+// Phase-3 launch timing inside real runs (bench.py's roofline: the dominant kernel's
+// duration measured in the timed region, on its own stream): when enabled, every digest
+// phase-3 launch is bracketed by a pair of CUDA events; the totals are read back later.
+struct Phase3Log {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<int64_t> products;
+};
+Phase3Log& phase3_log() {
+  static Phase3Log log;
+  return log;
+}
+struct Phase3Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  int64_t n;
+  Phase3Timer(cudaStream_t s, int64_t products) : st(s), n(products) {
+    Phase3Log& log = phase3_log();
+    std::lock_guard<std::mutex> lock(log.mu);
+    if (!log.on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  void stop() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    Phase3Log& log = phase3_log();
+    std::lock_guard<std::mutex> lock(log.mu);
+    log.ev.emplace_back(a, b);
+    log.products.push_back(n);
+  }
+};
 
 }  // namespace
 
@@ -255,8 +293,10 @@ int chain_finish(int64_t T, int d, int block, const TsBuf* carry, float2* out, f
     GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutGoom, out, (int64_t)d * d,
                           TsOut{}, nullptr, T, d, st));
   if (digests) {
+    Phase3Timer timer(st, T);
     GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutDigest, nullptr, 0, TsOut{},
                           w.parts, T, d, st));
+    timer.stop();
     GOOM_TRY(launch_digest_reduce(w.parts, (d / 32) * nJ, digests, T, st));
   }
   if (carry_out) GOOM_TRY(copy_ts(*carry_out, 0, w.Cx, nb, 1, 1, st));
@@ -313,6 +353,39 @@ TsBuf ts_of(float* U, float* q, uint32_t* G, int d) {
 }  // namespace
 
 extern "C" {
+
+// Phase-3 launch timing (profiling aid for bench.py): enable != 0 starts a fresh log;
+// goom_chain_ts_phase3_stats synchronises the logged events and returns the launches,
+// their total milliseconds and total products.
+void goom_chain_ts_phase3_timing(int enable) {
+  Phase3Log& log = phase3_log();
+  std::lock_guard<std::mutex> lock(log.mu);
+  for (auto& e : log.ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  log.ev.clear();
+  log.products.clear();
+  log.on = enable != 0;
+}
+int goom_chain_ts_phase3_stats(int64_t* launches, double* total_ms, int64_t* products) {
+  Phase3Log& log = phase3_log();
+  std::lock_guard<std::mutex> lock(log.mu);
+  double ms = 0.0;
+  int64_t prod = 0;
+  for (size_t i = 0; i < log.ev.size(); ++i) {
+    float t = 0.0f;
+    if (cudaEventSynchronize(log.ev[i].second) != cudaSuccess ||
+        cudaEventElapsedTime(&t, log.ev[i].first, log.ev[i].second) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "phase-3 timing events");
+    ms += t;
+    prod += log.products[i];
+  }
+  if (launches) *launches = (int64_t)log.ev.size();
+  if (total_ms) *total_ms = ms;
+  if (products) *products = prod;
+  return GOOM_OK;
+}
 
 size_t goom_chain_ts_workspace_size(int64_t T, int d, int block) {
   if (T < 1 || d < 256 || d % 256 || block < 1) return 0;
