@@ -137,9 +137,14 @@ def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: 
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     t0, n = shard_range(T, rank, world)
     if world > 1 and ops.ts_eligible(d) and not snapshot_every:
+        # a smaller window only pays when it lets the WHOLE shard stay resident (the engine's
+        # launches lose efficiency below ~8k products); otherwise keep the window and let
+        # run_shard_resident keep as many windows as fit
         w = window
         while w > 8192 and not resident_fits(n, d, w):
-            w //= 2  # a smaller window leaves room for more resident local products
+            w //= 2
+        if not resident_fits(n, d, w):
+            w = window
         # keeps as many windows' local products as fit; recomputes only the rest
         return t0, run_shard_resident(
             n, d, seed, t0, w, block,
