@@ -16,9 +16,11 @@ for G in (8, 4, 2):
     n = T // G
     for mode in ("resident", "recompute"):
         if mode == "resident":
-            w = 32768
+            w = 32768  # sharded.run_chain_sharded's choice: shrink only if all then fits
             while w > 8192 and not sharded.resident_fits(n, d, w):
                 w //= 2
+            if not sharded.resident_fits(n, d, w):
+                w = 32768
             fn = lambda: sharded.run_shard_resident(n, d, 1, 0, w, block, lambda t: t)  # noqa: E731
         else:
             w = 32768
