@@ -265,7 +265,7 @@ __device__ __forceinline__ double tree_sum16(double (&a)[16]) {
 // thread's column into x, the whole matrix into sm.R (row-major, for the Gram) and the
 // column log-norms nu_c = m + 1/2 log sum e^{2(L - m)} into sm.vec[0, d). Returns true
 // (CTA-uniform) when some column is all zero.
-template <class Rt>
+template <class Rt, bool kStoreR = true>
 __device__ bool unit_columns_regs(const Cx<Rt>* X, int d, double (&x)[16], const Smem<Rt>& sm) {
   const ColLane L = col_lane();
   const bool live = L.c < d;
@@ -299,7 +299,7 @@ __device__ bool unit_columns_regs(const Cx<Rt>* X, int d, double (&x)[16], const
   for (int i = 0; i < 16; ++i) {
     const int r = L.rc + 4 * i;
     x[i] = (live && r < d && !zero) ? x[i] * exp(lg[i] - nu) : 0.0;
-    if (live && r < d) sm.R[r * d + L.c] = x[i];
+    if (kStoreR && live && r < d) sm.R[r * d + L.c] = x[i];
   }
   if (live && L.rc == 0) sm.vec[L.c] = nu;
   return __syncthreads_or(zero) != 0;
@@ -754,18 +754,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 // from_goom: the input is a complex128 GOOM state, first log-unit-normalised per column
 // (spectrum_parallel stage (b), lyapunov.py:343-347); an all-zero column sets *status.
 // Outputs Q (real, row-major) and |diag R|.
-__global__ void __launch_bounds__(kThreads, 1)
+// Only the reflector table and the small vectors live in shared memory (the matrix is read
+// straight into registers), so several CTAs share an SM.
+inline size_t qr_lean_smem_bytes(int d) {
+  return ((size_t)d * d + 2 * d + 2 * kWarps + 4 * kMaxD) * sizeof(double) + 64;
+}
+__device__ Smem<double> carve_lean(char* base, int d) {
+  Smem<double> s{};
+  s.W = reinterpret_cast<double*>(base);
+  s.vec = s.W + (size_t)d * d;
+  s.red = s.vec + 2 * d;
+  s.part = s.red + 2 * kWarps;
+  return s;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
     qr_batched_kernel(const double* __restrict__ M, const double2* __restrict__ X,
                       double* __restrict__ Q, double* __restrict__ absdiag, int d,
                       int* __restrict__ status) {
   extern __shared__ __align__(16) char smem_raw[];
-  Smem<double> sm = carve<double>(smem_raw, d);
+  Smem<double> sm = carve_lean(smem_raw, d);
   const int64_t mat = (int64_t)d * d;
   const ColLane L = col_lane();
   double x[16];
   if (X) {
-    copy_mat(X + blockIdx.x * mat, sm.el, d);
-    if (unit_columns_regs(sm.el, d, x, sm)) {
+    if (unit_columns_regs<double, false>(X + blockIdx.x * mat, d, x, sm)) {
       if (threadIdx.x == 0) *status = GOOM_EINVAL;
       return;
     }
@@ -1104,8 +1117,11 @@ int qr_batched_entry(const double* M, const double2* X, double* Q, double* absdi
   if (cudaMallocAsync(&status, sizeof(int), st) != cudaSuccess ||
       cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
     return goom::cuda_fail(cudaGetLastError(), "qr status");
-  GOOM_TRY(goom::set_smem<double>((const void*)goom::qr_batched_kernel, d));
-  goom::qr_batched_kernel<<<(unsigned)batch, goom::kThreads, goom::smem_bytes<double>(d), st>>>(
+  if (cudaFuncSetAttribute((const void*)goom::qr_batched_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)goom::qr_lean_smem_bytes(d)) != cudaSuccess)
+    return goom::cuda_fail(cudaGetLastError(), "qr smem attribute");
+  goom::qr_batched_kernel<<<(unsigned)batch, goom::kThreads, goom::qr_lean_smem_bytes(d), st>>>(
       M, X, Q, absdiag, d, status);
   GOOM_CHECK_LAUNCH("qr_batched_kernel");
   int host_status = 0;
