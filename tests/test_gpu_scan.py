@@ -375,3 +375,29 @@ def test_warp_resident_small_chain_is_bitwise_the_blocked_tree(g, d, T, block, c
                                      np.zeros(T + 1, bool)))
     wl, ws = to_np(with_carry)
     assert scaled_real_err(wl, ws, want.alog[1:], want.asign[1:]).max() < (1e-9 if c128 else 5e-3)
+
+
+def test_parallel_beats_sequential_on_wide_chain(g):
+    """test_scan.py:340-360: 2^15 leaves of 8x8 through the pair API, parallel (block 256)
+    vs the sequential fold — same last state to 1e-10, and at least 2x faster."""
+    import time
+
+    rng = np.random.default_rng(49)
+    T, d = 2 ** 15, 8
+    alog = rng.uniform(-1, 1, (T, d, d))
+    asign = rng.choice([-1.0, 1.0], (T, d, d))
+    stack = g._Stack.from_arrays(alog, asign, np.full((T, d, d), -np.inf), np.ones((T, d, d)))
+    g.scan_parallel(stack, g.combine_affine, block_size=256)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    seq = g._scan_affine_stack(stack, T)  # block >= T: the sequential fold (scan.py:217-225)
+    torch.cuda.synchronize()
+    t_seq = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    par = g.scan_parallel(stack, g.combine_affine, block_size=256)
+    torch.cuda.synchronize()
+    t_par = time.perf_counter() - t0
+    pl = par.A[-1].real.cpu().numpy()
+    sl = seq.A[-1].real.cpu().numpy()
+    assert G.rel_log_diff(pl, sl) < 1e-10
+    assert t_seq / t_par >= 2.0, (t_seq, t_par)
