@@ -391,3 +391,25 @@ def test_lmme_whole_kernel_bitwise_equals_prepass_path(g, n, k, m):
         batch, n, k, m, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
     assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
+
+
+def test_lmme_64x64_against_50_digit_reference(g):
+    """test_core.py:196-203 with its 50-digit oracle (mpmath): complex128 LMME of two
+    64x64 N(0,1) matrices, Frobenius relative error < 1e-12; complex64 (3xTF32) < 1e-6."""
+    mpmath = pytest.importorskip("mpmath")
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((64, 64))
+    b = rng.standard_normal((64, 64))
+    with mpmath.workdps(50):
+        A = [[mpmath.mpf(float(x)) for x in row] for row in a]
+        B = [[mpmath.mpf(float(x)) for x in row] for row in b]
+        want = np.array([[float(mpmath.fsum(A[i][k] * B[k][j] for k in range(64)))
+                          for j in range(64)] for i in range(64)])
+    for dt, tol in ((torch.complex128, 1e-12), (torch.complex64, 1e-6)):
+        al, as_ = G.log_sign(a)
+        bl, bs = G.log_sign(b)
+        out = torch.ops.goom.lmme(g.join(al, as_, dt), g.join(bl, bs, dt))
+        gl, gs = to_np(out)
+        got = gs * np.exp(gl.astype(np.float64))
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err < tol, (dt, err)
