@@ -81,3 +81,28 @@ def test_lle_matches_reference(g):
     assert abs(g.lle_parallel(dbl, np.array([0.0, 1.0, 0.0])) - math.log(2.0)) < 1e-12
     with pytest.raises(ValueError):
         g.lle_parallel(ident, np.array([0.0, 0.0, 0.0]))
+
+
+def test_spectrum_sequential_and_parallel_properties(g):
+    """test_lyapunov.py:135-162 on both GPU estimators: c I gives log(c)/dt, scaling every
+    Jacobian by 4 shifts every exponent by log(4)/dt, the exponents sum to the mean log|det|
+    (sequential; the parallel one within its reset tolerance), invalid S0 raises."""
+    import math
+
+    chain = g.JacobianChain(dt=0.5, mats=np.tile(1.7 * np.eye(3), (50, 1, 1)))
+    for est in (g.spectrum_sequential, g.spectrum_parallel):
+        np.testing.assert_allclose(est(chain).lambdas, math.log(1.7) / 0.5, rtol=1e-12)
+    rng = np.random.default_rng(54)
+    mats = rng.standard_normal((64, 3, 3))
+    for est, tol in ((g.spectrum_sequential, 1e-9), (g.spectrum_parallel, 1e-6)):
+        base = est(g.JacobianChain(dt=0.1, mats=mats)).lambdas
+        scaled = est(g.JacobianChain(dt=0.1, mats=4.0 * mats)).lambdas
+        np.testing.assert_allclose(scaled - base, math.log(4.0) / 0.1, rtol=tol)
+    rng = np.random.default_rng(55)
+    mats = rng.standard_normal((200, 3, 3))
+    want = np.mean([math.log(abs(np.linalg.det(m))) for m in mats]) / 0.25
+    res = g.spectrum_sequential(g.JacobianChain(dt=0.25, mats=mats))
+    assert abs(res.lambdas.sum() - want) / abs(want) < 1e-6
+    with pytest.raises(ValueError):
+        g.spectrum_sequential(g.JacobianChain(dt=1.0, mats=np.tile(np.eye(2), (4, 1, 1))),
+                              s0=np.array([[2.0, 0.0], [0.0, 1.0]]))

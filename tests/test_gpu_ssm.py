@@ -188,3 +188,47 @@ def test_ssm_heads_forward_backward_match_per_head(s):
     (out * torch.tensor(gy, device=dev)).sum().backward()
     for t, ref in zip(ts, grads):
         assert _rel_max(t.grad.cpu().numpy(), ref) < 1e-12
+
+
+def test_ssm_matches_50_digit_recurrence_despite_growth(s):
+    """test_ssm.py:114-131: spectral radius 1.5, T = 512: the scaled states match a 50-digit
+    affine recurrence to 1e-9 at several steps while the states grow like 1.5^t."""
+    mpmath = pytest.importorskip("mpmath")
+    rng = np.random.default_rng(66)
+    d, T = 8, 512
+    a = rng.standard_normal((d, d))
+    a *= 1.5 / np.max(np.abs(np.linalg.eigvals(a)))
+    p = s.SsmParams(a, rng.standard_normal((d, d)), rng.standard_normal((2 * d, d)),
+                    rng.standard_normal((2 * d, d)))
+    x0 = rng.standard_normal(d)
+    u = rng.standard_normal((T, d))
+    run = s.ssm_forward_parallel(p, x0, u)
+    with mpmath.workdps(50):
+        A = [[mpmath.mpf(float(v)) for v in row] for row in p.A]
+        bu = (p.B @ u.T).T
+        x = [mpmath.mpf(float(v)) for v in x0]
+        checks = {0, 1, 63, 255, 511}
+        for t in range(T):
+            x = [mpmath.fsum(A[i][k] * x[k] for k in range(d)) + mpmath.mpf(float(bu[t][i]))
+                 for i in range(d)]
+            if t in checks:
+                ours = run.state_sign[t] * np.exp(run.state_log[t] - run.scales[t])
+                sc = mpmath.exp(-mpmath.mpf(float(run.scales[t])))
+                want = np.array([float(v * sc) for v in x])
+                np.testing.assert_allclose(ours, want, rtol=1e-9)
+    assert run.state_log[-1].max() > 512 * np.log(1.5) * 0.8
+
+
+def test_ssm_scaled_state_bound(s):
+    """test_ssm.py:155-163: every scaled state entry is at most e^2 and each state's max is e^2."""
+    rng = np.random.default_rng(68)
+    d = 4
+    a = rng.standard_normal((d, d))
+    a *= 1.8 / np.max(np.abs(np.linalg.eigvals(a)))
+    p = s.SsmParams(a, rng.standard_normal((d, d)), rng.standard_normal((2 * d, d)),
+                    rng.standard_normal((2 * d, d)))
+    run = s.ssm_forward_parallel(p, rng.standard_normal(d), rng.standard_normal((300, d)))
+    scaled = run.scaled_states()
+    e2 = np.exp(2.0)
+    assert np.all(np.abs(scaled) <= e2 * (1 + 1e-12))
+    np.testing.assert_allclose(np.max(np.abs(scaled), axis=1), e2)
