@@ -413,3 +413,41 @@ def test_lmme_64x64_against_50_digit_reference(g):
         got = gs * np.exp(gl.astype(np.float64))
         err = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert err < tol, (dt, err)
+
+
+def test_column_norms_and_scaled_export_reference_cases(g):
+    """test_core.py:258-311 (log_unit_norm_columns, to_real_scaled) and the 10^4 float64
+    round trip (test_core.py:318-323), on float64-backed GoomMatrix (the reference's default
+    backing; ours defaults to complex64, dtype=np.float64 selects complex128)."""
+    m = g.GoomMatrix.from_real(np.array([[1.0], [0.0]]), dtype=np.float64)
+    out, nu = g.log_unit_norm_columns(m)
+    assert abs(nu[0]) < 1e-14
+    np.testing.assert_allclose(out.to_real().cpu().numpy().ravel(), [1.0, 0.0])
+    m = g.GoomMatrix(np.full((2, 1), 1000.0), np.ones((2, 1)), dtype=np.float64)
+    out, _ = g.log_unit_norm_columns(m)
+    np.testing.assert_allclose(out.to_real().cpu().numpy().ravel(), [0.70710678, 0.70710678],
+                               rtol=1e-7)
+    rng = np.random.default_rng(14)
+    m = g.GoomMatrix(rng.uniform(-500, 500, (6, 6)), rng.choice([-1.0, 1.0], (6, 6)),
+                     dtype=np.float64)
+    out, _ = g.log_unit_norm_columns(m)
+    norms = np.log(np.linalg.norm(out.to_real().cpu().numpy(), axis=0))
+    assert np.max(np.abs(norms)) < 1e-10
+    out, c = g.to_real_scaled(g.GoomMatrix(np.full((3, 3), 1e6), np.ones((3, 3)),
+                                           dtype=np.float64))
+    assert c == 1e6
+    np.testing.assert_array_equal(out.cpu().numpy(), np.full((3, 3), np.exp(2.0)))
+    out, c = g.to_real_scaled(g.GoomMatrix.from_real(np.array([[1.0]]), dtype=np.float64))
+    assert c == 0.0 and float(out[0, 0]) == np.exp(2.0)
+    rng = np.random.default_rng(15)
+    m = g.GoomMatrix(rng.uniform(-1e8, 1e8, (4, 4)), rng.choice([-1.0, 1.0], (4, 4)),
+                     dtype=np.float64)
+    out, c = g.to_real_scaled(m)
+    o = np.abs(out.cpu().numpy())
+    assert o.max() == np.exp(2.0) and np.all(o <= np.exp(2.0))
+    rng = np.random.default_rng(20)
+    xs = rng.standard_normal(10_000) * np.exp(rng.uniform(-200, 200, 10_000))
+    xs = np.where(xs == 0, 1.0, xs)
+    back = g.GoomMatrix.from_real(xs.reshape(100, -1), dtype=np.float64).to_real()
+    back = back.cpu().numpy().ravel()
+    assert np.all(np.abs(back / xs - 1.0) < 1e-12)
