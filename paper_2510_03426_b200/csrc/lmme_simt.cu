@@ -199,9 +199,9 @@ __global__ void __launch_bounds__(256)
   extern __shared__ __align__(16) unsigned char whole_smem[];
   R* sA = reinterpret_cast<R*>(whole_smem);   // [kk][row]: log, then sign * exp(log - a)
   R* sB = sA + 64 * kWholePitch;              // [kk][col]
-  R* gA = sB + 64 * kWholePitch;              // signs, same layouts
-  R* gB = gA + 64 * kWholePitch;
-  R* sc = gB + 64 * kWholePitch;              // [0, 64) a_i, [64, 128) b_j
+  R* sc = sB + 64 * kWholePitch;              // [0, 64) a_i, [64, 128) b_j
+  signed char* gA = reinterpret_cast<signed char*>(sc + 128);  // signs (+1 / -1), same layouts
+  signed char* gB = gA + 64 * kWholePitch;
   const int64_t b = b_base + blockIdx.x;
   const Cx<R>* a = A.at(b);
   const Cx<R>* bm = B.at(b);
@@ -210,13 +210,13 @@ __global__ void __launch_bounds__(256)
     const int i = e / k, kk = e % k;
     const Cx<R> z = a[e];
     sA[kk * kWholePitch + i] = z.x;
-    gA[kk * kWholePitch + i] = goom_sign_t<R>(z.y);
+    gA[kk * kWholePitch + i] = goom_sign_t<R>(z.y) < R(0) ? -1 : 1;
   }
   for (int e = tid; e < k * m; e += 256) {
     const int kk = e / m, j = e % m;
     const Cx<R> z = bm[e];
     sB[kk * kWholePitch + j] = z.x;
-    gB[kk * kWholePitch + j] = goom_sign_t<R>(z.y);
+    gB[kk * kWholePitch + j] = goom_sign_t<R>(z.y) < R(0) ? -1 : 1;
   }
   __syncthreads();
   if (tid < 64) {  // clamped row maxima of A (max is exact: any order)
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(256)
   for (int e = tid; e < 64 * k; e += 256) {
     const int kk = e >> 6, c = e & 63;
     const int o = kk * kWholePitch + c;
-    sA[o] = c < n ? gA[o] * gexp(sA[o] - sc[c]) : R(0);
-    sB[o] = c < m ? gB[o] * gexp(sB[o] - sc[64 + c]) : R(0);
+    sA[o] = c < n ? R(gA[o]) * gexp(sA[o] - sc[c]) : R(0);
+    sB[o] = c < m ? R(gB[o]) * gexp(sB[o] - sc[64 + c]) : R(0);
   }
   __syncthreads();
   const int tx = tid & 15, ty = tid >> 4;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256)
 
 template <class R>
 size_t lmme_whole_smem() {
-  return (size_t)(4 * 64 * kWholePitch + 128) * sizeof(R);
+  return (size_t)(2 * 64 * kWholePitch + 128) * sizeof(R) + 2 * 64 * kWholePitch;
 }
 
 template <class R>
