@@ -368,14 +368,15 @@ def ssm_backward_heads(A, B, C, D, x0s, us, state_log, state_sign, scales, gy, c
     zero = torch.full((H, S, d), complex(NEG_INF, 0.0), dtype=torch.complex128, device=dev)
     lam = _chunked_scan(_goom(A.transpose(1, 2).contiguous()), g.flip(2), zero, chunk).flip(2)
     ll, ls = lam.real - K[..., None, None], _sign_of(lam)
-    # x_{t-1} / e^{c_{t-1}}, with x_{-1} = x0
+    # dA = sum_t lam_t x_{t-1}^T as (lam_t e^{c_{t-1}}) (x_{t-1} e^{-c_{t-1}})^T: for t >= 1
+    # x_{t-1} e^{-c_{t-1}} = z_{t-1} e^{-2} (already exported); t = 0 takes x_{-1} = x0
     x0g = _goom(x0s)
     c0 = _scales(x0g.real)
-    prev_l = torch.cat([x0g.real[:, :, None], sl[:, :, :-1]], dim=2)
-    prev_s = torch.cat([_sign_of(x0g)[:, :, None], ss[:, :, :-1]], dim=2)
-    prev_c = torch.cat([c0[:, :, None], c[:, :, :-1]], dim=2)
-    xn = prev_s * torch.exp(prev_l - prev_c[..., None])
-    dA = _scaled_outer(ll + prev_c[..., None], ls, xn, H)
+    x0n = _sign_of(x0g) * torch.exp(x0g.real - c0[..., None])
+    dA = _scaled_outer(ll[:, :, :1] + c0[:, :, None, None], ls[:, :, :1], x0n[:, :, None], H)
+    if T > 1:
+        dA = dA + _scaled_outer(ll[:, :, 1:] + c[:, :, :-1, None], ls[:, :, 1:],
+                                z[:, :, :-1] * math.exp(-2.0), H)
     dB = _scaled_outer(ll, ls, us, H)
     dus = _rowwise(ll, ls, B) + torch.bmm(gy.reshape(H, S * T, 2 * d), D).reshape(H, S, T, d)
     dx0s = _rowwise(ll[:, :, :1], ls[:, :, :1], A)[:, :, 0]

@@ -232,3 +232,21 @@ def test_ssm_scaled_state_bound(s):
     e2 = np.exp(2.0)
     assert np.all(np.abs(scaled) <= e2 * (1 + 1e-12))
     np.testing.assert_allclose(np.max(np.abs(scaled), axis=1), e2)
+
+
+@pytest.mark.parametrize("T", [1, 2])
+def test_ssm_backward_shortest_chains(s, T):
+    """T = 1 / 2: the x_{-1} = x0 term of dA alone / with one more step, vs the oracle."""
+    from oracle import gooms_port as G
+
+    rng = np.random.default_rng(70 + T)
+    d = 4
+    p = s.SsmParams(rng.standard_normal((d, d)), rng.standard_normal((d, d)),
+                    rng.standard_normal((2 * d, d)), rng.standard_normal((2 * d, d)))
+    x0, u = rng.standard_normal(d), rng.standard_normal((T, d))
+    gy = rng.standard_normal((T, 2 * d))
+    run = s.ssm_forward_parallel(p, x0, u)
+    g = s.ssm_backward(p, run, gy, chunk=16)
+    r = G.ssm_backward(p.A, p.B, p.C, p.D, x0, u, run.state_log, run.state_sign, run.scales, gy)
+    for k in ("A", "B", "C", "D", "x0", "u"):
+        assert _rel_max(getattr(g, k), r[k]) < 1e-10, k
