@@ -204,11 +204,14 @@ def lmme_gadd(a: torch.Tensor, b: torch.Tensor, d: torch.Tensor) -> torch.Tensor
 
 
 def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch: int,
-                 d: Optional[torch.Tensor] = None) -> torch.Tensor:
+                 d: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None
+                 ) -> torch.Tensor:
     """C[i] = A[i // a_div] (x) B[i // b_div] (+ D[i]) for i < batch, one launch.
-    a (Na, n, k) and b (Nb, k, m) are contiguous stacks (N = 1 broadcasts); d, when given,
-    is (batch, n, m). Shares operands across a batch without materialising the broadcast
-    (e.g. one chunk-entry panel per head against every power of A)."""
+    a (Na, n, k) and b (Nb, k, m) are stacks (N = 1 broadcasts); d, when given, is
+    (batch, n, m). Shares operands across a batch without materialising the broadcast
+    (e.g. one chunk-entry panel per head against every power of A). `out` may be any
+    (batch, n, m) view whose matrices are row-major (e.g. a strided slice of a larger
+    buffer): the kernel writes there directly, no copy."""
     _need_cuda(a, b, d)
     _need_goom(a, b, d)
     if a.dim() != 3 or b.dim() != 3 or a.shape[2] != b.shape[1]:
@@ -218,7 +221,12 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
         if t.shape[0] != 1 and (batch - 1) // div >= t.shape[0]:
             raise ValueError("operand stack too short for batch / div")
     a, b = a.contiguous(), b.contiguous()
-    out = torch.empty((batch, n, m), dtype=a.dtype, device=a.device)
+    if out is None:
+        out = torch.empty((batch, n, m), dtype=a.dtype, device=a.device)
+    elif (out.shape != (batch, n, m) or out.dtype != a.dtype or out.stride(-1) != 1 or
+          (n > 1 and out.stride(-2) != m)):
+        raise ValueError("out must be a (batch, n, m) view with row-major matrices")
+    strideC = out.stride(0) if batch > 1 else n * m
     if batch == 0:
         return out
     sa = 0 if a.shape[0] == 1 else n * k
@@ -227,14 +235,14 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
     oa = _lib.goom_operand(a.data_ptr(), sa, max(1, a_div))
     ob = _lib.goom_operand(b.data_ptr(), sb, max(1, b_div))
     if d is None:
-        _lib.call(_lib.fn("goom_lmme", a.dtype), oa, ob, out.data_ptr(), n * m, batch, n, k, m,
+        _lib.call(_lib.fn("goom_lmme", a.dtype), oa, ob, out.data_ptr(), strideC, batch, n, k, m,
                   _ptr(ws), nws, _stream())
     else:
         if d.shape != (batch, n, m) or d.dtype != a.dtype:
             raise ValueError("bias must be (batch, n, m) of the operands' dtype")
         d = d.contiguous()
         _lib.call(_lib.fn("goom_lmme_gadd", a.dtype), oa, ob, _lib.goom_operand(d.data_ptr(), n * m, 1),
-                  out.data_ptr(), n * m, batch, n, k, m, _ptr(ws), nws, _stream())
+                  out.data_ptr(), strideC, batch, n, k, m, _ptr(ws), nws, _stream())
     return out
 
 

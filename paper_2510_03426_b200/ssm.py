@@ -204,20 +204,22 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
     N = S * nC
     # panels: column index = s * nC + c; bi[i] (H, d, N)
     bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).contiguous().reshape(L, H, d, N)
+    Ag = Ag.contiguous()
+    # every step's LMME writes straight into its slot of the stacked buffers (no copies)
     Y = torch.empty((L, H, d, N), dtype=torch.complex128, device=dev)
     Y[0] = bi[0]
     for i in range(1, L):
-        Y[i] = torch.ops.goom.lmme_gadd(Ag, Y[i - 1], bi[i])
+        ops.lmme_indexed(Ag, 1, Y[i - 1], 1, H, bi[i], out=Y[i])
     P = torch.empty((H, L, d, d), dtype=torch.complex128, device=dev)  # P[h, i] = A_h^{i+1}
     P[:, 0] = Ag
     for i in range(1, L):
-        P[:, i] = torch.ops.goom.lmme(Ag, P[:, i - 1])
+        ops.lmme_indexed(Ag, 1, P[:, i - 1], 1, H, out=P[:, i])
     s = torch.empty((nC, H, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
     s[0] = s0.transpose(1, 2)
     Yl = Y[L - 1].reshape(H, d, S, nC).permute(3, 0, 1, 2).contiguous()  # (nC, H, d, S)
     PL = P[:, L - 1].contiguous()
     for c in range(1, nC):
-        s[c] = torch.ops.goom.lmme_gadd(PL, s[c - 1], Yl[c - 1])
+        ops.lmme_indexed(PL, 1, s[c - 1], 1, H, Yl[c - 1], out=s[c])
     S_all = s.permute(1, 2, 3, 0).reshape(H, d, N)                      # (H, d, S nC)
     Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
     X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)
