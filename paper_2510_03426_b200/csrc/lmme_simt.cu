@@ -271,6 +271,107 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// n = k = m = 64 complex64 with 16-byte aligned operands (the config-2 d = 64 shape): the
+// whole-product kernel with all of a thread's operand loads issued up front (16 x 16 B in
+// flight, where the generic loop above keeps one 8 B load per thread), the row scales of A
+// reduced by the warp that holds the row (shuffles), B's column scales through one 2 KB
+// table, and A kept row-major so the k loop reads four k at a time per row. Accumulation
+// order (ascending k, one FMA per term) and the epilogue are the generic kernel's, so the
+// results are bitwise identical.
+constexpr int kP64 = 68;
+
+__device__ __forceinline__ float2 unit_pair(float4 z, float s0, float s1) {
+  return make_float2(goom_sign_t<float>(z.y) * gexp(z.x - s0),
+                     goom_sign_t<float>(z.w) * gexp(z.z - s1));
+}
+
+__global__ void __launch_bounds__(256, 3)
+    lmme_whole64_kernel(OperandT<float2> A, OperandT<float2> B, OperandT<float2> D,
+                        float2* __restrict__ C, int64_t strideC, int64_t b_base) {
+  __shared__ __align__(16) float sA[64 * kP64];  // [i][kk]: sign * exp(log - a_i)
+  __shared__ __align__(16) float sB[64 * kP64];  // [kk][j]: sign * exp(log - b_j)
+  __shared__ __align__(16) float sRed[8][64];    // per-warp partial column maxima of B
+  __shared__ float sc[128];                      // a_i, then b_j
+  const int64_t b = b_base + blockIdx.x;
+  const float4* a4 = reinterpret_cast<const float4*>(A.at(b));
+  const float4* b4 = reinterpret_cast<const float4*>(B.at(b));
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // float4 q = tid + 256 r holds elements 2q, 2q + 1: row / k index w + 8 r, column 2 lane
+  float4 ra[8], rb[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) ra[r] = __ldcs(a4 + tid + 256 * r);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) rb[r] = __ldcs(b4 + tid + 256 * r);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {  // row w + 8 r of A lives in this warp
+    float v = gmax(ra[r].x, ra[r].z);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = gmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    v = gmax(v, 0.f);
+    if (lane == 0) sc[w + 8 * r] = v;
+    *reinterpret_cast<float2*>(&sA[(w + 8 * r) * kP64 + 2 * lane]) = unit_pair(ra[r], v, v);
+  }
+  float c0 = -INFINITY, c1 = -INFINITY;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) c0 = gmax(c0, rb[r].x), c1 = gmax(c1, rb[r].z);
+  *reinterpret_cast<float2*>(&sRed[w][2 * lane]) = make_float2(c0, c1);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float2 p = *reinterpret_cast<const float2*>(&sRed[u][2 * lane]);
+    c0 = gmax(c0, p.x), c1 = gmax(c1, p.y);
+  }
+  c0 = gmax(c0, 0.f), c1 = gmax(c1, 0.f);
+  if (w == 0) sc[64 + 2 * lane] = c0, sc[65 + 2 * lane] = c1;
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    *reinterpret_cast<float2*>(&sB[(w + 8 * r) * kP64 + 2 * lane]) = unit_pair(rb[r], c0, c1);
+  __syncthreads();
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+  for (int k0 = 0; k0 < 64; k0 += 4) {
+    float ar[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lds4(&sA[(ty * 4 + i) * kP64 + k0], ar[i]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float br[4];
+      lds4(&sB[(k0 + q) * kP64 + tx * 4], br);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = gfma(ar[i][q], br[j], acc[i][j]);
+    }
+  }
+  float2* c = C + b * strideC;
+  const float2* dd = D.ptr ? D.at(b) : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    float2 o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = lmme_out<float>(acc[i][j], sc[r], sc[64 + tx * 4 + j]);
+    if (dd) {
+      const float4* d4 = reinterpret_cast<const float4*>(dd + r * 64 + tx * 4);
+      const float4 d0 = d4[0], d1 = d4[1];
+      o[0] = gadd_elem(o[0], make_float2(d0.x, d0.y));
+      o[1] = gadd_elem(o[1], make_float2(d0.z, d0.w));
+      o[2] = gadd_elem(o[2], make_float2(d1.x, d1.y));
+      o[3] = gadd_elem(o[3], make_float2(d1.z, d1.w));
+    }
+    float4* c4 = reinterpret_cast<float4*>(c + r * 64 + tx * 4);
+    c4[0] = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+    c4[1] = make_float4(o[2].x, o[2].y, o[3].x, o[3].y);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 }  // namespace
 
 template <class R>
@@ -280,6 +381,25 @@ size_t lmme_whole_smem() {
 
 template <class R>
 int lmme_simt_whole(const LmmeProblemT<R>& p, cudaStream_t s) {
+  if constexpr (sizeof(R) == 4) {
+    const bool vec = p.n == 64 && p.k == 64 && p.m == 64 && aligned16(p.A.ptr) &&
+                     aligned16(p.B.ptr) && aligned16(p.C) && p.A.stride % 2 == 0 &&
+                     p.B.stride % 2 == 0 && p.strideC % 2 == 0 &&
+                     (!p.D.ptr || (aligned16(p.D.ptr) && p.D.stride % 2 == 0));
+    static const bool generic = [] {
+      const char* e = std::getenv("GOOM_WHOLE64_GENERIC");
+      return e && e[0] == '1';
+    }();
+    if (vec && !generic) {
+      const int64_t gmax_ = 2147483647;
+      for (int64_t b0 = 0; b0 < p.batch; b0 += gmax_) {
+        const int64_t nb = p.batch - b0 < gmax_ ? p.batch - b0 : gmax_;
+        lmme_whole64_kernel<<<(unsigned)nb, 256, 0, s>>>(p.A, p.B, p.D, p.C, p.strideC, b0);
+        GOOM_CHECK_LAUNCH("lmme_whole64_kernel");
+      }
+      return GOOM_OK;
+    }
+  }
   const size_t smem = lmme_whole_smem<R>();
   static bool attr = false;
   if (!attr) {

@@ -58,7 +58,8 @@ struct Cfg {
   static constexpr int kStage = (kGroupsA + kGroupsB) * kGroupBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered FP32 accumulator
   static constexpr int kRing = STAGES * kStage;
-  static constexpr int kSmem = kRing + 1024 + 256;
+  static constexpr int kOut = kRing + 256;  // epilogue staging: [4 warps][32 rows][32 cols]
+  static constexpr int kSmem = kOut + kEpiWarps * 8192 + 1024;
 };
 
 // (PTX helpers: tc_ptx.cuh)
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------ epilogue ------------------------------
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
+    const uint32_t stage = ring + G::kOut + (uint32_t)(warp - 2 - kXformWarps) * 8192u;
     int lt = 0;
     for (int64_t t = blockIdx.x; t < grid.tiles; t += gridDim.x, ++lt) {
       int64_t b;
@@ -325,11 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const float ai = rowA.at(b)[row0 + row];
       const float* cb = colB.at(b) + col0;
-      float2* crow = C + b * strideC + (int64_t)(row0 + row) * m + col0;
+      float2* cblk = C + b * strideC + (int64_t)(row0 + quad * 32) * m + col0;
       const float2* drow = D.ptr ? D.at(b) + (int64_t)(row0 + row) * m + col0 : nullptr;
       uint32_t rmax = 0;  // bits of max(log, 0): non-negative floats order like uints
 #pragma unroll 1
-      for (int col = 0; col < BN; col += 32) {
+      for (int col = 0; col < (debug == 7 ? 0 : BN); col += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
 #pragma unroll
@@ -340,7 +342,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             o0 = gadd_elem(o0, drow[col + j]);
             o1 = gadd_elem(o1, drow[col + j + 1]);
           }
-          *reinterpret_cast<float4*>(crow + col + j) = make_float4(o0.x, o0.y, o1.x, o1.y);
+          // row `lane`, 16-byte chunk j / 2, XOR-swizzled by the row: conflict-free both ways
+          st_shared_v4(stage + lane * 256 + ((((j >> 1) ^ lane) & 15) << 4),
+                       __float_as_uint(o0.x), __float_as_uint(o0.y), __float_as_uint(o1.x),
+                       __float_as_uint(o1.y));
           const uint32_t c0 = __float_as_uint(fmaxf(o0.x, 0.0f));
           const uint32_t c1 = __float_as_uint(fmaxf(o1.x, 0.0f));
           rmax = max(rmax, max(c0, c1));
@@ -355,6 +360,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        __syncwarp();
+        // copy-out: two full 256-byte row segments per instruction (coalesced), where a
+        // lane-per-row store would touch 32 lines per instruction
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int rr = 2 * it + (lane >> 4), c = lane & 15;
+          const float4 o = ld_shared_v4(stage + rr * 256 + (((c ^ rr) & 15) << 4));
+          if (debug != 8) *reinterpret_cast<float4*>(cblk + (int64_t)rr * m + col + 2 * c) = o;
+        }
+        __syncwarp();
       }
       if (emit.row)
         atomicMax(reinterpret_cast<unsigned int*>(emit.row + b * emit.row_stride + row0 + row), rmax);
@@ -374,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // GOOM_TC_DEBUG (profiling only; results invalid): 1 skips the transform, 2 the MMAs,
 // 3 the TMA loads and the transform, 4 the TMA loads, 5 transform and MMAs (TMA ring only),
-// 6 as 5 with B loaded as full-width rows
+// 6 as 5 with B loaded as full-width rows, 7 skips the epilogue, 8 its global stores
 int tc_debug() {
   static int v = [] {
     const char* e = getenv("GOOM_TC_DEBUG");

@@ -393,6 +393,35 @@ def test_lmme_whole_kernel_bitwise_equals_prepass_path(g, n, k, m):
     assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
 
 
+def test_lmme_64_vector_kernel_gadd_and_unaligned(g):
+    """The 16-byte-vector d = 64 kernel (aligned operands) against the generic whole kernel
+    (the same products read from storage shifted by one complex64, which is not 16-byte
+    aligned): bitwise equal, with and without the fused bias gadd, and with a broadcast
+    (stride 0) right operand."""
+    torch.manual_seed(64)
+    batch = 41
+    A = torch.ops.goom.from_real(torch.randn(batch, 64, 64, device="cuda") * 3, float("-inf"), False)
+    B = torch.ops.goom.from_real(torch.randn(batch, 64, 64, device="cuda") * 3, float("-inf"), False)
+    D = torch.ops.goom.from_real(torch.randn(batch, 64, 64, device="cuda") * 50, float("-inf"), False)
+    A[3, :, 5] = torch.complex(torch.tensor(float("-inf")), torch.tensor(0.0))
+
+    def shifted(x):
+        buf = torch.empty(x.numel() + 1, dtype=x.dtype, device=x.device)
+        v = buf[1:].view(x.shape)
+        v.copy_(x)
+        assert v.data_ptr() % 16 == 8
+        return v
+
+    As, Bs, Ds = shifted(A), shifted(B), shifted(D)
+    eq = lambda x, y: torch.equal(torch.view_as_real(x), torch.view_as_real(y))
+    assert eq(torch.ops.goom.lmme(A, B), torch.ops.goom.lmme(As, Bs))
+    assert eq(torch.ops.goom.lmme_gadd(A, B, D), torch.ops.goom.lmme_gadd(As, Bs, Ds))
+    assert eq(torch.ops.goom.lmme_gadd(A, B, D),
+              torch.ops.goom.gadd(torch.ops.goom.lmme(A, B), D))
+    b0 = B[:1].expand(batch, 64, 64)
+    assert eq(torch.ops.goom.lmme(A, b0), torch.ops.goom.lmme(As, shifted(B[:1]).expand(batch, 64, 64)))
+
+
 def test_lmme_64x64_against_50_digit_reference(g):
     """test_core.py:196-203 with its 50-digit oracle (mpmath): complex128 LMME of two
     64x64 N(0,1) matrices, Frobenius relative error < 1e-12; complex64 (3xTF32) < 1e-6."""
