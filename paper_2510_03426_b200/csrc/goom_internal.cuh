@@ -15,8 +15,13 @@ __device__ __forceinline__ Cx<R> gadd_elem_t(Cx<R> a, Cx<R> b) {
   R top = gmax(a.x, b.x);
   bool live = top != R(-INFINITY);
   R shift = live ? top : R(0);
-  R ea = gexp(sub_rn(a.x, shift));
-  R eb = gexp(sub_rn(b.x, shift));
+  // the operand at the top contributes exp(top - top) == 1 exactly (one exp per element,
+  // bitwise the same as two); a +inf top keeps exp(inf - inf) = NaN as the two-exp form
+  const bool a_top = a.x == top;
+  const R e = gexp(sub_rn(a_top ? b.x : a.x, shift));
+  const R e_top = top == R(INFINITY) ? R(NAN) : R(1);
+  R ea = a_top ? e_top : e;
+  R eb = a_top ? e : e_top;
   R t = add_rn(mul_rn(goom_sign_t<R>(a.y), ea), mul_rn(goom_sign_t<R>(b.y), eb));
   if (!live) return cx<R>(R(-INFINITY), R(0));
   return cx<R>(add_rn(shift, glog(fabs(t))), t < R(0) ? pi_of<R>() : R(0));
