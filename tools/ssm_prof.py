@@ -42,3 +42,6 @@ for name, fn in (("forward", lambda: ssm.ssm_forward_heads(A, B, C, D, x0, u)),
     print(f"{name}: wall {a.elapsed_time(b):.2f} ms, kernels {tot:.2f} ms")
     for k, (n, t) in sorted(groups.items(), key=lambda kv: -kv[1][1])[:12]:
         print(f"   {t:8.2f} ms  n={n:5d}  avg {t / n * 1e3:8.1f} us  {k}")
+    big = sorted(((e.device_time_total, e.name[:40]) for e in prof.events()
+                  if e.device_type.name == "CUDA" and e.device_time_total > 300), reverse=True)
+    print("   launches > 300 us:", ", ".join(f"{t / 1e3:.2f} ms {n}" for t, n in big[:14]))
