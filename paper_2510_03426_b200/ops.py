@@ -208,7 +208,7 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
                  ) -> torch.Tensor:
     """C[i] = A[i // a_div] (x) B[i // b_div] (+ D[i]) for i < batch, one launch.
     a (Na, n, k) and b (Nb, k, m) are stacks (N = 1 broadcasts); d, when given, is
-    (batch, n, m). Shares operands across a batch without materialising the broadcast
+    (batch, n, m), any batch stride. Shares operands across a batch without materialising the broadcast
     (e.g. one chunk-entry panel per head against every power of A). `out` may be any
     (batch, n, m) view whose matrices are row-major (e.g. a strided slice of a larger
     buffer): the kernel writes there directly, no copy."""
@@ -240,8 +240,10 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
     else:
         if d.shape != (batch, n, m) or d.dtype != a.dtype:
             raise ValueError("bias must be (batch, n, m) of the operands' dtype")
-        d = d.contiguous()
-        _lib.call(_lib.fn("goom_lmme_gadd", a.dtype), oa, ob, _lib.goom_operand(d.data_ptr(), n * m, 1),
+        if d.stride(-1) != 1 or (n > 1 and d.stride(-2) != m):
+            d = d.contiguous()  # row-major matrices at any batch stride are read in place
+        sd = d.stride(0) if batch > 1 else n * m
+        _lib.call(_lib.fn("goom_lmme_gadd", a.dtype), oa, ob, _lib.goom_operand(d.data_ptr(), sd, 1),
                   out.data_ptr(), strideC, batch, n, k, m, _ptr(ws), nws, _stream())
     return out
 

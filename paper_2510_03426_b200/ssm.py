@@ -14,6 +14,7 @@ sequences (each leading (0, x0) leaf zeroes the carry of the previous sequence).
 from __future__ import annotations
 
 import math
+from typing import Optional
 from dataclasses import dataclass
 
 import numpy as np
@@ -178,7 +179,22 @@ def ssm_forward_sequential(params, x0, u) -> SsmRun:
     return SsmRun(x0=x0, u=u, y=y, scales=c, state_log=sl, state_sign=ss)
 
 
-def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: int) -> torch.Tensor:
+def _bu_panels(B: torch.Tensor, u: torch.Tensor, L: int) -> torch.Tensor:
+    """_bu_heads produced directly in _chunked_scan's panel layout (T % L == 0): one LMME
+    of batch H L — head h's B against step i's panel of its d x (S nC) inputs, column
+    s nC + c = step c L + i of sequence s — so bi[i] (H, d, S nC) is a slice of the
+    (H, L, d, S nC) result instead of a 2 GB permuted copy of (H, S, T, d) GOOMs. Every
+    element is the same LMME as _bu_heads (same operands, scales and k order): bitwise equal."""
+    H, S, T, d = u.shape
+    nC = T // L
+    N = S * nC
+    ug = _goom(u.reshape(H, S, nC, L, d).permute(0, 3, 4, 1, 2).reshape(H * L, d, N))
+    out = ops.lmme_indexed(_goom(B), L, ug, 1, H * L)                   # (H L, d, N)
+    return out.view(H, L, d, N).transpose(0, 1)                         # (L, H, d, N)
+
+
+def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: int,
+                  bi: Optional[torch.Tensor] = None) -> torch.Tensor:
     """x_t = A (x) x_{t-1} (+) b_t for H heads x S sequences with the powers of A shared by
     every chunk of L = `chunk` steps — O(T d^2) matrix-vector work instead of the affine
     scan's O(T d^3) matrix-matrix work on a constant A slot. Ag (H, d, d), b (H, S, T, d),
@@ -195,7 +211,9 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
     L = max(1, min(chunk, T))
     nC = (T + L - 1) // L
     Tp = nC * L
-    if Tp != T:
+    if bi is not None:  # b only carries the shape: the steps come laid out (_bu_panels)
+        pass
+    elif Tp != T:
         zero = torch.complex(torch.tensor(NEG_INF, dtype=torch.float64),
                              torch.tensor(0.0, dtype=torch.float64))
         bp = torch.full((H, S, Tp, d), zero, dtype=torch.complex128, device=dev)
@@ -203,7 +221,8 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         b = bp
     N = S * nC
     # panels: column index = s * nC + c; bi[i] (H, d, N)
-    bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).contiguous().reshape(L, H, d, N)
+    if bi is None:
+        bi = b.reshape(H, S, nC, L, d).permute(3, 0, 4, 1, 2).contiguous().reshape(L, H, d, N)
     Ag = Ag.contiguous()
     # every step's LMME writes straight into its slot of the stacked buffers (no copies)
     Y = torch.empty((L, H, d, N), dtype=torch.complex128, device=dev)
@@ -294,7 +313,13 @@ def ssm_forward_heads(A, B, C, D, x0s, us, chunk=64):
     (H, S). Every launch covers all heads (the per-head loop of ssm_forward_batched folded
     into the LMME batch); the recurrence and output map are ssm.py:84-98, 110-137."""
     A, B, C, D, x0s, us = _heads_args(A, B, C, D, x0s, us)
-    state = _chunked_scan(_goom(A), _bu_heads(B, us), _goom(x0s), chunk)
+    H, S, T, d = us.shape
+    L = max(1, min(chunk, T))
+    if T % L == 0:
+        shape_only = us.new_empty(()).expand(H, S, T, d)  # no storage: bi carries the steps
+        state = _chunked_scan(_goom(A), shape_only, _goom(x0s), chunk, bi=_bu_panels(B, us, L))
+    else:
+        state = _chunked_scan(_goom(A), _bu_heads(B, us), _goom(x0s), chunk)
     sl, ss = state.real, _sign_of(state)
     c = _scales(sl)
     z = ss * torch.exp(sl - c[..., None] + 2.0)

@@ -250,3 +250,29 @@ def test_ssm_backward_shortest_chains(s, T):
     r = G.ssm_backward(p.A, p.B, p.C, p.D, x0, u, run.state_log, run.state_sign, run.scales, gy)
     for k in ("A", "B", "C", "D", "x0", "u"):
         assert _rel_max(getattr(g, k), r[k]) < 1e-10, k
+
+
+def test_ssm_bu_panel_layout_bitwise_equals_permuted_path(s):
+    """T % chunk == 0: B u is produced straight in the chunked scan's panel layout
+    (_bu_panels, one LMME of batch H L, bias read at its batch stride); the states are
+    bitwise those of the (H, S, T, d) B u permuted into panels."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    H, S, T, d, L = 3, 5, 96, 8, 16
+    dev = torch.device("cuda")
+    A = torch.tensor(rng.standard_normal((H, d, d)) * 0.5, device=dev)
+    B = torch.tensor(rng.standard_normal((H, d, d)), device=dev)
+    x0 = torch.tensor(rng.standard_normal((H, S, d)), device=dev)
+    u = torch.tensor(rng.standard_normal((H, S, T, d)), device=dev)
+    bi = s._bu_panels(B, u, L)
+    bu = s._bu_heads(B, u)
+    ref_bi = bu.reshape(H, S, T // L, L, d).permute(3, 0, 4, 1, 2).reshape(L, H, d, S * T // L)
+    assert torch.equal(torch.view_as_real(bi), torch.view_as_real(ref_bi))
+    got = s._chunked_scan(s._goom(A), u.new_empty(()).expand(H, S, T, d), s._goom(x0), L, bi=bi)
+    ref = s._chunked_scan(s._goom(A), bu, s._goom(x0), L)
+    assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
+    sl = s.ssm_forward_heads(A.cpu().numpy(), B.cpu().numpy(), np.ones((H, 2 * d, d)),
+                             np.ones((H, 2 * d, d)), x0.cpu().numpy(), u.cpu().numpy(),
+                             chunk=L)[0]
+    assert torch.equal(sl, ref.real)
