@@ -76,6 +76,14 @@ int goom_to_real_scaled_f32(const goom_c64* z, float* out, float* c, int64_t bat
                             void* stream);
 int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t batch, int64_t n,
                              void* stream);
+/* SSM output export (ssm.py:84-98) straight from the chunked scan's state-assembly panels:
+ * X is (H*L, d, S*nC) complex128, state (h, s, t = cc*L + i) = column s*nC + cc of matrix
+ * h*L + i, t < T <= nC*L. Writes, for every state, c = max log (0 if all zero) into
+ * c[(h*S + s)*T + t] and the d-vectors log, sign and sign*exp(log - c + 2) into sl / ss / z
+ * at [((h*S + s)*T + t)*d ...] (float64, (H, S, T, d)). d <= 64, H*L <= 65535.
+ * Replaces the permute + elementwise chain after ssm_forward's scan (ssm.py:84-98). */
+int goom_ssm_export_c128(const goom_c128* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC,
+                         int64_t T, double* sl, double* ss, double* c, double* z, void* stream);
 /* Elementwise signed log-sum-exp, bitwise commutative.  _gadd_arrays core.py:264-275. */
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream);
 int goom_gadd_c128(const goom_c128* a, const goom_c128* b, goom_c128* out, int64_t n,

@@ -71,6 +71,47 @@ __global__ void to_real_scaled_kernel(const Cx<R>* __restrict__ z, R* __restrict
   }
 }
 
+// SSM state export (ssm.py:84-98 on the chunked scan's output, no permuted copy): X is the
+// state-assembly LMME's (H L, d, S nC) panels — state (h, s, t = cc L + i) is column
+// s nC + cc of matrix h L + i. A CTA stages 32 columns x d rows (coalesced, padded against
+// bank conflicts), then each warp takes whole states: c = max log (0 if none), and writes
+// log, sign and sign * exp(log - c + 2) as contiguous d-vectors of the (H, S, T, d) outputs.
+constexpr int kExportCols = 32;
+__global__ void __launch_bounds__(256)
+    ssm_export_kernel(const double2* __restrict__ X, int64_t L, int d, int64_t S, int64_t nC,
+                      int64_t T, double* __restrict__ sl, double* __restrict__ ss,
+                      double* __restrict__ cvec, double* __restrict__ z) {
+  __shared__ double2 tile[64][kExportCols + 1];
+  const int64_t hi = blockIdx.y, N = S * nC;
+  const int64_t h = hi / L, i = hi % L;
+  const int64_t n0 = (int64_t)blockIdx.x * kExportCols;
+  const int ncols = (int)(N - n0 < kExportCols ? N - n0 : kExportCols);
+  const double2* xb = X + hi * d * N + n0;
+  for (int e = threadIdx.x; e < d * kExportCols; e += 256) {
+    const int r = e / kExportCols, j = e % kExportCols;
+    if (j < ncols) tile[r][j] = xb[(int64_t)r * N + j];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j = w; j < ncols; j += 8) {
+    const int64_t n = n0 + j, s = n / nC, t = (n % nC) * L + i;
+    if (t >= T) continue;
+    double m = -INFINITY;
+    for (int r = lane; r < d; r += 32) m = gmax(m, tile[r][j].x);
+    m = warp_max_t(m);
+    const double c = m == -INFINITY ? 0.0 : m;
+    const int64_t o = ((h * S + s) * T + t) * d;
+    if (lane == 0) cvec[o / d] = c;
+    for (int r = lane; r < d; r += 32) {
+      const double2 v = tile[r][j];
+      const double sg = cos(v.y) < 0.0 ? -1.0 : 1.0;
+      sl[o + r] = v.x;
+      ss[o + r] = sg;
+      z[o + r] = sg * gexp(add_rn(sub_rn(v.x, c), 2.0));
+    }
+  }
+}
+
 template <class R>
 __global__ void gadd_kernel(const Cx<R>* __restrict__ a, const Cx<R>* __restrict__ b,
                             Cx<R>* __restrict__ out, int64_t n) {
@@ -266,6 +307,20 @@ int to_real_scaled(const void* z, R* out, R* c, int64_t batch, int64_t n, void* 
   return GOOM_OK;
 }
 
+int ssm_export(const void* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC, int64_t T,
+               double* sl, double* ss, double* c, double* z, void* stream) {
+  if (H < 0 || L < 1 || d < 1 || d > 64 || S < 0 || nC < 0 || T < 0 || T > nC * L)
+    return fail(GOOM_ESHAPE, "ssm_export: need 1 <= d <= 64, L >= 1, T <= nC * L");
+  if (H == 0 || S == 0 || T == 0) return GOOM_OK;
+  if (!X || !sl || !ss || !c || !z) return fail(GOOM_EINVAL, "null pointer");
+  if (H * L > 65535) return fail(GOOM_EUNSUPPORTED, "ssm_export: H * L > 65535");
+  const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)(H * L));
+  ssm_export_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(X), L,
+                                                        d, S, nC, T, sl, ss, c, z);
+  GOOM_CHECK_LAUNCH("ssm_export");
+  return GOOM_OK;
+}
+
 template <class R>
 int gadd(const void* a, const void* b, void* out, int64_t n, void* stream) {
   if (n < 0) return fail(GOOM_EINVAL, "n must be >= 0");
@@ -322,6 +377,10 @@ int goom_to_real_scaled_f32(const goom_c64* z, float* out, float* c, int64_t bat
 int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t batch, int64_t n,
                              void* stream) {
   return to_real_scaled<double>(z, out, c, batch, n, stream);
+}
+int goom_ssm_export_c128(const goom_c128* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC,
+                         int64_t T, double* sl, double* ss, double* c, double* z, void* stream) {
+  return ssm_export(X, H, L, d, S, nC, T, sl, ss, c, z, stream);
 }
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream) {
   return gadd<float>(a, b, out, n, stream);

@@ -248,6 +248,22 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
     return out
 
 
+def ssm_export(X: torch.Tensor, H: int, L: int, S: int, nC: int, T: int):
+    """(state_log, state_sign, scales, z) of the SSM from the chunked scan's state-assembly
+    panels X (H L, d, S nC) complex128 (goom_ssm_export_c128): the same values as the
+    permuted states through ssm.py:84-98's max / shifted export, in one pass."""
+    _need_cuda(X)
+    d = X.shape[1]
+    if X.dtype != torch.complex128 or X.shape != (H * L, d, S * nC) or not X.is_contiguous():
+        raise ValueError("X must be a contiguous (H*L, d, S*nC) complex128 tensor")
+    opts = dict(dtype=torch.float64, device=X.device)
+    sl, ss, z = (torch.empty((H, S, T, d), **opts) for _ in range(3))
+    c = torch.empty((H, S, T), **opts)
+    _lib.call("goom_ssm_export_c128", X.data_ptr(), H, L, d, S, nC, T, sl.data_ptr(),
+              ss.data_ptr(), c.data_ptr(), z.data_ptr(), _stream())
+    return sl, ss, c, z
+
+
 # ---------------------------------------------------------------------------
 # scans
 

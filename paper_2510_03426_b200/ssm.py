@@ -14,8 +14,8 @@ sequences (each leading (0, x0) leaf zeroes the carry of the previous sequence).
 from __future__ import annotations
 
 import math
-from typing import Optional
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 import torch
@@ -194,7 +194,7 @@ def _bu_panels(B: torch.Tensor, u: torch.Tensor, L: int) -> torch.Tensor:
 
 
 def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: int,
-                  bi: Optional[torch.Tensor] = None) -> torch.Tensor:
+                  bi: Optional[torch.Tensor] = None, panels: bool = False):
     """x_t = A (x) x_{t-1} (+) b_t for H heads x S sequences with the powers of A shared by
     every chunk of L = `chunk` steps — O(T d^2) matrix-vector work instead of the affine
     scan's O(T d^3) matrix-matrix work on a constant A slot. Ag (H, d, d), b (H, S, T, d),
@@ -242,6 +242,8 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
     S_all = s.permute(1, 2, 3, 0).reshape(H, d, N)                      # (H, d, S nC)
     Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
     X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)
+    if panels:  # (H L, d, S nC): state (h, s, cc L + i) is column s nC + cc of matrix h L + i
+        return X, L, nC
     X = X.reshape(H, L, d, S, nC).permute(0, 3, 4, 1, 2).reshape(H, S, Tp, d)
     return X[:, :, :T]
 
@@ -317,13 +319,18 @@ def ssm_forward_heads(A, B, C, D, x0s, us, chunk=64):
     L = max(1, min(chunk, T))
     if T % L == 0:
         shape_only = us.new_empty(()).expand(H, S, T, d)  # no storage: bi carries the steps
-        state = _chunked_scan(_goom(A), shape_only, _goom(x0s), chunk, bi=_bu_panels(B, us, L))
+        bu, bi = shape_only, _bu_panels(B, us, L)
     else:
-        state = _chunked_scan(_goom(A), _bu_heads(B, us), _goom(x0s), chunk)
-    sl, ss = state.real, _sign_of(state)
-    c = _scales(sl)
-    z = ss * torch.exp(sl - c[..., None] + 2.0)
-    H, S, T, d = us.shape
+        bu, bi = _bu_heads(B, us), None
+    if d <= 64:  # the export reads the scan's panels directly (goom_ssm_export_c128)
+        X, L, nC = _chunked_scan(_goom(A), bu, _goom(x0s), chunk, bi=bi, panels=True)
+        sl, ss, c, z = ops.ssm_export(X, H, L, S, nC, T)
+        del X
+    else:
+        state = _chunked_scan(_goom(A), bu, _goom(x0s), chunk, bi=bi)
+        sl, ss = state.real, _sign_of(state)
+        c = _scales(sl)
+        z = ss * torch.exp(sl - c[..., None] + 2.0)
     y = (torch.bmm(z.reshape(H, S * T, d), C.transpose(1, 2)) +
          torch.bmm(us.reshape(H, S * T, d), D.transpose(1, 2))).reshape(H, S, T, 2 * d)
     return sl, ss, c, y

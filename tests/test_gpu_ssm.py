@@ -272,7 +272,15 @@ def test_ssm_bu_panel_layout_bitwise_equals_permuted_path(s):
     got = s._chunked_scan(s._goom(A), u.new_empty(()).expand(H, S, T, d), s._goom(x0), L, bi=bi)
     ref = s._chunked_scan(s._goom(A), bu, s._goom(x0), L)
     assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
-    sl = s.ssm_forward_heads(A.cpu().numpy(), B.cpu().numpy(), np.ones((H, 2 * d, d)),
-                             np.ones((H, 2 * d, d)), x0.cpu().numpy(), u.cpu().numpy(),
-                             chunk=L)[0]
-    assert torch.equal(sl, ref.real)
+    Cm, Dm = rng.standard_normal((H, 2 * d, d)), rng.standard_normal((H, 2 * d, d))
+    sl, ss, c, y = s.ssm_forward_heads(A.cpu().numpy(), B.cpu().numpy(), Cm, Dm,
+                                       x0.cpu().numpy(), u.cpu().numpy(), chunk=L)
+    # the fused export (goom_ssm_export_c128) against the permuted states through torch
+    rss = s._sign_of(ref)
+    rc = s._scales(ref.real)
+    rz = rss * torch.exp(ref.real - rc[..., None] + 2.0)
+    assert torch.equal(sl, ref.real) and torch.equal(ss, rss) and torch.equal(c, rc)
+    Ct, Dt = torch.tensor(Cm, device=dev), torch.tensor(Dm, device=dev)
+    ry = (torch.bmm(rz.reshape(H, S * T, d), Ct.transpose(1, 2)) +
+          torch.bmm(u.reshape(H, S * T, d), Dt.transpose(1, 2))).reshape(H, S, T, 2 * d)
+    assert torch.equal(y, ry)
