@@ -79,11 +79,21 @@ int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t
 /* SSM output export (ssm.py:84-98) straight from the chunked scan's state-assembly panels:
  * X is (H*L, d, S*nC) complex128, state (h, s, t = cc*L + i) = column s*nC + cc of matrix
  * h*L + i, t < T <= nC*L. Writes, for every state, c = max log (0 if all zero) into
- * c[(h*S + s)*T + t] and the d-vectors log, sign and sign*exp(log - c + 2) into sl / ss / z
- * at [((h*S + s)*T + t)*d ...] (float64, (H, S, T, d)). d <= 64, H*L <= 65535.
- * Replaces the permute + elementwise chain after ssm_forward's scan (ssm.py:84-98). */
+ * c[(h*S + s)*T + t'] and the d-vectors log, sign and sign*exp(log - c + 2) into sl / ss / z
+ * at [((h*S + s)*T + t')*d ...] (float64, (H, S, T, d)), t' = T-1-t if `reverse` else t.
+ * c and z may be NULL (not written); kshift (H*S, nullable) is subtracted from the logs.
+ * d <= 64, H*L <= 65535. Replaces the permute + elementwise chain after ssm_forward's scan
+ * (ssm.py:84-98) and after the derived adjoint scan. */
 int goom_ssm_export_c128(const goom_c128* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC,
-                         int64_t T, double* sl, double* ss, double* c, double* z, void* stream);
+                         int64_t T, double* sl, double* ss, double* c, double* z, int reverse,
+                         const double* kshift, void* stream);
+/* The inverse layout: real h (H, S, T, d) float64 -> GOOM panels out (L, H, d, S*nC)
+ * complex128, out[i][h][:, s*nC + cc] = from_real(h[h, s, t]) (log part + K[h,s] - c[h,s,t]
+ * when K is non-NULL; c is (H, S, T)), scan time cc*L + i, t = T-1-(cc*L + i) if `reverse`.
+ * T == nC*L, d <= 64. The adjoint scan's inputs without a flipped / permuted copy. */
+int goom_ssm_panels_c128(const double* h, const double* K, const double* c, int64_t H, int64_t L,
+                         int d, int64_t S, int64_t nC, int64_t T, int reverse, goom_c128* out,
+                         void* stream);
 /* Elementwise signed log-sum-exp, bitwise commutative.  _gadd_arrays core.py:264-275. */
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream);
 int goom_gadd_c128(const goom_c128* a, const goom_c128* b, goom_c128* out, int64_t n,

@@ -80,7 +80,8 @@ constexpr int kExportCols = 32;
 __global__ void __launch_bounds__(256)
     ssm_export_kernel(const double2* __restrict__ X, int64_t L, int d, int64_t S, int64_t nC,
                       int64_t T, double* __restrict__ sl, double* __restrict__ ss,
-                      double* __restrict__ cvec, double* __restrict__ z) {
+                      double* __restrict__ cvec, double* __restrict__ z, int reverse,
+                      const double* __restrict__ kshift) {
   __shared__ double2 tile[64][kExportCols + 1];
   const int64_t hi = blockIdx.y, N = S * nC;
   const int64_t h = hi / L, i = hi % L;
@@ -100,15 +101,50 @@ __global__ void __launch_bounds__(256)
     for (int r = lane; r < d; r += 32) m = gmax(m, tile[r][j].x);
     m = warp_max_t(m);
     const double c = m == -INFINITY ? 0.0 : m;
-    const int64_t o = ((h * S + s) * T + t) * d;
-    if (lane == 0) cvec[o / d] = c;
+    const int64_t o = ((h * S + s) * T + (reverse ? T - 1 - t : t)) * d;
+    const double k = kshift ? kshift[h * S + s] : 0.0;
+    if (lane == 0 && cvec) cvec[o / d] = c;
     for (int r = lane; r < d; r += 32) {
       const double2 v = tile[r][j];
       const double sg = cos(v.y) < 0.0 ? -1.0 : 1.0;
-      sl[o + r] = v.x;
+      sl[o + r] = kshift ? sub_rn(v.x, k) : v.x;
       ss[o + r] = sg;
-      z[o + r] = sg * gexp(add_rn(sub_rn(v.x, c), 2.0));
+      if (z) z[o + r] = sg * gexp(add_rn(sub_rn(v.x, c), 2.0));
     }
+  }
+}
+
+// The adjoint scan's inputs in _chunked_scan's panel layout (inverse of the export): from
+// real h (H, S, T, d) float64, out[i][h][r][s nC + cc] = GOOM of h at time t_src, log part
+// + (K[h, s] - c[h, s, t_src]) when K is given, with scan time cc L + i and t_src = T - 1 -
+// (cc L + i) when reversed. Reads whole d-vectors per state, writes 32-column row segments.
+__global__ void __launch_bounds__(256)
+    ssm_panels_kernel(const double* __restrict__ hsrc, const double* __restrict__ K,
+                      const double* __restrict__ cs, int64_t H, int64_t L, int d, int64_t S,
+                      int64_t nC, int64_t T, int reverse, double2* __restrict__ out) {
+  __shared__ double2 tile[64][kExportCols + 1];
+  const int64_t ih = blockIdx.y, i = ih / H, h = ih % H, N = S * nC;
+  const int64_t n0 = (int64_t)blockIdx.x * kExportCols;
+  const int ncols = (int)(N - n0 < kExportCols ? N - n0 : kExportCols);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j = w; j < ncols; j += 8) {
+    const int64_t n = n0 + j, s = n / nC, tin = (n % nC) * L + i;
+    const int64_t t = reverse ? T - 1 - tin : tin;
+    const int64_t row = (h * S + s) * T + t;
+    const double shift = K ? sub_rn(K[h * S + s], cs[row]) : 0.0;
+    for (int r = lane; r < d; r += 32) {
+      const double v = hsrc[row * d + r];
+      double2 g = v == 0.0 ? make_double2(-INFINITY, 0.0)
+                           : make_double2(glog(fabs(v)), v < 0.0 ? pi_of<double>() : 0.0);
+      if (K) g.x = add_rn(g.x, shift);
+      tile[r][j] = g;
+    }
+  }
+  __syncthreads();
+  double2* ob = out + ih * d * N + n0;
+  for (int e = threadIdx.x; e < d * kExportCols; e += 256) {
+    const int r = e / kExportCols, j = e % kExportCols;
+    if (j < ncols) ob[(int64_t)r * N + j] = tile[r][j];
   }
 }
 
@@ -308,16 +344,32 @@ int to_real_scaled(const void* z, R* out, R* c, int64_t batch, int64_t n, void* 
 }
 
 int ssm_export(const void* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC, int64_t T,
-               double* sl, double* ss, double* c, double* z, void* stream) {
+               double* sl, double* ss, double* c, double* z, int reverse, const double* kshift,
+               void* stream) {
   if (H < 0 || L < 1 || d < 1 || d > 64 || S < 0 || nC < 0 || T < 0 || T > nC * L)
     return fail(GOOM_ESHAPE, "ssm_export: need 1 <= d <= 64, L >= 1, T <= nC * L");
   if (H == 0 || S == 0 || T == 0) return GOOM_OK;
-  if (!X || !sl || !ss || !c || !z) return fail(GOOM_EINVAL, "null pointer");
+  if (!X || !sl || !ss) return fail(GOOM_EINVAL, "null pointer");
   if (H * L > 65535) return fail(GOOM_EUNSUPPORTED, "ssm_export: H * L > 65535");
   const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)(H * L));
   ssm_export_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(X), L,
-                                                        d, S, nC, T, sl, ss, c, z);
+                                                        d, S, nC, T, sl, ss, c, z, reverse,
+                                                        kshift);
   GOOM_CHECK_LAUNCH("ssm_export");
+  return GOOM_OK;
+}
+
+int ssm_panels(const double* h, const double* K, const double* c, int64_t H, int64_t L, int d,
+               int64_t S, int64_t nC, int64_t T, int reverse, void* out, void* stream) {
+  if (H < 0 || L < 1 || d < 1 || d > 64 || S < 0 || nC < 0 || T != nC * L)
+    return fail(GOOM_ESHAPE, "ssm_panels: need 1 <= d <= 64, L >= 1, T == nC * L");
+  if (H == 0 || S == 0 || T == 0) return GOOM_OK;
+  if (!h || !out || (K && !c)) return fail(GOOM_EINVAL, "null pointer");
+  if (H * L > 65535) return fail(GOOM_EUNSUPPORTED, "ssm_panels: H * L > 65535");
+  const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)(H * L));
+  ssm_panels_kernel<<<grid, 256, 0, as_stream(stream)>>>(h, K, c, H, L, d, S, nC, T, reverse,
+                                                        reinterpret_cast<double2*>(out));
+  GOOM_CHECK_LAUNCH("ssm_panels");
   return GOOM_OK;
 }
 
@@ -379,8 +431,14 @@ int goom_to_real_scaled_c128(const goom_c128* z, double* out, double* c, int64_t
   return to_real_scaled<double>(z, out, c, batch, n, stream);
 }
 int goom_ssm_export_c128(const goom_c128* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC,
-                         int64_t T, double* sl, double* ss, double* c, double* z, void* stream) {
-  return ssm_export(X, H, L, d, S, nC, T, sl, ss, c, z, stream);
+                         int64_t T, double* sl, double* ss, double* c, double* z, int reverse,
+                         const double* kshift, void* stream) {
+  return ssm_export(X, H, L, d, S, nC, T, sl, ss, c, z, reverse, kshift, stream);
+}
+int goom_ssm_panels_c128(const double* h, const double* K, const double* c, int64_t H, int64_t L,
+                         int d, int64_t S, int64_t nC, int64_t T, int reverse, goom_c128* out,
+                         void* stream) {
+  return ssm_panels(h, K, c, H, L, d, S, nC, T, reverse, out, stream);
 }
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream) {
   return gadd<float>(a, b, out, n, stream);

@@ -248,20 +248,46 @@ def lmme_indexed(a: torch.Tensor, a_div: int, b: torch.Tensor, b_div: int, batch
     return out
 
 
-def ssm_export(X: torch.Tensor, H: int, L: int, S: int, nC: int, T: int):
+def ssm_export(X: torch.Tensor, H: int, L: int, S: int, nC: int, T: int, full: bool = True,
+               reverse: bool = False, kshift: Optional[torch.Tensor] = None):
     """(state_log, state_sign, scales, z) of the SSM from the chunked scan's state-assembly
     panels X (H L, d, S nC) complex128 (goom_ssm_export_c128): the same values as the
-    permuted states through ssm.py:84-98's max / shifted export, in one pass."""
+    permuted states through ssm.py:84-98's max / shifted export, in one pass. full=False
+    returns (log - kshift[h, s], sign) only; reverse=True flips time (the adjoint scan)."""
     _need_cuda(X)
     d = X.shape[1]
     if X.dtype != torch.complex128 or X.shape != (H * L, d, S * nC) or not X.is_contiguous():
         raise ValueError("X must be a contiguous (H*L, d, S*nC) complex128 tensor")
+    if kshift is not None:
+        kshift = kshift.to(torch.float64).contiguous()
+        if kshift.shape != (H, S):
+            raise ValueError("kshift must be (H, S)")
     opts = dict(dtype=torch.float64, device=X.device)
-    sl, ss, z = (torch.empty((H, S, T, d), **opts) for _ in range(3))
-    c = torch.empty((H, S, T), **opts)
+    sl, ss = (torch.empty((H, S, T, d), **opts) for _ in range(2))
+    z = torch.empty((H, S, T, d), **opts) if full else None
+    c = torch.empty((H, S, T), **opts) if full else None
     _lib.call("goom_ssm_export_c128", X.data_ptr(), H, L, d, S, nC, T, sl.data_ptr(),
-              ss.data_ptr(), c.data_ptr(), z.data_ptr(), _stream())
-    return sl, ss, c, z
+              ss.data_ptr(), _ptr(c), _ptr(z), int(reverse), _ptr(kshift), _stream())
+    return (sl, ss, c, z) if full else (sl, ss)
+
+
+def ssm_panels(h: torch.Tensor, L: int, K: Optional[torch.Tensor] = None,
+               c: Optional[torch.Tensor] = None, reverse: bool = False) -> torch.Tensor:
+    """Real h (H, S, T, d) float64 -> complex128 GOOM panels (L, H, d, S T / L) in the
+    chunked scan's layout (goom_ssm_panels_c128), the log part shifted by K[h, s] -
+    c[h, s, t] when K is given, time reversed when `reverse`."""
+    _need_cuda(h)
+    H, S, T, d = h.shape
+    if h.dtype != torch.float64 or T % L:
+        raise ValueError("h must be float64 with T a multiple of L")
+    h = h.contiguous()
+    if K is not None:
+        K, c = K.to(torch.float64).contiguous(), c.to(torch.float64).contiguous()
+    nC = T // L
+    out = torch.empty((L, H, d, S * nC), dtype=torch.complex128, device=h.device)
+    _lib.call("goom_ssm_panels_c128", h.data_ptr(), _ptr(K), _ptr(c), H, L, d, S, nC, T,
+              int(reverse), out.data_ptr(), _stream())
+    return out
 
 
 # ---------------------------------------------------------------------------

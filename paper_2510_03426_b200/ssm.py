@@ -410,11 +410,23 @@ def ssm_backward_heads(A, B, C, D, x0s, us, state_log, state_sign, scales, gy, c
     # sequence's largest scale: the reference LMME clamps its scales at 0 (core.py:250-251),
     # so adjoints ~ e^{-c_t} below float64 range would vanish, while lam e^{K} >~ 1
     K = c.max(dim=-1).values                                           # (H, S)
-    g = _goom(h)
-    g = torch.complex(g.real + (K[..., None] - c)[..., None], g.imag)
     zero = torch.full((H, S, d), complex(NEG_INF, 0.0), dtype=torch.complex128, device=dev)
-    lam = _chunked_scan(_goom(A.transpose(1, 2).contiguous()), g.flip(2), zero, chunk).flip(2)
-    ll, ls = lam.real - K[..., None, None], _sign_of(lam)
+    At = _goom(A.transpose(1, 2).contiguous())
+    L = max(1, min(chunk, T))
+    if T % L == 0 and d <= 64:
+        # reversed, shifted GOOMs straight into the panel layout and the adjoints straight out
+        # of it (goom_ssm_panels_c128 / goom_ssm_export_c128): no flipped or permuted copies
+        bi = ops.ssm_panels(h, L, K, c, reverse=True)
+        X, L, nC = _chunked_scan(At, h.new_empty(()).expand(H, S, T, d), zero, chunk, bi=bi,
+                                 panels=True)
+        del bi
+        ll, ls = ops.ssm_export(X, H, L, S, nC, T, full=False, reverse=True, kshift=K)
+        del X
+    else:
+        g = _goom(h)
+        g = torch.complex(g.real + (K[..., None] - c)[..., None], g.imag)
+        lam = _chunked_scan(At, g.flip(2), zero, chunk).flip(2)
+        ll, ls = lam.real - K[..., None, None], _sign_of(lam)
     # dA = sum_t lam_t x_{t-1}^T as (lam_t e^{c_{t-1}}) (x_{t-1} e^{-c_{t-1}})^T: for t >= 1
     # x_{t-1} e^{-c_{t-1}} = z_{t-1} e^{-2} (already exported); t = 0 takes x_{-1} = x0
     x0g = _goom(x0s)

@@ -284,3 +284,31 @@ def test_ssm_bu_panel_layout_bitwise_equals_permuted_path(s):
     ry = (torch.bmm(rz.reshape(H, S * T, d), Ct.transpose(1, 2)) +
           torch.bmm(u.reshape(H, S * T, d), Dt.transpose(1, 2))).reshape(H, S, T, 2 * d)
     assert torch.equal(y, ry)
+
+
+def test_ssm_adjoint_panels_export_bitwise(s):
+    """The backward's panel kernels (goom_ssm_panels_c128 in, reversed goom_ssm_export_c128
+    out) against the flipped / permuted torch path they replace: bitwise equal adjoints."""
+    import torch
+    from paper_2510_03426_b200 import ops
+
+    rng = np.random.default_rng(23)
+    H, S, T, d, L = 2, 3, 48, 8, 16
+    dev = torch.device("cuda")
+    h = torch.tensor(rng.standard_normal((H, S, T, d)), device=dev)
+    h[0, 1, 5] = 0.0
+    c = torch.tensor(rng.standard_normal((H, S, T)) * 40, device=dev)
+    K = c.max(dim=-1).values
+    At = s._goom(torch.tensor(rng.standard_normal((H, d, d)) * 0.4, device=dev))
+    zero = torch.full((H, S, d), complex(float("-inf"), 0.0), dtype=torch.complex128, device=dev)
+    g = s._goom(h)
+    g = torch.complex(g.real + (K[..., None] - c)[..., None], g.imag)
+    ref_bi = g.flip(2).reshape(H, S, T // L, L, d).permute(3, 0, 4, 1, 2).reshape(L, H, d, -1)
+    bi = ops.ssm_panels(h, L, K, c, reverse=True)
+    assert torch.equal(torch.view_as_real(bi), torch.view_as_real(ref_bi))
+    lam = s._chunked_scan(At, g.flip(2), zero, L).flip(2)
+    X, L2, nC = s._chunked_scan(At, h.new_empty(()).expand(H, S, T, d), zero, L, bi=bi,
+                                panels=True)
+    ll, ls = ops.ssm_export(X, H, L2, S, nC, T, full=False, reverse=True, kshift=K)
+    assert torch.equal(ll, lam.real - K[..., None, None])
+    assert torch.equal(ls, s._sign_of(lam))
