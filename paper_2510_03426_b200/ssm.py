@@ -231,8 +231,12 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         ops.lmme_indexed(Ag, 1, Y[i - 1], 1, H, bi[i], out=Y[i])
     P = torch.empty((H, L, d, d), dtype=torch.complex128, device=dev)  # P[h, i] = A_h^{i+1}
     P[:, 0] = Ag
-    for i in range(1, L):
-        ops.lmme_indexed(Ag, 1, P[:, i - 1], 1, H, out=P[:, i])
+    k = 1
+    while k < L:  # doubling: A^{k+j+1} = A^k (x) A^{j+1}, j < k — log2 L launches, not L - 1
+        m = min(k, L - k)
+        blk = ops.lmme_indexed(P[:, k - 1], m, P[:, :m].reshape(H * m, d, d), 1, H * m)
+        P[:, k:k + m] = blk.view(H, m, d, d)
+        k += m
     s = torch.empty((nC, H, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
     s[0] = s0.transpose(1, 2)
     Yl = Y[L - 1].reshape(H, d, S, nC).permute(3, 0, 1, 2).contiguous()  # (nC, H, d, S)
