@@ -65,6 +65,17 @@ def test_argument_errors_without_gpu(lib):
     a = _lib.goom_operand(None, 0, 1)
     rc = L.goom_lmme_c64(a, a, None, 0, 1, 0, 4, 4, None, 0, None)
     assert rc == 2  # ESHAPE
+    # SSM panel kernels: shapes validated before any launch (d <= 64, T <= nC L / == nC L)
+    rc = L.goom_ssm_export_c128(None, 2, 16, 65, 3, 4, 64, None, None, None, None, 0, None, None)
+    assert rc == 2 and b"d <= 64" in L.goom_last_error()
+    rc = L.goom_ssm_export_c128(None, 2, 16, 8, 3, 4, 65, None, None, None, None, 0, None, None)
+    assert rc == 2
+    rc = L.goom_ssm_export_c128(None, 0, 16, 8, 3, 4, 64, None, None, None, None, 0, None, None)
+    assert rc == 0  # nothing to export
+    rc = L.goom_ssm_panels_c128(None, None, None, 2, 16, 8, 3, 4, 63, 1, None, None)
+    assert rc == 2 and b"T == nC * L" in L.goom_last_error()
+    rc = L.goom_ssm_panels_c128(None, None, None, 2, 16, 8, 3, 4, 64, 1, None, None)
+    assert rc == 1  # null pointers
     with pytest.raises(ValueError):
         _lib.check(1)
     with pytest.raises(_lib.GoomError):
