@@ -201,7 +201,7 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
     s0 (H, S, d) complex128 GOOMs -> states (H, S, T, d):
       local   y_{c,i} = A (x) y_{c,i-1} (+) b_{cL+i}   (L-1 launches, all heads and chunks)
       powers  P_i = A^{i+1}                            (L-1 launches, all heads)
-      entry   s_{c+1} = A^L (x) s_c (+) y_{c,L-1}     (nC-1 launches, s_0 = the initial state)
+      entry   s_{c+1} = A^L (x) s_c (+) y_{c,L-1}     (log2 nC launches, s_0 = the initial state)
       state   x_{cL+i} = A^{i+1} (x) s_c (+) y_{c,i}   (one launch: every (head, i) pair, the
                                                       head's entry panel shared via div = L)
     Every launch is an LMME of d x d matrices with d x (S nC) panels of column vectors.
@@ -237,13 +237,23 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         blk = ops.lmme_indexed(P[:, k - 1], m, P[:, :m].reshape(H * m, d, d), 1, H * m)
         P[:, k:k + m] = blk.view(H, m, d, d)
         k += m
-    s = torch.empty((nC, H, d, S), dtype=torch.complex128, device=dev)  # chunk-entry states
-    s[0] = s0.transpose(1, 2)
-    Yl = Y[L - 1].reshape(H, d, S, nC).permute(3, 0, 1, 2).contiguous()  # (nC, H, d, S)
-    PL = P[:, L - 1].contiguous()
-    for c in range(1, nC):
-        ops.lmme_indexed(PL, 1, s[c - 1], 1, H, Yl[c - 1], out=s[c])
-    S_all = s.permute(1, 2, 3, 0).reshape(H, d, N)                      # (H, d, S nC)
+    # chunk-entry states s_c = A^L (x) s_{c-1} (+) y_{c-1, L-1} by a Hillis-Steele scan over
+    # the chunks (log2 nC rounds of one batched LMME each, with A^L, A^2L, A^4L, ...) instead
+    # of nC - 1 sequential launches of H products
+    cur = torch.empty((H, nC, d, S), dtype=torch.complex128, device=dev)
+    cur[:, 0] = s0.transpose(1, 2)
+    cur[:, 1:] = Y[L - 1].reshape(H, d, S, nC).permute(0, 3, 1, 2)[:, :nC - 1]
+    Mp = P[:, L - 1].contiguous()
+    off = 1
+    while off < nC:
+        n = nC - off
+        nxt = ops.lmme_indexed(Mp, n, cur[:, :n].reshape(H * n, d, S), 1, H * n,
+                               cur[:, off:].reshape(H * n, d, S))
+        cur[:, off:] = nxt.view(H, n, d, S)  # stream-ordered after the reads above
+        off *= 2
+        if off < nC:
+            Mp = ops.lmme_indexed(Mp, 1, Mp, 1, H)
+    S_all = cur.permute(0, 2, 3, 1).reshape(H, d, N)                    # (H, d, S nC)
     Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
     X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)
     if panels:  # (H L, d, S nC): state (h, s, cc L + i) is column s nC + cc of matrix h L + i
