@@ -226,8 +226,17 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # re-anchored parity windows on the timed run itself: the block carries
+    # applied at two block starts (~2^19 and the last block) and the prefix 63 steps later
+    W = min(REANCHOR_W, args.block)
+    anchors = sorted({(a // args.block) * args.block for a in (T // 2, T - W - 1)
+                      if a >= args.block})
+    anchors = [a for a in anchors if a + W <= T]
+    snaps = sorted({a + W - 1 for a in anchors})
+
     def one_step():
-        return sharded.run_chain_sharded(T, d, args.seed, args.window, args.block)
+        return sharded.run_chain_sharded(T, d, args.seed, args.window, args.block,
+                                         snapshots=snaps, anchors=anchors)
 
     for _ in range(args.warmup):
         one_step()
@@ -253,10 +262,15 @@ def main():
             times.append(ms)
     launches = ops.kernel_launches() - launches0
     import ctypes
-    p3_n, p3_ms, p3_prod = ctypes.c_int64(0), ctypes.c_double(0.0), ctypes.c_int64(0)
-    goom._lib.check(lib.goom_chain_ts_phase3_stats(ctypes.byref(p3_n), ctypes.byref(p3_ms),
-                                                   ctypes.byref(p3_prod)))
+    phases = {}
+    for ph in range(4):
+        n_, ms_, u_ = ctypes.c_int64(0), ctypes.c_double(0.0), ctypes.c_int64(0)
+        goom._lib.check(lib.goom_chain_ts_phase_stats(ph, ctypes.byref(n_), ctypes.byref(ms_),
+                                                      ctypes.byref(u_)))
+        phases[ph] = (n_.value, ms_.value, u_.value)
     lib.goom_chain_ts_phase3_timing(0)
+    p3_n, p3_ms, p3_prod = (ctypes.c_int64(phases[3][0]), ctypes.c_double(phases[3][1]),
+                            ctypes.c_int64(phases[3][2]))
     if world > 1:
         lt = torch.tensor([launches], device=dev, dtype=torch.float64)
         dist.all_reduce(lt)
@@ -268,6 +282,7 @@ def main():
     dg = run.digests
     finite = bool((dg[:, 2] == 1).all().item())
     growth = harness.growth_rate(dg) if run.digests.shape[0] > 2 else float("nan")
+    reanchored = reanchor_checks(run, t0, anchors, W, d, args.seed, ops, world, dist)
 
     # ---- roofline of the dominant kernel: the phase-3 batched LMME of a window ----
     # out[b] = L[b] (x) Cx[b / block] with the digest epilogue: exactly the chain engine's
@@ -314,6 +329,29 @@ def main():
         tflops, avg_launch_ms, peak_3xtf32 = standalone_tflops, lmme_ms, burst_3xtf32
         timing = f"standalone phase-3 shape, {lmme_ms:.2f} ms/launch"
         peak_kind = "burst"
+    # every phase of the timed steps (CUDA events on the engine's stream), per GPU
+    peak_s = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) / 2 / 3
+    hbm = pk.get("hbm_gbs", 6650.0)
+    phase_rows = {}
+    names = {0: "leaf generation (random_normal_ts_kernel)",
+             1: "phase 1 local products (lmme_ts_kernel<ts out>, s-1 launches per window)",
+             2: "phase 2 block-carry Kogge-Stone tree (lmme_ts_kernel<ts out>)",
+             3: "phase 3 carry apply + digest (lmme_ts_kernel<digest>)"}
+    for ph, (n_, ms_, u_) in phases.items():
+        if n_ == 0 or ms_ <= 0:
+            continue
+        row = {"kernel": names[ph], "windows": n_, "ms_per_step": ms_ / max(args.steps, 1),
+               "share_of_step": ms_ / max(args.steps, 1) / ms_step}
+        if ph == 0:
+            gbs = u_ * d * d * 4 / (ms_ / 1e3) / 1e9
+            row.update(bound="hbm", achieved=gbs, unit="GB/s", frac=gbs / hbm,
+                       units="leaves (4 B/element written)")
+        else:
+            tf = 2.0 * d ** 3 * u_ / (ms_ / 1e3) / 1e12
+            row.update(bound="tensor", achieved=tf, unit="TFLOP/s", frac=tf / peak_s,
+                       units=f"{u_} products")
+        phase_rows[["rng", "phase1", "phase2", "phase3"][ph]] = row
+    step_tf = 4.0 * d ** 3 * T / world / (ms_step / 1e3) / 1e12
     tf32_cublas = cublas_tf32_tflops(torch)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -405,7 +443,12 @@ def main():
                          "standalone_tflops": standalone_tflops,
                          "frac_standalone_vs_burst": standalone_tflops / burst_3xtf32,
                          "tf32_cublas_tflops_in_run": tf32_cublas,
-                         "frac_vs_cublas_tf32_div3": tflops / (tf32_cublas / 3)},
+                         "frac_vs_cublas_tf32_div3": tflops / (tf32_cublas / 3),
+                         "phases": phase_rows,
+                         "whole_step": {"tflops_4d3_per_element": step_tf,
+                                        "frac": step_tf / peak_s,
+                                        "note": "4 d^3 flop per chain element (2 LMMEs), "
+                                                "per GPU, vs the sustained 3xTF32 peak"}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * d * d * 4,
                     "d2h_bytes_per_step": ne * 16,
                     "h2d_gbs_per_gpu": ne * d * d * 4 / (statistics.median(e2e_times) / 1e3) / 1e9,
@@ -415,13 +458,45 @@ def main():
             "gpu_launches": launches // max(args.steps, 1),
             "clocks": clocks.summary(),
             "check": {"finite": finite, "growth_per_step": growth,
-                      "expected_growth": 0.5 * (math.log(2) + _digamma(d / 2))},
+                      "expected_growth": 0.5 * (math.log(2) + _digamma(d / 2)),
+                      "reanchored": reanchored},
         }
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+REANCHOR_W = 64
+
+
+def reanchor_checks(run, t0, anchors, W, d, seed, ops, world, dist):
+    """SURVEY §8c(5) on the timed run itself: for each block start a in this rank's shard
+    the float64 oracle (oracle/reanchor.py; the checker, not the thing measured) folds the
+    regenerated leaves A_a .. A_{a+W-1} onto the block carry the engine applied there (its
+    own P_{a-1}), and compares P_{a+W-1} entry by entry and every digest of the stretch.
+    Runs after the timed region."""
+    from oracle import reanchor as R
+
+    out = []
+    for a in anchors:
+        if a not in run.anchors_ts or a + W - 1 not in run.snapshots_ts:
+            continue
+        l0, s0 = (x[0].cpu().numpy() for x in ops.ts_log_sign(run.anchors_ts[a]))
+        l1, s1 = (x[0].cpu().numpy() for x in ops.ts_log_sign(run.snapshots_ts[a + W - 1]))
+        leaves = ops.ts_random_normal(W, d, seed, a, run.digests.device).U.cpu().numpy()
+        dg = run.digests[a - t0:a - t0 + W, :2].cpu().numpy()
+        tt = time.perf_counter()
+        r = R.check_window(l0, s0, leaves, l1, s1, dg)
+        r["t0"] = a
+        r["cpu_s"] = round(time.perf_counter() - tt, 1)
+        out.append(r)
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, out)
+        out = [r for part in allr for r in part]
+    return sorted(out, key=lambda r: r["t0"])
 
 
 def _digamma(x):

@@ -141,6 +141,12 @@ int goom_lmme_scaled_c64(goom_operand A, const float* rowA, int64_t rowA_stride,
 /* Force a kernel family for testing: 0 auto, 1 SIMT, 2 tcgen05 3xTF32. Returns the
  * previous value. Process-wide. */
 int goom_set_lmme_backend(int backend);
+/* Engine of the complex64 chain scans for d % 256 == 0: 0 (default) the complex64 tcgen05
+ * kernels with the reference's per-column clamped scales (Eq. 11) exactly; 1 the tile-scaled
+ * engine (chain_ts.cu; faster, but entries more than ~e^87 below the largest of their
+ * (row, 256-column block) flush). Initial value from GOOM_CHAIN_TS (=1 selects 1). Returns
+ * the previous value; an out-of-range argument only queries. Process-wide. */
+int goom_set_chain_engine(int engine);
 
 /* ---- prefix scans (scan.py:181-214, 317-353, 529-563) ---------------------- */
 /* Inclusive product chain out[t] = A[t] (x) ... (x) A[0] (x) carry_in, blocked exactly
@@ -278,6 +284,19 @@ int goom_chain_ts_finish(int64_t T, int d, int block, const float* cU, const flo
                          const uint32_t* cG, goom_c64* out, float* digests4, float* oU, float* oq,
                          uint32_t* oG, void* ws, size_t ws_bytes, void* stream);
 
+/* Snapshots of the window just scanned by goom_chain_ts / goom_chain_ts_finish with the same
+ * ws: prefixes P_t (t = idx[i], window-local, host array of n), each recomputed as
+ * L_t (x) carry(t / block) from the workspace (no full-window output), as complex64 into
+ * out[i] and / or tile-scaled into oU/oq/oG[i] (either may be NULL, not both). */
+int goom_chain_ts_snapshots(int64_t T, int d, int block, const int64_t* idx, int n,
+                            goom_c64* out, float* oU, float* oq, uint32_t* oG, void* ws,
+                            size_t ws_bytes, void* stream);
+/* The block carries of that window (k = kidx[i], host array of n): the tile-scaled matrix
+ * the engine applies on the right of block k's local products — its own P_{k block - 1}
+ * (the window's carry-in for k = 0) — into oU/oq/oG[i]. */
+int goom_chain_ts_carries(int64_t T, int d, int block, const int64_t* kidx, int n, float* oU,
+                          float* oq, uint32_t* oG, void* ws, size_t ws_bytes, void* stream);
+
 /* Time-sharded chain scan over an NCCL communicator (replaces the reference's
  * _scan_affine_stack A slot, scan.py:181-214, for a chain split across the GPUs of a node;
  * SURVEY §8b / §8e). Every rank passes its contiguous chunk A (T_local leaves, rank order =
@@ -289,6 +308,16 @@ size_t goom_scan_chain_sharded_workspace_size(int64_t T_local, int d, int block,
 int goom_scan_chain_sharded_c64(const goom_c64* A, goom_c64* out, int64_t T_local, int d,
                                 int block, void* nccl_comm, void* ws, size_t ws_bytes,
                                 void* stream);
+/* The same scan with digest-only output (goom_digest_c64 per global prefix into
+ * digests4[4 t]): the prefixes are materialised a few blocks at a time in the workspace,
+ * never all at once (config 3's 2 TiB of d = 512 prefixes). Work per rank: phases 1-2 on
+ * the local chunk, one all-gather, the carry folded onto the block carries, phase 3 —
+ * about two LMMEs per leaf, as on one GPU. */
+size_t goom_scan_chain_sharded_digest_workspace_size(int64_t T_local, int d, int block,
+                                                     int nranks);
+int goom_scan_chain_sharded_digest_c64(const goom_c64* A, float* digests4, int64_t T_local, int d,
+                                       int block, void* nccl_comm, void* ws, size_t ws_bytes,
+                                       void* stream);
 
 /* Profiling aid (bench.py's roofline): time every digest phase-3 launch of the
  * tile-scaled chain engine with CUDA events on its own stream. _timing(1) starts a fresh
@@ -296,6 +325,10 @@ int goom_scan_chain_sharded_c64(const goom_c64* A, goom_c64* out, int64_t T_loca
  * their total milliseconds and total products. */
 void goom_chain_ts_phase3_timing(int enable);
 int goom_chain_ts_phase3_stats(int64_t* launches, double* total_ms, int64_t* products);
+/* The same log per phase of a window: 0 leaf generation (goom_random_normal_ts; units =
+ * leaf matrices), 1 local products (units = products), 2 block-carry fold / tree, 3 the
+ * digest phase-3 launch. Each logged entry brackets all of that phase's launches. */
+int goom_chain_ts_phase_stats(int phase, int64_t* launches, double* total_ms, int64_t* units);
 
 /* Kernels libgoom has launched in this process (bench accounting). */
 long long goom_kernel_launches(void);

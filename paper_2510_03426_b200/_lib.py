@@ -72,6 +72,7 @@ SIGNATURES = {
         [goom_operand, goom_operand, goom_operand, _P, _I64, _I64, _I, _I, _I, _P, _SZ, _P],
     ),
     "goom_set_lmme_backend": (_I, [_I]),
+    "goom_set_chain_engine": (_I, [_I]),
     "goom_lmme_scaled_c64": (
         _I,
         [goom_operand, _P, _I64, goom_operand, _P, _I64, _P, _I64, _I64, _I, _I, _I, _P],
@@ -141,10 +142,15 @@ SIGNATURES = {
         _I,
         [_I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
     ),
+    "goom_chain_ts_snapshots": (_I, [_I64, _I, _I, _P, _I, _P, _P, _P, _P, _P, _SZ, _P]),
+    "goom_chain_ts_carries": (_I, [_I64, _I, _I, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "goom_chain_ts_phase3_timing": (None, [_I]),
     "goom_chain_ts_phase3_stats": (_I, [_P, _P, _P]),
+    "goom_chain_ts_phase_stats": (_I, [_I, _P, _P, _P]),
     "goom_scan_chain_sharded_workspace_size": (_SZ, [_I64, _I, _I, _I]),
     "goom_scan_chain_sharded_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
+    "goom_scan_chain_sharded_digest_workspace_size": (_SZ, [_I64, _I, _I, _I]),
+    "goom_scan_chain_sharded_digest_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
     "goom_chain_ts": (
         _I,
         [_P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
@@ -210,6 +216,12 @@ def operand(t, stride=None, div=1):
 
 def null_operand():
     return goom_operand(None, 0, 1)
+
+
+def set_chain_engine(engine: int) -> int:
+    """Complex64 chain-scan engine for d % 256 == 0: 0 exact complex64 kernels (default),
+    1 tile-scaled. Returns the previous setting (-1 queries)."""
+    return int(load().goom_set_chain_engine(int(engine)))
 
 
 def set_backend(backend: int) -> int:

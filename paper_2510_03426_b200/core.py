@@ -216,9 +216,14 @@ def _like_input(t: torch.Tensor, ref):
 
 
 class GoomMatrix:
-    """Dense 2-D GOOM matrix backed by a complex64 CUDA tensor (`.data`)."""
+    """Dense 2-D GOOM matrix (core.py:148-226), backed on the GPU by ONE complex tensor
+    (`.data`: complex64 for a float32 backing, complex128 for float64 — the reference's
+    default). The reference's host-side view is kept as its API has it: `.log_mag` and
+    `.sign` are numpy arrays of the backing dtype, `.dtype` is that numpy dtype and
+    `to_real()` returns a numpy array; they are materialised from the device on first use
+    (instances are immutable, core.py:153-154, so the copy is cached)."""
 
-    __slots__ = ("data",)
+    __slots__ = ("data", "_host")
 
     def __init__(self, log_mag, sign=None, dtype=None):
         if sign is None:
@@ -227,18 +232,36 @@ class GoomMatrix:
                 raise ValueError("single-argument GoomMatrix takes a complex GOOM tensor")
             z = z.to(device=_device(), dtype=complex_dtype(dtype, z.dtype))
         else:
+            if dtype is None:  # the backing is the dtype of log_mag (core.py:158-170)
+                lm = log_mag if isinstance(log_mag, torch.Tensor) else np.asarray(log_mag)
+                if isinstance(lm, torch.Tensor):
+                    dtype = lm.dtype
+                elif lm.dtype in (np.float32, np.float64):
+                    dtype = lm.dtype
+                else:
+                    raise ValueError("backing dtype must be float32 or float64")
             z = join(log_mag, sign, dtype)
         if z.dim() != 2:
             raise ValueError("GoomMatrix is 2-D")
         if bool(torch.isnan(z.real).any()):
             raise ValueError("log_mag must not contain NaN")
         self.data = z
+        self._host = None
 
     @classmethod
     def _wrap(cls, z: torch.Tensor) -> "GoomMatrix":
         obj = cls.__new__(cls)
         obj.data = z
+        obj._host = None
         return obj
+
+    def _host_view(self):
+        if self._host is None:
+            rt = np.float64 if self.data.dtype == torch.complex128 else np.float32
+            l, s = split(self.data)
+            self._host = (l.cpu().numpy().astype(rt, copy=False),
+                          s.cpu().numpy().astype(rt, copy=False))
+        return self._host
 
     @property
     def rows(self):
@@ -254,29 +277,37 @@ class GoomMatrix:
 
     @property
     def dtype(self):
+        """The backing float dtype (numpy), as the reference's `log_mag.dtype`."""
+        return np.dtype(np.float64 if self.data.dtype == torch.complex128 else np.float32)
+
+    @property
+    def backing(self) -> torch.dtype:
+        """The device tensor's dtype (torch.complex64 / torch.complex128)."""
         return self.data.dtype
 
     @property
-    def log_mag(self) -> torch.Tensor:
-        return self.data.real
+    def log_mag(self) -> np.ndarray:
+        return self._host_view()[0]
 
     @property
-    def sign(self) -> torch.Tensor:
-        return split(self.data)[1]
+    def sign(self) -> np.ndarray:
+        return self._host_view()[1]
 
     def numpy(self):
-        """(log_mag, sign) as float64 numpy arrays (the reference's storage)."""
-        l, s = split(self.data)
-        return l.double().cpu().numpy(), s.double().cpu().numpy()
+        """(log_mag, sign) as float64 numpy arrays."""
+        l, s = self._host_view()
+        return l.astype(np.float64), s.astype(np.float64)
 
     @classmethod
-    def from_real(cls, values, policy=SENTINEL, dtype=None):
-        """Elementwise real -> GOOM on the GPU (core.py:188-199)."""
+    def from_real(cls, values, policy=SENTINEL, dtype=np.float64):
+        """Elementwise real -> GOOM on the GPU (core.py:188-199); float64 backing by default
+        as in the reference, float32 -> complex64."""
+        if dtype is None:
+            dtype = np.float64
         v = _to_tensor(values)
         if v.dtype not in (torch.float32, torch.float64):
             v = v.to(torch.float64)
-        if dtype is not None and np.dtype(dtype) == np.float32:
-            v = v.to(torch.float32)
+        v = v.to(torch.float32 if np.dtype(dtype) == np.float32 else torch.float64)
         if v.dim() != 2:
             raise ValueError("expected a 2-D array")
         if bool(torch.isnan(v).any()):
@@ -287,20 +318,27 @@ class GoomMatrix:
         return cls._wrap(torch.ops.goom.from_real(v, float(policy.zero_log), double))
 
     @classmethod
-    def zeros(cls, rows, cols, policy=SENTINEL, dtype=None):
-        z = torch.full((rows, cols), complex(policy.zero_log, 0.0), dtype=complex_dtype(dtype),
+    def zeros(cls, rows, cols, policy=SENTINEL, dtype=np.float64):
+        z = torch.full((rows, cols), complex(policy.zero_log, 0.0),
+                       dtype=complex_dtype(np.float64 if dtype is None else dtype),
                        device=_device())
         return cls._wrap(z)
 
     @classmethod
-    def identity(cls, n, policy=SENTINEL, dtype=None):
-        z = torch.full((n, n), complex(policy.zero_log, 0.0), dtype=complex_dtype(dtype),
+    def identity(cls, n, policy=SENTINEL, dtype=np.float64):
+        z = torch.full((n, n), complex(policy.zero_log, 0.0),
+                       dtype=complex_dtype(np.float64 if dtype is None else dtype),
                        device=_device())
         z.diagonal().real.zero_()
         return cls._wrap(z)
 
-    def to_real(self, double=False):
-        """sign * exp(log) on the GPU; overflow -> +-inf (core.py:213-216)."""
+    def to_real(self):
+        """sign * exp(log) in the backing dtype, overflow -> +-inf (core.py:213-216): a numpy
+        array, as the reference returns (computed on the GPU, copied to the host)."""
+        return self.to_real_device().cpu().numpy()
+
+    def to_real_device(self, double=False):
+        """sign * exp(log) as a CUDA tensor (float64 for a complex128 backing or `double`)."""
         return torch.ops.goom.to_real(self.data, bool(double))
 
     def __getitem__(self, idx):
@@ -311,7 +349,8 @@ class GoomMatrix:
         return Goom(z.real, -1 if math.cos(z.imag) < 0 else 1)
 
     def __repr__(self):
-        return f"GoomMatrix({self.rows}x{self.cols}, complex64 on {self.data.device})"
+        return f"GoomMatrix({self.rows}x{self.cols}, dtype={self.dtype}, {self.data.dtype} on " \
+               f"{self.data.device})"
 
 
 # ---------------------------------------------------------------------------
@@ -379,6 +418,7 @@ def log_unit_norm_columns(m: GoomMatrix):
 
 
 def to_real_scaled(m: GoomMatrix):
-    """Eq. 29: sign*exp(log - c + 2) with c the max log (core.py:313-323)."""
+    """Eq. 29: sign*exp(log - c + 2) with c the max log (core.py:313-323); returns
+    (numpy array in the backing dtype, c) as the reference does."""
     out, c = torch.ops.goom.to_real_scaled(m.data)
-    return out, float(c.item())
+    return out.cpu().numpy(), float(c.item())

@@ -101,40 +101,41 @@ int lmme_ts_call(TsIn a, TsIn b, int kind, float2* C, int64_t strideC, TsOut T, 
   return lmme_ts(p, st);
 }
 
-// Phase-3 launch timing inside real runs (bench.py's roofline: the dominant kernel's
-// duration measured in the timed region, on its own stream): when enabled, every digest
-// phase-3 launch is bracketed by a pair of CUDA events; the totals are read back later.
-struct Phase3Log {
+}  // namespace
+
+// Per-phase launch timing inside real runs (bench.py's roofline: every kernel of the step
+// measured in the timed region, on the stream it runs on): when enabled, each phase of a
+// window (0 leaf generation, 1 local products, 2 block-carry tree, 3 digest / prefix
+// output) is bracketed by a pair of CUDA events; the totals are read back later.
+struct PhaseLog {
   std::mutex mu;
   bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-  std::vector<int64_t> products;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
+  std::vector<int64_t> units[kPhases];
 };
-Phase3Log& phase3_log() {
-  static Phase3Log log;
+static PhaseLog& phase_log() {
+  static PhaseLog log;
   return log;
 }
-struct Phase3Timer {
-  cudaEvent_t a = nullptr, b = nullptr;
-  cudaStream_t st;
-  int64_t n;
-  Phase3Timer(cudaStream_t s, int64_t products) : st(s), n(products) {
-    Phase3Log& log = phase3_log();
-    std::lock_guard<std::mutex> lock(log.mu);
-    if (!log.on) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, st);
-  }
-  void stop() {
-    if (!a) return;
-    cudaEventRecord(b, st);
-    Phase3Log& log = phase3_log();
-    std::lock_guard<std::mutex> lock(log.mu);
-    log.ev.emplace_back(a, b);
-    log.products.push_back(n);
-  }
-};
+PhaseTimer::PhaseTimer(cudaStream_t s, int phase, int64_t units) : st(s), ph(phase), n(units) {
+  PhaseLog& log = phase_log();
+  std::lock_guard<std::mutex> lock(log.mu);
+  if (!log.on) return;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+}
+void PhaseTimer::stop() {
+  if (!a) return;
+  cudaEventRecord(b, st);
+  PhaseLog& log = phase_log();
+  std::lock_guard<std::mutex> lock(log.mu);
+  log.ev[ph].emplace_back(a, b);
+  log.units[ph].push_back(n);
+  a = nullptr;
+}
+
+namespace {
 
 }  // namespace
 
@@ -206,6 +207,7 @@ int chain_local(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_
     GOOM_TRY(launch_goom_to_ts(ident, 0, Cx.out(0), 1, d, d, st));
   }
   // phase 1
+  PhaseTimer t1(st, 1, T - nb);
   GOOM_TRY(copy_ts(L, 0, A, 0, nb, s, st));  // L[ks] = A[ks]
   if (s > 1 && T % s == 0 && chain_persistent()) {
     // every step of every block chain in ONE persistent launch: tiles run step-major and
@@ -231,7 +233,14 @@ int chain_local(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_
     GOOM_TRY(lmme_ts_call(A.in(i, s), L.in(i - 1, s), kTsOutTs, nullptr, 0, L.out(i, s), nullptr,
                           cnt, d, st));
   }
+  t1.stop();
   // phase 2: Cx[k+1] = L[last of block k] (x) Cx[k]
+  int64_t p2 = 0;  // products of the carry tree
+  if (tree_carries && nb > 1)
+    for (int64_t h = 1; h < nb; h <<= 1) p2 += nb - h;
+  else
+    p2 = carry_in ? nb : nb - 1;
+  PhaseTimer t2(st, 2, p2 + (tree_carries && nb > 1 && carry_in ? 1 : 0));
   if (tree_carries && nb > 1) {
     // X[k] (block k's carry-out, stored at Cx[k+1]) starts as the block total L[last of k]
     // (block 0: L[s-1] (x) Cx[0]); level j: X[k] <- X[k] (x) X[k - 2^j] for k >= 2^j
@@ -271,6 +280,7 @@ int chain_local(const TsBuf& A, int64_t T, int d, int block, const TsBuf* carry_
                             Cx.out(kb + 1, 0), nullptr, 1, d, st));
     }
   }
+  t2.stop();
   return GOOM_OK;
 }
 
@@ -293,7 +303,7 @@ int chain_finish(int64_t T, int d, int block, const TsBuf* carry, float2* out, f
     GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutGoom, out, (int64_t)d * d,
                           TsOut{}, nullptr, T, d, st));
   if (digests) {
-    Phase3Timer timer(st, T);
+    PhaseTimer timer(st, 3, T);
     GOOM_TRY(lmme_ts_call(w.L.in(0, 1), w.Cx.in(0, 1, s), kTsOutDigest, nullptr, 0, TsOut{},
                           w.parts, T, d, st));
     timer.stop();
@@ -354,37 +364,44 @@ TsBuf ts_of(float* U, float* q, uint32_t* G, int d) {
 
 extern "C" {
 
-// Phase-3 launch timing (profiling aid for bench.py): enable != 0 starts a fresh log;
-// goom_chain_ts_phase3_stats synchronises the logged events and returns the launches,
-// their total milliseconds and total products.
+// Per-phase launch timing (profiling aid for bench.py): enable != 0 starts a fresh log;
+// goom_chain_ts_phase_stats synchronises the logged events of one phase and returns its
+// bracketed launches, their total milliseconds and total units (products; leaf matrices for
+// phase 0). The phase3 pair is the phase-3 special case, kept for existing callers.
 void goom_chain_ts_phase3_timing(int enable) {
-  Phase3Log& log = phase3_log();
+  PhaseLog& log = phase_log();
   std::lock_guard<std::mutex> lock(log.mu);
-  for (auto& e : log.ev) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+  for (int p = 0; p < kPhases; ++p) {
+    for (auto& e : log.ev[p]) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    log.ev[p].clear();
+    log.units[p].clear();
   }
-  log.ev.clear();
-  log.products.clear();
   log.on = enable != 0;
 }
-int goom_chain_ts_phase3_stats(int64_t* launches, double* total_ms, int64_t* products) {
-  Phase3Log& log = phase3_log();
+int goom_chain_ts_phase_stats(int phase, int64_t* launches, double* total_ms, int64_t* units) {
+  if (phase < 0 || phase >= kPhases) return fail(GOOM_EINVAL, "phase must be 0..3");
+  PhaseLog& log = phase_log();
   std::lock_guard<std::mutex> lock(log.mu);
   double ms = 0.0;
   int64_t prod = 0;
-  for (size_t i = 0; i < log.ev.size(); ++i) {
+  for (size_t i = 0; i < log.ev[phase].size(); ++i) {
     float t = 0.0f;
-    if (cudaEventSynchronize(log.ev[i].second) != cudaSuccess ||
-        cudaEventElapsedTime(&t, log.ev[i].first, log.ev[i].second) != cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "phase-3 timing events");
+    if (cudaEventSynchronize(log.ev[phase][i].second) != cudaSuccess ||
+        cudaEventElapsedTime(&t, log.ev[phase][i].first, log.ev[phase][i].second) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "phase timing events");
     ms += t;
-    prod += log.products[i];
+    prod += log.units[phase][i];
   }
-  if (launches) *launches = (int64_t)log.ev.size();
+  if (launches) *launches = (int64_t)log.ev[phase].size();
   if (total_ms) *total_ms = ms;
-  if (products) *products = prod;
+  if (units) *units = prod;
   return GOOM_OK;
+}
+int goom_chain_ts_phase3_stats(int64_t* launches, double* total_ms, int64_t* products) {
+  return goom_chain_ts_phase_stats(3, launches, total_ms, products);
 }
 
 size_t goom_chain_ts_workspace_size(int64_t T, int d, int block) {
@@ -437,6 +454,72 @@ int goom_chain_ts_finish(int64_t T, int d, int block, const float* cU, const flo
   return chain_finish(T, d, block, cU ? &ci : nullptr, reinterpret_cast<float2*>(out),
                       reinterpret_cast<float4*>(digests4), oU ? &co : nullptr,
                       reinterpret_cast<char*>(ws), ws_bytes, as_stream(stream));
+}
+
+// Prefixes P_t = L_t (x) Cx[t / s] of a window that goom_chain_ts / goom_chain_ts_finish has
+// just scanned with this workspace (L and the final block carries stay in it), for the
+// window-local indices idx[0..n) (host array), as complex64 into out[i] and / or tile-scaled
+// into (oU, oq, oG)[i]: the harness's snapshots (SURVEY §8c(5) re-anchored checks) without
+// materialising the window. The tile-scaled form keeps the engine's own precision (fp32 U,
+// log scale q): a complex64 log at |log| ~ 1e6 is quantised to 0.125 nats.
+int goom_chain_ts_snapshots(int64_t T, int d, int block, const int64_t* idx, int n,
+                            goom_c64* out, float* oU, float* oq, uint32_t* oG, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (T < 1 || block < 1 || n < 0) return fail(GOOM_EINVAL, "T, block >= 1 and n >= 0");
+  if (d < 256 || d % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled chain needs d % 256 == 0");
+  if (n == 0) return GOOM_OK;
+  if (!idx || !ws || (!out && !(oU && oq && oG))) return fail(GOOM_EINVAL, "null pointer");
+  ChainWs w;
+  GOOM_TRY(chain_ws(T, d, block, reinterpret_cast<char*>(ws), ws_bytes, w));
+  cudaStream_t st = as_stream(stream);
+  const int nJ = d / 256;
+  TsBuf tso;
+  if (oU) {
+    tso.U = oU;
+    tso.q = oq;
+    tso.G = oG;
+    tso.d = d;
+    tso.nJ = nJ;
+    if (cudaMemsetAsync(oG, 0, sizeof(uint32_t) * (size_t)n * nJ, st) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "snapshot G reset");
+  }
+  for (int i = 0; i < n; ++i) {
+    const int64_t t = idx[i];
+    if (t < 0 || t >= T) return fail(GOOM_EINVAL, "snapshot index outside the window");
+    if (out)
+      GOOM_TRY(lmme_ts_call(w.L.in(t, 0), w.Cx.in(t / w.s, 0), kTsOutGoom,
+                            reinterpret_cast<float2*>(out) + (int64_t)i * d * d, (int64_t)d * d,
+                            TsOut{}, nullptr, 1, d, st));
+    if (oU)
+      GOOM_TRY(lmme_ts_call(w.L.in(t, 0), w.Cx.in(t / w.s, 0), kTsOutTs, nullptr, 0, tso.out(i, 0),
+                            nullptr, 1, d, st));
+  }
+  return GOOM_OK;
+}
+
+// The block carries Cx[k] (k = kidx[i], host array of n; 0 <= k < number of blocks) of the
+// window just scanned with this workspace, tile-scaled into (oU, oq, oG)[i]: the matrix the
+// engine applies on the right of every local product of block k, i.e. its own P_{k s - 1}
+// (the window's carry-in for k = 0). Re-anchored checks start the oracle from it.
+int goom_chain_ts_carries(int64_t T, int d, int block, const int64_t* kidx, int n, float* oU,
+                          float* oq, uint32_t* oG, void* ws, size_t ws_bytes, void* stream) {
+  if (T < 1 || block < 1 || n < 0) return fail(GOOM_EINVAL, "T, block >= 1 and n >= 0");
+  if (d < 256 || d % 256) return fail(GOOM_EUNSUPPORTED, "tile-scaled chain needs d % 256 == 0");
+  if (n == 0) return GOOM_OK;
+  if (!kidx || !ws || !oU || !oq || !oG) return fail(GOOM_EINVAL, "null pointer");
+  ChainWs w;
+  GOOM_TRY(chain_ws(T, d, block, reinterpret_cast<char*>(ws), ws_bytes, w));
+  TsBuf dst;
+  dst.U = oU;
+  dst.q = oq;
+  dst.G = oG;
+  dst.d = d;
+  dst.nJ = d / 256;
+  for (int i = 0; i < n; ++i) {
+    if (kidx[i] < 0 || kidx[i] >= w.nb) return fail(GOOM_EINVAL, "block index outside the window");
+    GOOM_TRY(copy_ts(dst, i, w.Cx, kidx[i], 1, 1, as_stream(stream)));
+  }
+  return GOOM_OK;
 }
 
 int goom_ts_from_c64(const goom_c64* X, int64_t batch, int rows, int cols, float* U, float* q,

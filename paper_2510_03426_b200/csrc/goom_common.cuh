@@ -152,5 +152,10 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 int num_sms();
+// once per (kernel, device), thread-safe (abi.cu): opt a kernel into `bytes` of dynamic
+// shared memory on the current device
+int smem_attr(const void* kernel, int bytes, const char* what);
+// a value computed once per (key, device), thread-safe (e.g. an occupancy query)
+int per_device_value(const void* key, int (*query)());
 
 }  // namespace goom

@@ -106,6 +106,17 @@ struct TsProblem {
   uint32_t* chain_done = nullptr;
 };
 bool lmme_ts_eligible(int n, int k, int m);
+// bench instrumentation (chain_ts.cu): CUDA events around a phase of the chain engine,
+// recorded only while goom_chain_ts_phase3_timing(1) is on
+constexpr int kPhases = 4;
+struct PhaseTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  int ph;
+  int64_t n;
+  PhaseTimer(cudaStream_t s, int phase, int64_t units);
+  void stop();
+};
 int lmme_ts(const TsProblem& p, cudaStream_t s);
 // complex64 GOOM <-> tile-scaled (elementwise, one warp per (row, 256-column block))
 int launch_goom_to_ts(const float2* X, int64_t strideX, TsOut out, int64_t batch, int rows,

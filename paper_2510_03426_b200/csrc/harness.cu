@@ -151,9 +151,11 @@ int goom_random_normal_ts(float* U, float* q, uint32_t* G, int64_t T, int d, uin
   int64_t blocks = (n / 4 + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
+  PhaseTimer timer(as_stream(stream), 0, T);
   random_normal_ts_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       U, q, G, n, T * d * (d / 256), T * (d / 256), seed, (uint64_t)offset);
   GOOM_CHECK_LAUNCH("random_normal_ts_kernel");
+  timer.stop();
   return GOOM_OK;
 }
 

@@ -401,13 +401,7 @@ int lmme_simt_whole(const LmmeProblemT<R>& p, cudaStream_t s) {
     }
   }
   const size_t smem = lmme_whole_smem<R>();
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(lmme_whole_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "lmme_whole smem attribute");
-    attr = true;
-  }
+  GOOM_TRY(smem_attr((const void*)lmme_whole_kernel<R>, (int)smem, "lmme_whole smem attribute"));
   const int64_t gmax_ = 2147483647;
   for (int64_t b0 = 0; b0 < p.batch; b0 += gmax_) {
     const int64_t nb = p.batch - b0 < gmax_ ? p.batch - b0 : gmax_;

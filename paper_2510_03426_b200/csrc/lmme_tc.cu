@@ -400,13 +400,7 @@ int tc_debug() {
 
 template <int BN>
 int launch_tc(const LmmeProblem& p, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(lmme_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<BN>::kSmem) != cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "lmme_tc smem attribute");
-    attr_set = true;
-  }
+  GOOM_TRY(smem_attr((const void*)lmme_tc_kernel<BN>, Cfg<BN>::kSmem, "lmme_tc smem attribute"));
   alignas(64) CUtensorMap mapA, mapB;
   int64_t mats, mstride;
   // A: (k, n, matrix) complex64 moved as int64, box 16 k x 128 rows

@@ -399,8 +399,8 @@ int tc_debug() {
   return v;
 }
 
-int max_clusters() {
-  static int v = [] {
+int query_clusters() {
+  return [] {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74);
     cfg.blockDim = dim3(kThreads);
@@ -419,7 +419,9 @@ int max_clusters() {
     }
     return n;
   }();
-  return v;
+}
+int max_clusters() {  // per device (abi.cu per_device_value)
+  return per_device_value((const void*)lmme_tc2_kernel, &query_clusters);
 }
 
 }  // namespace
@@ -436,13 +438,7 @@ int lmme_tc2(const LmmeProblem& p, cudaStream_t s) {
         reinterpret_cast<uintptr_t>(p.C) | reinterpret_cast<uintptr_t>(p.colB.ptr)) & 15) ||
       ((p.A.stride | p.B.stride | p.strideC) & 1) || (p.colB.stride & 3))
     return GOOM_EUNSUPPORTED;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(lmme_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) !=
-        cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "lmme_tc2 smem attribute");
-    attr_set = true;
-  }
+  GOOM_TRY(smem_attr((const void*)lmme_tc2_kernel, kSmem, "lmme_tc2 smem attribute"));
   alignas(64) CUtensorMap mapA, mapB;
   int64_t mats, mstride;
   // A: (k, n, matrix) complex64 moved as int64; box 16 k x 128 rows (one CTA's half)

@@ -13,9 +13,13 @@
 //     accumulator S within its 256-column block) and q = rowmax_A + G_B + e ln 2: no log;
 //   * or, for prefixes that are only digested, it reduces (max log, log Frobenius,
 //     finiteness) per 32 rows and never writes the product.
-// The scale choice differs from the reference's clamped per-row/per-column maxima only
-// in how intermediate values are rounded and where they underflow (a column more than
-// e^87 below the largest entry of its 256-column block flushes), not in the product.
+// Scales follow Eq. 11's clamp (core.py:252-253): a = max(row scale, 0), b = max(G, 0), so a
+// shrinking chain underflows where the reference's float32 run does (GOOM_TS_SCALES=truemax
+// opts out). They differ from the reference's per-COLUMN maxima of the right operand in one
+// way that the format cannot avoid: an entry more than ~e^87 below the largest entry of its
+// (row, 256-column block) — or a right-operand row whose block lies e^87 below the block's
+// G — flushes. The public scan therefore runs the complex64 kernels (exact Eq. 11 per
+// column) unless GOOM_CHAIN_TS=1; this engine serves the long-chain harness (config 3).
 //
 // Pipeline per CTA (pair tile 256 x 256, full K, cta_group::2 like lmme_tc2.cu):
 //   warp 0       TMA: raw fp32 K-block (A [128 rows][16 k], B [16 k][128 cols]) into a
@@ -26,6 +30,7 @@
 //                K-block into a double-buffered TMEM accumulator;
 //   warps 18..21 epilogue (GOOM complex64 | tile-scaled fp32 | digest partials).
 #include <cstdlib>
+#include <string>
 
 #include "tc_ptx.cuh"
 
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
                    float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug,
-                   ChainArgs ch) {
+                   ChainArgs ch, int clampz) {
   using Y = Lay<kOut, S>;
   constexpr int kStages = S, kOutOff = Y::kOutOff;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) qbn[h] = u + 512 * h < k ? qb[(int64_t)(u + 512 * h) * nJm] : 0.0f;
       gBn = decode_g(B.G[ib * B.sG + JB]);
+      if (clampz) gBn = fmaxf(gBn, 0.0f);  // Eq. 11: b = max(colmax B, 0)
       return true;
     };
     bool fetched = cluster < grid.tiles && fetch(cluster, true);
@@ -329,7 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float qac[4];
 #pragma unroll
       for (int J = 0; J < 4; ++J) qac[J] = qan[J];
-      const float rho = fmaxf(fmaxf(qac[0], qac[1]), fmaxf(qac[2], qac[3]));
+      float rho = fmaxf(fmaxf(qac[0], qac[1]), fmaxf(qac[2], qac[3]));
+      if (clampz) rho = fmaxf(rho, 0.0f);  // Eq. 11: a = max(rowmax A, 0)
       asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");  // table complete
       fetched = t + nclusters < grid.tiles && fetch(t + nclusters, false);
       float fa = 0.0f;
@@ -394,7 +401,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* qa = A.q + (kChain ? idx_a(b, step) : b / A.div) * A.sq + (int64_t)grow * nJk;
       float rho = kNegInf;
       for (int J = 0; J < nJk; ++J) rho = fmaxf(rho, qa[J]);
-      const float gB = decode_g(B.G[(kChain ? idx_b(b, step) : b / B.div) * B.sG + JB]);
+      float gB = decode_g(B.G[(kChain ? idx_b(b, step) : b / B.div) * B.sG + JB]);
+      if (clampz) {  // the same clamped scales as the transform (Eq. 11, core.py:252-253)
+        rho = fmaxf(rho, 0.0f);
+        gB = fmaxf(gB, 0.0f);
+      }
       mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
       tc_fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * kPairN);
@@ -521,6 +532,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// GOOM_TS_SCALES=truemax: scale by the operands' true maxima instead of Eq. 11's clamped
+// max(rowmax, 0) / max(colmax, 0) (core.py:252-253). Opt-in only: with the clamp a shrinking
+// chain underflows to -inf exactly where the reference's float32 run (and this library's
+// complex64 kernels) do; without it the engine returns the finite product instead.
+int ts_clamp() {
+  static int v = [] {
+    const char* e = getenv("GOOM_TS_SCALES");
+    return (e && std::string(e) == "truemax") ? 0 : 1;
+  }();
+  return v;
+}
+
 int ts_debug() {
   static int v = [] {
     const char* e = getenv("GOOM_TS_DEBUG");
@@ -530,8 +553,8 @@ int ts_debug() {
 }
 
 template <int kOut, int S>
-int max_clusters() {
-  static int v = [] {
+int query_clusters() {
+  return [] {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74);
     cfg.blockDim = dim3(kThreads);
@@ -551,20 +574,18 @@ int max_clusters() {
     }
     return n;
   }();
-  return v;
+}
+template <int kOut, int S>
+int max_clusters() {  // per device (abi.cu per_device_value)
+  return per_device_value((const void*)lmme_ts_kernel<kOut, S, false>, &query_clusters<kOut, S>);
 }
 
 template <int kOut, int S, bool kChain = false>
 int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
                const CUtensorMap& mapOut, cudaStream_t s) {
   constexpr int kSmem = Lay<kOut, S>::kSmem;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(lmme_ts_kernel<kOut, S, kChain>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
-      return cuda_fail(cudaGetLastError(), "lmme_ts smem attribute");
-    attr_set = true;
-  }
+  GOOM_TRY(smem_attr((const void*)lmme_ts_kernel<kOut, S, kChain>, kSmem,
+                     "lmme_ts smem attribute"));
   PairGrid pg;
   pg.nct = p.m / kPairN;
   pg.nrt = p.n / 256;
@@ -587,7 +608,7 @@ int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& m
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S, kChain>, mapA, mapB, mapOut, p.A, p.B, p.T,
                      p.parts, pg,
-                     p.n, p.k, p.m, ts_debug(), ch);
+                     p.n, p.k, p.m, ts_debug(), ch, ts_clamp());
   GOOM_CHECK_LAUNCH("lmme_ts_kernel");
   return GOOM_OK;
 }

@@ -14,6 +14,7 @@
 //
 // Buffers: local products L (T matrices) and carries Cx (nblocks+1) live in the
 // caller's workspace; the input is never written; out may not alias the input.
+#include <atomic>
 #include <cstdlib>
 
 #include "goom_internal.cuh"
@@ -85,12 +86,23 @@ int copy_strided(C* dst, const C* src, size_t width, size_t pitch, size_t rows, 
 
 }  // namespace
 
-bool chain_ts_path(int d) {
-  static const bool on = [] {
+// The public complex64 chain scan keeps the reference's per-column clamped scales (Eq. 11,
+// core.py:252-253) for every d: the tile-scaled engine (chain_ts.cu) is opt-in here
+// (GOOM_CHAIN_TS=1) because its per-(row, 256-column block) format flushes entries more than
+// ~e^87 below their block's largest (lmme_ts.cu header), where the reference is exact.
+std::atomic<int> g_chain_engine{-1};  // -1: not read yet; 0 complex64 (exact); 1 tile-scaled
+int chain_engine() {
+  int v = g_chain_engine.load();
+  if (v < 0) {
     const char* e = getenv("GOOM_CHAIN_TS");
-    return !(e && atoi(e) == 0);
-  }();
-  return on && lmme_backend() != 1 && lmme_ts_eligible(d, d, d);
+    int want = (e && atoi(e) == 1) ? 1 : 0;
+    g_chain_engine.compare_exchange_strong(v, want);
+    v = g_chain_engine.load();
+  }
+  return v;
+}
+bool chain_ts_path(int d) {
+  return chain_engine() == 1 && lmme_backend() != 1 && lmme_ts_eligible(d, d, d);
 }
 
 template <class R>
@@ -418,3 +430,9 @@ int goom_scan_affine_c128(const goom_c128* A, const goom_c128* B, const uint8_t*
 }
 
 }  // extern "C"
+
+extern "C" int goom_set_chain_engine(int engine) {
+  goom::chain_engine();  // settle the environment default first
+  if (engine < 0 || engine > 1) return goom::g_chain_engine.load();
+  return goom::g_chain_engine.exchange(engine);
+}

@@ -12,8 +12,8 @@ kept at a stride.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-from typing import Dict, Optional
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Sequence
 
 import torch
 
@@ -25,6 +25,12 @@ class ChainRun:
     digests: torch.Tensor             # (T, 4) float32: max log, log ||P_t||_F, finite, 0
     final: torch.Tensor               # P_{T-1} (d, d) complex64
     snapshots: Dict[int, torch.Tensor]
+    # tile-scaled engine only: the same snapshots at the engine's own precision
+    # (ops.ts_log_sign gives exact float64 logs; the complex64 ones round to float32)
+    snapshots_ts: Dict[int, "ops.TsMats"] = field(default_factory=dict)
+    # tile-scaled engine only: for each requested block start t, the block carry the engine
+    # applies to prefixes t .. t + block - 1 (its own P_{t-1}; ops.chain_ts `carries`)
+    anchors_ts: Dict[int, "ops.TsMats"] = field(default_factory=dict)
 
 
 def random_chain(T: int, d: int, seed: int = 0, t0: int = 0, device=None) -> torch.Tensor:
@@ -32,11 +38,29 @@ def random_chain(T: int, d: int, seed: int = 0, t0: int = 0, device=None) -> tor
     return torch.ops.goom.random_normal(torch.empty(0, device=dev), T, d, seed, t0)
 
 
+def _snapshot_set(T: int, t0: int, snapshot_every: int, snapshots: Sequence[int]):
+    """Absolute prefix indices in [t0, t0 + T) to keep as full complex64 matrices."""
+    want = {int(t) for t in snapshots if t0 <= int(t) < t0 + T}
+    if snapshot_every:
+        first = -(-t0 // snapshot_every) * snapshot_every
+        want.update(range(first, t0 + T, snapshot_every))
+    return want
+
+
 def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
               t0: int = 0, carry: Optional[torch.Tensor] = None, snapshot_every: int = 0,
-              leaves: Optional[torch.Tensor] = None) -> ChainRun:
+              leaves: Optional[torch.Tensor] = None, snapshots: Sequence[int] = (),
+              anchors: Sequence[int] = ()) -> ChainRun:
     """Scan leaves t0 .. t0+T-1 (generated, or the given `leaves` tensor) with an
     optional right carry; returns per-prefix digests, the final prefix, snapshots.
+
+    Snapshots: the full prefixes P_t for every absolute t in `snapshots` (and every multiple
+    of `snapshot_every`) inside the run, keyed by t. On the tile-scaled engine each one is
+    recomputed from the window's workspace (L_t (x) its block carry, one product), so
+    keeping them costs no full-window output. Anchors (tile-scaled engine): absolute block
+    starts t (multiples of `block` from a window start; windows are multiples of `block`)
+    whose block carry — the engine's own P_{t-1}, applied on the right of every local
+    product of that block — is returned in `anchors_ts[t]` (re-anchored parity checks).
 
     `leaves` may be complex64 GOOMs on the device, or real float32 matrices — on the
     device, or in pinned host memory, in which case each window's host->device copy
@@ -46,8 +70,9 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
     (or imported) tile-scaled, prefixes are digested inside the phase-3 LMME epilogue
     and the carry between windows stays tile-scaled. Other d use the complex64 scan +
     digest kernels."""
+    want = _snapshot_set(T, t0, snapshot_every, snapshots)
     if ops.ts_eligible(d):
-        return _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves)
+        return _run_chain_ts(T, d, seed, window, block, t0, carry, want, leaves, anchors)
     dev = torch.device("cuda", torch.cuda.current_device())
     if leaves is not None and leaves.dtype == torch.float32:  # real matrices -> GOOMs
         leaves = torch.ops.goom.from_real(leaves.to(dev), float("-inf"), False)
@@ -58,10 +83,9 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
         A = leaves[w0:w0 + n] if leaves is not None else random_chain(n, d, seed, t0 + w0, dev)
         P = torch.ops.goom.scan_chain(A, block, carry)
         digests[w0:w0 + n] = torch.ops.goom.digest(P)
-        if snapshot_every:
-            for t in range(w0, w0 + n):
-                if (t0 + t) % snapshot_every == 0:
-                    snaps[t0 + t] = P[t - w0].clone()
+        for t in range(w0, w0 + n):
+            if t0 + t in want:
+                snaps[t0 + t] = P[t - w0].clone()
         carry = P[n - 1].clone()
         del P, A
     return ChainRun(digests, carry, snaps)
@@ -79,10 +103,26 @@ def real_leaves_ts(x: torch.Tensor) -> "ops.TsMats":
     return ops.TsMats(x, q, G)
 
 
-def _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves) -> ChainRun:
+def _window_anchor_blocks(anchors, a0: int, n: int, block: int):
+    """Block indices of a window starting at absolute index a0 (n leaves) for the anchors
+    that fall inside it."""
+    ks = []
+    for t in anchors:
+        if a0 <= t < a0 + n:
+            if (t - a0) % block:
+                raise ValueError(f"anchor {t} is not a block start (block {block})")
+            ks.append((t - a0) // block)
+    return sorted(ks)
+
+
+def _run_chain_ts(T, d, seed, window, block, t0, carry, want, leaves, anchors=()) -> ChainRun:
     dev = torch.device("cuda", torch.cuda.current_device())
     digests = torch.empty((T, 4), dtype=torch.float32, device=dev)
     snaps: Dict[int, torch.Tensor] = {}
+    snaps_ts: Dict[int, ops.TsMats] = {}
+    anch: Dict[int, ops.TsMats] = {}
+    if anchors and window % block:
+        raise ValueError("anchors need window to be a multiple of block")
     c = ops.ts_from_goom(carry.reshape(1, d, d)) if carry is not None else None
     streamed = leaves is not None and not leaves.is_cuda
     if streamed:
@@ -117,18 +157,22 @@ def _run_chain_ts(T, d, seed, window, block, t0, carry, snapshot_every, leaves) 
             A = real_leaves_ts(x.contiguous()) if x.dtype == torch.float32 else ops.ts_from_goom(x)
         else:
             A = ops.ts_random_normal(n, d, seed, t0 + w0, dev)
-        want = bool(snapshot_every) and any((t0 + t) % snapshot_every == 0
-                                            for t in range(w0, w0 + n))
-        P, dg, c = ops.chain_ts(A, block, c, out=want, digests=True, carry_out=True)
+        local = sorted(t - t0 - w0 for t in want if t0 + w0 <= t < t0 + w0 + n)
+        ks = _window_anchor_blocks(anchors, t0 + w0, n, block)
+        _, dg, c, S, K = ops.chain_ts(A, block, c, digests=True, carry_out=True,
+                                      snapshots=local, carries=ks)
         digests[w0:w0 + n] = dg
+        for j, k in enumerate(ks):
+            anch[t0 + w0 + k * block] = K[j:j + 1]
         if streamed:
             free[i % 2].record(main)
-        if want:
-            for t in range(w0, w0 + n):
-                if (t0 + t) % snapshot_every == 0:
-                    snaps[t0 + t] = P[t - w0].clone()
-        del P, A
-    return ChainRun(digests, ops.ts_to_goom(c)[0], snaps)
+        if local:
+            S64 = ops.ts_to_goom(S)
+            for j, t in enumerate(local):
+                snaps[t0 + w0 + t] = S64[j]
+                snaps_ts[t0 + w0 + t] = S[j:j + 1]
+        del A, S, K
+    return ChainRun(digests, ops.ts_to_goom(c)[0], snaps, snaps_ts, anch)
 
 
 def chain_total(A: torch.Tensor) -> torch.Tensor:

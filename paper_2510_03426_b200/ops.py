@@ -511,10 +511,41 @@ def lmme_ts(a: TsMats, b: TsMats, kind: int = 0, b_div: int = 1):
     return dg
 
 
+def _ts_extras(T: int, d: int, block: int, snapshots, carries, ws: torch.Tensor,
+               nws: int) -> Tuple["TsMats", "TsMats"]:
+    """From the window just scanned in `ws`: the prefixes at window-local indices
+    `snapshots` (goom_chain_ts_snapshots) and the block carries of the blocks `carries`
+    (goom_chain_ts_carries), both tile-scaled — the engine's own precision (ts_log_sign)."""
+    res = []
+    for name, idx in (("goom_chain_ts_snapshots", snapshots), ("goom_chain_ts_carries", carries)):
+        idx = [int(i) for i in (idx or ())]
+        out = ts_empty(len(idx), d, ws.device)
+        if idx:
+            arr = ctypes.cast((ctypes.c_int64 * len(idx))(*idx), ctypes.c_void_p)
+            extra = (None,) if name == "goom_chain_ts_snapshots" else ()
+            _lib.call(name, T, d, int(block), arr, len(idx), *extra, out.U.data_ptr(),
+                      out.q.data_ptr(), out.G.data_ptr(), ws.data_ptr(), nws, _stream())
+        res.append(out)
+    return res[0], res[1]
+
+
+def ts_log_sign(m: TsMats) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Tile-scaled matrices as float64 (log|x|, sign): log = q[i][j // 256] + log|U_ij|
+    evaluated in float64, so the value is exactly what the engine holds (a complex64 export
+    rounds the log to float32: 0.125 nats at |log| ~ 1e6)."""
+    d = m.U.shape[-1]
+    q = m.q.double().repeat_interleave(256, dim=-1)
+    u = m.U.double()
+    log = torch.where(u == 0, torch.full_like(u, NEG_INF), torch.log(u.abs()) + q)
+    return log, torch.where(u < 0, -1.0, 1.0).to(torch.float64)
+
+
 def chain_ts(leaves: TsMats, block: int, carry: Optional[TsMats] = None, out: bool = False,
-             digests: bool = True, carry_out: bool = True):
+             digests: bool = True, carry_out: bool = True, snapshots=None, carries=None):
     """One window of the long-chain scan on tile-scaled leaves: returns
-    (prefixes complex64 or None, digests (T, 4) or None, last prefix TsMats or None)."""
+    (prefixes complex64 or None, digests (T, 4) or None, last prefix TsMats or None), plus —
+    when `snapshots` (window-local prefix indices) or `carries` (block indices) is given —
+    the tile-scaled snapshots and block carries as a 4th and 5th element."""
     T, d = leaves.U.shape[0], leaves.U.shape[-1]
     dev = leaves.U.device
     ws, nws = _ws(int(_lib.load().goom_chain_ts_workspace_size(T, d, int(block))), dev)
@@ -529,6 +560,8 @@ def chain_ts(leaves: TsMats, block: int, carry: Optional[TsMats] = None, out: bo
               int(block), p(carry.U if carry else None), p(carry.q if carry else None),
               p(carry.G if carry else None), p(P), p(dg), p(co.U if co else None),
               p(co.q if co else None), p(co.G if co else None), ws.data_ptr(), nws, _stream())
+    if snapshots is not None or carries is not None:
+        return (P, dg, co) + _ts_extras(T, d, block, snapshots, carries, ws, nws)
     return P, dg, co
 
 
@@ -554,8 +587,10 @@ def chain_ts_local(leaves: TsMats, block: int):
 
 
 def chain_ts_finish(win: ChainWindow, carry: Optional[TsMats], out: bool = False,
-                    digests: bool = True, carry_out: bool = True):
-    """Phase 3 of a window prepared by chain_ts_local, with a right carry (or none)."""
+                    digests: bool = True, carry_out: bool = True, snapshots=None,
+                    carries=None):
+    """Phase 3 of a window prepared by chain_ts_local, with a right carry (or none);
+    `snapshots` / `carries` as in chain_ts (the carries then include the right carry)."""
     dev = win.ws.device
     P = torch.empty((win.T, win.d, win.d), dtype=torch.complex64, device=dev) if out else None
     dg = torch.empty((win.T, 4), dtype=torch.float32, device=dev) if digests else None
@@ -568,4 +603,7 @@ def chain_ts_finish(win: ChainWindow, carry: Optional[TsMats], out: bool = False
               p(carry.q if carry else None), p(carry.G if carry else None), p(P), p(dg),
               p(co.U if co else None), p(co.q if co else None), p(co.G if co else None),
               win.ws.data_ptr(), win.nbytes, _stream())
+    if snapshots is not None or carries is not None:
+        return (P, dg, co) + _ts_extras(win.T, win.d, win.block, snapshots, carries, win.ws,
+                                        win.nbytes)
     return P, dg, co

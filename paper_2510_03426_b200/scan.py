@@ -408,8 +408,11 @@ def scan_sequential(leaves, combiner):
         out, _ = _selective_sequential_pairs(leaves, combiner.policy)
         return out
     if combiner is combine_affine:
-        # block >= T: the blocked engine degenerates to the left fold (scan.py:217-225)
-        return _scan_affine_stack(_Stack.from_pairs(leaves), len(leaves)).to_pairs()
+        # block >= T: the blocked engine degenerates to the left fold (scan.py:217-225);
+        # the fold's first state IS the first leaf (scan.py:521, test_scan.py:182-186)
+        out = _scan_affine_stack(_Stack.from_pairs(leaves), len(leaves)).to_pairs()
+        out[0] = leaves[0]
+        return out
     out = [leaves[0]]
     for leaf in leaves[1:]:
         out.append(combiner(out[-1], leaf))

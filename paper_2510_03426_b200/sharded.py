@@ -72,7 +72,8 @@ def shard_total(n: int, d: int, seed: int, t0: int, window: int, block: int) -> 
 
 
 def run_shard_resident(n: int, d: int, seed: int, t0: int, window: int, block: int,
-                       exchange: Callable, max_resident: Optional[int] = None):
+                       exchange: Callable, max_resident: Optional[int] = None,
+                       snapshots=(), anchors=()):
     """This rank's shard with its local products kept on the device (d % 256 == 0).
 
     Pass 1 runs the carry-independent phases 1-2 of every window (ops.chain_ts_local) and
@@ -83,9 +84,11 @@ def run_shard_resident(n: int, d: int, seed: int, t0: int, window: int, block: i
     others. A fully resident rank does ~2 n products (the single-GPU work); one that keeps
     nothing does ~3 n (the totals recomputed, as shard_total + run_chain)."""
     from . import ops
-    from .harness import ChainRun
+    from .harness import ChainRun, _window_anchor_blocks
 
     dev = torch.device("cuda", torch.cuda.current_device())
+    if anchors and window % block:
+        raise ValueError("anchors need window to be a multiple of block")
     if max_resident is None:
         per = min(window, n) * d * d * 4 * 1.08
         max_resident = max(0, int((0.92 * _free_bytes() - per) // per))
@@ -102,15 +105,28 @@ def run_shard_resident(n: int, d: int, seed: int, t0: int, window: int, block: i
     carry = exchange(ops.ts_to_goom(total)[0])
     c = ops.ts_from_goom(carry.reshape(1, d, d)) if carry is not None else None
     digests = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    want = sorted({int(t) - t0 for t in snapshots if t0 <= int(t) < t0 + n})
+    snaps, snaps_ts, anch = {}, {}, {}
     for i, (w0, m, win) in enumerate(wins):
+        local = [t - w0 for t in want if w0 <= t < w0 + m]
+        ks = _window_anchor_blocks(anchors, t0 + w0, m, block)
         if win is not None:
-            _, dg, c = ops.chain_ts_finish(win, c, digests=True, carry_out=True)
+            _, dg, c, S, K = ops.chain_ts_finish(win, c, digests=True, carry_out=True,
+                                                 snapshots=local, carries=ks)
         else:
-            _, dg, c = ops.chain_ts(ops.ts_random_normal(m, d, seed, t0 + w0, dev), block, c,
-                                    digests=True, carry_out=True)
+            _, dg, c, S, K = ops.chain_ts(ops.ts_random_normal(m, d, seed, t0 + w0, dev), block,
+                                          c, digests=True, carry_out=True, snapshots=local,
+                                          carries=ks)
         digests[w0:w0 + m] = dg
+        for j, k in enumerate(ks):
+            anch[t0 + w0 + k * block] = K[j:j + 1]
+        if local:
+            S64 = ops.ts_to_goom(S)
+            for j, t in enumerate(local):
+                snaps[t0 + w0 + t] = S64[j]
+                snaps_ts[t0 + w0 + t] = S[j:j + 1]
         wins[i] = None  # release the window's workspace
-    return ChainRun(digests, ops.ts_to_goom(c)[0], {})
+    return ChainRun(digests, ops.ts_to_goom(c)[0], snaps, snaps_ts, anch)
 
 
 def _free_bytes() -> int:
@@ -128,8 +144,9 @@ def resident_fits(n: int, d: int, window: int) -> bool:
 
 
 def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
-                      group=None, snapshot_every: int = 0):
-    """Rank-local part of a time-sharded chain run; returns (t0, ChainRun)."""
+                      group=None, snapshot_every: int = 0, snapshots=(), anchors=()):
+    """Rank-local part of a time-sharded chain run; returns (t0, ChainRun). `snapshots`:
+    absolute prefix indices to keep (those inside this rank's shard come back)."""
     from . import ops
     from .harness import run_chain
 
@@ -148,22 +165,25 @@ def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: 
         # keeps as many windows' local products as fit; recomputes only the rest
         return t0, run_shard_resident(
             n, d, seed, t0, w, block,
-            lambda tot: exclusive_carry(tot, torch.ops.goom.lmme, group))
+            lambda tot: exclusive_carry(tot, torch.ops.goom.lmme, group), snapshots=snapshots,
+            anchors=anchors)
     carry = None
     if world > 1:
         total = shard_total(n, d, seed, t0, window, block)
         carry = exclusive_carry(total, torch.ops.goom.lmme, group)
     return t0, run_chain(n, d, seed, window, block, t0=t0, carry=carry,
-                         snapshot_every=snapshot_every)
+                         snapshot_every=snapshot_every, snapshots=snapshots, anchors=anchors)
 
 
 def scan_chain_nccl(A_local: torch.Tensor, block: int = 64, group=None,
-                    comm: Optional[int] = None) -> torch.Tensor:
+                    comm: Optional[int] = None, digests: bool = False) -> torch.Tensor:
     """Global prefixes of this rank's contiguous chunk of a chain split across ranks, in ONE
-    C-ABI call (goom_scan_chain_sharded_c64: local scan, ncclAllGather of the chunk totals,
-    exclusive carry, one batched LMME). A_local: complex64 (T_local, d, d) on this rank's
-    GPU; ranks hold consecutive chunks in rank order. `comm` is a raw ncclComm_t; by default
-    the NCCL communicator of `group` (torch's ProcessGroupNCCL)."""
+    C-ABI call (goom_scan_chain_sharded_c64: local phases 1-2, ncclAllGather of the chunk
+    totals, exclusive carry folded onto the block carries, phase 3 — two LMMEs per leaf).
+    A_local: complex64 (T_local, d, d) on this rank's GPU; ranks hold consecutive chunks in
+    rank order. `comm` is a raw ncclComm_t; by default the NCCL communicator of `group`
+    (torch's ProcessGroupNCCL). digests=True returns the (T_local, 4) float32 digests of
+    the global prefixes instead (goom_scan_chain_sharded_digest_c64)."""
     import ctypes
 
     from . import _lib
@@ -177,10 +197,105 @@ def scan_chain_nccl(A_local: torch.Tensor, block: int = 64, group=None,
     T, d = A_local.shape[0], A_local.shape[1]
     lib = _lib.load()
     nranks = dist.get_world_size(group) if dist.is_initialized() else 1
-    nws = int(lib.goom_scan_chain_sharded_workspace_size(T, d, int(block), nranks))
+    size = (lib.goom_scan_chain_sharded_digest_workspace_size if digests
+            else lib.goom_scan_chain_sharded_workspace_size)
+    nws = int(size(T, d, int(block), nranks))
     ws = torch.empty(nws, dtype=torch.uint8, device=A_local.device)
-    out = torch.empty_like(A_local)
-    _lib.call("goom_scan_chain_sharded_c64", A_local.data_ptr(), out.data_ptr(), T, d, int(block),
-              ctypes.c_void_p(comm), ws.data_ptr(), nws,
-              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if digests:
+        out = torch.empty((T, 4), dtype=torch.float32, device=A_local.device)
+    else:
+        out = torch.empty_like(A_local)
+    _lib.call("goom_scan_chain_sharded_digest_c64" if digests else "goom_scan_chain_sharded_c64",
+              A_local.data_ptr(), out.data_ptr(), T, d, int(block), ctypes.c_void_p(comm),
+              ws.data_ptr(), nws, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     return out
+
+
+# ---------------------------------------------------------------------------
+# batch-only workloads: no communication on the data path
+
+
+def _world(group=None):
+    if dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def lmme_batch_sharded(A: torch.Tensor, B: torch.Tensor, group=None, gather: bool = True,
+                       lmme: Optional[Callable] = None):
+    """Config 2 (`_lmme_arrays` over a batch, core.py:242-261) sharded by batch: rank r
+    computes products shard_range(batch, r, world) of A (batch, n, k) (x) B (batch, k, m)
+    (a single-matrix operand broadcasts). No exchange on the data path; with gather=True
+    the shards are all-gathered so every rank returns the whole batch, else the rank's
+    slice and its first index."""
+    lmme = lmme if lmme is not None else torch.ops.goom.lmme
+    rank, world = _world(group)
+    batch = max(A.shape[0], B.shape[0])
+    t0, n = shard_range(batch, rank, world)
+    a = A[t0:t0 + n] if A.shape[0] > 1 else A
+    b = B[t0:t0 + n] if B.shape[0] > 1 else B
+    local = lmme(a, b)
+    if not gather or world == 1:
+        return local if gather else (t0, local)
+    real = torch.view_as_real(local.contiguous())
+    sizes = [shard_range(batch, r, world)[1] for r in range(world)]
+    parts = [torch.empty((sz,) + tuple(real.shape[1:]), dtype=real.dtype, device=real.device)
+             for sz in sizes]
+    if len(set(sizes)) == 1:
+        dist.all_gather(parts, real, group=group)
+    else:  # uneven shards: pad to the largest
+        mx = max(sizes)
+        pad = torch.zeros((mx,) + tuple(real.shape[1:]), dtype=real.dtype, device=real.device)
+        pad[:real.shape[0]] = real
+        full = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(full, pad, group=group)
+        parts = [f[:sz] for f, sz in zip(full, sizes)]
+    return torch.view_as_complex(torch.cat(parts).contiguous())
+
+
+def ssm_sequences_shard(x0s: torch.Tensor, us: torch.Tensor, group=None):
+    """Config 5 data parallelism: this rank's slice of the S sequences of every head
+    (x0s (H, S, d), us (H, S, T, d)) — the heads share A's powers, so sequences, not heads,
+    are split. Returns (first sequence, x0s slice, us slice)."""
+    rank, world = _world(group)
+    s0, n = shard_range(us.shape[1], rank, world)
+    return s0, x0s[:, s0:s0 + n], us[:, s0:s0 + n]
+
+
+def allreduce_grads(params, group=None):
+    """Sum the parameter gradients of a sequence-sharded SSM layer over the ranks (the one
+    collective of data-parallel training; the forward and backward scans themselves have
+    no exchange). In place on p.grad; parameters without a gradient are skipped."""
+    _, world = _world(group)
+    if world == 1:
+        return
+    for p in params:
+        if p.grad is not None:
+            dist.all_reduce(p.grad, op=dist.ReduceOp.SUM, group=group)
+
+
+def ssm_layer_sharded(A, B, C, D, x0s, us, chunk: int = 64, group=None):
+    """ssm.ssm_layer on this rank's sequences (ssm_sequences_shard): returns (first
+    sequence, y slice). After backward, call allreduce_grads((A, B, C, D)) so every rank
+    holds the gradient of the whole batch's loss."""
+    from .ssm import ssm_layer
+
+    s0, x, u = ssm_sequences_shard(x0s, us, group)
+    return s0, ssm_layer(A, B, C, D, x, u, chunk)
+
+
+def replicas(items, fn: Callable, group=None):
+    """Config 4 (selective-reset scans do not shard: their reset sites are sequential,
+    scan.py:9-12): independent items — trajectories, systems, seeds — are spread round-robin
+    over the ranks, each processed whole by `fn` on its own GPU, and the results
+    all-gathered (as Python objects) in item order on every rank."""
+    rank, world = _world(group)
+    mine = {i: fn(items[i]) for i in range(rank, len(items), world)}
+    if world == 1:
+        return [mine[i] for i in range(len(items))]
+    parts = [None] * world
+    dist.all_gather_object(parts, mine, group=group)
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    return [merged[i] for i in range(len(items))]

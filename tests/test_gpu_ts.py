@@ -11,8 +11,8 @@ import numpy as np
 import pytest
 import torch
 
-from goom_testlib import (chain_parity, lmme_parity, scaled_real_err, tc_chain_scaled_floor,
-                          to_np)
+from goom_testlib import (chain_kappa, chain_parity, lmme_parity, scaled_real_err,
+                          tc_chain_scaled_floor, to_np)
 from oracle import gooms_port as G
 
 pytestmark = pytest.mark.gpu
@@ -113,29 +113,148 @@ def test_lmme_ts_edge_cases(g, ops):
                                  as_[b:b + 1], bl[b:b + 1], bs[b:b + 1])
         assert err < 1e-4 and flips == 0, (b, err, flips)
     # b = 1: the reference's clamped scales (core.py:252-253: b = max(colmax(B), 0) = 0 for
-    # a B of logs ~ -3000) underflow its exp(B - b) to zero, so it returns -inf everywhere.
-    # The tile-scaled engine scales by the true maxima and returns the finite product:
-    # check it against the oracle on the shifted operands plus the shift.
+    # a B of logs ~ -3000) underflow its exp(B - b) to zero, so it returns -inf everywhere;
+    # the tile-scaled engine keeps Eq. 11's clamp by default and does the same
     assert np.all(wl[1] == -np.inf)
-    sl, ss = G.lmme(al[1:2].astype(np.float64) - 5000.0, as_[1:2].astype(np.float64),
-                    bl[1:2].astype(np.float64) + 3000.0, bs[1:2].astype(np.float64))
-    assert np.isfinite(gl[1]).all()
-    kap = G.cancellation(al[1:2].astype(np.float64) - 5000.0, as_[1:2].astype(np.float64),
-                         bl[1:2].astype(np.float64) + 3000.0, bs[1:2].astype(np.float64))[0]
-    rel = np.abs(gl[1] - (sl[0] + 2000.0)) / np.abs(sl[0] + 2000.0)
+    assert np.all(gl[1] == -np.inf) and np.all(gs[1] == 1)
+
+
+def test_lmme_ts_truemax_opt_in(g, ops):
+    """GOOM_TS_SCALES=truemax (opt-in, read once per process): true-max scales return the
+    finite product where the clamp underflows (checked against the oracle on the shifted
+    operands plus the shift)."""
+    import os
+    import subprocess
+    import sys
+
+    d = 256
+    rng = np.random.default_rng(11)
+    al, as_ = rand_ls(rng, 1, d, d)
+    bl, bs = rand_ls(rng, 1, d, d)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.path.join(root, "gpurun_out", "_truemax.npz")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    np.savez(path, al=al + 5000.0, as_=as_, bl=bl - 3000.0, bs=bs)
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import paper_2510_03426_b200 as goom; from paper_2510_03426_b200 import ops;"
+        "z = np.load(sys.argv[1]);"
+        "A = goom.join(z['al'], z['as_']); B = goom.join(z['bl'], z['bs']);"
+        "out = ops.lmme_ts(ops.ts_from_goom(A), ops.ts_from_goom(B), 0).cpu();"
+        "np.savez(sys.argv[1] + '.out.npz', l=out.real.double().numpy(),"
+        " s=np.where(np.cos(out.imag.double().numpy()) < 0, -1.0, 1.0))")
+    env = dict(os.environ, GOOM_TS_SCALES="truemax")
+    subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True, timeout=300)
+    with np.load(path + ".out.npz") as z:
+        gl, gs = z["l"], z["s"]
+    os.remove(path)
+    os.remove(path + ".out.npz")
+    sl, ss = G.lmme(al.astype(np.float64), as_.astype(np.float64), bl.astype(np.float64),
+                    bs.astype(np.float64))
+    assert np.isfinite(gl).all()
+    kap = G.cancellation(al.astype(np.float64), as_.astype(np.float64), bl.astype(np.float64),
+                         bs.astype(np.float64))[0]
+    rel = np.abs(gl[0] - (sl[0] + 2000.0)) / np.abs(sl[0] + 2000.0)
     assert np.max(np.where(kap >= 1e-2, rel, 0.0)) < 1e-4
-    assert np.all((gs[1] == ss[0]) | (kap < 1e-4))
+    assert np.all((gs[0] == ss[0]) | (kap < 1e-4))
 
 
+def _engine(lib, e):
+    return lib.set_chain_engine(e)
+
+
+@pytest.mark.parametrize("kind", ["shrinking_identity", "gauss_rho_half"])
+def test_ts_clamp_underflows_like_the_reference(g, ops, kind):
+    """Eq. 11's clamp on shrinking chains: 0.55 I and a spectral-radius
+    ~0.5 Gaussian chain, T = 300, d = 256 / 512, next to the d = 128 path. The exact
+    complex64 engine (the public default) and the tile-scaled engine (opt-in) both follow
+    the float64 oracle where its logs are above `hi`, and both return -inf below `lo` — the
+    reference's float32 exp flushes there (its scales are clamped at 0, so the operands'
+    exps underflow; core.py:252-253). 0.55 I is exact in every engine (powers of one scalar,
+    the float32 flush at e^-87.3 falls between steps), so its band is narrow and its -inf
+    pattern is the same for every d and engine."""
+    T, block = 300, 16
+    hi, lo = (-85.0, -105.0) if kind == "shrinking_identity" else (-70.0, -120.0)
+    pats = {}
+    for d in (128, 256, 512):
+        rng = np.random.default_rng(d)
+        if kind == "shrinking_identity":
+            mats = np.broadcast_to(0.55 * np.eye(d), (T, d, d)).copy()
+        else:
+            mats = rng.standard_normal((T, d, d)) * (0.5 / np.sqrt(d))
+        al, as_ = G.log_sign(mats)
+        A = cz(al, as_)
+        want, wsign = G.chain_blocked(al, as_, block)
+        kap = chain_kappa(al, as_, want, wsign)  # entries that are not cancellation noise
+        engines = (0, 1) if d % 256 == 0 else (0,)
+        for e in engines:
+            prev = _engine(g._lib, e)
+            try:
+                gl, gs = to_np(g.scan_chain(A, block_size=block))
+            finally:
+                _engine(g._lib, prev)
+            up = want > hi
+            assert np.isfinite(gl[up]).all(), (d, e)
+            up &= kap >= 1e-2
+            rel = np.abs(gl[up] - want[up]) / np.maximum(1.0, np.abs(want[up]))
+            assert rel.max() < 2e-3, (d, e, rel.max())
+            down = want < lo
+            assert down.any()
+            assert np.all(gl[down] == -np.inf), (d, e, int(np.sum(gl[down] != -np.inf)))
+            if kind == "shrinking_identity":
+                pats[(d, e)] = np.isfinite(np.diagonal(gl, axis1=1, axis2=2)).all(axis=1)
+    if kind == "shrinking_identity":
+        ref = pats[(128, 0)]
+        assert 0 < ref.sum() < T
+        for k, v in pats.items():
+            assert np.array_equal(v, ref), (k, np.flatnonzero(v != ref)[:5])
+
+
+def test_ts_engine_block_flush_is_the_documented_limit(g, ops):
+    """A right-operand column far below the largest entry of its 256-column block while its
+    own column maximum is >= 0 (P_t = diag(e^{3t}, e^{t}, ...)): the reference keeps it (its
+    column scales are per column), the public scan (exact complex64 engine) matches the
+    oracle, and the opt-in tile-scaled engine flushes it once the spread passes ~e^87 —
+    the format limit documented in lmme_ts.cu / DESIGN.md."""
+    d, T, block = 256, 64, 8
+    diag = np.ones(d)
+    diag[0] = np.e ** 3
+    diag[1:] = np.e
+    mats = np.broadcast_to(np.diag(diag), (T, d, d)).copy()
+    al, as_ = G.log_sign(mats)
+    A = cz(al, as_)
+    want, _ = G.chain_blocked(al, as_, block)
+    prev = _engine(g._lib, 0)
+    try:
+        gl, _ = to_np(g.scan_chain(A, block_size=block))
+        _engine(g._lib, 1)
+        tl, _ = to_np(g.scan_chain(A, block_size=block))
+    finally:
+        _engine(g._lib, prev)
+    d1 = np.arange(T)
+    w11 = want[:, 1, 1]
+    assert np.allclose(gl[:, 1, 1], w11, rtol=1e-5)           # exact engine: kept
+    spread = want[:, 0, 0] - want[:, 1, 1]                     # 2 (t + 1) nats
+    assert np.allclose(tl[spread < 60, 1, 1], w11[spread < 60], rtol=1e-5)
+    assert np.all(tl[spread > 110, 1, 1] == -np.inf)           # tile-scaled: flushed
+    assert d1.size == T
+
+
+@pytest.mark.parametrize("engine", [0, 1])
 @pytest.mark.parametrize("d,T,block", [(256, 64, 8), (256, 33, 64), (512, 24, 5), (1024, 6, 2),
                                        (256, 1, 4)])
-def test_chain_ts_matches_float64_oracle(g, ops, d, T, block):
-    """The public chain scan (tile-scaled engine for d % 256 == 0) vs the float64 oracle,
-    calibrated by the reference's own float32 runs (SURVEY §8c chain criterion)."""
+def test_chain_ts_matches_float64_oracle(g, ops, d, T, block, engine):
+    """The public chain scan for d % 256 == 0 on both engines (0: exact complex64 kernels,
+    the default; 1: tile-scaled) vs the float64 oracle, calibrated by the reference's own
+    float32 runs (SURVEY §8c chain criterion)."""
     rng = np.random.default_rng(d * T + block)
     mats = rng.standard_normal((T, d, d))
     al, as_ = G.log_sign(mats)
-    out = g.scan_chain(cz(al, as_), block_size=block)
+    prev = g._lib.set_chain_engine(engine)
+    try:
+        out = g.scan_chain(cz(al, as_), block_size=block)
+    finally:
+        g._lib.set_chain_engine(prev)
     gl, gs = to_np(out)
     want = G.chain_blocked(al, as_, T)
     l32, s32 = G.log_sign(mats.astype(np.float32))

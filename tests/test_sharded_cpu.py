@@ -109,3 +109,135 @@ def test_fold_carry_order():
     assert sharded.fold_carry(["t0", "t1", "t2"], 0, fake) is None
     assert sharded.fold_carry(["t0", "t1", "t2"], 1, fake) == "t0"
     assert sharded.fold_carry(["t0", "t1", "t2"], 3, fake) == "(t2*(t1*t0))"
+
+
+# ---------------------------------------------------------------------------
+# batch-only sharding (configs 2, 5) and replicas (config 4): gloo, world 2 and 3
+
+
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(parts, key=lambda x: x[0])
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _lmme_batch_worker(rank, world, port, q, batch, d):
+    _init(rank, world, port)
+    try:
+        from paper_2510_03426_b200 import sharded
+
+        rng = np.random.default_rng(5)
+        al, as_ = G.log_sign(rng.standard_normal((batch, d, d)))
+        bl, bs = G.log_sign(rng.standard_normal((1, d, d)))  # broadcast right operand
+        A = torch.from_numpy(G.join_complex(al, as_, np.complex128))
+        B = torch.from_numpy(G.join_complex(bl, bs, np.complex128))
+        full = sharded.lmme_batch_sharded(A, B, lmme=oracle_lmme)
+        t0, part = sharded.lmme_batch_sharded(A, B, gather=False, lmme=oracle_lmme)
+        q.put((rank, full.numpy(), t0, part.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,batch", [(2, 6), (3, 7)])
+def test_lmme_batch_sharded_equals_unsharded(world, batch):
+    """Config 2 sharded by batch (uneven shards included): every rank's gathered result
+    equals the one-process batched LMME bitwise, and each slice is the rank's shard."""
+    from paper_2510_03426_b200 import sharded
+
+    d = 4
+    parts = _spawn(_lmme_batch_worker, world, batch, d)
+    rng = np.random.default_rng(5)
+    al, as_ = G.log_sign(rng.standard_normal((batch, d, d)))
+    bl, bs = G.log_sign(rng.standard_normal((1, d, d)))
+    want = G.join_complex(*G.lmme(al, as_, np.broadcast_to(bl, al.shape),
+                                  np.broadcast_to(bs, as_.shape)), np.complex128)
+    for rank, full, t0, part in parts:
+        np.testing.assert_array_equal(full, want)
+        s0, n = sharded.shard_range(batch, rank, world)
+        assert t0 == s0 and part.shape[0] == n
+        np.testing.assert_array_equal(part, want[s0:s0 + n])
+
+
+def _ssm_dp_worker(rank, world, port, q, H, S, T, d):
+    _init(rank, world, port)
+    try:
+        from paper_2510_03426_b200 import sharded
+
+        rng = np.random.default_rng(9)
+        A = torch.tensor(rng.standard_normal((H, d, d)), requires_grad=True)
+        us = torch.tensor(rng.standard_normal((H, S, T, d)))
+        x0s = torch.tensor(rng.standard_normal((H, S, d)))
+        s0, x, u = sharded.ssm_sequences_shard(x0s, us)
+        # a stand-in for the GOOM layer with the same data-parallel structure: per-sequence
+        # outputs depending on the shared parameter, loss summed over the batch
+        y = torch.einsum("hij,hstj->hsti", A, u) + x[:, :, None, :]
+        (y ** 2).sum().backward()
+        sharded.allreduce_grads([A])
+        q.put((rank, s0, x.shape[1], A.grad.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ssm_sequence_sharding_gradients_sum(world):
+    """Config 5 data parallelism: sequences split over the ranks (heads share A's powers),
+    the one collective is the gradient all-reduce; every rank ends with the full-batch
+    gradient."""
+    H, S, T, d = 2, 5, 3, 4
+    parts = _spawn(_ssm_dp_worker, world, H, S, T, d)
+    rng = np.random.default_rng(9)
+    A = torch.tensor(rng.standard_normal((H, d, d)), requires_grad=True)
+    us = torch.tensor(rng.standard_normal((H, S, T, d)))
+    x0s = torch.tensor(rng.standard_normal((H, S, d)))
+    y = torch.einsum("hij,hstj->hsti", A, us) + x0s[:, :, None, :]
+    (y ** 2).sum().backward()
+    covered = 0
+    for rank, s0, n, g in parts:
+        assert s0 == covered
+        covered += n
+        np.testing.assert_allclose(g, A.grad.numpy(), rtol=1e-12, atol=1e-10)
+    assert covered == S
+
+
+def _replica_worker(rank, world, port, q, items):
+    _init(rank, world, port)
+    try:
+        from paper_2510_03426_b200 import sharded
+
+        seen = []
+
+        def fn(x):
+            seen.append(x)
+            return {"item": x, "square": x * x}
+
+        out = sharded.replicas(items, fn)
+        q.put((rank, out, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_replicas_round_robin(world):
+    """Config 4 replicas: each item is processed exactly once, round-robin over the ranks,
+    and every rank gets all results in item order."""
+    items = list(range(7))
+    parts = _spawn(_replica_worker, world, items)
+    processed = sorted(x for _, _, seen in parts for x in seen)
+    assert processed == items
+    for rank, out, seen in parts:
+        assert seen == items[rank::world]
+        assert out == [{"item": x, "square": x * x} for x in items]
