@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=128, help="leaves in the CPU baseline sample")
     p.add_argument("--e2e-T", type=int, default=8192)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-reanchor", action="store_true", help="skip the re-anchored checks")
     return p.parse_args()
 
 
@@ -231,7 +232,7 @@ def main():
     W = min(REANCHOR_W, args.block)
     anchors = sorted({(a // args.block) * args.block for a in (T // 2, T - W - 1)
                       if a >= args.block})
-    anchors = [a for a in anchors if a + W <= T]
+    anchors = [a for a in anchors if a + W <= T and not args.no_reanchor]
     snaps = sorted({a + W - 1 for a in anchors})
 
     def one_step():

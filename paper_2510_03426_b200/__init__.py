@@ -33,7 +33,7 @@ from .core import (  # noqa: F401
 )
 from .lyapunov import (JacobianChain, SpectrumResult, colinearity_policy,  # noqa: F401
                        colinearity_select, lle_parallel, lle_sequential, orthonormal_reset,
-                       load_jacobian_chain, qr_factor_batched, save_jacobian_chain,
+                       load_jacobian_chain, qr_factor, qr_factor_batched, save_jacobian_chain,
                        spectrum_parallel, spectrum_sequential)
 from .scan import (  # noqa: F401
     ResetPolicy,

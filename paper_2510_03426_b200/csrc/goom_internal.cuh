@@ -175,5 +175,10 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
 template <class R>
 int chain_scan_small(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int64_t s,
                      const Cx<R>* carry_in, Cx<R>* L, Cx<R>* Cx_, cudaStream_t st);
+// 32 < d <= 64 CTA-resident variant (scan_cta.cu), same tree and bitwise the same products
+bool chain_cta_eligible(int d);
+template <class R>
+int chain_scan_cta(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int64_t s,
+                   const Cx<R>* carry_in, Cx<R>* L, Cx<R>* Cx_, cudaStream_t st);
 
 }  // namespace goom

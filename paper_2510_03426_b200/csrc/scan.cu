@@ -101,6 +101,16 @@ int chain_engine() {
   }
   return v;
 }
+// GOOM_CHAIN_CTA=0 routes 32 < d <= 64 chains through the batched launches instead of the
+// CTA-resident walks (bitwise-equality tests compare the two)
+bool chain_cta_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("GOOM_CHAIN_CTA");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 bool chain_ts_path(int d) {
   return chain_engine() == 1 && lmme_backend() != 1 && lmme_ts_eligible(d, d, d);
 }
@@ -237,6 +247,9 @@ int chain_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int block, const Cx
 
   // d <= 32: the warp-resident scan (scan_small.cu), same tree, three launches
   if (d <= 32) return chain_scan_small<R>(A, out, T, d, s, carry_in, L, Cx_, st);
+  // 32 < d <= 64: the CTA-resident walks (scan_cta.cu), three launches
+  if (chain_cta_eligible(d) && !chain_cta_disabled())
+    return chain_scan_cta<R>(A, out, T, d, s, carry_in, L, Cx_, st);
 
   // phase 1: L[k*s] = A[k*s]; L[k*s+i] = A[k*s+i] (x) L[k*s+i-1]
   GOOM_TRY(copy_strided(L, A, mat, mat * s, nb, st, "chain phase-1 copy"));

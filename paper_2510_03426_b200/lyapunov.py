@@ -104,6 +104,27 @@ def _stream():
 
 
 def qr_factor_batched(ms):
+    """Householder QR over a stack with diag(R) >= 0 (lyapunov.py:79-99), the reference's
+    return: (Q, R) float64 numpy stacks. Q and |diag R| come from the batched GPU kernel
+    (goom_qr_batched_f64, d <= 64); R = triu(Q^T M) by one batched FP64 product."""
+    m = torch.as_tensor(np.asarray(ms, dtype=np.float64), device=_dev()).contiguous()
+    q, _ = _qr_device(m)
+    r = torch.triu(torch.bmm(q.transpose(1, 2), m))
+    return q.cpu().numpy(), r.cpu().numpy()
+
+
+def qr_factor(m):
+    """Householder QR of one square matrix with R[i, i] >= 0 (lyapunov.py:54-76)."""
+    a = np.array(m, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("expected a square matrix")
+    if not np.isfinite(a).all():
+        raise ValueError("non-finite entries")
+    q, r = qr_factor_batched(a[None])
+    return q[0], r[0]
+
+
+def _qr_device(ms):
     """Householder QR over a stack with diag(R) >= 0 (lyapunov.py:79-99) on the GPU:
     returns (Q, |diag R|) as float64 CUDA tensors (d <= 64)."""
     m = torch.as_tensor(ms, dtype=torch.float64, device=_dev()).contiguous()
@@ -151,7 +172,7 @@ def spectrum_parallel(chain, s0=None, colinearity_threshold=0.99, check_interval
     # (c) output states J_t Q_{t-1}
     outputs = torch.bmm(mats, bases)
     # (d) exponents from the triangular factors
-    _, diag = qr_factor_batched(outputs)
+    _, diag = _qr_device(outputs)
     if bool((diag == 0.0).any()):
         raise ValueError("degenerate Jacobian chain")
     lam = (torch.log(diag).mean(dim=0) / chain.dt).cpu().numpy()
@@ -166,10 +187,10 @@ def spectrum_sequential(chain, s0=None) -> SpectrumResult:
     start = time.perf_counter()
     dev = _dev()
     mats = torch.as_tensor(chain.mats, dtype=torch.float64, device=dev)
-    q, _ = qr_factor_batched(torch.as_tensor(s0, device=dev)[None])
+    q, _ = _qr_device(torch.as_tensor(s0, device=dev)[None])
     acc = torch.zeros(chain.dim, dtype=torch.float64, device=dev)
     for t in range(chain.T):
-        q, diag = qr_factor_batched((mats[t] @ q[0])[None])
+        q, diag = _qr_device((mats[t] @ q[0])[None])
         if bool((diag == 0.0).any()):
             raise ValueError(f"degenerate Jacobian chain at step {t}")
         acc += torch.log(diag[0])

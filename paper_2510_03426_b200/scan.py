@@ -150,7 +150,7 @@ class SelectiveCombiner:
             value = self.policy.reset(tested)
             if value.shape != tested.shape:
                 raise ValueError("reset must preserve the state's shape")
-            return ScanPair(GoomMatrix.zeros(prev.A.rows, prev.A.cols), value, True)
+            return ScanPair(GoomMatrix.zeros(prev.A.rows, prev.A.cols, dtype=prev.A.dtype), value, True)
         return combine_affine(prev, curr)
 
 
@@ -163,16 +163,51 @@ def combine_selective(policy):
 
 
 class _Stack:
-    """Scan elements as stacked complex64 CUDA tensors (scan.py:138-170)."""
+    """Scan elements as stacked complex CUDA tensors (scan.py:138-170).
 
-    __slots__ = ("A", "B", "flags")
+    Two constructors: `_Stack(A, B, flags)` with complex tensors (this package's form) and
+    the reference's `_Stack(alog, asign, blog, bsign, flags)` with numpy arrays (float64 ->
+    complex128), as its callers build it (lyapunov.py:422, ssm.py:142). A stack built from
+    numpy arrays hands numpy back from `.alog` / `.asign` / `.blog` / `.bsign` / `.flags`,
+    and so do the stacks the scans derive from it."""
 
-    def __init__(self, A, B, flags=None):
+    __slots__ = ("A", "B", "_flags", "host")
+
+    def __init__(self, *args):
+        self.host = False
+        if len(args) == 5:
+            alog, asign, blog, bsign, flags = args
+            src = _Stack.from_arrays(alog, asign, blog, bsign, flags)
+            A, B, flags = src.A, src.B, src._flags
+            self.host = isinstance(alog, np.ndarray)
+        elif len(args) in (2, 3):
+            A, B = args[0], args[1]
+            flags = args[2] if len(args) == 3 else None
+        else:
+            raise TypeError("_Stack(A, B[, flags]) or _Stack(alog, asign, blog, bsign, flags)")
         self.A = A
         self.B = B
         if flags is None:
             flags = torch.zeros(A.shape[0], dtype=torch.bool, device=A.device)
-        self.flags = flags
+        elif not isinstance(flags, torch.Tensor):
+            flags = torch.as_tensor(np.asarray(flags), dtype=torch.bool, device=A.device)
+        self._flags = flags
+
+    @property
+    def flags(self):
+        return self._flags.cpu().numpy() if self.host else self._flags
+
+    @flags.setter
+    def flags(self, v):
+        self._flags = v
+
+    def _derived(self, A, B, flags):
+        out = _Stack(A, B, flags)
+        out.host = self.host
+        return out
+
+    def _view(self, t):
+        return t.cpu().numpy() if self.host else t
 
     @classmethod
     def from_arrays(cls, alog, asign, blog, bsign, flags=None, dtype=None):
@@ -193,36 +228,36 @@ class _Stack:
         return cls(A, B, f)
 
     def to_pairs(self):
-        flags = self.flags.cpu().tolist()
+        flags = self._flags.cpu().tolist()
         return [ScanPair(GoomMatrix._wrap(self.A[i]), GoomMatrix._wrap(self.B[i]), bool(flags[i]))
                 for i in range(len(flags))]
 
     @property
     def alog(self):
-        return split(self.A)[0]
+        return self._view(split(self.A)[0])
 
     @property
     def asign(self):
-        return split(self.A)[1]
+        return self._view(split(self.A)[1])
 
     @property
     def blog(self):
-        return split(self.B)[0]
+        return self._view(split(self.B)[0])
 
     @property
     def bsign(self):
-        return split(self.B)[1]
+        return self._view(split(self.B)[1])
 
     def states(self):
         """Per-element compound state (B after a reset, else A); square B only."""
-        return torch.where(self.flags[:, None, None], self.B, self.A)
+        return torch.where(self._flags[:, None, None], self.B, self.A)
 
     def __len__(self):
         return self.A.shape[0]
 
 
 def _all_zero_bias(stack: _Stack) -> bool:
-    return (not bool(stack.flags.any())) and bool((stack.B.real == NEG_INF).all())
+    return (not bool(stack._flags.any())) and bool((stack.B.real == NEG_INF).all())
 
 
 def _scan_affine_stack(stack: _Stack, block_size: int) -> _Stack:
@@ -231,9 +266,9 @@ def _scan_affine_stack(stack: _Stack, block_size: int) -> _Stack:
         raise ValueError("block_size must be >= 1")
     if _all_zero_bias(stack):
         A = torch.ops.goom.scan_chain(stack.A, int(block_size), None)
-        return _Stack(A, stack.B.clone(), stack.flags.clone())
-    A, B, f = torch.ops.goom.scan_affine(stack.A, stack.B, stack.flags, int(block_size))
-    return _Stack(A, B, f.bool())
+        return stack._derived(A, stack.B.clone(), stack._flags.clone())
+    A, B, f = torch.ops.goom.scan_affine(stack.A, stack.B, stack._flags, int(block_size))
+    return stack._derived(A, B, f.bool())
 
 
 def scan_chain(A: torch.Tensor, block_size: int = 64, carry: Optional[torch.Tensor] = None):
@@ -274,25 +309,35 @@ def _selective_chain_core(A, *args):
             A, int(policy.kind), int(policy.check_interval), bool(policy.consume_leaf),
             float(policy.threshold), float(policy.log_volume_floor), int(block_size))
         return V, [int(s) for s in sites.cpu().tolist()]
-    return _selective_chain_host(A, policy)
+    return _selective_chain_host(A, policy, block_size)
 
 
-def _selective_chain_host(A: torch.Tensor, policy: ResetPolicy):
-    """Sequential selective fold for host-callable policies; combines on the GPU.
-    Same value-determined sites as the reference's tile walks (scan.py:9-12)."""
-    T, d = A.shape[0], A.shape[-1]
-    V = torch.empty_like(A)
-    V[0] = A[0]
+def _selective_chain_host(A: torch.Tensor, policy: ResetPolicy, block_size: int):
+    """Selective chain for host-callable policies; every combine on the GPU, the
+    predicate / reset on the host. Until the first fire the states are the blocked chain
+    scan with the walk's tile (`block_size` for check_interval 1, else check_interval;
+    scan.py:356-358) — the reference's tile walk computes exactly that tree (local
+    products (x) the previous tile's last state), so a policy that never fires gives the
+    affine scan bitwise (test_scan.py:255-265). After a fire at site q the rest is rescanned
+    from the reset state. Sites are the value-determined ones of the reference
+    (scan.py:9-12)."""
+    T = A.shape[0]
+    tile = int(block_size) if policy.check_interval == 1 else int(policy.check_interval)
+    V = torch.ops.goom.scan_chain(A, tile, None)
     sites = []
-    for t in range(1, T):
-        if _tested(t - 1, policy.check_interval):
-            tested = GoomMatrix._wrap(V[t - 1])
-            if policy.select(tested):
-                value = policy.reset(tested).data
-                V[t] = value if policy.consume_leaf else torch.ops.goom.lmme(A[t], value)
-                sites.append(t)
-                continue
-        V[t] = torch.ops.goom.lmme(A[t], V[t - 1])
+    p = 0
+    while p <= T - 2:
+        if _tested(p, policy.check_interval) and policy.select(GoomMatrix._wrap(V[p])):
+            q = p + 1
+            value = policy.reset(GoomMatrix._wrap(V[p])).data
+            V[q] = value if policy.consume_leaf else torch.ops.goom.lmme(A[q], value)
+            sites.append(q)
+            if q + 1 < T:
+                V[q + 1:] = torch.ops.goom.scan_chain(A[q + 1:].contiguous(), tile,
+                                                      V[q].contiguous())
+            p = q
+            continue
+        p += 1
     return V, sites
 
 
@@ -308,7 +353,7 @@ def _selective_tiled(stack: _Stack, policy: ResetPolicy, block_size: int):
         flags[f:] = True
         A[f:] = complex(NEG_INF, 0.0)
         B[f:] = V[f:]
-    return _Stack(A, B, flags), sites
+    return stack._derived(A, B, flags), sites
 
 
 def _select_positions(states: torch.Tensor, policy: ResetPolicy) -> torch.Tensor:
@@ -337,7 +382,7 @@ def _selective_rounds(stack: _Stack, policy: ResetPolicy, block_size: int):
         fired = None
         if cand:
             idx = torch.tensor(cand, device=out.A.device)
-            st = torch.where(out.flags[idx][:, None, None], out.B[idx], out.A[idx])
+            st = torch.where(out._flags[idx][:, None, None], out.B[idx], out.A[idx])
             fire = _select_positions(st, policy).cpu().numpy()
             hits = np.flatnonzero(fire)
             if hits.size:
@@ -345,7 +390,7 @@ def _selective_rounds(stack: _Stack, policy: ResetPolicy, block_size: int):
         if fired is None:
             break
         q = fired + 1
-        tested = out.B[fired] if bool(out.flags[fired]) else out.A[fired]
+        tested = out.B[fired] if bool(out._flags[fired]) else out.A[fired]
         value = policy.reset(GoomMatrix._wrap(tested)).data
         sites.append(q)
         if policy.consume_leaf:
@@ -354,11 +399,11 @@ def _selective_rounds(stack: _Stack, policy: ResetPolicy, block_size: int):
         else:
             out.A[q] = torch.ops.goom.lmme(stack.A[q], torch.full_like(value, complex(NEG_INF, 0)))
             out.B[q] = torch.ops.goom.lmme_gadd(stack.A[q], value, stack.B[q])
-        out.flags[q:] = True
+        out._flags[q:] = True
         if q == T - 1:
             break
         suffix = _Stack(torch.cat([out.A[q:q + 1], stack.A[q + 1:]]),
-                        torch.cat([out.B[q:q + 1], stack.B[q + 1:]]), out.flags[q:].clone())
+                        torch.cat([out.B[q:q + 1], stack.B[q + 1:]]), out._flags[q:].clone())
         sc = _scan_affine_stack_full(suffix, block_size)
         out.A[q:] = sc.A
         out.B[q:] = sc.B
@@ -367,7 +412,7 @@ def _selective_rounds(stack: _Stack, policy: ResetPolicy, block_size: int):
 
 
 def _scan_affine_stack_full(stack: _Stack, block_size: int) -> _Stack:
-    A, B, f = torch.ops.goom.scan_affine(stack.A, stack.B, stack.flags, int(block_size))
+    A, B, f = torch.ops.goom.scan_affine(stack.A, stack.B, stack._flags, int(block_size))
     return _Stack(A, B, f.bool())
 
 
@@ -381,7 +426,7 @@ def _selective_sequential_pairs(leaves, policy):
             tested = prev.state
             if policy.select(tested):
                 value = policy.reset(tested)
-                reset_pair = ScanPair(GoomMatrix.zeros(prev.A.rows, prev.A.cols), value, True)
+                reset_pair = ScanPair(GoomMatrix.zeros(prev.A.rows, prev.A.cols, dtype=prev.A.dtype), value, True)
                 out.append(reset_pair if policy.consume_leaf else combine_affine(reset_pair, leaves[t]))
                 sites.append(t)
                 continue

@@ -112,8 +112,8 @@ def test_harness_snapshots_equal_full_window_output(h):
     d, T, block = 256, 96, 16
     L = ops.ts_random_normal(T, d, 5, 0, torch.device("cuda"))
     P, _, _ = ops.chain_ts(L, block, None, out=True, digests=False, carry_out=False)
-    _, _, _, S = ops.chain_ts(L, block, None, digests=True, carry_out=False,
-                              snapshots=[0, 15, 16, 95])
+    _, _, _, S, _ = ops.chain_ts(L, block, None, digests=True, carry_out=False,
+                                 snapshots=[0, 15, 16, 95])
     S64 = ops.ts_to_goom(S)
     for j, t in enumerate([0, 15, 16, 95]):
         # the same product through the tile-scaled epilogue, exported: equal to the complex64

@@ -26,10 +26,12 @@ def test_qr_factor_batched_matches_reference(g):
     only its leading columns, orthonormality and |diag R| are compared; the zero matrix
     (index 4) gives Q = I, R = 0 in both."""
     z = load_golden("qr_batched")
-    q, diag = g.qr_factor_batched(z["ms"])
-    q = q.cpu().numpy()
+    q, r = g.qr_factor_batched(z["ms"])  # the reference's return: (Q, R) numpy
     want_diag = np.abs(np.diagonal(z["r"], axis1=1, axis2=2))
-    got_diag = diag.cpu().numpy()
+    got_diag = np.diagonal(r, axis1=1, axis2=2)
+    assert np.all(got_diag >= 0)
+    for b in (0, 1, 2, 4, 5):
+        np.testing.assert_allclose(r[b], z["r"][b], rtol=0, atol=1e-12)
     for b in (0, 1, 2, 4, 5):
         np.testing.assert_allclose(got_diag[b], want_diag[b], rtol=0, atol=1e-12)
     np.testing.assert_allclose(got_diag[3][:3], want_diag[3][:3], rtol=0, atol=1e-12)

@@ -401,3 +401,75 @@ def test_parallel_beats_sequential_on_wide_chain(g):
     sl = seq.A[-1].real.cpu().numpy()
     assert G.rel_log_diff(pl, sl) < 1e-10
     assert t_seq / t_par >= 2.0, (t_seq, t_par)
+
+
+# ---------------------------------------------------------------------------
+# CTA-resident chain scan, 32 < d <= 64 (scan_cta.cu)
+
+
+@pytest.mark.parametrize("d,T,block", [(64, 300, 16), (48, 97, 10), (33, 64, 64), (64, 1, 4),
+                                       (40, 130, 128)])
+def test_chain_cta_matches_float64_oracle(g, d, T, block):
+    """The CTA-resident walks (phase 1 and the carry fold in shared memory, the carry
+    applied once per block) vs the float64 oracle of the same tree, calibrated by the
+    reference's own float32 runs (SURVEY §8c chain criterion)."""
+    rng = np.random.default_rng(d * 1000 + T)
+    mats = rng.standard_normal((T, d, d))
+    al, as_ = G.log_sign(mats)
+    out = g.scan_chain(cz(al, as_), block_size=block)
+    gl, gs = to_np(out)
+    want = G.chain_blocked(al, as_, block)
+    l32, s32 = G.log_sign(mats.astype(np.float32))
+    refs = [G.chain_blocked(l32, s32, block), G.chain_blocked(l32, s32, T)]
+    r = chain_parity(gl, gs, al, as_, want, refs)
+    assert r["ok"], (r["bad"], r["flips"], r["scaled_bad"])
+
+
+def test_chain_cta_complex128_and_carry(g):
+    """complex128 (FP64) walks vs the float64 oracle at 1e-10, with and without a carry."""
+    d, T, block = 64, 80, 8
+    rng = np.random.default_rng(77)
+    al, as_ = G.log_sign(rng.standard_normal((T, d, d)))
+    cl, cs = G.log_sign(rng.standard_normal((d, d)))
+    A = g.join(al, as_, np.float64)
+    out = torch.ops.goom.scan_chain(A, block, None)
+    gl = out.real.cpu().numpy()
+    want, wsign = G.chain_blocked(al, as_, block)
+    assert G.rel_log_diff(gl, want) < 1e-10
+    outc = torch.ops.goom.scan_chain(A, block, g.join(cl, cs, np.float64))
+    wl, _ = G.lmme(want, wsign, np.broadcast_to(cl, want.shape), np.broadcast_to(cs, want.shape))
+    assert G.rel_log_diff(outc.real.cpu().numpy(), wl) < 1e-9
+
+
+def test_chain_cta_bitwise_equals_batched_launches(g):
+    """Same products, same arithmetic (lmme_whole_kernel's): the CTA-resident engine is
+    bitwise equal to the batched per-step launches (GOOM_CHAIN_CTA=0), complex64 and
+    complex128, with and without a carry."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import paper_2510_03426_b200 as g;"
+        "rng = np.random.default_rng(5); outs = [];\n"
+        "for d, T, blk, dt in ((64, 200, 16, np.float32), (48, 77, 9, np.float32),"
+        " (64, 50, 8, np.float64)):\n"
+        "    x = rng.standard_normal((T, d, d)); c = rng.standard_normal((d, d))\n"
+        "    A = torch.ops.goom.from_real(torch.tensor(x).cuda(), float('-inf'), dt == np.float64)\n"
+        "    C = torch.ops.goom.from_real(torch.tensor(c).cuda(), float('-inf'), dt == np.float64)\n"
+        "    outs += [torch.view_as_real(torch.ops.goom.scan_chain(A, blk, None)).cpu(),"
+        " torch.view_as_real(torch.ops.goom.scan_chain(A, blk, C)).cpu()]\n"
+        "torch.save(outs, sys.argv[1])")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for flag in ("0", "1"):
+        path = os.path.join(root, "gpurun_out", f"_cta_{flag}.pt")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        env = dict(os.environ, GOOM_CHAIN_CTA=flag)
+        subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True,
+                       timeout=300)
+        res.append(torch.load(path))
+        os.remove(path)
+    for a, b in zip(*res):
+        assert torch.equal(a, b)

@@ -25,7 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--T", type=int, default=100_000)
     ap.add_argument("--d", type=int, default=64)
-    ap.add_argument("--T-cpu", type=int, default=4000)
+    ap.add_argument("--T-cpu", type=int, default=100_000, help="oracle prefix (default: all)")
+    ap.add_argument("--sites-only", action="store_true",
+                    help="print the GPU reset sites (JSON) and exit (direct-volume A/B)")
     args = ap.parse_args()
     import torch
 
@@ -40,6 +42,10 @@ def main():
 
     pol = g.colinearity_policy(0.99, 12, 1e-9)
     A = g.join(al, as_, torch.complex128)
+    if args.sites_only:
+        _, sites = g._selective_chain_core(A, pol, 256)
+        print(json.dumps({"sites": sites}))
+        return
     g._selective_chain_core(A[:64], pol, 256)  # warm-up
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -71,6 +77,15 @@ def main():
     vs = np.where(np.cos(Vp.imag.cpu().numpy()) < 0, -1.0, 1.0)
     c = Vc.max(axis=(1, 2), keepdims=True)
     err = np.abs(vs * np.exp(vl - c) - Sc * np.exp(Vc - c)).max()
+    margins = decision_margins(Vc, Sc, 12, 0.99, 1e-9)
+    # the walk's volume test by determinant multiplicativity vs a direct factorisation of
+    # every tested state (GOOM_WALK_DIRECT_VOLUME=1): same sites?
+    import subprocess
+    env = dict(os.environ, GOOM_WALK_DIRECT_VOLUME="1")
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--T", str(args.T), "--d",
+                          str(args.d), "--sites-only"], env=env, capture_output=True, text=True,
+                         timeout=1800)
+    direct_sites = json.loads(out.stdout.strip().splitlines()[-1])["sites"]
     print(json.dumps({
         "config": "lyapunov_lorenz96_selective", "d": args.d, "T": args.T,
         "policy": "colinearity(0.99, interval 12, volume 1e-9), consume_leaf=False",
@@ -83,7 +98,41 @@ def main():
         "cpu_cores": os.cpu_count(), "cpu_kind": "port (oracle/gooms_port.selective_chain, float64)",
         "sites_identical_on_prefix": sites_pref == sites_cpu, "prefix_resets": len(sites_cpu),
         "prefix_max_scaled_err": float(err),
+        "sites_identical_full_length": sites == sites_cpu if Tc == args.T else None,
+        "decision_margins": margins,
+        "direct_volume_sites_identical": direct_sites == sites,
     }), flush=True)
+
+
+def decision_margins(V, Sg, interval, threshold, volume_floor):
+    """For every tested state of the oracle's run (positions p with (p+1) % interval == 0,
+    lyapunov.py:255-269): the distance of max |cos| to the threshold and of log|det| of the
+    unit-column state to log(volume_floor) — how close the reference's own decisions are to
+    flipping (a GPU decision can only differ from the reference's inside rounding of these)."""
+    T = V.shape[0]
+    tested = np.array([p for p in range(T - 1) if (p + 1) % interval == 0])
+    cos_m, vol_m = [], []
+    fired = []
+    for i in range(0, len(tested), 512):
+        idx = tested[i:i + 512]
+        lg, sg = V[idx], Sg[idx]
+        top = lg.max(axis=1, keepdims=True)
+        nu = top + 0.5 * np.log(np.sum(np.exp(2.0 * (lg - top)), axis=1, keepdims=True))
+        real = sg * np.exp(lg - nu)
+        gram = np.einsum("nki,nkj->nij", real, real)
+        iu, ju = np.triu_indices(gram.shape[1], k=1)
+        mx = np.abs(gram[:, iu, ju]).max(axis=1)
+        sgn, ld = np.linalg.slogdet(real)
+        cos_m.append(mx - threshold)
+        vol_m.append(ld - np.log(volume_floor))
+        fired.append((mx > threshold) | (sgn == 0) | (ld < np.log(volume_floor)))
+    cos_m, vol_m, fired = np.concatenate(cos_m), np.concatenate(vol_m), np.concatenate(fired)
+    return {"tested": int(len(tested)), "fired": int(fired.sum()),
+            "min_abs_cos_margin": float(np.abs(cos_m).min()),
+            "min_abs_logvol_margin": float(np.abs(vol_m).min()),
+            "fired_by_cos": int((cos_m > 0).sum()), "fired_by_volume": int((vol_m < 0).sum()),
+            "within_1e-6_cos": int((np.abs(cos_m) < 1e-6).sum()),
+            "within_1e-6_logvol": int((np.abs(vol_m) < 1e-6).sum())}
 
 
 if __name__ == "__main__":
