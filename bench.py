@@ -57,24 +57,70 @@ def parse():
 # CPU baseline: the reference algorithm (numpy restatement, oracle/gooms_port.py)
 
 
-def cpu_chain_rate(d: int, T: int, seed: int):
-    """Time the reference's blocked chain (A slot of _scan_affine_stack, scan.py:181-214)
-    in float64 — the reference's default backing — on T random-normal leaves."""
+def cpu_chain_rate(d: int, T: int, seed: int, dtype="float32", stock=False):
+    """Time the reference's blocked scan (scan.py:181-214) on T random-normal leaves.
+    dtype "float32": the reference's own float32 path (dtype preserved end to end; the
+    precision the GPU's complex64 computes at) — the fastest CPU variant, the headline
+    baseline; "float64": its default backing. stock=False times the A slot only (the
+    product chain, 2 LMMEs/element at the block tree); stock=True the stock
+    _scan_affine_stack on (A, zero-bias) pairs as scan_parallel runs it, bias LMMEs
+    included (scan.py:173-178)."""
     import numpy as np
 
     from oracle import gooms_port as G
 
     rng = np.random.default_rng(seed)
-    al, as_ = G.log_sign(rng.standard_normal((T, d, d)))
-    G.chain_blocked(al[:4], as_[:4], 2)  # warm BLAS
+    al, as_ = G.log_sign(rng.standard_normal((T, d, d)).astype(dtype))
+
+    def run(a, s, blk):
+        if not stock:
+            return G.chain_blocked(a, s, blk)
+        st = G.Stack(a, s, np.full(a.shape, -np.inf, dtype=a.dtype), np.ones_like(s),
+                     np.zeros(a.shape[0], dtype=bool))
+        return G.scan_affine_blocked(st, blk)
+
+    run(al[:4], as_[:4], 2)  # warm BLAS
     t0 = time.perf_counter()
-    G.chain_blocked(al, as_, 32)
+    run(al, as_, 32)
     dt = time.perf_counter() - t0
     return T / dt, dt
 
 
 def cpu_cores():
     return os.cpu_count() or 1
+
+
+def cpu_info():
+    """Host CPU model, core count and the BLAS numpy runs on."""
+    import numpy as np
+
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '?')} {b.get('version', '')}".strip()
+    except Exception:  # pragma: no cover
+        pass
+    return {"nproc": cpu_cores(), "cpu_model": model, "blas": blas}
+
+
+def cpu_variants(d: int, T: int, seed: int):
+    """The CPU baseline beside its variants: float32 / float64, chain-only / stock."""
+    out = {}
+    for name, dt, stock in (("float32_chain", "float32", False), ("float64_chain", "float64", False),
+                            ("float64_stock_affine", "float64", True)):
+        r, s = cpu_chain_rate(d, T, seed, dt, stock)
+        out[name] = {"matrices_per_s": r, "seconds": round(s, 2)}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -179,13 +225,15 @@ def reference_arm(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": T / v * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic N(0,1) leaves",
         "config": {"workload": f"chain d={args.d}, sample of T={T} leaves of the T={args.T} chain",
                    "d": args.d, "T": args.T, "sample_T": T, "block": 32},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-                         "sample": f"{T} leaves, reference blocked chain (scan.py:181-214) in "
-                                   f"float64 via oracle/gooms_port.chain_blocked"},
+                         "sample": f"{T} leaves, the reference's float32 blocked chain "
+                                   f"(scan.py:181-214, its fastest CPU variant and the GPU's "
+                                   f"precision) via oracle/gooms_port.chain_blocked",
+                         "host": cpu_info(), "variants": cpu_variants(args.d, T, args.seed)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -421,8 +469,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt = cpu_chain_rate(d, args.cpu_sample, args.seed)
         cpu = {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": f"{args.cpu_sample} leaves of 512x512, reference blocked chain "
-                         f"(scan.py:181-214) in float64 via oracle/gooms_port, {dt:.1f} s"}
+               "sample": f"{args.cpu_sample} leaves of {d}x{d}, the reference's float32 "
+                         f"blocked chain (scan.py:181-214; its fastest CPU variant, the GPU's "
+                         f"precision) via oracle/gooms_port, {dt:.1f} s",
+               "host": cpu_info(), "variants": cpu_variants(d, args.cpu_sample, args.seed)}
 
     if rank == 0:
         line = {

@@ -193,6 +193,16 @@ def _bu_panels(B: torch.Tensor, u: torch.Tensor, L: int) -> torch.Tensor:
     return out.view(H, L, d, N).transpose(0, 1)                         # (L, H, d, N)
 
 
+def _max_normalised(M: torch.Tensor, shift: torch.Tensor):
+    """(M - m, shift + m) per leading index with m = max finite log of M (0 for an
+    all-zero matrix): the same GOOM matrices with their largest entry at log 0."""
+    m = M.real.amax(dim=(-2, -1))
+    m = torch.where(torch.isfinite(m), m, torch.zeros_like(m))
+    out = M.clone()
+    out.real.sub_(m.view(-1, 1, 1))
+    return out, shift + m
+
+
 def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: int,
                   bi: Optional[torch.Tensor] = None, panels: bool = False):
     """x_t = A (x) x_{t-1} (+) b_t for H heads x S sequences with the powers of A shared by
@@ -239,20 +249,26 @@ def _chunked_scan(Ag: torch.Tensor, b: torch.Tensor, s0: torch.Tensor, chunk: in
         k += m
     # chunk-entry states s_c = A^L (x) s_{c-1} (+) y_{c-1, L-1} by a Hillis-Steele scan over
     # the chunks (log2 nC rounds of one batched LMME each, with A^L, A^2L, A^4L, ...) instead
-    # of nC - 1 sequential launches of H products
+    # of nC - 1 sequential launches of H products. The powers A^(L 2^j) are kept max-
+    # normalised with their log shift carried per head: squaring a contractive A^L under the
+    # LMME's 0-clamped scales (core.py:252-253) would otherwise underflow to all -inf once
+    # ||A^(L 2^j)|| < e^-745 and silently drop the A^(L off) (x) s term, which the
+    # sequential recurrence keeps whenever the product itself is representable.
     cur = torch.empty((H, nC, d, S), dtype=torch.complex128, device=dev)
     cur[:, 0] = s0.transpose(1, 2)
     cur[:, 1:] = Y[L - 1].reshape(H, d, S, nC).permute(0, 3, 1, 2)[:, :nC - 1]
-    Mp = P[:, L - 1].contiguous()
+    Mp, shift = _max_normalised(P[:, L - 1].contiguous(), torch.zeros(H, dtype=torch.float64,
+                                                                       device=dev))
     off = 1
     while off < nC:
         n = nC - off
-        nxt = ops.lmme_indexed(Mp, n, cur[:, :n].reshape(H * n, d, S), 1, H * n,
-                               cur[:, off:].reshape(H * n, d, S))
-        cur[:, off:] = nxt.view(H, n, d, S)  # stream-ordered after the reads above
+        t = ops.lmme_indexed(Mp, n, cur[:, :n].reshape(H * n, d, S), 1, H * n).view(H, n, d, S)
+        t.real.add_(shift.view(H, 1, 1, 1))
+        nxt = torch.ops.goom.gadd(t, cur[:, off:])
+        cur[:, off:] = nxt  # stream-ordered after the reads above
         off *= 2
         if off < nC:
-            Mp = ops.lmme_indexed(Mp, 1, Mp, 1, H)
+            Mp, shift = _max_normalised(ops.lmme_indexed(Mp, 1, Mp, 1, H), 2.0 * shift)
     S_all = cur.permute(0, 2, 3, 1).reshape(H, d, N)                    # (H, d, S nC)
     Yh = Y.permute(1, 0, 2, 3).reshape(H * L, d, N)                     # batch index h L + i
     X = ops.lmme_indexed(P.reshape(H * L, d, d), 1, S_all, L, H * L, Yh)

@@ -312,3 +312,29 @@ def test_ssm_adjoint_panels_export_bitwise(s):
     ll, ls = ops.ssm_export(X, H, L2, S, nC, T, full=False, reverse=True, kshift=K)
     assert torch.equal(ll, lam.real - K[..., None, None])
     assert torch.equal(ls, s._sign_of(lam))
+
+
+def test_ssm_chunked_contractive_powers_keep_the_carry(s):
+    """the Hillis-Steele chunk carry squares A^L up to A^(L nC / 2). With a
+    contractive A (spectral radius ~0.6) those powers fall below e^-745 long before the
+    states do when x0 is large and the inputs are zero: x_t = A^t x0 stays representable
+    (e^{690 - 0.51 t} at t ~ 2048), and the chunked evaluation must keep the
+    A^(L off) (x) s term (max-normalised powers) — compared with the per-step sequential
+    recurrence (ssm.py:99-108)."""
+    rng = np.random.default_rng(31)
+    H, S, T, d, L = 1, 2, 4096, 8, 64
+    A = rng.standard_normal((d, d))
+    A *= 0.6 / np.max(np.abs(np.linalg.eigvals(A)))
+    B, C, D = rng.standard_normal((d, d)), rng.standard_normal((2 * d, d)), rng.standard_normal(
+        (2 * d, d))
+    x0s = rng.standard_normal((H, S, d)) * 1e300
+    us = np.zeros((H, S, T, d))
+    sl, ss, c, y = (t.cpu().numpy() for t in s.ssm_forward_heads(A[None], B[None], C[None],
+                                                                    D[None], x0s, us, chunk=L))
+    p = s.SsmParams(A, B, C, D)
+    for i in range(S):
+        seq = s.ssm_forward_sequential(p, x0s[0, i], us[0, i])
+        fin = np.isfinite(seq.state_log)
+        assert fin[2500:].any()  # the states after chunk 32 are representable
+        assert np.all(np.isfinite(sl[0, i][fin]))
+        assert rel_log(sl[0, i], seq.state_log) < 1e-9

@@ -79,9 +79,12 @@ def install_shim(mode: str):
     for name in ("core", "scan", "lyapunov", "ssm"):
         if name not in ours:
             continue
-        spec = importlib.util.spec_from_file_location(f"_ref_{name}", os.path.join(REF, f"{name}.py"))
+        # the reference module itself (registered under a private name so its relative
+        # imports resolve inside the shim package), only to list the names it defines
+        spec = importlib.util.spec_from_file_location(f"gooms._ref_{name}",
+                                                      os.path.join(REF, f"{name}.py"))
         refmod = importlib.util.module_from_spec(spec)
-        refmod.__package__ = "gooms"
+        sys.modules[f"gooms._ref_{name}"] = refmod
         try:
             spec.loader.exec_module(refmod)
         except Exception as e:  # pragma: no cover
