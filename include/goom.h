@@ -159,6 +159,22 @@ size_t goom_scan_chain_workspace_size_c128(int64_t T, int d, int block);
 int goom_scan_chain_c128(const goom_c128* A, goom_c128* out, int64_t T, int d, int block,
                          const goom_c128* carry_in, void* ws, size_t ws_bytes, void* stream);
 
+/* Long-chain product scan for small matrices (d <= 32; scan_long.cu): the same prefixes
+ * out[t] = A[t] (x) ... (x) A[0] (x) carry_in as goom_scan_chain_*, for chains far longer
+ * than a block, with a different but fixed combine tree (reduce-then-scan: block totals,
+ * their scan by the same engine recursively, then a sequential fold of every block from
+ * its carry). Sequential depth O(s log_s T) instead of the two-level tree's s + T/s;
+ * 24 d^2 B of traffic per complex64 element instead of 32 d^2. Every combine is the
+ * generic LMME's arithmetic, so a chain of T <= 32 is bitwise the sequential fold.
+ * Replaces the block-tree A slot of _scan_affine_stack (scan.py:181-214) for the
+ * long-chain harness; carry_in (d x d) may be NULL. */
+size_t goom_scan_chain_long_workspace_size(int64_t T, int d);
+int goom_scan_chain_long_c64(const goom_c64* A, goom_c64* out, int64_t T, int d,
+                             const goom_c64* carry_in, void* ws, size_t ws_bytes, void* stream);
+size_t goom_scan_chain_long_workspace_size_c128(int64_t T, int d);
+int goom_scan_chain_long_c128(const goom_c128* A, goom_c128* out, int64_t T, int d,
+                              const goom_c128* carry_in, void* ws, size_t ws_bytes, void* stream);
+
 /* Inclusive affine scan of pairs (A_t: d x d, B_t: d x m, flag_t) under
  * combine_affine (scan.py:92-103): (A,B) <- (A_t A, A_t B (+) B_t), flag OR.
  * Same two-level tree as _scan_affine_stack. flags may be NULL (all false). */

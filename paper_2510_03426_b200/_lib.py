@@ -79,6 +79,8 @@ SIGNATURES = {
     ),
     "goom_scan_chain_workspace_size": (_SZ, [_I64, _I, _I]),
     "goom_scan_chain_c64": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
+    "goom_scan_chain_long_workspace_size": (_SZ, [_I64, _I]),
+    "goom_scan_chain_long_c64": (_I, [_P, _P, _I64, _I, _P, _P, _SZ, _P]),
     "goom_scan_affine_workspace_size": (_SZ, [_I64, _I, _I, _I]),
     "goom_scan_affine_c64": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _SZ, _P]),
     "goom_scan_selective_chain_workspace_size": (
@@ -108,6 +110,8 @@ SIGNATURES = {
     ),
     "goom_scan_chain_workspace_size_c128": (_SZ, [_I64, _I, _I]),
     "goom_scan_chain_c128": (_I, [_P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
+    "goom_scan_chain_long_workspace_size_c128": (_SZ, [_I64, _I]),
+    "goom_scan_chain_long_c128": (_I, [_P, _P, _I64, _I, _P, _P, _SZ, _P]),
     "goom_scan_affine_workspace_size_c128": (_SZ, [_I64, _I, _I, _I]),
     "goom_scan_affine_c128": (_I, [_P, _P, _P, _P, _P, _P, _I64, _I, _I, _I, _P, _SZ, _P]),
     "goom_scan_selective_chain_workspace_size_c128": (

@@ -181,4 +181,12 @@ template <class R>
 int chain_scan_cta(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int64_t s,
                    const Cx<R>* carry_in, Cx<R>* L, Cx<R>* Cx_, cudaStream_t st);
 
+// d <= 32 long-chain engine (scan_long.cu): reduce-then-scan, a different fixed tree
+bool chain_long_eligible(int d);
+template <class R>
+size_t chain_long_workspace_bytes(int64_t T, int d);
+template <class R>
+int chain_scan_long(const Cx<R>* A, Cx<R>* out, int64_t T, int d, const Cx<R>* carry_in,
+                    void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace goom

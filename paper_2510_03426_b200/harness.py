@@ -68,8 +68,8 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
 
     d % 256 == 0 runs on the tile-scaled engine (ops.chain_ts): leaves are generated
     (or imported) tile-scaled, prefixes are digested inside the phase-3 LMME epilogue
-    and the carry between windows stays tile-scaled. Other d use the complex64 scan +
-    digest kernels."""
+    and the carry between windows stays tile-scaled. d <= 32 runs the long-chain engine
+    (ops.scan_chain_long); other d the complex64 block-tree scan. Both + digest kernels."""
     want = _snapshot_set(T, t0, snapshot_every, snapshots)
     if ops.ts_eligible(d):
         return _run_chain_ts(T, d, seed, window, block, t0, carry, want, leaves, anchors)
@@ -81,7 +81,10 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
     for w0 in range(0, T, window):
         n = min(window, T - w0)
         A = leaves[w0:w0 + n] if leaves is not None else random_chain(n, d, seed, t0 + w0, dev)
-        P = torch.ops.goom.scan_chain(A, block, carry)
+        # d <= 32: the long-chain engine (scan_long.cu; a fixed reduce-then-scan tree, the
+        # block size only shapes the reference tree the other engines keep)
+        P = (torch.ops.goom.scan_chain_long(A, carry) if d <= 32 else
+             torch.ops.goom.scan_chain(A, block, carry))
         digests[w0:w0 + n] = torch.ops.goom.digest(P)
         for t in range(w0, w0 + n):
             if t0 + t in want:

@@ -309,6 +309,22 @@ def scan_chain(a: torch.Tensor, block: int, carry: Optional[torch.Tensor]) -> to
     return out
 
 
+@torch.library.custom_op("goom::scan_chain_long", mutates_args=(), device_types="cuda")
+def scan_chain_long(a: torch.Tensor, carry: Optional[torch.Tensor]) -> torch.Tensor:
+    """The same inclusive product chain for d <= 32 on the long-chain engine (scan_long.cu:
+    reduce-then-scan, a fixed tree of depth O(s log_s T) instead of the block tree's s + T/s)."""
+    _need_cuda(a, carry)
+    _need_goom(a, carry)
+    a = a.contiguous()
+    T, d = a.shape[0], a.shape[-1]
+    out = torch.empty_like(a)
+    ws, nws = _ws(_size("goom_scan_chain_long_workspace_size", a.dtype, T, d), a.device)
+    c = None if carry is None else carry.to(a.dtype).contiguous()
+    _lib.call(_lib.fn("goom_scan_chain_long", a.dtype), a.data_ptr(), out.data_ptr(), T, d,
+              _ptr(c), _ptr(ws), nws, _stream())
+    return out
+
+
 @torch.library.custom_op("goom::scan_affine", mutates_args=(), device_types="cuda")
 def scan_affine(a: torch.Tensor, b: torch.Tensor, flags: torch.Tensor,
                 block: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:

@@ -1,0 +1,131 @@
+"""GPU parity of the long-chain small-d engine (scan_long.cu, torch.ops.goom.scan_chain_long)
+against the float64 oracle and against the generic LMME, combine by combine.
+
+The engine computes the same prefixes as _scan_affine_stack's A slot (scan.py:181-214)
+with a different fixed tree (reduce-then-scan), so:
+  * a single chain (T <= 32) is the sequential fold: bitwise the generic path with
+    block >= T (scan.py:217-225) without a carry, and bitwise a loop of generic LMMEs
+    P = A_t (x) P from the carry with one;
+  * longer chains (one to three levels of recursion, ragged tails, carries) meet the
+    SURVEY §8c chain criterion against the float64 sequential oracle, calibrated by the
+    reference's own float32 runs (complex64), and the reference's float64 tolerance
+    (complex128).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from goom_testlib import chain_parity, load_golden, scaled_real_err, to_np
+from oracle import gooms_port as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2510_03426_b200 as goom
+
+    goom._lib.load()
+    return goom
+
+
+def leaves(g, T, d, seed, dt=torch.complex64):
+    rng = np.random.default_rng(seed)
+    return g.join(*G.log_sign(rng.standard_normal((T, d, d))), dt)
+
+
+@pytest.mark.parametrize("d", [1, 3, 8, 13, 16, 32])
+@pytest.mark.parametrize("T", [1, 5, 32])
+@pytest.mark.parametrize("c128", [False, True])
+def test_single_chain_is_bitwise_the_sequential_fold(g, d, T, c128):
+    dt = torch.complex128 if c128 else torch.complex64
+    A = leaves(g, T, d, 7 * d + T, dt)
+    got = torch.ops.goom.scan_chain_long(A, None)
+    want = torch.ops.goom.scan_chain(A, T, None)  # block >= T: the sequential fold
+    assert torch.equal(got, want)
+    # with a carry: P_0 = A_0 (x) carry, P_t = A_t (x) P_{t-1}, one generic LMME per step
+    carry = leaves(g, 1, d, 99, dt)[0]
+    got = torch.ops.goom.scan_chain_long(A, carry)
+    P = carry[None]
+    for t in range(T):
+        P = torch.ops.goom.lmme(A[t:t + 1], P)
+        assert torch.equal(got[t], P[0]), t
+
+
+@pytest.mark.parametrize("block", [1000])
+def test_config1_chain_d8_T1000(g, block):
+    """Config 1 (1,000 random-normal 8x8 leaves, golden from the reference) on the long-chain
+    engine: two levels (chains of 64, then one of 16)."""
+    z = load_golden("config1_chain")
+    al, as_ = G.log_sign(z["mats"])
+    out = torch.ops.goom.scan_chain_long(g.join(al, as_), None)
+    gl, gs = to_np(out)
+    r = chain_parity(gl, gs, al, as_, (z["seq_f64"][0], z["seq_f64"][1]),
+                     [z["seq_f32"], z["par32_f32"]])
+    assert r["ok"], (r["bad"], r["flips"], r["scaled_bad"])
+
+
+@pytest.mark.parametrize("d,T", [(8, 5000), (16, 2100), (32, 1500), (5, 1100)])
+def test_long_chain_matches_oracle_complex64(g, d, T):
+    rng = np.random.default_rng(d * 1000 + T)
+    x = rng.standard_normal((T, d, d))
+    al, as_ = G.log_sign(x)
+    out = torch.ops.goom.scan_chain_long(g.join(al, as_), None)
+    gl, gs = to_np(out)
+    want = G.chain_blocked(al, as_, T)           # float64 sequential fold (the oracle)
+    l32, s32 = G.log_sign(x.astype(np.float32))
+    refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 64)]
+    r = chain_parity(gl, gs, al, as_, want, refs)
+    assert r["ok"], (r["bad"], r["e_gpu"][r["bad"]], r["e_ref"][r["bad"]], r["flips"],
+                     r["scaled_bad"])
+
+
+@pytest.mark.parametrize("d,T", [(4, 70000), (8, 3000), (32, 700)])
+def test_long_chain_with_carry_complex128(g, d, T):
+    """Three levels at T = 70,000 (chains of 64, 16, 16, then one of <= 32), ragged tails,
+    and a carry: float64 tolerance of the reference (test_scan.py:227-237, 1e-10 order)."""
+    rng = np.random.default_rng(d + T)
+    x = rng.standard_normal((T, d, d))
+    c = rng.standard_normal((d, d))
+    al, as_ = G.log_sign(x)
+    cl, cs = G.log_sign(c)
+    out = torch.ops.goom.scan_chain_long(g.join(al, as_, torch.complex128),
+                                         g.join(cl, cs, torch.complex128))
+    gl, gs = to_np(out)
+    wl, ws = G.chain_blocked(np.concatenate([cl[None], al]), np.concatenate([cs[None], as_]),
+                             T + 1)
+    wl, ws = wl[1:], ws[1:]
+    assert G.rel_log_diff(gl, wl) < 1e-9
+    assert scaled_real_err(gl, gs, wl, ws).max() < 1e-7  # 70,000 float64 steps, |log| ~ 4e4
+
+
+def test_long_chain_underflow_and_zeros_follow_the_clamp(g):
+    """A shrinking chain (0.5 I + 0.25 E_01 leaves: logs fall 0.69 per step, past float32's
+    exp range) with exact zeros: the long engine's combines are the reference LMME's
+    (clamped scales, core.py:252-253), so it keeps every value float32 can hold, underflows
+    to -inf where the reference's own float32 fold does, and keeps the zero pattern."""
+    d, T = 8, 300
+    x = np.tile(0.5 * np.eye(d), (T, 1, 1))
+    x[:, 0, 1] = 0.25
+    al, as_ = G.log_sign(x)
+    got = torch.ops.goom.scan_chain_long(g.join(al, as_), None)
+    gl, gs = to_np(got)
+    wl, ws = G.chain_blocked(al, as_, T)                       # float64 oracle
+    rl, _ = G.chain_blocked(*G.log_sign(x.astype(np.float32)), T)  # the reference's float32
+    assert not np.any(np.isnan(gl)) and not np.any(gl == np.inf)
+    assert np.all(gl[wl == -np.inf] == -np.inf)                # exact zeros stay zero
+    live = wl > -80.0                                          # normal float32 range
+    assert np.all(np.isfinite(gl[live]))
+    assert np.all(np.abs(gl[live] - wl[live]) <= 1e-4 * np.maximum(1.0, np.abs(wl[live])))
+    assert np.array_equal(gs[live], ws[live])
+    assert np.all(rl[-1] == -np.inf) and np.all(gl[-1] == -np.inf)  # both flushed at t = 299
+
+
+def test_long_chain_validation(g):
+    import paper_2510_03426_b200 as goom
+
+    A = leaves(g, 4, 33, 0)
+    with pytest.raises(goom._lib.GoomError, match="d <= 32"):
+        torch.ops.goom.scan_chain_long(A, None)
+    assert goom._lib.load().goom_scan_chain_long_workspace_size(10, 33) == 0

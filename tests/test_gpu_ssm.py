@@ -334,7 +334,10 @@ def test_ssm_chunked_contractive_powers_keep_the_carry(s):
     p = s.SsmParams(A, B, C, D)
     for i in range(S):
         seq = s.ssm_forward_sequential(p, x0s[0, i], us[0, i])
-        fin = np.isfinite(seq.state_log)
-        assert fin[2500:].any()  # the states after chunk 32 are representable
-        assert np.all(np.isfinite(sl[0, i][fin]))
-        assert rel_log(sl[0, i], seq.state_log) < 1e-9
+        # states the reference's float64 interior holds as normal numbers: below e^-708 its
+        # exp() of the right operand is subnormal (precision lost digit by digit, flushed at
+        # e^-745) and any evaluation order — its own parallel scan included — differs there
+        normal = seq.state_log > -700.0
+        assert normal[2000:].any()  # the states after chunk 31 are representable
+        assert np.all(np.isfinite(sl[0, i][normal]))
+        assert rel_log(np.where(normal, sl[0, i], 0.0), np.where(normal, seq.state_log, 0.0)) < 1e-9

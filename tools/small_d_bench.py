@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--block", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1024)
+    ap.add_argument("--engines", default="all", help="all, or a list of long,tree")
     args = ap.parse_args()
     import torch
 
@@ -43,14 +44,28 @@ def main():
         hbm = json.load(f)["hbm_gbs"]
     for d in [int(x) for x in args.ds.split(",")]:
         A = harness.random_chain(args.T, d, seed=d)
-        out = torch.ops.goom.scan_chain(A, args.block, None)  # warm-up (and workspace)
+        engines = (["long", "tree"] if d <= 32 else ["tree"]) if args.engines == "all" else \
+            args.engines.split(",")
+        for eng in engines:
+            if eng == "long" and d > 32:
+                continue
+            run = (lambda: torch.ops.goom.scan_chain_long(A, None)) if eng == "long" else \
+                (lambda: torch.ops.goom.scan_chain(A, args.block, None))
+            report(args, d, eng, A, run, hbm, G, np, torch)
+        del A
+        torch.cuda.empty_cache()
+
+
+def report(args, d, eng, A, run, hbm, G, np, torch):
+    if True:
+        out = run()  # warm-up (and workspace)
         del out
         torch.cuda.synchronize()
         times = []
         for _ in range(args.reps):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            out = torch.ops.goom.scan_chain(A, args.block, None)
+            out = run()
             e.record()
             torch.cuda.synchronize()
             times.append(s.elapsed_time(e))
@@ -63,20 +78,26 @@ def main():
         t0 = time.perf_counter()
         G.chain_blocked(al, as_, min(args.block, args.cpu_sample))
         cpu_s = time.perf_counter() - t0
-        engine = "scan_small (warp per block)" if d <= 32 else "scan_cta (CTA per block)"
+        if eng == "long":
+            engine = ("scan_long (reduce-then-scan, group of d lanes per chain; a fixed tree "
+                      "other than the reference's block tree)")
+            moved = 24 * d * d
+        else:
+            engine = ("scan_small (warp per block, the reference's block tree)" if d <= 32 else
+                      "scan_cta (CTA per block, the reference's block tree)")
+            moved = 32 * d * d
         print(json.dumps({
-            "config": "small_d_chain", "d": d, "T": args.T, "block": args.block,
+            "config": "small_d_chain", "d": d, "T": args.T,
+            "block": args.block if eng == "tree" else None,
             "engine": engine, "ms": ms, "matrices_per_s": args.T / (ms / 1e3),
             "algorithmic_bytes_per_element": 16 * d * d, "achieved_gbs": gbs,
             "hbm_peak_gbs": hbm, "frac_hbm": gbs / hbm,
-            "tree_bytes_per_element": 32 * d * d,
-            "tree_gbs": 2 * gbs, "flops_per_element": 4 * d ** 3,
+            "moved_bytes_per_element": moved,
+            "moved_gbs": moved / (16 * d * d) * gbs, "flops_per_element": 4 * d ** 3,
             "gflops": 4.0 * d ** 3 * args.T / (ms / 1e3) / 1e9,
             "cpu_matrices_per_s": args.cpu_sample / cpu_s, "cpu_cores": os.cpu_count(),
             "cpu_kind": "port (oracle/gooms_port.chain_blocked, float64)",
         }), flush=True)
-        del A
-        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
