@@ -12,9 +12,11 @@ kept at a stride.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 from typing import Dict, Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import ops  # registers torch.ops.goom.*
@@ -276,7 +278,9 @@ def chain_survival(cfg: ChainConfig) -> ChainResult:
     else:
         ct = torch.complex128 if cfg.backend == "goom64" else torch.complex64
         for L in leaves:
-            P = torch.ops.goom.scan_chain(L.to(ct), 64, None)
+            L = L.to(ct)
+            P = torch.ops.goom.scan_chain_long(L, None) if d <= 32 else \
+                torch.ops.goom.scan_chain(L, 64, None)
             lg = P.real.reshape(T, -1)
             bad = torch.isnan(lg).any(dim=1) | torch.isposinf(lg).any(dim=1)
             first = int(_first_failure(bad[:, None])[0])
@@ -285,3 +289,184 @@ def chain_survival(cfg: ChainConfig) -> ChainResult:
                          ("nan" if bool(torch.isnan(lg[first]).any()) else "overflow"))
     return ChainResult(survived_steps=steps, completed=[s == T for s in steps],
                        failure_mode=modes)
+
+
+# ---------------------------------------------------------------------------
+# error benchmarking against a 50-digit reference (Appendix D)
+
+ERRBENCH_OPS = ("identity", "reciprocal", "sqrt", "square", "log", "exp", "add", "mul", "matmul")
+ORACLE_DIGITS = 50
+
+
+@dataclass
+class ErrorStats:
+    """SPEC ErrorStats plus the paper's Appendix D figures.
+
+    abs_log10_error per sample = |log10|y| - log10|y_ref||: the error of the result's
+    decimal order of magnitude (relative error / ln 10 for small errors). error_digits per
+    sample = log10|y - y_ref|, the paper's "number of decimal digits of error" (exact
+    results are left out of its statistics). matmul reports the Frobenius error normalised
+    by ||C_ref||_F in max / mean (one sample). `direct_*` is the same operation evaluated in
+    the backing float format itself, for comparison."""
+
+    op_name: str
+    input_range: tuple
+    max_abs_log10_error: float
+    mean_abs_log10_error: float
+    samples: int
+    backing: int
+    max_error_digits: float
+    mean_error_digits: float
+    direct_max_abs_log10_error: float
+    direct_mean_abs_log10_error: float
+
+
+def oracle_eval(op: str, *args):
+    """The operation in >= 50-digit software arithmetic (mpmath): scalars for the scalar
+    ops (args are Python floats, converted exactly), a list of lists for matmul (args are
+    two 2-D float arrays). Domain violations (log or sqrt of a negative) raise ValueError."""
+    import mpmath
+
+    with mpmath.workdps(ORACLE_DIGITS):
+        if op == "matmul":
+            a, b = args
+            n, k, m = len(a), len(b), len(b[0])
+            A = [[mpmath.mpf(float(a[i][j])) for j in range(k)] for i in range(n)]
+            B = [[mpmath.mpf(float(b[i][j])) for j in range(m)] for i in range(k)]
+            return [[mpmath.fsum(A[i][q] * B[q][j] for q in range(k)) for j in range(m)]
+                    for i in range(n)]
+        x = [mpmath.mpf(float(v)) for v in args]
+        if op in ("log", "sqrt") and x[0] < 0:
+            raise ValueError(f"{op} of a negative value in real arithmetic")
+        table = {
+            "identity": lambda: x[0],
+            "reciprocal": lambda: 1 / x[0],
+            "sqrt": lambda: mpmath.sqrt(x[0]),
+            "square": lambda: x[0] * x[0],
+            "log": lambda: mpmath.log(x[0]),
+            "exp": lambda: mpmath.exp(x[0]),
+            "add": lambda: x[0] + x[1],
+            "mul": lambda: x[0] * x[1],
+        }
+        if op not in table:
+            raise ValueError(f"unknown op {op!r}; one of {ERRBENCH_OPS}")
+        return table[op]()
+
+
+def _goom_eval(op: str, xs, ys, backing: int):
+    """op over GOOMs on the GPU: inputs mapped by from_real, computed in the log domain
+    (the library's kernels for add = gadd and matmul = LMME), mapped back by to_real."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    double = backing == 64
+    rt = torch.float64 if double else torch.float32
+
+    def goom(v):
+        return torch.ops.goom.from_real(torch.as_tensor(v, dtype=rt, device=dev), float("-inf"),
+                                        double)
+
+    def real(z):
+        return torch.ops.goom.to_real(z, double).cpu().numpy().astype(np.float64)
+
+    gx = goom(xs)
+    if op == "identity":
+        return real(gx)
+    if op == "reciprocal":
+        return real(torch.complex(-gx.real, gx.imag))
+    if op == "sqrt":
+        return real(torch.complex(0.5 * gx.real, gx.imag))
+    if op == "square":
+        return real(torch.complex(2.0 * gx.real, torch.zeros_like(gx.imag)))
+    if op == "log":   # the log-magnitude is the GOOM's real part (x > 0)
+        return real(goom(gx.real))
+    if op == "exp":   # e^x as a GOOM is (x, 0)
+        return real(torch.complex(torch.as_tensor(xs, dtype=rt, device=dev),
+                                  torch.zeros(len(xs), dtype=rt, device=dev)))
+    gy = goom(ys)
+    if op == "add":
+        return real(torch.ops.goom.gadd(gx, gy))
+    if op == "mul":
+        return real(torch.complex(gx.real + gy.real, gx.imag + gy.imag))
+    if op == "matmul":
+        return real(torch.ops.goom.lmme(gx, gy))
+    raise ValueError(f"unknown op {op!r}; one of {ERRBENCH_OPS}")
+
+
+def _direct_eval(op: str, xs, ys, backing: int):
+    dt = np.float64 if backing == 64 else np.float32
+    x = np.asarray(xs, dtype=dt)
+    y = None if ys is None else np.asarray(ys, dtype=dt)
+    with np.errstate(all="ignore"):
+        out = {"identity": lambda: x, "reciprocal": lambda: dt(1) / x, "sqrt": lambda: np.sqrt(x),
+               "square": lambda: x * x, "log": lambda: np.log(x), "exp": lambda: np.exp(x),
+               "add": lambda: x + y, "mul": lambda: x * y, "matmul": lambda: x @ y}[op]()
+    return np.asarray(out, dtype=np.float64)
+
+
+def errbench(op: str, range_low: float = 1e-6, range_high: float = 1e6, samples: int = 10_000,
+             backing: int = 32, seed: int = 0) -> ErrorStats:
+    """Errors of `op` evaluated over GOOMs against the 50-digit reference (SPEC errbench,
+    PAPER.md:880). One-argument ops: `samples` inputs equally spaced in decimal digits over
+    [range_low, range_high]; two-argument ops: a ceil(sqrt(samples))^2 grid of such pairs;
+    matmul: two `samples` x `samples` N(0,1) matrices (the range does not apply), error
+    normalised by the product's Frobenius norm. backing 32 / 64: complex64 / complex128."""
+    import mpmath
+
+    if op not in ERRBENCH_OPS:
+        raise ValueError(f"unknown op {op!r}; one of {ERRBENCH_OPS}")
+    if backing not in (32, 64):
+        raise ValueError("backing must be 32 or 64")
+    if samples < 1:
+        raise ValueError("samples must be >= 1")
+    dt = np.float64 if backing == 64 else np.float32
+    if op == "matmul":
+        rng = np.random.default_rng(seed)
+        a = rng.standard_normal((samples, samples)).astype(dt)
+        b = rng.standard_normal((samples, samples)).astype(dt)
+        ref = oracle_eval("matmul", a.tolist(), b.tolist())
+        got = _goom_eval(op, a, b, backing)
+        direct = _direct_eval(op, a, b, backing)
+        with mpmath.workdps(ORACLE_DIGITS):
+            fro = mpmath.sqrt(mpmath.fsum(v * v for row in ref for v in row))
+
+            def nerr(c):
+                return float(mpmath.sqrt(mpmath.fsum((mpmath.mpf(float(c[i][j])) - ref[i][j]) ** 2
+                                                     for i in range(samples)
+                                                     for j in range(samples))) / fro)
+            e, e_dir = nerr(got), nerr(direct)
+        return ErrorStats(op, (samples, samples), e, e, 1, backing, math.log10(e) if e else
+                          float("-inf"), math.log10(e) if e else float("-inf"), e_dir, e_dir)
+    if not (0.0 < range_low < range_high) and op != "exp":
+        raise ValueError("need 0 < range_low < range_high (log-spaced sampling)")
+    if op == "exp" and not range_low < range_high:
+        raise ValueError("need range_low < range_high")
+    lo, hi = (math.log10(range_low), math.log10(range_high)) if range_low > 0 else (None, None)
+    if op in ("add", "mul"):
+        n = int(math.ceil(math.sqrt(samples)))
+        grid = np.logspace(lo, hi, n).astype(dt)
+        xs, ys = np.repeat(grid, n), np.tile(grid, n)
+    else:
+        xs = (np.logspace(lo, hi, samples) if lo is not None else
+              np.linspace(range_low, range_high, samples)).astype(dt)
+        ys = None
+    got = _goom_eval(op, xs, ys, backing)
+    direct = _direct_eval(op, xs, ys, backing)
+    errs, digits, errs_dir = [], [], []
+    with mpmath.workdps(ORACLE_DIGITS):
+        for i in range(len(xs)):
+            r = oracle_eval(op, xs[i]) if ys is None else oracle_eval(op, xs[i], ys[i])
+            if r == 0:
+                continue
+            lr = mpmath.log10(abs(r))
+            for val, sink in ((got[i], errs), (direct[i], errs_dir)):
+                v = mpmath.mpf(float(val))
+                sink.append(float(abs(mpmath.log10(abs(v)) - lr)) if v != 0 and
+                            (v > 0) == (r > 0) else float("inf"))
+            diff = abs(mpmath.mpf(float(got[i])) - r)
+            if diff != 0:
+                digits.append(float(mpmath.log10(diff)))
+    e = np.asarray(errs)
+    ed = np.asarray(errs_dir)
+    dg = np.asarray(digits) if digits else np.asarray([float("-inf")])
+    return ErrorStats(op, (float(range_low), float(range_high)), float(e.max()), float(e.mean()),
+                      len(xs), backing, float(dg.max()), float(dg.mean()), float(ed.max()),
+                      float(ed.mean()))

@@ -83,6 +83,29 @@ class JacobianChain:
         return self.mats.shape[1]
 
 
+def integrate_chain(system, x0=None, burn_in=0, T=1, seed=0) -> JacobianChain:
+    """Step Jacobians J(x_0), J(x_1), ... along a trajectory of `system` after `burn_in`
+    discarded steps (lyapunov.py:106-130). Without x0 the start is the system's default
+    state jittered by 1e-3 N(0, 1) from the (seed, 0) Philox stream, as the reference does."""
+    from .systems import make_rng
+
+    if T < 1:
+        raise ValueError("T must be >= 1")
+    x = (system.default_state + 1e-3 * make_rng(seed).standard_normal(system.dim)
+         if x0 is None else np.array(x0, dtype=np.float64))
+    for i in range(burn_in):
+        x = system.step(x)
+        if not np.all(np.isfinite(x)):
+            raise ValueError(f"non-finite state at burn-in step {i}")
+    mats = np.empty((T, system.dim, system.dim))
+    for t in range(T):
+        mats[t] = system.jacobian(x)
+        x = system.step(x)
+        if not np.all(np.isfinite(x)):
+            raise ValueError(f"non-finite state at step {burn_in + t}")
+    return JacobianChain(dt=system.dt, mats=mats)
+
+
 @dataclass
 class SpectrumResult:
     lambdas: np.ndarray  # descending, units 1/time

@@ -1,0 +1,129 @@
+"""The command-line front end on the GPU: SPEC.md cli examples (457-510) and the
+acceptance criteria it can check at test scale (1 chain survival,
+2 LMME accuracy vs the 50-digit oracle, 3 scan equivalence with resets, 5 Lyapunov sum
+rules, 7 LLE, 8 SSM vs a 50-digit recurrence, errbench examples)."""
+
+import csv
+import io
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def run(argv, capsys):
+    from paper_2510_03426_b200 import cli
+
+    rc = cli.main(argv)
+    out = capsys.readouterr().out
+    manifest = [l[2:] for l in out.splitlines() if l.startswith("# ")]
+    body = [l for l in out.splitlines() if not l.startswith("#")]
+    rows = list(csv.DictReader(io.StringIO("\n".join(body))))
+    return rc, manifest, rows
+
+
+def test_manifest_first_and_body_reproducible(capsys):
+    argv = ["chain", "--d", "8", "--steps", "300", "--backend", "real64", "--trials", "3",
+            "--seed", "1"]
+    rc, man, rows = run(argv, capsys)
+    assert rc == 0
+    keys = [m.split(":")[0] for m in man[:7]]
+    assert keys == ["command", "seed", "backing", "workers", "rng", "version", "wall_clock_s"]
+    rc2, _, rows2 = run(argv, capsys)
+    assert rows == rows2
+
+
+def test_chain_examples(capsys):
+    # real64 fails by overflow before step 5000 at d = 8 (acceptance 1; ~700 steps)
+    rc, _, rows = run(["chain", "--d", "8", "--steps", "3000", "--backend", "real64",
+                       "--trials", "4", "--seed", "1"], capsys)
+    assert rc == 0 and len(rows) == 4
+    assert all(int(r["survived_steps"]) < 3000 and r["failure_mode"] == "overflow" for r in rows)
+    # too short to fail
+    rc, _, rows = run(["chain", "--d", "8", "--steps", "100", "--backend", "real64"], capsys)
+    assert [int(r["survived_steps"]) for r in rows] == [100]
+    # goom64 completes (acceptance 1 at test scale)
+    rc, _, rows = run(["chain", "--d", "16", "--steps", "20000", "--backend", "goom64",
+                       "--trials", "2"], capsys)
+    assert all(int(r["survived_steps"]) == 20000 and r["failure_mode"] == "none" for r in rows)
+
+
+def test_scanselftest_passes(capsys):
+    rc, man, rows = run(["scanselftest", "--len", "1024", "--d", "8", "--blocks", "4,16,64"],
+                        capsys)
+    assert rc == 0, rows
+    assert all(r["ok"] == "True" for r in rows)
+    sel = [r for r in rows if r["scan"] == "selective"]
+    assert len(sel) == 3 and all(int(r["resets"]) >= 3 for r in sel)
+    assert man[-1] == "selftest: ok"
+
+
+@pytest.mark.parametrize("backing,bound", [(64, 1e-12), (32, 1e-5)])
+def test_errbench_matmul_acceptance_2(capsys, backing, bound):
+    rc, _, rows = run(["errbench", "--op", "matmul", "--samples", "64", "--backing",
+                       str(backing)], capsys)
+    assert rc == 0
+    assert float(rows[0]["max_abs_log10_error"]) <= bound
+
+
+def test_errbench_spec_examples(capsys):
+    # square over [1e-6, 1e6], binary32: within 1 decimal digit of the direct computation
+    rc, _, rows = run(["errbench", "--op", "square", "--low", "1e-6", "--high", "1e6",
+                       "--samples", "2000", "--backing", "32"], capsys)
+    r = rows[0]
+    assert rc == 0
+    assert math.log10(float(r["max_abs_log10_error"])) <= \
+        math.log10(float(r["direct_max_abs_log10_error"])) + 1.0
+    # identity over [1e-10, 1e10], binary64: mean relative error <= 1e-12
+    rc, _, rows = run(["errbench", "--op", "identity", "--low", "1e-10", "--high", "1e10",
+                       "--samples", "2000", "--backing", "64"], capsys)
+    assert float(rows[0]["mean_abs_log10_error"]) * math.log(10) <= 1e-12
+    # exp over [1e-5, 10]: finite errors for every sample
+    rc, _, rows = run(["errbench", "--op", "exp", "--low", "1e-5", "--high", "10",
+                       "--samples", "1000"], capsys)
+    assert rc == 0 and math.isfinite(float(rows[0]["max_abs_log10_error"]))
+    for op in ("reciprocal", "sqrt", "log", "add", "mul"):
+        rc, _, rows = run(["errbench", "--op", op, "--samples", "400"], capsys)
+        assert rc == 0 and float(rows[0]["max_abs_log10_error"]) < 1e-5, (op, rows)
+
+
+def test_ssm_check_acceptance_8(capsys):
+    rc, man, rows = run(["ssm", "--d", "8", "--T", "512", "--rho", "1.5", "--check"], capsys)
+    assert rc == 0, man
+    assert len(rows) == 512
+    assert "check: direct_binary64_recurrence_finite=False" in man
+    assert man[-1] == "check: ok"
+
+
+def test_lyapunov_sum_rules_acceptance_5(capsys):
+    rc, _, rows = run(["lyapunov", "spectrum", "--system", "lorenz", "--steps", "30000",
+                       "--method", "par", "--burn-in", "2000"], capsys)
+    assert rc == 0 and len(rows) == 3
+    total = sum(float(r["lambda"]) for r in rows)
+    assert abs(total - (-13.6667)) < 0.02 * 13.6667
+    rc, _, rows = run(["lyapunov", "spectrum", "--system", "henon", "--steps", "30000",
+                       "--method", "par", "--burn-in", "1000"], capsys)
+    total = sum(float(r["lambda"]) for r in rows)
+    assert abs(total - math.log(0.3)) < 0.01 * abs(math.log(0.3))
+
+
+def test_lle_henon_and_file_system(capsys, tmp_path):
+    rc, _, rows = run(["lyapunov", "lle", "--system", "henon", "--steps", "30000",
+                       "--method", "par"], capsys)
+    lam_par = float(rows[0]["lambda"])
+    assert abs(lam_par - 0.419) < 0.02
+    rc, _, rows = run(["lyapunov", "lle", "--system", "henon", "--steps", "30000",
+                       "--method", "seq"], capsys)
+    assert abs(float(rows[0]["lambda"]) - lam_par) < 1e-8  # Appendix B identity (acceptance 7)
+    # file:<path> round trip through goomjac v1
+    from paper_2510_03426_b200 import lyapunov, systems
+
+    ch = lyapunov.integrate_chain(systems.rossler(), burn_in=500, T=4000, seed=2)
+    path = tmp_path / "r.jac"
+    lyapunov.save_jacobian_chain(ch, str(path))
+    rc, _, rows = run(["lyapunov", "spectrum", "--system", f"file:{path}", "--method", "seq"],
+                      capsys)
+    assert rc == 0 and len(rows) == 3
+    assert np.isfinite([float(r["lambda"]) for r in rows]).all()
