@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     lmme_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapOut, TsIn A, TsIn B, TsOut T,
                    float4* __restrict__ parts, PairGrid grid, int n, int k, int m, int debug,
-                   ChainArgs ch, int clampz) {
+                   ChainArgs ch, int clampz, int pdl) {
   using Y = Lay<kOut, S>;
   constexpr int kStages = S, kOutOff = Y::kOutOff;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -183,6 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+  if (pdl) {
+    // programmatic dependent launch: the next launch's CTAs may start their prologue
+    // (barriers, TMEM, descriptor prefetch) as this grid's CTAs retire; nothing below reads
+    // global memory before the previous grid has completed and flushed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const uint32_t tmem = *tmem_slot;
   const uint32_t base = smem_u32(smem);
   // tile -> (matrix pair b, row / column offsets, chain step); matrix indices of the
@@ -552,6 +559,15 @@ int ts_debug() {
   return v;
 }
 
+// GOOM_TS_PDL=0 launches without programmatic dependent launch (A/B probe)
+int ts_pdl() {
+  static int v = [] {
+    const char* e = getenv("GOOM_TS_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int kOut, int S>
 int query_clusters() {
   return [] {
@@ -599,16 +615,19 @@ int launch_cfg(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& m
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  const int pdl = ts_pdl();
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, lmme_ts_kernel<kOut, S, kChain>, mapA, mapB, mapOut, p.A, p.B, p.T,
                      p.parts, pg,
-                     p.n, p.k, p.m, ts_debug(), ch, ts_clamp());
+                     p.n, p.k, p.m, ts_debug(), ch, ts_clamp(), pdl);
   GOOM_CHECK_LAUNCH("lmme_ts_kernel");
   return GOOM_OK;
 }
