@@ -164,6 +164,8 @@ bool lmme_tc_eligible(int n, int k, int m);
 // it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s);
 bool lmme_tc2_eligible(int n, int k, int m);
+// the pair kernel reduces Eq. 11's scales itself (no pre-pass) for this shape
+bool lmme_tc2_fuse_scales(int n, int k, int m);
 
 // ---- scans (scan.cu) --------------------------------------------------------
 template <class R>

@@ -43,6 +43,14 @@ int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (whole_shape(p.n, p.k, p.m) && !p.rowA.ptr &&
       !(sizeof(R) == 4 && backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)))
     return lmme_simt_whole<R>(p, s);
+  if constexpr (sizeof(R) == 4) {
+    // n = m = 256 (config 2's HBM-bound shape): the pair kernel reduces the clamped scales
+    // of its own A rows / B columns from HBM and its ring re-reads them from L2 (no pre-pass)
+    if (backend != 1 && (!p.rowA.ptr || !p.colB.ptr) && lmme_tc2_fuse_scales(p.n, p.k, p.m)) {
+      const int rc = lmme_tc2(p, s);
+      if (rc != GOOM_EUNSUPPORTED) return rc;
+    }
+  }
   if (!p.rowA.ptr || !p.colB.ptr) {
     size_t need = lmme_workspace_bytes<R>(p.batch, p.n, p.k, p.m, p.A.stride, p.A.div,
                                           p.B.stride, p.B.div);

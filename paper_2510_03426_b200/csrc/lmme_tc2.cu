@@ -41,18 +41,27 @@ using namespace tc;
 constexpr int kRowsCta = 128;            // accumulator rows per CTA (M = 256 per pair)
 constexpr int kPairN = 256;              // N per pair tile (128 B columns per CTA)
 constexpr int BK = 16;
-constexpr int kStages = 6;
 constexpr int kXformWarps = 16;
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 64 + (kXformWarps + kEpiWarps) * 32;  // 704
 constexpr int kBytesA = (kRowsCta / 8) * kGroupBytes;          // 16 KB
 constexpr int kBytesB = (kPairN / 2 / 8) * kGroupBytes;         // 16 KB
 constexpr int kStage = kBytesA + kBytesB;                       // 32 KB
-constexpr int kRing = kStages * kStage;                         // 192 KB
 constexpr int kTmemCols = 2 * kPairN;                           // 512: double buffer
 constexpr int kStageOut = 32 * 16 * 8;                         // 4 KB: 32 rows x 16 cols c64
 constexpr int kOutBytes = kEpiWarps * 2 * kStageOut;            // 32 KB: 2 buffers per warp
-constexpr int kSmem = kRing + kOutBytes + 1024 /*align*/ + 512 /*barriers*/;
+// kFuse (scales reduced in-kernel, no pre-pass): a 4-slot ring of per-tile scale tables
+// (this CTA's 128 row scales, the pair tile's 256 column scales) and a column-max scratch
+constexpr int kScaleSlots = 4;
+constexpr int kScaleBytes = kScaleSlots * (kRowsCta + kPairN) * 4 + kRowsCta * 4 + 16;
+template <bool kFuse>
+struct Tc2Cfg {
+  static constexpr int S = kFuse ? 5 : 6;                       // ring stages
+  static constexpr int kRing = S * kStage;                      // 160 / 192 KB
+  static constexpr int kScaleOff = kRing + kOutBytes;
+  static constexpr int kBarOff = kScaleOff + (kFuse ? kScaleBytes : 0);
+  static constexpr int kSmem = kBarOff + 1024 /*align*/ + 512 /*barriers*/;
+};
 
 // (cluster / pair helpers: tc_ptx.cuh)
 
@@ -60,6 +69,7 @@ constexpr int kSmem = kRing + kOutBytes + 1024 /*align*/ + 512 /*barriers*/;
 // l%8) and B group xw (lane (n = l%8, c = l/8): k = 4c..4c+3 of column n, landed at smem
 // rows c + 4j so each LDS.64 covers 4 consecutive 64-byte rows: conflict-free).
 // ring position (stage, phase parity) advanced incrementally: no divisions in the loops
+template <int kStages>
 struct RingPos {
   int s = 0;
   uint32_t ph = 0;
@@ -111,6 +121,33 @@ __device__ __forceinline__ void store_planes(uint32_t stage, int xw, int lane, c
   st_shared_v4(gb + 512 + ob, lb[0], lb[1], lb[2], lb[3]);
 }
 
+// DSMEM store into CTA `rank` of the cluster at this CTA's shared offset
+__device__ __forceinline__ void st_cluster_f32(uint32_t local, uint32_t rank, float v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+// release at cluster scope: the DSMEM stores before it are visible to the waiter
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 0x989680;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool noncanonical(float im) { return im != 0.0f && im != kPi; }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 struct PairGrid {
   int nct, nrt;    // pair-tile columns / rows per product
   int64_t tiles;   // pair tiles in this launch
@@ -130,21 +167,33 @@ struct Emit {
   int64_t col_stride;
 };
 
+template <bool kFuse>
 __global__ void __launch_bounds__(kThreads, 1)
     lmme_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     const __grid_constant__ CUtensorMap mapC,
                     Operand A, Operand B, Operand D, Scales rowA, Scales colB,
                     float2* __restrict__ C, int64_t strideC, PairGrid grid, int k, int m,
                     const int* __restrict__ noncanon, Emit emit, int debug) {
+  using Cfg = Tc2Cfg<kFuse>;
+  constexpr int kStages = Cfg::S, kRing = Cfg::kRing;
+  using Ring = RingPos<kStages>;
+  const bool prefetch = (debug & 64) != 0;  // kFuse probe: L2 prefetch of the next tile
+  debug &= 63;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRing + kOutBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
   uint64_t* full = bars;                    // [S] local: TMA bytes landed
   uint64_t* ready = bars + kStages;         // [S] leader: both CTAs' stage transformed
   uint64_t* freed = bars + 2 * kStages;     // [S] local: stage's MMAs retired (multicast)
   uint64_t* acc_full = bars + 3 * kStages;  // [2] local: accumulator complete (multicast)
   uint64_t* acc_empty = acc_full + 2;       // [2] leader: both CTAs drained the buffer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* sc_full = acc_empty + 2;        // [4] kFuse: a tile's scale tables complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + kScaleSlots);
+  // kFuse scale area: rowS [slot][128], colS [slot][256], column-max scratch, flags
+  float* rowS = reinterpret_cast<float*>(smem + Cfg::kScaleOff);
+  float* colS = rowS + kScaleSlots * kRowsCta;
+  uint32_t* colBits = reinterpret_cast<uint32_t*>(colS + kScaleSlots * kPairN);
+  int* ncflag = reinterpret_cast<int*>(colBits + kRowsCta);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -162,7 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 2 * kEpiWarps);
     }
+    if (kFuse)  // 4 local + 4 remote column-scale writer warps per tile
+      for (int i = 0; i < kScaleSlots; ++i) mbar_init(smem_u32(&sc_full[i]), 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (kFuse) {
+    if (tid < kRowsCta) colBits[tid] = 0u;  // below every ordered float ("unset")
+    if (tid == 0) *ncflag = 0;
   }
   if (warp == 1) {  // one warp of EACH CTA takes part in the pair allocation
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -180,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------ loader (both CTAs) ------------------------------
     if (lane == 0) {
-      RingPos rp;
+      Ring rp;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
         int64_t b;
         int prow0, pcol0;
@@ -202,6 +257,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * BK;
           tma_load_3d(dst, &mapA, k0, row0, ma, bar);                              // [128][16 k]
           tma_load_5d(dst + kBytesA, &mapB, 0, k0 / 4, 0, col0 / 8, mb, bar);      // [16][4][4][8]
+          if (kFuse && prefetch && kb == 0 && t + nclusters < grid.tiles) {
+            // probe (measured slower, profiles/r2_config2_fused_scales.txt): the next tile's
+            // A rows and B columns into L2 under this tile's main loop
+            int64_t b2;
+            int pr2, pc2;
+            grid.at(t + nclusters, b2, pr2, pc2);
+            prefetch_l2(A.at(b2) + (int64_t)(pr2 + (int)rank * kRowsCta) * k,
+                        (uint32_t)kRowsCta * (uint32_t)k * 8u);
+            const float2* bc = B.at(b2) + pc2 + (int)rank * (kPairN / 2);
+            for (int kr = 0; kr < k; ++kr) prefetch_l2(bc + (int64_t)kr * m, (kPairN / 2) * 8);
+          }
         }
       }
     }
@@ -210,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------ MMA issuer (leader CTA) ------------------------------
     if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN);
-      RingPos rp;
+      Ring rp;
       int lt = 0;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
         const int buf = lt & 1;
@@ -242,19 +308,102 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 2 + kXformWarps) {
     // ------------------------------ transform (both CTAs) ------------------------------
     const int xw = warp - 2;
-    const bool canon = noncanon != nullptr && *noncanon == 0;
+    bool canon = noncanon != nullptr && *noncanon == 0;
     const int r8 = lane >> 3, bn = lane & 7;
     const uint32_t ready0 = smem_u32(&ready[0]);
     int64_t t = cluster;
     float sa0 = 0.f, sa1 = 0.f, sb = 0.f;
+    int st_lt = 0;  // kFuse: tiles of this cluster so far (scale-table slot = st_lt % 4)
     auto load_scales = [&](int64_t tile) {
       int64_t b;
       int prow0, pcol0;
       grid.at(tile, b, prow0, pcol0);
-      const float* ra = rowA.at(b) + prow0 + rank * kRowsCta + xw * 8;
-      sa0 = ra[r8];
-      sa1 = ra[r8 + 4];
-      sb = colB.at(b)[pcol0 + rank * (kPairN / 2) + xw * 8 + bn];
+      if constexpr (kFuse) {
+        // Eq. 11's clamped scales for this tile, reduced here instead of by a pre-pass
+        // (core.py:252-253): the CTA's 128 A rows (row max over k) and its 128 B columns
+        // (column max over k), read once from HBM; the ring's TMA loads of the same data
+        // then hit L2. The 16 transform warps share the work; the column scales go to both
+        // CTAs' tables (the pair's epilogues need all 256), signalled by sc_full[slot].
+        const int slot = st_lt & (kScaleSlots - 1);
+        float* rs = rowS + slot * kRowsCta;
+        float* cs = colS + slot * kPairN;
+        const int kq = k >> 1;  // float4 (two complex) per row of A
+        const float4* arow = reinterpret_cast<const float4*>(A.at(b) + (int64_t)(prow0 + rank * kRowsCta) * k);
+        bool nc = false;
+#pragma unroll 1
+        for (int r = 0; r < 8; r += 4) {  // rows 8 xw + r .. + 3: 4 rows' loads in flight
+          float mx[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
+          for (int j = lane; j < kq; j += 32) {
+            float4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = __ldg(arow + (int64_t)(8 * xw + r + q) * kq + j);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              mx[q] = fmaxf(mx[q], fmaxf(v[q].x, v[q].z));
+              nc |= noncanonical(v[q].y) | noncanonical(v[q].w);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float w = warp_max(mx[q]);
+            if (lane == 0) rs[8 * xw + r + q] = fmaxf(w, 0.0f);
+          }
+        }
+        // columns 2 lane, 2 lane + 1, 64 + 2 lane, 65 + 2 lane of this CTA's 128; rows xw + 16 i
+        const float2* bcol = B.at(b) + pcol0 + rank * (kPairN / 2);
+        float c4[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
+#pragma unroll 1
+        for (int kr = xw; kr < k; kr += 64) {  // 4 rows' loads in flight
+          float4 v[4], w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int row = kr + 16 * q;
+            const float4* pr = reinterpret_cast<const float4*>(bcol + (int64_t)(row < k ? row : kr) * m);
+            v[q] = __ldg(pr + lane);
+            w[q] = __ldg(pr + 32 + lane);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            c4[0] = fmaxf(c4[0], v[q].x);
+            c4[1] = fmaxf(c4[1], v[q].z);
+            c4[2] = fmaxf(c4[2], w[q].x);
+            c4[3] = fmaxf(c4[3], w[q].z);
+            nc |= noncanonical(v[q].y) | noncanonical(v[q].w) | noncanonical(w[q].y) |
+                  noncanonical(w[q].w);
+          }
+        }
+        atomicMax(&colBits[2 * lane], float_to_ordered(c4[0]));
+        atomicMax(&colBits[2 * lane + 1], float_to_ordered(c4[1]));
+        atomicMax(&colBits[64 + 2 * lane], float_to_ordered(c4[2]));
+        atomicMax(&colBits[65 + 2 * lane], float_to_ordered(c4[3]));
+        if (__any_sync(0xffffffffu, nc) && lane == 0) atomicOr(ncflag, 1);
+        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");
+        const int u = xw * 32 + lane;
+        if (u < kRowsCta) {  // warps 0..3: publish the column scales to both CTAs' tables
+          const float v = fmaxf(ordered_to_float(colBits[u]), 0.0f);
+          colBits[u] = 0u;
+          const int ci = rank * (kPairN / 2) + u;
+          cs[ci] = v;
+          st_cluster_f32(smem_u32(cs + ci), rank ^ 1u, v);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");
+        canon = *ncflag == 0;
+        sa0 = rs[xw * 8 + r8];
+        sa1 = rs[xw * 8 + r8 + 4];
+        sb = cs[rank * (kPairN / 2) + xw * 8 + bn];
+        if (xw < kRowsCta / 32 && lane == 0) {
+          mbar_arrive(smem_u32(&sc_full[slot]));                            // local writes
+          mbar_arrive_release_cluster(smem_u32(&sc_full[slot]), rank ^ 1u);  // peer's table
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");  // flag read
+        if (u == 0) *ncflag = 0;
+        ++st_lt;
+      } else {
+        const float* ra = rowA.at(b) + prow0 + rank * kRowsCta + xw * 8;
+        sa0 = ra[r8];
+        sa1 = ra[r8 + 4];
+        sb = colB.at(b)[pcol0 + rank * (kPairN / 2) + xw * 8 + bn];
+      }
     };
     if (t < grid.tiles) {
       load_scales(t);
@@ -262,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(&full[0]), 0);
       load_raw(ring, xw, lane, cur);
       int kb = 0;
-      RingPos rc, rn;  // current stage and the next one
+      Ring rc, rn;  // current stage and the next one
       rn.next();
       for (;;) {
         int64_t tn = t;
@@ -310,8 +459,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
       tc_fence_after();
       const int grow = prow0 + (int)rank * kRowsCta + row;
-      const float ai = rowA.at(b)[grow];
-      const float* cb = colB.at(b) + pcol0;
+      float ai;
+      const float* cb;
+      if constexpr (kFuse) {
+        const int slot = lt & (kScaleSlots - 1);
+        mbar_wait_acquire_cluster(smem_u32(&sc_full[slot]), (uint32_t)((lt >> 2) & 1));
+        ai = rowS[slot * kRowsCta + row];
+        cb = colS + slot * kPairN;
+      } else {
+        ai = rowA.at(b)[grow];
+        cb = colB.at(b) + pcol0;
+      }
       const float2* drow = D.ptr ? D.at(b) + (int64_t)grow * m + pcol0 : nullptr;
       uint32_t rmax = 0;  // bits of max(log, 0): non-negative floats order like uints
       const int wrow0 = prow0 + (int)rank * kRowsCta + quad * 32;  // this warp's 32 rows
@@ -388,7 +546,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// GOOM_TC_DEBUG (profiling only; results invalid): 1 no transform, 2 no MMA, 3 no loads
+// GOOM_TC_DEBUG (profiling only; results invalid unless noted): +64 L2 prefetch of the next
+// tile in the fused-scale pair kernel (results valid); 1 no transform, 2 no MMA, 3 no loads
 // and no transform, 4 no loads, 5 loads only (no transform / MMA), 7 as 5 without the
 // epilogue body, 8 MMA only (no loads / transform / epilogue body), 9 epilogue only
 int tc_debug() {
@@ -399,12 +558,13 @@ int tc_debug() {
   return v;
 }
 
+template <bool kFuse>
 int query_clusters() {
   return [] {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 74);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmem;
+    cfg.dynamicSmemBytes = Tc2Cfg<kFuse>::kSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -413,15 +573,28 @@ int query_clusters() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, lmme_tc2_kernel, &cfg) != cudaSuccess || n < 1) {
+    if (cudaOccupancyMaxActiveClusters(&n, lmme_tc2_kernel<kFuse>, &cfg) != cudaSuccess || n < 1) {
       cudaGetLastError();
       n = num_sms() / 2;
     }
     return n;
   }();
 }
+template <bool kFuse>
 int max_clusters() {  // per device (abi.cu per_device_value)
-  return per_device_value((const void*)lmme_tc2_kernel, &query_clusters);
+  return per_device_value((const void*)lmme_tc2_kernel<kFuse>, &query_clusters<kFuse>);
+}
+
+// GOOM_TC2_FUSE: 1 always reduce the scales in-kernel when the caller gives none, 0 never
+// (pre-pass), unset: in-kernel when every A row block and B column block is read by exactly
+// one pair tile (n == m == 256: the HBM-bound config-2 shape), so the reduction adds no
+// second read of anything
+int fuse_mode() {
+  static int v = [] {
+    const char* e = getenv("GOOM_TC2_FUSE");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -430,15 +603,34 @@ bool lmme_tc2_eligible(int n, int k, int m) {
   return n > 0 && k > 0 && m > 0 && n % 256 == 0 && m % 256 == 0 && k % BK == 0;
 }
 
+bool lmme_tc2_fuse_scales(int n, int k, int m) {
+  if (!lmme_tc2_eligible(n, k, m) || k < 128) return false;  // >= 8 K-blocks per tile (slot reuse)
+  const int f = fuse_mode();
+  return f == 1 || (f < 0 && n == 256 && m == 256);
+}
+
+template <bool kFuse>
+int lmme_tc2_run(const LmmeProblem& p, cudaStream_t s);
+
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s) {
   if (!lmme_tc2_eligible(p.n, p.k, p.m)) return GOOM_EUNSUPPORTED;
+  if (!p.rowA.ptr || !p.colB.ptr) {
+    if (!lmme_tc2_fuse_scales(p.n, p.k, p.m)) return GOOM_EUNSUPPORTED;
+    return lmme_tc2_run<true>(p, s);
+  }
+  return lmme_tc2_run<false>(p, s);
+}
+
+template <bool kFuse>
+int lmme_tc2_run(const LmmeProblem& p, cudaStream_t s) {
+  constexpr int kSmem = Tc2Cfg<kFuse>::kSmem;
   // TMA: 16-byte aligned bases and even matrix strides; epilogue: float4 column-scale
   // loads and 16-byte output stores
   if (((reinterpret_cast<uintptr_t>(p.A.ptr) | reinterpret_cast<uintptr_t>(p.B.ptr) |
         reinterpret_cast<uintptr_t>(p.C) | reinterpret_cast<uintptr_t>(p.colB.ptr)) & 15) ||
       ((p.A.stride | p.B.stride | p.strideC) & 1) || (p.colB.stride & 3))
     return GOOM_EUNSUPPORTED;
-  GOOM_TRY(smem_attr((const void*)lmme_tc2_kernel, kSmem, "lmme_tc2 smem attribute"));
+  GOOM_TRY(smem_attr((const void*)lmme_tc2_kernel<kFuse>, kSmem, "lmme_tc2 smem attribute"));
   alignas(64) CUtensorMap mapA, mapB;
   int64_t mats, mstride;
   // A: (k, n, matrix) complex64 moved as int64; box 16 k x 128 rows (one CTA's half)
@@ -473,7 +665,7 @@ int lmme_tc2(const LmmeProblem& p, cudaStream_t s) {
   pg.nct = p.m / kPairN;
   pg.nrt = p.n / 256;
   pg.tiles = p.batch * pg.nct * pg.nrt;
-  const int64_t mc = max_clusters();
+  const int64_t mc = max_clusters<kFuse>();
   const int64_t clusters = pg.tiles < mc ? pg.tiles : mc;
   Emit emit{p.emitRow, p.emitRowStride, p.emitCol, p.emitColStride};
 
@@ -489,7 +681,7 @@ int lmme_tc2(const LmmeProblem& p, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, lmme_tc2_kernel, mapA, mapB, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C,
+  cudaLaunchKernelEx(&cfg, lmme_tc2_kernel<kFuse>, mapA, mapB, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C,
                      p.strideC, pg, p.k, p.m, p.noncanon, emit, tc_debug());
   GOOM_CHECK_LAUNCH("lmme_tc2_kernel");
   return GOOM_OK;

@@ -1,0 +1,24 @@
+"""Profiling driver: one batched complex64 LMME of `batch` d x d N(0,1) products (config 2's
+shape), repeated `reps` times (for ncu / nsys-free CUDA-event timing)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2510_03426_b200 as g  # noqa: E402
+
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+g._lib.load()
+A = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
+B = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(reps):
+    flush.add_(1)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    torch.ops.goom.lmme(A, B)
+    e.record()
+    torch.cuda.synchronize()
+print(f"d={d} batch={batch} {s.elapsed_time(e):.3f} ms")
