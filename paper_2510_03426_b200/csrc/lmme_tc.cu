@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             o1 = gadd_elem(o1, drow[col + j + 1]);
           }
           // row `lane`, 16-byte chunk j / 2, XOR-swizzled by the row: conflict-free both ways
-          st_shared_v4(stage + lane * 256 + ((((j >> 1) ^ lane) & 15) << 4),
+          // (no memory clobber: the column-scale loads above may be hoisted past it)
+          st_shared_v4_staging(stage + lane * 256 + ((((j >> 1) ^ lane) & 15) << 4),
                        __float_as_uint(o0.x), __float_as_uint(o0.y), __float_as_uint(o1.x),
                        __float_as_uint(o1.y));
           const uint32_t c0 = __float_as_uint(fmaxf(o0.x, 0.0f));

@@ -499,10 +499,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // [32 rows][16 cols] complex64, 128B-swizzled: 16-byte chunk c of row r at c ^ (r & 7)
             const uint32_t rb = sbuf + (uint32_t)lane * 128;
-            st_shared_v4(rb + ((((j >> 1) + 0) ^ (lane & 7)) << 4), __float_as_uint(o0.x),
-                         __float_as_uint(o0.y), __float_as_uint(o1.x), __float_as_uint(o1.y));
-            st_shared_v4(rb + ((((j >> 1) + 1) ^ (lane & 7)) << 4), __float_as_uint(o2.x),
-                         __float_as_uint(o2.y), __float_as_uint(o3.x), __float_as_uint(o3.y));
+            // staging stores without a memory clobber: the column-scale / bias loads of the
+            // following columns may be hoisted past them (with it, each waited serially)
+            st_shared_v4_staging(rb + ((((j >> 1) + 0) ^ (lane & 7)) << 4), __float_as_uint(o0.x),
+                                 __float_as_uint(o0.y), __float_as_uint(o1.x), __float_as_uint(o1.y));
+            st_shared_v4_staging(rb + ((((j >> 1) + 1) ^ (lane & 7)) << 4), __float_as_uint(o2.x),
+                                 __float_as_uint(o2.y), __float_as_uint(o3.x), __float_as_uint(o3.y));
             const uint32_t c0 = __float_as_uint(fmaxf(o0.x, 0.0f));
             const uint32_t c1 = __float_as_uint(fmaxf(o1.x, 0.0f));
             const uint32_t c2 = __float_as_uint(fmaxf(o2.x, 0.0f));

@@ -178,6 +178,14 @@ __device__ __forceinline__ void goom_split(float2 z, float scale, uint32_t& big,
   small = __float_as_uint(v - __uint_as_float(big));
 }
 
+// epilogue staging store: volatile (ordered with the other asm shared-memory accesses and
+// the async-proxy fence that precedes a TMA store) but no "memory" clobber, so ordinary
+// global loads (column scales, the fused bias) may be scheduled across it
+__device__ __forceinline__ void st_shared_v4_staging(uint32_t addr, uint32_t a, uint32_t b,
+                                                     uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d));
+}
 __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
