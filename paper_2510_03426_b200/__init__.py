@@ -32,7 +32,8 @@ from .core import (  # noqa: F401
     to_real_scaled,
 )
 from .lyapunov import (JacobianChain, SpectrumResult, colinearity_policy,  # noqa: F401
-                       colinearity_select, lle_parallel, lle_sequential, orthonormal_reset,
+                       colinearity_select, integrate_chain, lle_parallel, lle_sequential,
+                       orthonormal_reset,
                        load_jacobian_chain, qr_factor, qr_factor_batched, save_jacobian_chain,
                        spectrum_parallel, spectrum_sequential)
 from .scan import (  # noqa: F401

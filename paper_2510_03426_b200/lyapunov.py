@@ -28,6 +28,7 @@ import torch
 from . import _lib
 from .core import GoomMatrix
 from .scan import ResetPolicy, _selective_chain_core, builtin_policy
+from .systems import make_rng, worker_count  # noqa: F401  (the reference's lyapunov namespace)
 
 
 def colinearity_policy(threshold=0.99, check_interval=12, volume_floor=1e-9) -> ResetPolicy:
