@@ -160,6 +160,8 @@ template <class R> int lmme_simt_whole(const LmmeProblemT<R>& p, cudaStream_t s)
 // tcgen05 3xTF32 (lmme_tc.cu), complex64 only; GOOM_EUNSUPPORTED if not tileable
 int lmme_tc(const LmmeProblem& p, cudaStream_t s);
 bool lmme_tc_eligible(int n, int k, int m);
+// one-SM kernel with the scales reduced in-kernel (scale pass through its ring)
+bool lmme_tc1_fuse_scales(int n, int k, int m);
 // cta_group::2 pair-tile variant (lmme_tc2.cu) for n, m multiples of 256; lmme_tc() prefers
 // it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s);

@@ -46,8 +46,10 @@ int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
   if constexpr (sizeof(R) == 4) {
     // n = m = 256 (config 2's HBM-bound shape): the pair kernel reduces the clamped scales
     // of its own A rows / B columns from HBM and its ring re-reads them from L2 (no pre-pass)
-    if (backend != 1 && (!p.rowA.ptr || !p.colB.ptr) && lmme_tc2_fuse_scales(p.n, p.k, p.m)) {
-      const int rc = lmme_tc2(p, s);
+    // n = m = 128: the one-SM kernel reduces them in a scale pass through its ring
+    if (backend != 1 && (!p.rowA.ptr || !p.colB.ptr) &&
+        (lmme_tc2_fuse_scales(p.n, p.k, p.m) || lmme_tc1_fuse_scales(p.n, p.k, p.m))) {
+      const int rc = lmme_tc(p, s);
       if (rc != GOOM_EUNSUPPORTED) return rc;
     }
   }

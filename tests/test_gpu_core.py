@@ -481,20 +481,27 @@ def test_column_norms_and_scaled_export_reference_cases(g):
     assert np.all(np.abs(back / xs - 1.0) < 1e-12)
 
 
-@pytest.mark.parametrize("bcast", [False, True])
-def test_lmme_pair_fused_scales_bitwise_equals_scaled_path(g, bcast):
-    """n = m = 256 (config 2's HBM-bound shape): the pair kernel reduces Eq. 11's clamped row /
-    column maxima itself (lmme_tc2.cu kFuse, no pre-pass). Bitwise equal to the same kernel
-    fed precomputed clamped maxima (goom_lmme_scaled_c64), over enough products that every
-    cluster cycles through its 4 scale-table slots, with all-negative rows (clamp), zero rows
-    and columns, rows near 1e5, non-canonical phases (2 pi, -pi) in some products, a
-    broadcast right operand, and the fused bias gadd."""
+@pytest.mark.parametrize("shape,bcast,bias", [
+    ((256, 256, 256), False, False), ((256, 256, 256), True, False),
+    ((128, 128, 128), False, False), ((128, 128, 128), True, False),
+    ((128, 64, 128), False, True), ((128, 512, 128), False, False),
+    ((128, 128, 128), False, True)])
+def test_lmme_fused_scales_bitwise_equals_scaled_path(g, shape, bcast, bias):
+    """The config-2 HBM-bound shapes reduce Eq. 11's clamped row / column maxima in-kernel (no
+    pre-pass): n = m = 256 in the pair kernel (lmme_tc2.cu kFuse), n = m = 128 through the
+    one-SM kernel's scale pass (lmme_tc.cu kFuse: every K-block read once ahead for the
+    maxima, once for the main loop). Bitwise equal to the same shape fed precomputed clamped
+    maxima (goom_lmme_scaled_c64), over enough products that every CTA cycles through its 4
+    scale-table slots, with all-negative rows (clamp), zero rows and columns, rows near 1e5,
+    non-canonical phases (2 pi, -pi) in some products, a broadcast right operand, and the
+    fused bias gadd (the scaled entry has no bias: it is added by the same gadd kernel)."""
     import ctypes
 
-    torch.manual_seed(256 + bcast)
-    batch, d = 700, 256
-    A = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda") * 3, float("-inf"), False)
-    B = torch.ops.goom.from_real(torch.randn(1 if bcast else batch, d, d, device="cuda") * 3,
+    n, k, m = shape
+    torch.manual_seed(n + k + bcast + 7 * bias)
+    batch = 700
+    A = torch.ops.goom.from_real(torch.randn(batch, n, k, device="cuda") * 3, float("-inf"), False)
+    B = torch.ops.goom.from_real(torch.randn(1 if bcast else batch, k, m, device="cuda") * 3,
                                  float("-inf"), False)
     A.real[5, 7, :] -= 200.0                                     # row entirely below 0: a = 0
     A[9, 3, :] = torch.complex(torch.tensor(float("-inf")), torch.tensor(0.0))   # zero row
@@ -502,29 +509,32 @@ def test_lmme_pair_fused_scales_bitwise_equals_scaled_path(g, bcast):
     A.real[17, 100:120, :] += 1e5                                # huge logs
     A.imag[40] = torch.where(A.imag[40] != 0, torch.full_like(A.imag[40], -math.pi),
                              torch.full_like(A.imag[40], 2 * math.pi))  # non-canonical phases
-    Bx = B.expand(batch, d, d) if bcast else B
-    got = torch.ops.goom.lmme(A, Bx)
+    Bx = B.expand(batch, k, m) if bcast else B
     ra = A.real.amax(dim=2).clamp_min(0).contiguous()
     cb = B.real.amax(dim=1).clamp_min(0).contiguous()
-    ref = torch.empty_like(got)
+    ref = torch.empty(batch, n, m, dtype=A.dtype, device="cuda")
     lib = g._lib.load()
     g._lib.check(lib.goom_lmme_scaled_c64(
-        g._lib.goom_operand(A.data_ptr(), d * d, 1), ra.data_ptr(), d,
-        g._lib.goom_operand(B.data_ptr(), 0 if bcast else d * d, 1), cb.data_ptr(),
-        0 if bcast else d, ref.data_ptr(), d * d, batch, d, d, d,
+        g._lib.goom_operand(A.data_ptr(), n * k, 1), ra.data_ptr(), n,
+        g._lib.goom_operand(B.data_ptr(), 0 if bcast else k * m, 1), cb.data_ptr(),
+        0 if bcast else m, ref.data_ptr(), n * m, batch, n, k, m,
         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    if bias:
+        D = torch.ops.goom.from_real(torch.randn(batch, n, m, device="cuda") * 40, float("-inf"),
+                                     False)
+        got = torch.ops.goom.lmme_gadd(A, Bx, D)
+        ref = torch.ops.goom.gadd(ref, D)
+    else:
+        got = torch.ops.goom.lmme(A, Bx)
     torch.cuda.synchronize()
     assert torch.equal(torch.view_as_real(got), torch.view_as_real(ref))
     # parity with the float64 oracle on a few products, including the edge cases (product 5's
     # row 7 is the clamp case: it underflows exactly like the reference float32 run, which the
     # float64 oracle does not, so it is pinned by the bitwise check above only)
+    if bias:
+        return
     for i in (9, 17, 40, batch - 1):
         al, as_ = to_np(A[i:i + 1])
         bl, bs = to_np(B[0 if bcast else i:(0 if bcast else i) + 1])
         err, flips = lmme_parity(to_np(got[i:i + 1]), al, as_, bl, bs)
         assert err < 1e-4 and flips == 0, (i, err, flips)
-    # fused bias gadd on the same path
-    D = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda") * 50, float("-inf"), False)
-    fused = torch.ops.goom.lmme_gadd(A, Bx, D)
-    assert torch.equal(torch.view_as_real(fused),
-                       torch.view_as_real(torch.ops.goom.gadd(got, D)))

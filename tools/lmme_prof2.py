@@ -14,6 +14,7 @@ g._lib.load()
 A = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
 B = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ts = []
 for _ in range(reps):
     flush.add_(1)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -21,4 +22,7 @@ for _ in range(reps):
     torch.ops.goom.lmme(A, B)
     e.record()
     torch.cuda.synchronize()
-print(f"d={d} batch={batch} {s.elapsed_time(e):.3f} ms")
+    ts.append(s.elapsed_time(e))
+ts.sort()
+gbs = 24 * d * d * batch / (ts[len(ts) // 2] * 1e-3) / 1e9
+print(f"d={d} batch={batch} median {ts[len(ts) // 2]:.4f} ms min {ts[0]:.4f} ms ({gbs:.0f} GB/s)")
