@@ -64,9 +64,9 @@ struct Cfg {
   static constexpr int kEpiWarps = BN == 128 ? 8 : 4;  // 2 / 1 per TMEM lane quadrant
   static constexpr int kEpiCols = BN / (kEpiWarps / 4);  // accumulator columns per warp
   static constexpr int kThreads = 64 + (kXformWarps + kEpiWarps) * 32;
-  static constexpr int kStages = BN == 128 ? 5 : 4;      // ring depth
-  static constexpr int kStageOut = BN == 128 ? 4096 : 8192;  // staging per warp: 32 rows x 16 / 32 cols
-  static constexpr bool kTmaOut = BN == 128;  // staging stored by TMA (128B-swizzled box)
+  static constexpr int kStages = BN == 128 ? 6 : 4;      // ring depth
+  static constexpr int kStageOut = BN == 128 ? 2048 : 8192;  // staging per warp: 32 rows x 8 / 32 cols
+  static constexpr bool kTmaOut = BN == 128;  // staging stored by TMA (64B-swizzled box)
   static constexpr int kGroupsA = BM / 8;
   static constexpr int kGroupsB = BN / 8;
   static constexpr int kBytesA = kGroupsA * kGroupBytes;
@@ -154,7 +154,6 @@ __device__ __forceinline__ void store_stage(uint32_t base, int xw, int lane,
   }
 }
 
-__device__ __forceinline__ bool odd_phase(float im) { return im != 0.0f && im != kPi; }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -169,60 +168,6 @@ struct TileGrid {
     row0 = (int)(q % nrt) * BM;
     col0 = ct * BN;
     b = b_base + q / nrt;
-  }
-};
-
-// kFuse: the ring positions of one CTA in issue order. The first tile's scale stages, then
-// per tile t: [main(t, kb), scale(t + step, kb)] for kb = 0 .. nk-1 (no scale stages after
-// the last tile). Every role walks the same sequence, so slot and phase bookkeeping agree.
-struct FuseSeq {
-  int64_t t, step, tiles;
-  int kb, nk;
-  bool prologue, sub_scale;
-  __device__ __forceinline__ FuseSeq(int64_t t0, int64_t step_, int64_t tiles_, int nk_)
-      : t(t0), step(step_), tiles(tiles_), kb(0), nk(nk_), prologue(true), sub_scale(false) {}
-  __device__ __forceinline__ bool valid() const { return t < tiles; }
-  __device__ __forceinline__ bool scale() const { return prologue || sub_scale; }
-  // tile whose data the stage holds
-  __device__ __forceinline__ int64_t tile() const { return sub_scale ? t + step : t; }
-  __device__ __forceinline__ void next() {
-    if (prologue) {
-      if (++kb == nk) {
-        prologue = false;
-        kb = 0;
-      }
-      return;
-    }
-    if (!sub_scale && t + step < tiles) {
-      sub_scale = true;
-      return;
-    }
-    sub_scale = false;
-    if (++kb == nk) {
-      kb = 0;
-      t += step;
-    }
-  }
-};
-
-// per-slot phase bits of the shared ring (kFuse: slots carry main and scale stages)
-template <int STAGES>
-struct RingBits {
-  int s = 0;
-  uint32_t full = 0, mainp = 0, scalep = 0, last_scale = 0, used = 0;
-  __device__ __forceinline__ uint32_t bit(uint32_t v) const { return (v >> s) & 1u; }
-  __device__ __forceinline__ void advance(bool scale) {
-    const uint32_t m = 1u << s;
-    full ^= m;
-    used |= m;
-    if (scale) {
-      scalep ^= m;
-      last_scale |= m;
-    } else {
-      mainp ^= m;
-      last_scale &= ~m;
-    }
-    s = s + 1 == STAGES ? 0 : s + 1;
   }
 };
 
@@ -259,7 +204,8 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
   constexpr int kEpiWarps = G::kEpiWarps;
   constexpr int STAGES = G::kStages;
   const int pf = debug >> 8;  // kFuse: L2 prefetch distance (GOOM_TC_PREFETCH)
-  debug &= 255;
+  const int fflags = debug & 0xF0;  // kFuse probes: 16 A row chunks, 32 no L2 hints, 64 late
+  debug &= 15;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB-align the ring while keeping the pointer's shared-space provenance
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -307,11 +253,12 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
 
   // kFuse scale stages: A as contiguous 16 KB row chunks (one bulk copy) instead of the
   // K-block box (GOOM_TC_DEBUG bit 16; k % 64 == 0) — measured slower, kept as a probe
-  const bool rowsA = kFuse && (k % 64) == 0 && (debug & 16) != 0;
+  const bool rowsA = kFuse && (k % 64) == 0 && (fflags & 16) != 0;
   // kFuse L2 policy (GOOM_TC_DEBUG bit 32 off): scale-pass loads evict_last (the main pass
   // re-reads them one tile later), main-pass loads evict_first, output stores evict_first
-  const bool hints = kFuse && (debug & 32) == 0;
+  const bool hints = kFuse && (fflags & 32) == 0;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+  const bool late = (fflags & 64) != 0;  // FuseSeq late interleave (GOOM_TC_DEBUG bit 64)
   // a tile's load coordinates, computed once per tile (the loader is one thread: int64
   // divisions per stage measured ~1.5 k clocks per issue, slower than the ring drains)
   struct TileAt {
@@ -367,7 +314,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
         RingBits<STAGES> rb;
         int gpos = 0;
         TileAt cm, cs;  // coordinates of the main-pass and the scale-pass tile
-        for (FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk); q.valid(); q.next()) {
+        for (FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk, late); q.valid(); q.next()) {
           const int s = rb.s;
           if (pf > 0 && !q.scale() && q.kb == 0) prefetch_tile(q.t + (int64_t)pf * q.step);
           if (rb.bit(rb.used)) {  // wait for the slot's previous occupant to be released
@@ -379,7 +326,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
           TC_TRACE(0, gpos, clock64());
           TileAt& c = q.scale() ? cs : cm;
           tile_at(q.tile(), c);
-          issue_loads(s, c, q.kb, q.scale());
+          issue_loads(s, c, q.block(), q.scale());
           rb.advance(q.scale());
           ++gpos;
         }
@@ -423,7 +370,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
         int gpos = 0;
         int lt = -1;  // local tile counter -> accumulator buffer lt & 1
         uint32_t acc = tmem;
-        for (FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk); q.valid(); q.next()) {
+        for (FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk, late); q.valid(); q.next()) {
           const int s = rb.s;
           const bool sc = q.scale();
           if (!sc) {
@@ -477,7 +424,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
       int64_t lt_scale = 0;  // local index of the tile the scale stages belong to
       RingBits<STAGES> rb;
       int gpos = 0;
-      FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk);
+      FuseSeq q(blockIdx.x, gridDim.x, grid.tiles, nk, late);
       // no cross-stage software pipeline here: a main stage must not wait for the scale
       // stage behind it (an HBM read) before it is transformed; the 16 warps hide LDS latency
       for (; q.valid(); q.next()) {
@@ -495,7 +442,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
           if (rowsA) {
             // this warp's rows 8 xw .. 8 xw + 7 as float4 indices [lo, hi) of the tile, the
             // part of them in chunk kb; one warp instruction never straddles a row (k % 64)
-            const int k2 = k >> 1, c0 = q.kb * (G::kBytesA / 16);
+            const int k2 = k >> 1, c0 = q.block() * (G::kBytesA / 16);
             const int lo = max(8 * xw * k2, c0), hi = min((8 * xw + 8) * k2, c0 + G::kBytesA / 16);
             const uint32_t base = ring + s * G::kStage;
             for (int f = lo; f < hi; f += 32) {
@@ -517,7 +464,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&sfreed[s]));
-          if (q.kb == nk - 1) {
+          if (q.block() == nk - 1) {
             if (rowsA) {  // rows r, r + 4 of the group from lanes r, r + 4
               const float m8 = ma0;
               ma0 = __shfl_sync(0xffffffffu, m8, r);
@@ -662,8 +609,10 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
               o1 = gadd_elem(o1, drow[col + j + 1]);
             }
             // (no memory clobber: the column-scale loads above may be hoisted past it)
-            st_shared_v4_staging(stage + lane * (kSub * 8) +
-                                     (((((j - h) >> 1) ^ lane) & (kChunks - 1)) << 4),
+            // TMA path: SWIZZLE_64B (chunk c of row r at c ^ ((r >> 1) & 3)), else c ^ r
+            const int cs = G::kTmaOut ? (((j - h) >> 1) ^ (lane >> 1)) & 3
+                                      : (((j - h) >> 1) ^ lane) & (kChunks - 1);
+            st_shared_v4_staging(stage + lane * (kSub * 8) + (cs << 4),
                                  __float_as_uint(o0.x), __float_as_uint(o0.y),
                                  __float_as_uint(o1.x), __float_as_uint(o1.y));
             const uint32_t c0 = __float_as_uint(fmaxf(o0.x, 0.0f));
@@ -685,7 +634,10 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0 && debug != 8) {
-              tma_store_3d(&mapC, stage, col0 + col + h, row0 + quad * 32, (int)b);
+              if (hints)  // the output streams out: evict_first
+                tma_store_3d_hint(&mapC, stage, col0 + col + h, row0 + quad * 32, (int)b, pol_drop);
+              else
+                tma_store_3d(&mapC, stage, col0 + col + h, row0 + quad * 32, (int)b);
               tma_store_wait_read<0>();  // the buffer is rewritten by the next sub-chunk
             }
             __syncwarp();
@@ -765,7 +717,7 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
     cuuint32_t box[3] = {BN, BK, 1};
     GOOM_TRY(encode(&mapB3, p.B, 3, dims, strides, box));
   }
-  // C: (m, n, batch) complex64 as int64, box 16 cols x 32 rows, 128B swizzle (TMA epilogue)
+  // C: (m, n, batch) complex64 as int64, box 8 cols x 32 rows, 64B swizzle (TMA epilogue)
   alignas(64) CUtensorMap mapC;
   if (G::kTmaOut) {
     if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.strideC & 1))
@@ -774,8 +726,8 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
     const int64_t cs = p.strideC == 0 ? (int64_t)p.n * p.m : p.strideC;
     cuuint64_t dims[3] = {(cuuint64_t)p.m, (cuuint64_t)p.n, (cuuint64_t)cb};
     cuuint64_t strides[2] = {(cuuint64_t)p.m * 8, (cuuint64_t)cs * 8};
-    cuuint32_t box[3] = {16, 32, 1};
-    GOOM_TRY(encode(&mapC, Operand{p.C, 0, 1}, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
+    cuuint32_t box[3] = {8, 32, 1};
+    GOOM_TRY(encode(&mapC, Operand{p.C, 0, 1}, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   TileGrid tg;
   tg.nct = p.m / BN;

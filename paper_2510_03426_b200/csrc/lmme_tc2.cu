@@ -50,10 +50,13 @@ constexpr int kStage = kBytesA + kBytesB;                       // 32 KB
 constexpr int kTmemCols = 2 * kPairN;                           // 512: double buffer
 constexpr int kStageOut = 32 * 16 * 8;                         // 4 KB: 32 rows x 16 cols c64
 constexpr int kOutBytes = kEpiWarps * 2 * kStageOut;            // 32 KB: 2 buffers per warp
-// kFuse (scales reduced in-kernel, no pre-pass): a 4-slot ring of per-tile scale tables
-// (this CTA's 128 row scales, the pair tile's 256 column scales) and a column-max scratch
+// kFuse (scales reduced in-kernel, no pre-pass): every K-block is loaded twice through the
+// ring, once a tile ahead as a SCALE stage (the transform warps reduce the maxima of exactly
+// the A rows / B columns they later transform) and once for the main loop (lmme_tc.cu kFuse,
+// FuseSeq); a 4-slot ring of per-tile tables (this CTA's 128 row scales, the pair tile's 256
+// column scales, the peer's half written over DSMEM) feeds the epilogue
 constexpr int kScaleSlots = 4;
-constexpr int kScaleBytes = kScaleSlots * (kRowsCta + kPairN) * 4 + kRowsCta * 4 + 16;
+constexpr int kScaleBytes = kScaleSlots * (kRowsCta + kPairN) * 4;
 template <bool kFuse>
 struct Tc2Cfg {
   static constexpr int S = kFuse ? 5 : 6;                       // ring stages
@@ -143,10 +146,6 @@ __device__ __forceinline__ void mbar_wait_acquire_cluster(uint32_t bar, uint32_t
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ bool noncanonical(float im) { return im != 0.0f && im != kPi; }
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 struct PairGrid {
   int nct, nrt;    // pair-tile columns / rows per product
@@ -177,7 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = Tc2Cfg<kFuse>;
   constexpr int kStages = Cfg::S, kRing = Cfg::kRing;
   using Ring = RingPos<kStages>;
-  const bool prefetch = (debug & 64) != 0;  // kFuse probe: L2 prefetch of the next tile
+  // kFuse: the late interleave (FuseSeq) by default — scale-read lines wait ~3/4 of a tile for
+  // their main-pass re-read instead of a whole one, which the L2 holds better (d = 256: DRAM
+  // reads 2.02 -> 1.50 GB, 422 -> 397 us); GOOM_TC_DEBUG bit 64 restores one per main stage
+  const bool late = (debug & 64) == 0;
   debug &= 63;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -188,12 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 3 * kStages;  // [2] local: accumulator complete (multicast)
   uint64_t* acc_empty = acc_full + 2;       // [2] leader: both CTAs drained the buffer
   uint64_t* sc_full = acc_empty + 2;        // [4] kFuse: a tile's scale tables complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_full + kScaleSlots);
+  uint64_t* sfreed = sc_full + kScaleSlots;  // [S] kFuse local: scale stage read (16 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfreed + kStages);
   // kFuse scale area: rowS [slot][128], colS [slot][256], column-max scratch, flags
   float* rowS = reinterpret_cast<float*>(smem + Cfg::kScaleOff);
   float* colS = rowS + kScaleSlots * kRowsCta;
-  uint32_t* colBits = reinterpret_cast<uint32_t*>(colS + kScaleSlots * kPairN);
-  int* ncflag = reinterpret_cast<int*>(colBits + kRowsCta);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -211,13 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), 2 * kEpiWarps);
     }
-    if (kFuse)  // 4 local + 4 remote column-scale writer warps per tile
-      for (int i = 0; i < kScaleSlots; ++i) mbar_init(smem_u32(&sc_full[i]), 8);
+    if (kFuse) {  // every transform warp of both CTAs publishes its part of a tile's tables
+      for (int i = 0; i < kScaleSlots; ++i) mbar_init(smem_u32(&sc_full[i]), 2 * kXformWarps);
+      for (int i = 0; i < kStages; ++i) mbar_init(smem_u32(&sfreed[i]), kXformWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (kFuse) {
-    if (tid < kRowsCta) colBits[tid] = 0u;  // below every ordered float ("unset")
-    if (tid == 0) *ncflag = 0;
   }
   if (warp == 1) {  // one warp of EACH CTA takes part in the pair allocation
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -234,7 +233,48 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------ loader (both CTAs) ------------------------------
-    if (lane == 0) {
+    if (kFuse && lane == 0) {
+      // scale pass one tile ahead through the same ring (lmme_tc.cu kFuse, FuseSeq): scale
+      // stages keep their lines in L2 for the main pass, which frees them
+      const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
+      RingBits<kStages> rb;
+      int64_t ct = -1;
+      int row0 = 0, col0 = 0, ma = 0, mb = 0;
+      int64_t ct2 = -1;
+      int row02 = 0, col02 = 0, ma2 = 0, mb2 = 0;
+      for (FuseSeq q(cluster, nclusters, grid.tiles, nk, late); q.valid(); q.next()) {
+        const int s = rb.s;
+        if (rb.bit(rb.used)) {
+          if (rb.bit(rb.last_scale))
+            mbar_wait(smem_u32(&sfreed[s]), rb.bit(rb.scalep) ^ 1u);
+          else
+            mbar_wait(smem_u32(&freed[s]), rb.bit(rb.mainp) ^ 1u);
+        }
+        const bool sc = q.scale();
+        // coordinates once per tile (one thread: no int64 divisions per stage)
+        int64_t& tt = sc ? ct2 : ct;
+        int &r0 = sc ? row02 : row0, &c0 = sc ? col02 : col0, &a0 = sc ? ma2 : ma,
+            &b0 = sc ? mb2 : mb;
+        if (tt != q.tile()) {
+          tt = q.tile();
+          int64_t b;
+          int prow0, pcol0;
+          grid.at(tt, b, prow0, pcol0);
+          r0 = prow0 + (int)rank * kRowsCta;
+          c0 = pcol0 + (int)rank * (kPairN / 2);
+          a0 = A.stride == 0 ? 0 : (int)(b / A.div);
+          b0 = B.stride == 0 ? 0 : (int)(b / B.div);
+        }
+        const uint32_t bar = smem_u32(&full[s]);
+        mbar_expect_tx(bar, kStage);
+        const uint32_t dst = ring + s * kStage;
+        const int k0 = q.block() * BK;
+        const uint64_t pol = sc ? pol_keep : pol_drop;
+        tma_load_3d_hint(dst, &mapA, k0, r0, a0, bar, pol);
+        tma_load_5d_hint(dst + kBytesA, &mapB, 0, k0 / 4, 0, c0 / 8, b0, bar, pol);
+        rb.advance(sc);
+      }
+    } else if (lane == 0) {
       Ring rp;
       for (int64_t t = cluster; t < grid.tiles; t += nclusters) {
         int64_t b;
@@ -257,24 +297,45 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * BK;
           tma_load_3d(dst, &mapA, k0, row0, ma, bar);                              // [128][16 k]
           tma_load_5d(dst + kBytesA, &mapB, 0, k0 / 4, 0, col0 / 8, mb, bar);      // [16][4][4][8]
-          if (kFuse && prefetch && kb == 0 && t + nclusters < grid.tiles) {
-            // probe (measured slower, profiles/r2_config2_fused_scales.txt): the next tile's
-            // A rows and B columns into L2 under this tile's main loop
-            int64_t b2;
-            int pr2, pc2;
-            grid.at(t + nclusters, b2, pr2, pc2);
-            prefetch_l2(A.at(b2) + (int64_t)(pr2 + (int)rank * kRowsCta) * k,
-                        (uint32_t)kRowsCta * (uint32_t)k * 8u);
-            const float2* bc = B.at(b2) + pc2 + (int)rank * (kPairN / 2);
-            for (int kr = 0; kr < k; ++kr) prefetch_l2(bc + (int64_t)kr * m, (kPairN / 2) * 8);
-          }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------ MMA issuer (leader CTA) ------------------------------
-    if (rank == 0 && lane == 0) {
+    if (kFuse && rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN);
+      RingBits<kStages> rb;
+      int lt = -1;
+      uint32_t acc = tmem;
+      for (FuseSeq q(cluster, nclusters, grid.tiles, nk, late); q.valid(); q.next()) {
+        const int s = rb.s;
+        const bool sc = q.scale();
+        if (!sc) {
+          if (q.kb == 0) {
+            ++lt;
+            mbar_wait(smem_u32(&acc_empty[lt & 1]), (uint32_t)((lt >> 1) & 1) ^ 1u);
+            tc_fence_after();
+            acc = tmem + (uint32_t)((lt & 1) * kPairN);
+          }
+          mbar_wait(smem_u32(&ready[s]), rb.bit(rb.mainp));
+          tc_fence_after();
+          const uint32_t base = ring + s * kStage;
+          const uint64_t dAb = sw64_desc(base), dAs = sw64_desc(base + 512);
+          const uint64_t dBb = sw64_desc(base + kBytesA), dBs = sw64_desc(base + kBytesA + 512);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+            mma_tf32_pair(acc, dAs + adv, dBb + adv, idesc, (q.kb | kk) != 0);
+            mma_tf32_pair(acc, dAb + adv, dBs + adv, idesc, 1);
+            mma_tf32_pair(acc, dAb + adv, dBb + adv, idesc, 1);
+          }
+          mma_commit_pair(smem_u32(&freed[s]));
+          if (q.kb == nk - 1) mma_commit_pair(smem_u32(&acc_full[lt & 1]));
+        }
+        rb.advance(sc);
+      }
+    } else if (!kFuse && rank == 0 && lane == 0) {
       constexpr uint32_t idesc = tf32_idesc(2 * kRowsCta, kPairN);
       Ring rp;
       int lt = 0;
@@ -308,140 +369,128 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 2 + kXformWarps) {
     // ------------------------------ transform (both CTAs) ------------------------------
     const int xw = warp - 2;
-    bool canon = noncanon != nullptr && *noncanon == 0;
     const int r8 = lane >> 3, bn = lane & 7;
     const uint32_t ready0 = smem_u32(&ready[0]);
-    int64_t t = cluster;
     float sa0 = 0.f, sa1 = 0.f, sb = 0.f;
-    int st_lt = 0;  // kFuse: tiles of this cluster so far (scale-table slot = st_lt % 4)
-    auto load_scales = [&](int64_t tile) {
-      int64_t b;
-      int prow0, pcol0;
-      grid.at(tile, b, prow0, pcol0);
-      if constexpr (kFuse) {
-        // Eq. 11's clamped scales for this tile, reduced here instead of by a pre-pass
-        // (core.py:252-253): the CTA's 128 A rows (row max over k) and its 128 B columns
-        // (column max over k), read once from HBM; the ring's TMA loads of the same data
-        // then hit L2. The 16 transform warps share the work; the column scales go to both
-        // CTAs' tables (the pair's epilogues need all 256), signalled by sc_full[slot].
-        const int slot = st_lt & (kScaleSlots - 1);
-        float* rs = rowS + slot * kRowsCta;
-        float* cs = colS + slot * kPairN;
-        const int kq = k >> 1;  // float4 (two complex) per row of A
-        const float4* arow = reinterpret_cast<const float4*>(A.at(b) + (int64_t)(prow0 + rank * kRowsCta) * k);
-        bool nc = false;
-#pragma unroll 1
-        for (int r = 0; r < 8; r += 4) {  // rows 8 xw + r .. + 3: 4 rows' loads in flight
-          float mx[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
-          for (int j = lane; j < kq; j += 32) {
-            float4 v[4];
+    if constexpr (kFuse) {
+      // Eq. 11's clamped scales (core.py:252-253) from the scale stages: running maxima of
+      // this lane's A rows (r8, r8 + 4 of group xw) and B column (bn of group xw); at the
+      // tile's last K-block, reduced over the lanes sharing them, clamped at 0, published to
+      // the epilogue tables (the column scales to both CTAs: each epilogue needs all 256)
+      float ma0 = kNegInf, ma1 = kNegInf, mb = kNegInf;
+      bool odd = false, canon = false;
+      int lt_scale = 0;
+      RingBits<kStages> rb;
+      for (FuseSeq q(cluster, nclusters, grid.tiles, nk, late); q.valid(); q.next()) {
+        const int s = rb.s;
+        const bool sc = q.scale();
+        Raw cur;
+        mbar_wait(smem_u32(&full[s]), rb.bit(rb.full));
+        load_raw(ring + s * kStage, xw, lane, cur);
+        if (sc) {
+          ma0 = fmaxf(ma0, fmaxf(cur.a0.x, cur.a0.z));
+          ma1 = fmaxf(ma1, fmaxf(cur.a1.x, cur.a1.z));
+          odd |= odd_phase(cur.a0.y) | odd_phase(cur.a0.w) | odd_phase(cur.a1.y) |
+                 odd_phase(cur.a1.w);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = __ldg(arow + (int64_t)(8 * xw + r + q) * kq + j);
+          for (int j = 0; j < 4; ++j) {
+            mb = fmaxf(mb, cur.b[j].x);
+            odd |= odd_phase(cur.b[j].y);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&sfreed[s]));
+          if (q.block() == nk - 1) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              mx[q] = fmaxf(mx[q], fmaxf(v[q].x, v[q].z));
-              nc |= noncanonical(v[q].y) | noncanonical(v[q].w);
+            for (int o = 1; o < 8; o <<= 1) {
+              ma0 = fmaxf(ma0, __shfl_xor_sync(0xffffffffu, ma0, o));
+              ma1 = fmaxf(ma1, __shfl_xor_sync(0xffffffffu, ma1, o));
             }
+            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+            mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+            sa0 = fmaxf(ma0, 0.0f);
+            sa1 = fmaxf(ma1, 0.0f);
+            sb = fmaxf(mb, 0.0f);
+            canon = !__any_sync(0xffffffffu, odd);
+            const int slot = lt_scale & (kScaleSlots - 1);
+            if (bn == 0) {
+              rowS[slot * kRowsCta + xw * 8 + r8] = sa0;
+              rowS[slot * kRowsCta + xw * 8 + r8 + 4] = sa1;
+            }
+            if (lane < 8) {
+              float* cs = colS + slot * kPairN + rank * (kPairN / 2) + xw * 8 + bn;
+              *cs = sb;
+              st_cluster_f32(smem_u32(cs), rank ^ 1u, sb);
+            }
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive(smem_u32(&sc_full[slot]));                            // local tables
+              mbar_arrive_release_cluster(smem_u32(&sc_full[slot]), rank ^ 1u);  // peer's
+            }
+            ma0 = ma1 = mb = kNegInf;
+            odd = false;
+            ++lt_scale;
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float w = warp_max(mx[q]);
-            if (lane == 0) rs[8 * xw + r + q] = fmaxf(w, 0.0f);
-          }
-        }
-        // columns 2 lane, 2 lane + 1, 64 + 2 lane, 65 + 2 lane of this CTA's 128; rows xw + 16 i
-        const float2* bcol = B.at(b) + pcol0 + rank * (kPairN / 2);
-        float c4[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
-#pragma unroll 1
-        for (int kr = xw; kr < k; kr += 64) {  // 4 rows' loads in flight
-          float4 v[4], w[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int row = kr + 16 * q;
-            const float4* pr = reinterpret_cast<const float4*>(bcol + (int64_t)(row < k ? row : kr) * m);
-            v[q] = __ldg(pr + lane);
-            w[q] = __ldg(pr + 32 + lane);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            c4[0] = fmaxf(c4[0], v[q].x);
-            c4[1] = fmaxf(c4[1], v[q].z);
-            c4[2] = fmaxf(c4[2], w[q].x);
-            c4[3] = fmaxf(c4[3], w[q].z);
-            nc |= noncanonical(v[q].y) | noncanonical(v[q].w) | noncanonical(w[q].y) |
-                  noncanonical(w[q].w);
-          }
-        }
-        atomicMax(&colBits[2 * lane], float_to_ordered(c4[0]));
-        atomicMax(&colBits[2 * lane + 1], float_to_ordered(c4[1]));
-        atomicMax(&colBits[64 + 2 * lane], float_to_ordered(c4[2]));
-        atomicMax(&colBits[65 + 2 * lane], float_to_ordered(c4[3]));
-        if (__any_sync(0xffffffffu, nc) && lane == 0) atomicOr(ncflag, 1);
-        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");
-        const int u = xw * 32 + lane;
-        if (u < kRowsCta) {  // warps 0..3: publish the column scales to both CTAs' tables
-          const float v = fmaxf(ordered_to_float(colBits[u]), 0.0f);
-          colBits[u] = 0u;
-          const int ci = rank * (kPairN / 2) + u;
-          cs[ci] = v;
-          st_cluster_f32(smem_u32(cs + ci), rank ^ 1u, v);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");
-        canon = *ncflag == 0;
-        sa0 = rs[xw * 8 + r8];
-        sa1 = rs[xw * 8 + r8 + 4];
-        sb = cs[rank * (kPairN / 2) + xw * 8 + bn];
-        if (xw < kRowsCta / 32 && lane == 0) {
-          mbar_arrive(smem_u32(&sc_full[slot]));                            // local writes
-          mbar_arrive_release_cluster(smem_u32(&sc_full[slot]), rank ^ 1u);  // peer's table
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kXformWarps * 32) : "memory");  // flag read
-        if (u == 0) *ncflag = 0;
-        ++st_lt;
-      } else {
-        const float* ra = rowA.at(b) + prow0 + rank * kRowsCta + xw * 8;
-        sa0 = ra[r8];
-        sa1 = ra[r8 + 4];
-        sb = colB.at(b)[pcol0 + rank * (kPairN / 2) + xw * 8 + bn];
-      }
-    };
-    if (t < grid.tiles) {
-      load_scales(t);
-      Raw cur, nxt;
-      mbar_wait(smem_u32(&full[0]), 0);
-      load_raw(ring, xw, lane, cur);
-      int kb = 0;
-      Ring rc, rn;  // current stage and the next one
-      rn.next();
-      for (;;) {
-        int64_t tn = t;
-        int kbn = kb + 1;
-        if (kbn == nk) {
-          kbn = 0;
-          tn += nclusters;
-        }
-        const bool more = tn < grid.tiles;
-        const int s = rc.s;
-        if (more) {
-          mbar_wait(smem_u32(&full[rn.s]), rn.ph);
-          load_raw(ring + rn.s * kStage, xw, lane, nxt);
-        }
-        if (debug == 0 || debug == 2 || debug == 4) {
+        } else {
           if (canon)
             store_planes<true>(ring + s * kStage, xw, lane, cur, sa0, sa1, sb);
           else
             store_planes<false>(ring + s * kStage, xw, lane, cur, sa0, sa1, sb);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_rank(ready0 + s * 8, 0);
         }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_rank(ready0 + s * 8, 0);
-        if (!more) break;
-        rc.next();
+        rb.advance(sc);
+      }
+    } else {
+      const bool canon = noncanon != nullptr && *noncanon == 0;
+      int64_t t = cluster;
+      auto load_scales = [&](int64_t tile) {
+        int64_t b;
+        int prow0, pcol0;
+        grid.at(tile, b, prow0, pcol0);
+        const float* ra = rowA.at(b) + prow0 + rank * kRowsCta + xw * 8;
+        sa0 = ra[r8];
+        sa1 = ra[r8 + 4];
+        sb = colB.at(b)[pcol0 + rank * (kPairN / 2) + xw * 8 + bn];
+      };
+      if (t < grid.tiles) {
+        load_scales(t);
+        Raw cur, nxt;
+        mbar_wait(smem_u32(&full[0]), 0);
+        load_raw(ring, xw, lane, cur);
+        int kb = 0;
+        Ring rc, rn;  // current stage and the next one
         rn.next();
-        if (tn != t) load_scales(tn);
-        t = tn;
-        kb = kbn;
-        cur = nxt;
+        for (;;) {
+          int64_t tn = t;
+          int kbn = kb + 1;
+          if (kbn == nk) {
+            kbn = 0;
+            tn += nclusters;
+          }
+          const bool more = tn < grid.tiles;
+          const int s = rc.s;
+          if (more) {
+            mbar_wait(smem_u32(&full[rn.s]), rn.ph);
+            load_raw(ring + rn.s * kStage, xw, lane, nxt);
+          }
+          if (debug == 0 || debug == 2 || debug == 4) {
+            if (canon)
+              store_planes<true>(ring + s * kStage, xw, lane, cur, sa0, sa1, sb);
+            else
+              store_planes<false>(ring + s * kStage, xw, lane, cur, sa0, sa1, sb);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_rank(ready0 + s * 8, 0);
+          if (!more) break;
+          rc.next();
+          rn.next();
+          if (tn != t) load_scales(tn);
+          t = tn;
+          kb = kbn;
+          cur = nxt;
+        }
       }
     }
   } else {
@@ -450,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quad * 32 + lane;
     const uint32_t obuf = smem_u32(smem + kRing) + (uint32_t)(warp - 2 - kXformWarps) * 2 * kStageOut;
     const uint32_t acc_empty0 = smem_u32(&acc_empty[0]);
+    const uint64_t pol_out = policy_evict_first();
     int lt = 0;
     for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
       int64_t b;
@@ -527,7 +577,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) tma_store_3d(&mapC, sbuf, pcol0 + col + 16 * h, wrow0, (int)b);
+          if (lane == 0) {
+            if (kFuse)  // the output streams out: evict_first keeps L2 for the scale-pass lines
+              tma_store_3d_hint(&mapC, sbuf, pcol0 + col + 16 * h, wrow0, (int)b, pol_out);
+            else
+              tma_store_3d(&mapC, sbuf, pcol0 + col + 16 * h, wrow0, (int)b);
+          }
         }
       }
       if (emit.row)

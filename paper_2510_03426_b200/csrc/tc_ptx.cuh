@@ -287,6 +287,16 @@ __device__ __forceinline__ void mbar_arrive_rank(uint32_t bar, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_hint(uint32_t dst, const CUtensorMap* map, int c0,
+                                                 int c1, int c2, int c3, int c4, uint32_t bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar),
+      "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, int c3, int c4, uint32_t bar) {
   asm volatile(
@@ -301,6 +311,16 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
       "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
           reinterpret_cast<uint64_t>(map)),
       "r"(c0), "r"(c1), "r"(c2), "r"(src)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// TMA store with an L2 eviction policy (streamed outputs: evict_first)
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* map, uint32_t src, int c0,
+                                                  int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2, %3}], [%4], %5;" ::"l"(reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(src), "l"(policy)
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -325,6 +345,77 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+
+// Fused-scale kernels (lmme_tc.cu, lmme_tc2.cu kFuse): the ring positions of one CTA (pair)
+// in issue order. The first tile's scale stages, then per tile t the main K-blocks
+// main(t, kb) with the NEXT tile's scale stages interleaved. `late` (nk even): the scale
+// stages come two per main stage in the second half of the tile, so a scale-read line waits
+// ~3/4 of a tile (not a whole one) in L2 for its main-pass re-read; else one per main stage.
+// Every role walks the same sequence, so slot and phase bookkeeping agree.
+struct FuseSeq {
+  int64_t t, step, tiles;
+  int kb, nk, sub, skb;  // sub: 0 main, 1 / 2 scale stage skb of tile t + step
+  bool prologue, late;
+  __device__ __forceinline__ FuseSeq(int64_t t0, int64_t step_, int64_t tiles_, int nk_,
+                                     bool late_ = false)
+      : t(t0), step(step_), tiles(tiles_), kb(0), nk(nk_), sub(0), skb(0), prologue(true),
+        late(late_ && (nk_ % 2) == 0) {}
+  __device__ __forceinline__ bool valid() const { return t < tiles; }
+  __device__ __forceinline__ bool scale() const { return prologue || sub != 0; }
+  // tile whose data the stage holds, and its K-block
+  __device__ __forceinline__ int64_t tile() const { return sub ? t + step : t; }
+  __device__ __forceinline__ int block() const { return prologue ? kb : (sub ? skb : kb); }
+  __device__ __forceinline__ void next() {
+    if (prologue) {
+      if (++kb == nk) {
+        prologue = false;
+        kb = 0;
+      }
+      return;
+    }
+    const bool more = t + step < tiles;
+    if (late) {
+      const int h = nk / 2;
+      if (more && kb >= h && sub < 2) {  // main(kb) -> scale(2 (kb - h)) -> scale(2 (kb - h) + 1)
+        ++sub;
+        skb = 2 * (kb - h) + sub - 1;
+        return;
+      }
+    } else if (more && sub == 0) {
+      sub = 1;
+      skb = kb;
+      return;
+    }
+    sub = 0;
+    if (++kb == nk) {
+      kb = 0;
+      t += step;
+    }
+  }
+};
+
+// per-slot phase bits of the shared ring (kFuse: slots carry main and scale stages)
+template <int STAGES>
+struct RingBits {
+  int s = 0;
+  uint32_t full = 0, mainp = 0, scalep = 0, last_scale = 0, used = 0;
+  __device__ __forceinline__ uint32_t bit(uint32_t v) const { return (v >> s) & 1u; }
+  __device__ __forceinline__ void advance(bool scale) {
+    const uint32_t m = 1u << s;
+    full ^= m;
+    used |= m;
+    if (scale) {
+      scalep ^= m;
+      last_scale |= m;
+    } else {
+      mainp ^= m;
+      last_scale &= ~m;
+    }
+    s = s + 1 == STAGES ? 0 : s + 1;
+  }
+};
+
+__device__ __forceinline__ bool odd_phase(float im) { return im != 0.0f && im != kPi; }
 
 }  // namespace tc
 }  // namespace goom

@@ -11,6 +11,13 @@ d = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 g._lib.load()
+import os
+if os.environ.get("PERSIST_L2_MB"):  # probe: L2 set-aside for evict_last lines
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    torch.cuda.init()
+    if rt is not None:
+        print("set limit rc", rt.cudaDeviceSetLimit(0x06, ctypes.c_size_t(int(os.environ["PERSIST_L2_MB"]) << 20)))
 A = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
 B = torch.ops.goom.from_real(torch.randn(batch, d, d, device="cuda"), float("-inf"), False)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
