@@ -63,6 +63,10 @@ struct LmmeProblemT {
   int64_t emitRowStride;
   R* emitCol;
   int64_t emitColStride;
+  // public entry points only: n = m = k = 64 may take the two-products-per-tile tcgen05
+  // kernel; the scan / selective engines keep lmme_whole's arithmetic (their bitwise
+  // invariants against the CTA-resident engines)
+  bool allow_duo;
 };
 using LmmeProblem = LmmeProblemT<float>;
 
@@ -162,6 +166,8 @@ int lmme_tc(const LmmeProblem& p, cudaStream_t s);
 bool lmme_tc_eligible(int n, int k, int m);
 // one-SM kernel with the scales reduced in-kernel (scale pass through its ring)
 bool lmme_tc1_fuse_scales(int n, int k, int m);
+// n = m = 64: two products per tcgen05 tile, scales in-kernel (GOOM_EUNSUPPORTED otherwise)
+int lmme_tc_duo(const LmmeProblem& p, cudaStream_t s);
 // cta_group::2 pair-tile variant (lmme_tc2.cu) for n, m multiples of 256; lmme_tc() prefers
 // it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s);

@@ -39,6 +39,13 @@ int lmme_run(LmmeProblemT<R> p, void* ws, size_t ws_bytes, cudaStream_t s) {
   const int backend = g_backend.load();
   const bool small = small_shape<R>(p.n, p.k, p.m);
   if (small && !p.rowA.ptr) return lmme_simt_small<R>(p, s);
+  if constexpr (sizeof(R) == 4) {
+    // n = m = 64 (config 2): two products per tcgen05 tile, scales by the kernel's scale pass
+    if (p.allow_duo && backend != 1 && !p.rowA.ptr && !p.colB.ptr && !p.emitRow && !p.emitCol) {
+      const int rc = lmme_tc_duo(p, s);
+      if (rc != GOOM_EUNSUPPORTED) return rc;
+    }
+  }
   // n, k, m <= 64 (and not a tcgen05 shape): one CTA per product, scales fused
   if (whole_shape(p.n, p.k, p.m) && !p.rowA.ptr &&
       !(sizeof(R) == 4 && backend != 1 && lmme_tc_eligible(p.n, p.k, p.m)))
@@ -131,6 +138,7 @@ int lmme_entry(goom_operand A, goom_operand B, goom_operand D, void* C, int64_t 
   p.m = m;
   p.rowA = ScalesT<R>{nullptr, 0, 1};
   p.colB = ScalesT<R>{nullptr, 0, 1};
+  p.allow_duo = true;
   return lmme_run<R>(p, ws, ws_bytes, as_stream(stream));
 }
 

@@ -162,6 +162,7 @@ struct TileGrid {
   int nct, nrt;       // column / row tiles per product
   int64_t b_base;     // first product of this launch
   int64_t tiles;      // tiles in this launch
+  int64_t batch;      // kDuo: products (a tile holds products 2t, 2t + 1)
   __device__ __forceinline__ void at(int64_t t, int64_t& b, int& row0, int& col0, int BN) const {
     const int ct = (int)(t % nct);
     const int64_t q = t / nct;
@@ -193,7 +194,7 @@ struct Emit {
 
 // Persistent kernel: grid = min(tiles, SMs); tiles in row-major (product, row tile, column
 // tile) order, so concurrently resident tiles share operand panels in L2.
-template <int BN, bool kFuse>
+template <int BN, bool kFuse, bool kDuo>
 __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
     lmme_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapB3, const __grid_constant__ CUtensorMap mapC,
@@ -265,12 +266,23 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
     int64_t t = -1;
     const float2* abase;  // the tile's 128 A rows (contiguous)
     int row0, col0, ma, mb;
+    int ma1, mb1;  // kDuo: matrices of the tile's second product
   };
   auto tile_at = [&](int64_t t, TileAt& c) {
     if (c.t == t) return;
+    c.t = t;
+    if constexpr (kDuo) {  // products 2t and 2t + 1 (the last tile of an odd batch repeats 2t)
+      const int64_t b = 2 * t, b1 = b + 1 < grid.batch ? b + 1 : b;
+      c.row0 = c.col0 = 0;
+      c.ma = A.stride == 0 ? 0 : (int)(b / A.div);
+      c.mb = B.stride == 0 ? 0 : (int)(b / B.div);
+      c.ma1 = A.stride == 0 ? 0 : (int)(b1 / A.div);
+      c.mb1 = B.stride == 0 ? 0 : (int)(b1 / B.div);
+      c.abase = A.ptr;
+      return;
+    }
     int64_t b;
     grid.at(t, b, c.row0, c.col0, BN);
-    c.t = t;
     c.ma = A.stride == 0 ? 0 : (int)(b / A.div);
     c.mb = B.stride == 0 ? 0 : (int)(b / B.div);
     c.abase = A.at(b) + (int64_t)c.row0 * k;
@@ -281,6 +293,16 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
     mbar_expect_tx(bar, G::kStage);
     const uint32_t dst = ring + s * G::kStage;
     const int k0 = kb * BK;
+    if constexpr (kDuo) {
+      // [product 0: 64 rows | product 1: 64 rows][16 k]; B groups 0-7 product 0, 8-15 product 1
+      const uint64_t pol = scale ? pol_keep : pol_drop;
+      tma_load_3d_hint(dst, &mapA, k0, 0, c.ma, bar, pol);
+      tma_load_3d_hint(dst + G::kBytesA / 2, &mapA, k0, 0, c.ma1, bar, pol);
+      tma_load_4d_hint(dst + G::kBytesA, &mapB, 0, k0, 0, c.mb, bar, pol);
+      tma_load_4d_hint(dst + G::kBytesA + (G::kStage - G::kBytesA) / 2, &mapB, 0, k0, 0, c.mb1, bar,
+                       pol);
+      return;
+    }
     if (scale && rowsA)  // float4 chunk kb of the tile's 128 contiguous A rows
       bulk_g2s(dst, c.abase + kb * (G::kBytesA / 8), G::kBytesA, bar);
     else if (hints)  // kFuse: the scale pass keeps its lines for the main pass, which frees them
@@ -299,7 +321,20 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
   if (warp == 0) {
     // ------------------------------ loader ------------------------------
     if (lane == 0) {
-      if constexpr (kFuse) {
+      if constexpr (kDuo) {
+        // resident tiles: each K-block is loaded once; the transform reduces the scales from
+        // the landed stages of the whole tile before it transforms any of them
+        TileAt c;
+        int64_t g = 0;
+        for (int64_t t = blockIdx.x; t < grid.tiles; t += gridDim.x) {
+          tile_at(t, c);
+          for (int kb = 0; kb < nk; ++kb, ++g) {
+            const int s = (int)(g % STAGES);
+            mbar_wait(smem_u32(&freed[s]), (uint32_t)((g / STAGES) & 1) ^ 1u);
+            issue_loads(s, c, kb, false);
+          }
+        }
+      } else if constexpr (kFuse) {
         // L2 prefetch of a whole tile (A panel, and the B panel when it is contiguous) `pf`
         // tiles ahead of the main loop, so its scale stages hit L2 (GOOM_TC_PREFETCH)
         auto prefetch_tile = [&](int64_t tp) {
@@ -365,7 +400,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
           mma_tf32(acc, dAb + adv, dBb + adv, idesc, 1);
         }
       };
-      if constexpr (kFuse) {
+      if constexpr (kFuse && !kDuo) {
         RingBits<STAGES> rb;
         int gpos = 0;
         int lt = -1;  // local tile counter -> accumulator buffer lt & 1
@@ -415,7 +450,63 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
     const int xw = warp - 2;
     const int r = lane >> 3, bn = lane & 7;
     float sa0 = 0.f, sa1 = 0.f, sb[2] = {0.f, 0.f};
-    if constexpr (kFuse) {
+    if constexpr (kDuo) {
+      // resident tiles (k = 64: a tile's 4 K-blocks fit the ring): wait for all of them,
+      // reduce this lane's row / column maxima from the landed raw stages, publish the
+      // tables, then transform every stage in place (re-read from shared memory)
+      int64_t g = 0;
+      int lt = 0;
+      for (int64_t t = blockIdx.x; t < grid.tiles; t += gridDim.x, ++lt, g += nk) {
+        float ma0 = kNegInf, ma1 = kNegInf, mb = kNegInf;
+        bool odd = false;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int s = (int)((g + kb) % STAGES);
+          mbar_wait(smem_u32(&full[s]), (uint32_t)(((g + kb) / STAGES) & 1));
+          RawStage<G::kGroupsB> cur;
+          load_stage<G::kGroupsB>(ring + s * G::kStage, xw, lane, cur);
+          ma0 = fmaxf(ma0, fmaxf(cur.a0.x, cur.a0.z));
+          ma1 = fmaxf(ma1, fmaxf(cur.a1.x, cur.a1.z));
+          odd |= odd_phase(cur.a0.y) | odd_phase(cur.a0.w) | odd_phase(cur.a1.y) |
+                 odd_phase(cur.a1.w);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            mb = fmaxf(mb, cur.b[0][j].x);
+            odd |= odd_phase(cur.b[0][j].y);
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          ma0 = fmaxf(ma0, __shfl_xor_sync(0xffffffffu, ma0, o));
+          ma1 = fmaxf(ma1, __shfl_xor_sync(0xffffffffu, ma1, o));
+        }
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+        mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+        sa0 = fmaxf(ma0, 0.0f);
+        sa1 = fmaxf(ma1, 0.0f);
+        sb[0] = fmaxf(mb, 0.0f);
+        const bool canon = !__any_sync(0xffffffffu, odd);
+        const int slot = lt & (kScaleSlots - 1);
+        if (bn == 0) {
+          rowS[slot * BM + xw * 8 + r] = sa0;
+          rowS[slot * BM + xw * 8 + r + 4] = sa1;
+        }
+        if (lane < 8) colS[slot * BN + xw * 8 + bn] = sb[0];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sc_full[slot]));
+        for (int kb = 0; kb < nk; ++kb) {
+          const int s = (int)((g + kb) % STAGES);
+          RawStage<G::kGroupsB> cur;
+          load_stage<G::kGroupsB>(ring + s * G::kStage, xw, lane, cur);
+          if (canon)
+            store_stage<G::kGroupsB, true>(ring + s * G::kStage, xw, lane, cur, sa0, sa1, sb);
+          else
+            store_stage<G::kGroupsB, false>(ring + s * G::kStage, xw, lane, cur, sa0, sa1, sb);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&ready[s]));
+        }
+      }
+    } else if constexpr (kFuse) {
       // scale stages: running maxima of this lane's A rows (r, r + 4 of group xw) and B
       // column (bn of group xw) over its k; at a tile's last K-block, reduce over the lanes
       // sharing them, clamp at 0 and publish (core.py:252-253)
@@ -564,13 +655,22 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
     const int e = warp - 2 - kXformWarps;
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const int c_begin = (e >> 2) * G::kEpiCols;  // this warp's accumulator columns
+    // this warp's accumulator columns (kDuo: the diagonal block of its rows' product only)
+    const int half = quad >> 1;
+    const int c_begin = kDuo ? 64 * half + 32 * (e >> 2) : (e >> 2) * G::kEpiCols;
+    constexpr int kCols = kDuo ? 32 : G::kEpiCols;
     const uint32_t stage = ring + G::kOut + (uint32_t)(e * G::kStageOut);
     int lt = 0;
     for (int64_t t = blockIdx.x; t < grid.tiles; t += gridDim.x, ++lt) {
       int64_t b;
       int row0, col0;
-      grid.at(t, b, row0, col0, BN);
+      if constexpr (kDuo) {
+        b = 2 * t + half;  // this warp's product; its rows / columns start at 64 * half
+        row0 = col0 = -64 * half;
+      } else {
+        grid.at(t, b, row0, col0, BN);
+      }
+      const bool live = !kDuo || b < grid.batch;
       const int buf = lt & 1;
       if (e == 0 && lane == 0) TC_TRACE(5, lt, clock64());
       mbar_wait(smem_u32(&acc_full[buf]), (uint32_t)((lt >> 1) & 1));
@@ -591,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
       const float2* drow = D.ptr ? D.at(b) + (int64_t)(row0 + row) * m + col0 : nullptr;
       uint32_t rmax = 0;  // bits of max(log, 0): non-negative floats order like uints
 #pragma unroll 1
-      for (int col = c_begin; col < (debug == 7 ? c_begin : c_begin + G::kEpiCols); col += 32) {
+      for (int col = c_begin; col < (debug == 7 || !live ? c_begin : c_begin + kCols); col += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + col), v);
         // kSub columns per staging round: [32 rows][kSub] complex64, 16-byte chunks XOR-swizzled
@@ -657,7 +757,7 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
           }
         }
       }
-      if (emit.row)
+      if (!kDuo && emit.row)
         atomicMax(reinterpret_cast<unsigned int*>(emit.row + b * emit.row_stride + row0 + row), rmax);
       tc_fence_before();
       __syncwarp();
@@ -688,10 +788,11 @@ int tc_debug() {
   return v;
 }
 
-template <int BN, bool kFuse>
+template <int BN, bool kFuse, bool kDuo = false>
 int launch_tc(const LmmeProblem& p, cudaStream_t s) {
   using G = Cfg<BN, kFuse>;
-  GOOM_TRY(smem_attr((const void*)lmme_tc_kernel<BN, kFuse>, G::kSmem, "lmme_tc smem attribute"));
+  GOOM_TRY(smem_attr((const void*)lmme_tc_kernel<BN, kFuse, kDuo>, G::kSmem, "lmme_tc smem attribute"));
+  constexpr int kRowsBox = kDuo ? BM / 2 : BM;  // kDuo: each product half is its own box
   alignas(64) CUtensorMap mapA, mapB;
   int64_t mats, mstride;
   // A: (k, n, matrix) complex64 moved as int64, box 16 k x 128 rows
@@ -699,7 +800,7 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
   {
     cuuint64_t dims[3] = {(cuuint64_t)p.k, (cuuint64_t)p.n, (cuuint64_t)mats};
     cuuint64_t strides[2] = {(cuuint64_t)p.k * 8, (cuuint64_t)mstride * 8};
-    cuuint32_t box[3] = {BK, BM, 1};
+    cuuint32_t box[3] = {BK, kRowsBox, 1};
     GOOM_TRY(encode(&mapA, p.A, 3, dims, strides, box));
   }
   // B: (8 cols, k, m/8 column groups, matrix), box 8 x 16 k x BN/8 -> [group][k][8] in smem
@@ -707,7 +808,7 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
   {
     cuuint64_t dims[4] = {8, (cuuint64_t)p.k, (cuuint64_t)(p.m / 8), (cuuint64_t)mats};
     cuuint64_t strides[3] = {(cuuint64_t)p.m * 8, 64, (cuuint64_t)mstride * 8};
-    cuuint32_t box[4] = {8, BK, BN / 8, 1};
+    cuuint32_t box[4] = {8, BK, (kDuo ? BN / 2 : BN) / 8, 1};
     GOOM_TRY(encode(&mapB, p.B, 4, dims, strides, box));
   }
   alignas(64) CUtensorMap mapB3;  // GOOM_TC_DEBUG=6 only: B as [16 k][BN] rows of BN*8 bytes
@@ -730,14 +831,15 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
     GOOM_TRY(encode(&mapC, Operand{p.C, 0, 1}, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   TileGrid tg;
-  tg.nct = p.m / BN;
-  tg.nrt = p.n / BM;
+  tg.nct = kDuo ? 1 : p.m / BN;
+  tg.nrt = kDuo ? 1 : p.n / BM;
   tg.b_base = 0;
-  tg.tiles = p.batch * tg.nct * tg.nrt;
+  tg.batch = p.batch;
+  tg.tiles = kDuo ? (p.batch + 1) / 2 : p.batch * tg.nct * tg.nrt;
   const int64_t sms = num_sms();
   const unsigned grid = (unsigned)(tg.tiles < sms ? tg.tiles : sms);
   Emit emit{p.emitRow, p.emitRowStride, p.emitCol, p.emitColStride};
-  lmme_tc_kernel<BN, kFuse><<<grid, G::kThreads, G::kSmem, s>>>(
+  lmme_tc_kernel<BN, kFuse, kDuo><<<grid, G::kThreads, G::kSmem, s>>>(
       mapA, mapB, mapB3, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C, p.strideC, tg, p.n, p.k, p.m, p.noncanon,
       emit, tc_debug());
   GOOM_CHECK_LAUNCH("lmme_tc_kernel");
@@ -767,6 +869,25 @@ bool lmme_tc1_fuse_scales(int n, int k, int m) {
   if (!lmme_tc_eligible(n, k, m) || k < 4 * BK) return false;
   const int f = tc_fuse_mode();
   return f == 1 || (f < 0 && n == 128 && m == 128);
+}
+
+// n = m = 64 (config 2's smallest shape): two products per 128 x 128 tile, A rows
+// [product 2t | product 2t + 1], B columns likewise; the MMA also forms the two cross blocks,
+// which the epilogue drops (the tensor core has the headroom: the shape is HBM-bound).
+// k = 64: a tile's four K-blocks (128 KB) fit the ring, so they are loaded ONCE and the
+// transform reduces the clamped scales from the landed stages before transforming them
+// (no second read). No row / column emission.
+bool lmme_tc_duo_eligible(int n, int k, int m) {
+  return n == 64 && m == 64 && k == 64 && tc_fuse_mode() != 0;  // a tile's K-blocks fit the ring
+}
+
+int lmme_tc_duo(const LmmeProblem& p, cudaStream_t s) {
+  if (!lmme_tc_duo_eligible(p.n, p.k, p.m) || p.rowA.ptr || p.colB.ptr || p.emitRow || p.emitCol)
+    return GOOM_EUNSUPPORTED;
+  if (((reinterpret_cast<uintptr_t>(p.A.ptr) | reinterpret_cast<uintptr_t>(p.B.ptr)) & 15) ||
+      ((p.A.stride | p.B.stride) & 1))
+    return GOOM_EUNSUPPORTED;
+  return launch_tc<128, true, true>(p, s);
 }
 
 int lmme_tc(const LmmeProblem& p, cudaStream_t s) {
