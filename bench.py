@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--seed", type=int, default=2510)
     p.add_argument("--cpu-sample", type=int, default=128, help="leaves in the CPU baseline sample")
     p.add_argument("--e2e-T", type=int, default=8192)
+    p.add_argument("--e2e-goom-T", type=int, default=4096,
+                   help="leaves of the drop-in-boundary e2e (complex64 GOOMs from pinned host)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-reanchor", action="store_true", help="skip the re-anchored checks")
     return p.parse_args()
@@ -465,6 +467,74 @@ def main():
     h2d_gbs = host.numel() * host.element_size() / (min(h2d_ms) / 1e3) / 1e9
     del dcopy
 
+    # ---- e2e at the drop-in boundary: complex64 GOOM leaves (the reference's own data
+    # format: log|x| + sign, scan.py:138-170) in pinned host memory -> the public drop-in scan
+    # (torch.ops.goom.scan_chain = goom_scan_chain_c64, the _scan_affine_stack path, exact
+    # complex64 engine) window by window; the H2D copy of window w+1 runs on a copy stream
+    # under the scan of window w; per-prefix digests D2H. Every leaf crosses PCIe at 8 B per
+    # element (twice the real-float32 variant above), so this is the link-bound figure.
+    Tg = max(args.e2e_goom_T // world, 1) * world
+    t0g, ng = sharded.shard_range(Tg, rank, world)
+    wg = max(1, min(512, ng))
+    hostg = torch.empty((ng, d, d), dtype=torch.complex64).pin_memory()
+    for w0 in range(0, ng, wg):
+        n = min(wg, ng - w0)
+        hostg[w0:w0 + n].copy_(harness.random_chain(n, d, args.seed + 11, t0g + w0, dev))
+    copy_stream = torch.cuda.Stream()
+    bufs = [torch.empty((wg, d, d), dtype=torch.complex64, device=dev) for _ in range(2)]
+    free_ev = [torch.cuda.Event(), torch.cuda.Event()]
+    goom_times = []
+    nw = (ng + wg - 1) // wg
+    for it in range(2):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        carry = None
+        if world > 1:  # the shard's exclusive carry (one all-gather of the shard totals)
+            dl = hostg.to(dev, non_blocking=True)
+            carry = sharded.exclusive_carry(harness.chain_total(dl), torch.ops.goom.lmme)
+            del dl
+        dig = torch.empty((ng, 4), dtype=torch.float32, device=dev)
+        cur = torch.cuda.current_stream()
+        landed = []
+
+        def issue(i):  # H2D of window i on the copy stream, into the buffer window i - 2 freed
+            w0 = i * wg
+            n = min(wg, ng - w0)
+            with torch.cuda.stream(copy_stream):
+                if i >= 2:
+                    copy_stream.wait_event(free_ev[i % 2])
+                bufs[i % 2][:n].copy_(hostg[w0:w0 + n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                landed.append(ev)
+
+        issue(0)
+        for i in range(nw):
+            if i + 1 < nw:
+                issue(i + 1)
+            w0 = i * wg
+            n = min(wg, ng - w0)
+            cur.wait_event(landed[i])
+            P = torch.ops.goom.scan_chain(bufs[i % 2][:n], args.block, carry)
+            dig[w0:w0 + n] = torch.ops.goom.digest(P)
+            carry = P[n - 1].clone()
+            free_ev[i % 2].record(cur)
+            del P
+        out = dig.to("cpu", non_blocking=True)
+        e.record()
+        barrier()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        if it > 0:
+            goom_times.append(ms)
+        del out, dig
+    goom_value = Tg / (statistics.median(goom_times) / 1e3)
+    del hostg, bufs
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt = cpu_chain_rate(d, args.cpu_sample, args.seed)
@@ -500,12 +570,21 @@ def main():
                                         "frac": step_tf / peak_s,
                                         "note": "4 d^3 flop per chain element (2 LMMEs), "
                                                 "per GPU, vs the sustained 3xTF32 peak"}},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": ne * d * d * 4,
-                    "d2h_bytes_per_step": ne * 16,
-                    "h2d_gbs_per_gpu": ne * d * d * 4 / (statistics.median(e2e_times) / 1e3) / 1e9,
+            "e2e": {"value": goom_value, "unit": UNIT, "h2d_bytes_per_step": ng * d * d * 8,
+                    "d2h_bytes_per_step": ng * 16,
+                    "h2d_gbs_per_gpu": ng * d * d * 8 / (statistics.median(goom_times) / 1e3) / 1e9,
                     "h2d_gbs_plain_copy_in_run": h2d_gbs,
-                    "workload": f"T={Te} real float32 leaves in pinned host memory -> "
-                                f"harness.run_chain (window {we}, H2D overlapped), digests D2H"},
+                    "workload": f"T={Tg} complex64 GOOM leaves (log|x| + sign, the reference's "
+                                f"format) in pinned host memory -> the drop-in scan "
+                                f"(torch.ops.goom.scan_chain / goom_scan_chain_c64, window {wg}, "
+                                f"H2D of the next window overlapped), per-prefix digests D2H",
+                    "real_f32_leaves": {
+                        "value": e2e_value, "h2d_bytes_per_step": ne * d * d * 4,
+                        "d2h_bytes_per_step": ne * 16,
+                        "h2d_gbs_per_gpu": ne * d * d * 4 / (statistics.median(e2e_times) / 1e3) / 1e9,
+                        "workload": f"T={Te} real float32 leaves in pinned host memory -> "
+                                    f"harness.run_chain (window {we}, H2D overlapped), digests D2H "
+                                    f"(the chain experiment's input, SPEC.md:391-455)"}},
             "gpu_launches": launches // max(args.steps, 1),
             "clocks": clocks.summary(),
             "check": {"finite": finite, "growth_per_step": growth,

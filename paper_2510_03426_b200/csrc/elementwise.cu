@@ -81,9 +81,9 @@ __global__ void __launch_bounds__(256)
     ssm_export_kernel(const double2* __restrict__ X, int64_t L, int d, int64_t S, int64_t nC,
                       int64_t T, double* __restrict__ sl, double* __restrict__ ss,
                       double* __restrict__ cvec, double* __restrict__ z, int reverse,
-                      const double* __restrict__ kshift) {
+                      const double* __restrict__ kshift, int64_t hi0) {
   __shared__ double2 tile[64][kExportCols + 1];
-  const int64_t hi = blockIdx.y, N = S * nC;
+  const int64_t hi = hi0 + blockIdx.y, N = S * nC;  // (head, step) slice: grid.y <= 65535
   const int64_t h = hi / L, i = hi % L;
   const int64_t n0 = (int64_t)blockIdx.x * kExportCols;
   const int ncols = (int)(N - n0 < kExportCols ? N - n0 : kExportCols);
@@ -121,9 +121,10 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     ssm_panels_kernel(const double* __restrict__ hsrc, const double* __restrict__ K,
                       const double* __restrict__ cs, int64_t H, int64_t L, int d, int64_t S,
-                      int64_t nC, int64_t T, int reverse, double2* __restrict__ out) {
+                      int64_t nC, int64_t T, int reverse, double2* __restrict__ out,
+                      int64_t ih0) {
   __shared__ double2 tile[64][kExportCols + 1];
-  const int64_t ih = blockIdx.y, i = ih / H, h = ih % H, N = S * nC;
+  const int64_t ih = ih0 + blockIdx.y, i = ih / H, h = ih % H, N = S * nC;
   const int64_t n0 = (int64_t)blockIdx.x * kExportCols;
   const int ncols = (int)(N - n0 < kExportCols ? N - n0 : kExportCols);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -350,12 +351,15 @@ int ssm_export(const void* X, int64_t H, int64_t L, int d, int64_t S, int64_t nC
     return fail(GOOM_ESHAPE, "ssm_export: need 1 <= d <= 64, L >= 1, T <= nC * L");
   if (H == 0 || S == 0 || T == 0) return GOOM_OK;
   if (!X || !sl || !ss) return fail(GOOM_EINVAL, "null pointer");
-  if (H * L > 65535) return fail(GOOM_EUNSUPPORTED, "ssm_export: H * L > 65535");
-  const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)(H * L));
-  ssm_export_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(X), L,
-                                                        d, S, nC, T, sl, ss, c, z, reverse,
-                                                        kshift);
-  GOOM_CHECK_LAUNCH("ssm_export");
+  // H * L (head, step) rows ride in grid.y, launched in slices of at most 65535
+  for (int64_t hi0 = 0; hi0 < H * L; hi0 += 65535) {
+    const int64_t rows = H * L - hi0 < 65535 ? H * L - hi0 : 65535;
+    const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)rows);
+    ssm_export_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(X), L,
+                                                          d, S, nC, T, sl, ss, c, z, reverse,
+                                                          kshift, hi0);
+    GOOM_CHECK_LAUNCH("ssm_export");
+  }
   return GOOM_OK;
 }
 
@@ -365,11 +369,13 @@ int ssm_panels(const double* h, const double* K, const double* c, int64_t H, int
     return fail(GOOM_ESHAPE, "ssm_panels: need 1 <= d <= 64, L >= 1, T == nC * L");
   if (H == 0 || S == 0 || T == 0) return GOOM_OK;
   if (!h || !out || (K && !c)) return fail(GOOM_EINVAL, "null pointer");
-  if (H * L > 65535) return fail(GOOM_EUNSUPPORTED, "ssm_panels: H * L > 65535");
-  const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)(H * L));
-  ssm_panels_kernel<<<grid, 256, 0, as_stream(stream)>>>(h, K, c, H, L, d, S, nC, T, reverse,
-                                                        reinterpret_cast<double2*>(out));
-  GOOM_CHECK_LAUNCH("ssm_panels");
+  for (int64_t ih0 = 0; ih0 < H * L; ih0 += 65535) {  // grid.y slices of at most 65535
+    const int64_t rows = H * L - ih0 < 65535 ? H * L - ih0 : 65535;
+    const dim3 grid((unsigned)((S * nC + kExportCols - 1) / kExportCols), (unsigned)rows);
+    ssm_panels_kernel<<<grid, 256, 0, as_stream(stream)>>>(h, K, c, H, L, d, S, nC, T, reverse,
+                                                          reinterpret_cast<double2*>(out), ih0);
+    GOOM_CHECK_LAUNCH("ssm_panels");
+  }
   return GOOM_OK;
 }
 

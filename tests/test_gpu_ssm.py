@@ -341,3 +341,27 @@ def test_ssm_chunked_contractive_powers_keep_the_carry(s):
         assert normal[2000:].any()  # the states after chunk 31 are representable
         assert np.all(np.isfinite(sl[0, i][normal]))
         assert rel_log(np.where(normal, sl[0, i], 0.0), np.where(normal, seq.state_log, 0.0)) < 1e-9
+
+
+def test_ssm_heads_past_grid_y_limit(s):
+    """H * L > 65535 (head, step) rows: the panel / export kernels launch in grid.y slices
+     instead of refusing; heads on both sides of the slice boundary match the
+    per-head single-sequence path, forward and backward."""
+    rng = np.random.default_rng(65536)
+    H, S, T, d, L = 2100, 1, 64, 2, 32  # H * L = 67200
+    A = rng.standard_normal((H, d, d)) * 0.5
+    B, C, D = (rng.standard_normal((H, r, d)) for r in (d, 2 * d, 2 * d))
+    x0s, us = rng.standard_normal((H, S, d)), rng.standard_normal((H, S, T, d))
+    gy = rng.standard_normal((H, S, T, 2 * d))
+    sl, ss, c, y = (t.cpu().numpy() for t in s.ssm_forward_heads(A, B, C, D, x0s, us, chunk=L))
+    grads = [t.cpu().numpy() for t in s.ssm_backward_heads(A, B, C, D, x0s, us, sl, ss, c, gy,
+                                                           chunk=L)]
+    for h in (0, 2047, 2048, H - 1):  # rows h L + i on both sides of 65535
+        p = s.SsmParams(A[h], B[h], C[h], D[h])
+        run = s.ssm_forward_parallel(p, x0s[h, 0], us[h, 0], block_size=32)
+        assert rel_log(sl[h, 0], run.state_log) < 1e-10
+        np.testing.assert_allclose(y[h, 0], run.y, rtol=1e-9, atol=1e-12)
+        g = s.ssm_backward(p, run, gy[h, 0], chunk=32)
+        for k, got in zip("ABCD", grads[:4]):
+            assert _rel_max(got[h], getattr(g, k)) < 1e-9, (h, k)
+        assert _rel_max(grads[5][h, 0], g.u) < 1e-9
