@@ -168,6 +168,11 @@ bool lmme_tc_eligible(int n, int k, int m);
 bool lmme_tc1_fuse_scales(int n, int k, int m);
 // n = m = 64: two products per tcgen05 tile, scales in-kernel (GOOM_EUNSUPPORTED otherwise)
 int lmme_tc_duo(const LmmeProblem& p, cudaStream_t s);
+// long-chain fold for d = 64 complex64 on tcgen05 (scan_long64.cu): chains of s leaves,
+// chain k from carry0 (k = 0) / carries[k - 1], or its first leaf; out: every prefix,
+// tot: every chain's last state
+int launch_fold64(const float2* A, int64_t T, int64_t s, const float2* carry0,
+                  const float2* carries, float2* out, float2* tot, cudaStream_t st);
 // cta_group::2 pair-tile variant (lmme_tc2.cu) for n, m multiples of 256; lmme_tc() prefers
 // it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s);
@@ -191,7 +196,9 @@ template <class R>
 int chain_scan_cta(const Cx<R>* A, Cx<R>* out, int64_t T, int d, int64_t s,
                    const Cx<R>* carry_in, Cx<R>* L, Cx<R>* Cx_, cudaStream_t st);
 
-// d <= 32 long-chain engine (scan_long.cu): reduce-then-scan, a different fixed tree
+// d <= 32 (and d = 64 complex64) long-chain engine (scan_long.cu): reduce-then-scan, a
+// different fixed tree
+template <class R>
 bool chain_long_eligible(int d);
 template <class R>
 size_t chain_long_workspace_bytes(int64_t T, int d);

@@ -1,4 +1,5 @@
-// Long-chain scan for small matrices (d <= 32): reduce-then-scan over LMME combines.
+// Long-chain scan for small matrices (d <= 32; d = 64 complex64 folds on tcgen05,
+// scan_long64.cu): reduce-then-scan over LMME combines.
 //
 // The reference's two-level tree (_scan_affine_stack, scan.py:181-214) has a sequential
 // depth of s + T/s combines — ~2,000 dependent LMMEs at T = 2^20 however s is chosen —
@@ -271,6 +272,9 @@ int launch_fold_d(const Cx<R>* A, int64_t T, int d, int64_t s, const Cx<R>* carr
 template <class R>
 int launch_fold(const Cx<R>* A, int64_t T, int d, int64_t s, const Cx<R>* carry0,
                 const Cx<R>* carries, Cx<R>* out, Cx<R>* tot, cudaStream_t st) {
+  if constexpr (sizeof(R) == 4) {  // d = 64: the tcgen05 fold (scan_long64.cu)
+    if (d == 64) return launch_fold64(A, T, s, carry0, carries, out, tot, st);
+  }
   if (d <= 8) return launch_fold_d<R, 8>(A, T, d, s, carry0, carries, out, tot, st);
   if (d <= 16) return launch_fold_d<R, 16>(A, T, d, s, carry0, carries, out, tot, st);
   return launch_fold_d<R, 32>(A, T, d, s, carry0, carries, out, tot, st);
@@ -292,7 +296,8 @@ int long_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, const Cx<R>* carry_i
 
 }  // namespace
 
-bool chain_long_eligible(int d) { return d >= 1 && d <= 32; }
+template <class R>
+bool chain_long_eligible(int d) { return (d >= 1 && d <= 32) || (sizeof(R) == 4 && d == 64); }
 
 template <class R>
 size_t chain_long_workspace_bytes(int64_t T, int d) {
@@ -310,12 +315,15 @@ size_t chain_long_workspace_bytes(int64_t T, int d) {
 template <class R>
 int chain_scan_long(const Cx<R>* A, Cx<R>* out, int64_t T, int d, const Cx<R>* carry_in,
                     void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (!chain_long_eligible(d)) return fail(GOOM_EUNSUPPORTED, "long-chain scan needs d <= 32");
+  if (!chain_long_eligible<R>(d))
+    return fail(GOOM_EUNSUPPORTED, "long-chain scan needs d <= 32 (or d = 64, complex64)");
   if (ws_bytes < chain_long_workspace_bytes<R>(T, d) || !ws)
     return fail(GOOM_EWORKSPACE, "long-chain scan workspace too small");
   return long_scan<R>(A, out, T, d, carry_in, reinterpret_cast<char*>(ws), st, 0);
 }
 
+template bool chain_long_eligible<float>(int);
+template bool chain_long_eligible<double>(int);
 template size_t chain_long_workspace_bytes<float>(int64_t, int);
 template size_t chain_long_workspace_bytes<double>(int64_t, int);
 template int chain_scan_long<float>(const float2*, float2*, int64_t, int, const float2*, void*,
@@ -343,11 +351,11 @@ int long_entry(const void* A, void* out, int64_t T, int d, const void* carry_in,
 extern "C" {
 
 size_t goom_scan_chain_long_workspace_size(int64_t T, int d) {
-  if (T < 1 || !chain_long_eligible(d)) return 0;
+  if (T < 1 || !chain_long_eligible<float>(d)) return 0;
   return chain_long_workspace_bytes<float>(T, d);
 }
 size_t goom_scan_chain_long_workspace_size_c128(int64_t T, int d) {
-  if (T < 1 || !chain_long_eligible(d)) return 0;
+  if (T < 1 || !chain_long_eligible<double>(d)) return 0;
   return chain_long_workspace_bytes<double>(T, d);
 }
 int goom_scan_chain_long_c64(const goom_c64* A, goom_c64* out, int64_t T, int d,

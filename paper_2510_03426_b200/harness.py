@@ -49,6 +49,11 @@ def _snapshot_set(T: int, t0: int, snapshot_every: int, snapshots: Sequence[int]
     return want
 
 
+def long_chain_eligible(d: int, dtype) -> bool:
+    """The long-chain engine (ops.scan_chain_long) takes d <= 32, and d = 64 in complex64."""
+    return d <= 32 or (d == 64 and dtype == torch.complex64)
+
+
 def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
               t0: int = 0, carry: Optional[torch.Tensor] = None, snapshot_every: int = 0,
               leaves: Optional[torch.Tensor] = None, snapshots: Sequence[int] = (),
@@ -70,7 +75,7 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
 
     d % 256 == 0 runs on the tile-scaled engine (ops.chain_ts): leaves are generated
     (or imported) tile-scaled, prefixes are digested inside the phase-3 LMME epilogue
-    and the carry between windows stays tile-scaled. d <= 32 runs the long-chain engine
+    and the carry between windows stays tile-scaled. d <= 32 and d = 64 run the long-chain engine
     (ops.scan_chain_long); other d the complex64 block-tree scan. Both + digest kernels."""
     want = _snapshot_set(T, t0, snapshot_every, snapshots)
     if ops.ts_eligible(d):
@@ -85,7 +90,7 @@ def run_chain(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64
         A = leaves[w0:w0 + n] if leaves is not None else random_chain(n, d, seed, t0 + w0, dev)
         # d <= 32: the long-chain engine (scan_long.cu; a fixed reduce-then-scan tree, the
         # block size only shapes the reference tree the other engines keep)
-        P = (torch.ops.goom.scan_chain_long(A, carry) if d <= 32 else
+        P = (torch.ops.goom.scan_chain_long(A, carry) if long_chain_eligible(d, A.dtype) else
              torch.ops.goom.scan_chain(A, block, carry))
         digests[w0:w0 + n] = torch.ops.goom.digest(P)
         for t in range(w0, w0 + n):
@@ -279,7 +284,7 @@ def chain_survival(cfg: ChainConfig) -> ChainResult:
         ct = torch.complex128 if cfg.backend == "goom64" else torch.complex64
         for L in leaves:
             L = L.to(ct)
-            P = torch.ops.goom.scan_chain_long(L, None) if d <= 32 else \
+            P = torch.ops.goom.scan_chain_long(L, None) if long_chain_eligible(d, L.dtype) else \
                 torch.ops.goom.scan_chain(L, 64, None)
             lg = P.real.reshape(T, -1)
             bad = torch.isnan(lg).any(dim=1) | torch.isposinf(lg).any(dim=1)

@@ -122,6 +122,63 @@ def test_long_chain_underflow_and_zeros_follow_the_clamp(g):
     assert np.all(rl[-1] == -np.inf) and np.all(gl[-1] == -np.inf)  # both flushed at t = 299
 
 
+@pytest.mark.parametrize("T,with_carry", [(1, True), (2, False), (63, False), (64, True),
+                                          (65, False), (130, True), (700, False), (4500, True)])
+def test_long_chain_d64_tcgen05_matches_oracle(g, T, with_carry):
+    """d = 64 complex64 folds on tcgen05 (scan_long64.cu: two chains per MMA, 3xTF32): one to
+    three levels of recursion (4,500 = 71 chains of 64 -> 5 of 16 -> one), an odd chain count
+    (a pair with one chain missing), ragged tails, chains that start from their first leaf
+    and from a carry, against the float64 oracle by the §8c chain criterion (scaled-real floor
+    for the tensor core's truncating FP32 accumulation, goom_testlib.tc_chain_scaled_floor)."""
+    from goom_testlib import tc_chain_scaled_floor
+
+    d = 64
+    rng = np.random.default_rng(64 + T)
+    x = rng.standard_normal((T, d, d))
+    al, as_ = G.log_sign(x)
+    if with_carry:
+        c = rng.standard_normal((d, d))
+        cl, cs = G.log_sign(c)
+        out = torch.ops.goom.scan_chain_long(g.join(al, as_), g.join(cl, cs))
+        xl, xs = np.concatenate([cl[None], al]), np.concatenate([cs[None], as_])
+        wl, ws = G.chain_blocked(xl, xs, T + 1)
+        want = (wl[1:], ws[1:])
+        x32 = np.concatenate([c[None], x]).astype(np.float32)
+        l32, s32 = G.log_sign(x32)
+        refs = [tuple(v[1:] for v in G.chain_blocked(l32, s32, T + 1))]
+    else:
+        out = torch.ops.goom.scan_chain_long(g.join(al, as_), None)
+        want = G.chain_blocked(al, as_, T)
+        l32, s32 = G.log_sign(x.astype(np.float32))
+        refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 64)]
+    gl, gs = to_np(out)
+    if not with_carry:  # the first prefix is the first leaf, raw
+        assert np.array_equal(gl[0], al[0].astype(np.float32)) and np.array_equal(gs[0], as_[0])
+    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=tc_chain_scaled_floor(d, T))
+    assert r["ok"], (r["bad"], r["e_gpu"][r["bad"]], r["e_ref"][r["bad"]], r["flips"],
+                     r["scaled_bad"], r["scaled_max"])
+
+
+def test_long_chain_d64_underflow_and_zeros(g):
+    """A shrinking d = 64 chain (0.5 I + 0.25 E_01 + a zero row in every leaf): Eq. 11's clamp
+    (state scale max(., 0)) makes it underflow like the other tcgen05 paths (FTZ exp, ~e^-87),
+    exact zeros stay zero, every value above the flush meets 1e-4, no NaN."""
+    d, T = 64, 300
+    x = np.tile(0.5 * np.eye(d), (T, 1, 1))
+    x[:, 0, 1] = 0.25
+    x[:, 5, :] = 0.0
+    al, as_ = G.log_sign(x)
+    gl, gs = to_np(torch.ops.goom.scan_chain_long(g.join(al, as_), None))
+    wl, ws = G.chain_blocked(al, as_, T)
+    assert not np.any(np.isnan(gl)) and not np.any(gl == np.inf)
+    assert np.all(gl[wl == -np.inf] == -np.inf)
+    live = wl > -80.0
+    assert np.all(np.isfinite(gl[live]))
+    assert np.all(np.abs(gl[live] - wl[live]) <= 1e-4 * np.maximum(1.0, np.abs(wl[live])))
+    assert np.array_equal(gs[live], ws[live])
+    assert np.all(gl[-1] == -np.inf)
+
+
 def test_long_chain_validation(g):
     import paper_2510_03426_b200 as goom
 

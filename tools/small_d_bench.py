@@ -44,10 +44,10 @@ def main():
         hbm = json.load(f)["hbm_gbs"]
     for d in [int(x) for x in args.ds.split(",")]:
         A = harness.random_chain(args.T, d, seed=d)
-        engines = (["long", "tree"] if d <= 32 else ["tree"]) if args.engines == "all" else \
-            args.engines.split(",")
+        engines = (["long", "tree"] if d <= 32 or d == 64 else ["tree"]) \
+            if args.engines == "all" else args.engines.split(",")
         for eng in engines:
-            if eng == "long" and d > 32:
+            if eng == "long" and d > 32 and d != 64:
                 continue
             run = (lambda: torch.ops.goom.scan_chain_long(A, None)) if eng == "long" else \
                 (lambda: torch.ops.goom.scan_chain(A, args.block, None))
@@ -78,7 +78,11 @@ def report(args, d, eng, A, run, hbm, G, np, torch):
         t0 = time.perf_counter()
         G.chain_blocked(al, as_, min(args.block, args.cpu_sample))
         cpu_s = time.perf_counter() - t0
-        if eng == "long":
+        if eng == "long" and d == 64:
+            engine = ("scan_long64 (reduce-then-scan; each fold step one tcgen05 3xTF32 MMA "
+                      "for two chains, state resident in shared memory / TMEM)")
+            moved = 24 * d * d
+        elif eng == "long":
             engine = ("scan_long (reduce-then-scan, group of d lanes per chain; a fixed tree "
                       "other than the reference's block tree)")
             moved = 24 * d * d
