@@ -48,6 +48,19 @@ constexpr int kBarOff = kQxOff + 64;
 constexpr int kSmem = kBarOff + 128 + 1024;          // + barriers, + 1 KB alignment slack
 static_assert(kSmem <= 232448, "shared memory budget");
 
+#ifdef GOOM_L64_TRACE
+// profiling build only (tools/tc_trace.sh): clock64 stamps of CTA 0's first 256 steps
+__device__ long long g_l64_trace[8][256];
+#define L64_TRACE(row, i, v) \
+  do {                       \
+    if (blockIdx.x == 0 && (i) < 256) g_l64_trace[row][i] = (v); \
+  } while (0)
+#else
+#define L64_TRACE(row, i, v) \
+  do {                       \
+  } while (0)
+#endif
+
 __device__ __forceinline__ float2 canon(float2 z) {
   z.y = phase_negative(z.y) ? kPi : 0.0f;
   return z;
@@ -162,8 +175,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t j = 0; j < n; ++j, ++g, ++bw) {
           const int buf = (int)(g & 1);
           mbar_wait(smem_u32(&a_ready[buf]), (uint32_t)((g >> 1) & 1));
+          L64_TRACE(0, g, clock64());
           mbar_wait(smem_u32(b_ready), (uint32_t)(bw & 1));
           tc_fence_after();
+          L64_TRACE(1, g, clock64());
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb) {
             const uint32_t sa = base + (uint32_t)buf * kAbuf + kb * kKB, sb = base + kBoff + kb * kKB;
@@ -198,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = (int)(g & 1);
         const uint32_t ab = base + (uint32_t)buf * kAbuf;
         mbar_wait(smem_u32(&a_full[buf]), (uint32_t)((g >> 1) & 1));
+        if (w == 0 && lane == 0) L64_TRACE(6, g, clock64());
         const bool valid = j < mysteps;
         float sc[4] = {0.f, 0.f, 0.f, 0.f};  // rows (group 2w: r, r+4), (group 2w+1: r, r+4)
         if (valid) {
@@ -259,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&a_ready[buf]));
+        if (w == 0 && lane == 0) L64_TRACE(7, g, clock64());
       }
     }
   } else {
@@ -366,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = (int)(g & 1);
         mbar_wait(smem_u32(acc_full), (uint32_t)(g & 1));
         tc_fence_after();
+        if (e == 0 && lane == 0) L64_TRACE(2, g, clock64());
         const float a = rS[buf * 128 + i];
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&rs_free[buf]));
@@ -382,7 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < 64; ++q) m = fmaxf(m, fabsf(__uint_as_float(acc[q])));
         if (!(m >= 1.17549435e-38f)) m = 0.0f;  // subnormal rows (and NaN) leave the state
         const float lmax = m > 0.0f ? __fadd_rn(__fadd_rn(fast_log_abs(m), a), Q) : kNegInf;
+        if (e == 0 && lane == 0) L64_TRACE(3, g, clock64());
         const float Qn = chain_max(valid ? lmax : kNegInf);
+        if (e == 0 && lane == 0) L64_TRACE(4, g, clock64());
         if (more) {
           if (valid && m > 0.0f) {
             const int ex = ((__float_as_int(m) >> 23) & 0xff) - 126;  // m = f 2^ex, f in [0.5, 1)
@@ -401,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(b_ready));
+          if (e == 0 && lane == 0) L64_TRACE(5, g, clock64());
         }
         // outputs: every prefix (S-pass), the chain's last state (R-pass)
         auto outc = [&](int q) { return tc_out(__uint_as_float(acc[q]), a, Q); };
@@ -453,3 +474,9 @@ int launch_fold64(const float2* A, int64_t T, int64_t s, const float2* carry0,
 }
 
 }  // namespace goom
+
+#ifdef GOOM_L64_TRACE
+extern "C" int goom_l64_trace_read(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, goom::g_l64_trace, sizeof(goom::g_l64_trace));
+}
+#endif
