@@ -168,11 +168,12 @@ bool lmme_tc_eligible(int n, int k, int m);
 bool lmme_tc1_fuse_scales(int n, int k, int m);
 // n = m = 64: two products per tcgen05 tile, scales in-kernel (GOOM_EUNSUPPORTED otherwise)
 int lmme_tc_duo(const LmmeProblem& p, cudaStream_t s);
-// long-chain fold for d = 64 complex64 on tcgen05 (scan_long64.cu): chains of s leaves,
-// chain k from carry0 (k = 0) / carries[k - 1], or its first leaf; out: every prefix,
-// tot: every chain's last state
-int launch_fold64(const float2* A, int64_t T, int64_t s, const float2* carry0,
-                  const float2* carries, float2* out, float2* tot, cudaStream_t st);
+// tile-resident long-chain fold for complex64 d = 16 / 32 / 64 on tcgen05 (scan_long_tc.cu):
+// chains of s leaves, chain k from carry0 (k = 0) / carries[k - 1], or its first leaf; out:
+// every prefix, tot: every chain's last state
+bool fold_tc_eligible(int d);
+int launch_fold_tc(const float2* A, int64_t T, int d, int64_t s, const float2* carry0,
+                   const float2* carries, float2* out, float2* tot, cudaStream_t st);
 // cta_group::2 pair-tile variant (lmme_tc2.cu) for n, m multiples of 256; lmme_tc() prefers
 // it (GOOM_TC2=0 disables); GOOM_EUNSUPPORTED if the shape / alignment does not fit
 int lmme_tc2(const LmmeProblem& p, cudaStream_t s);

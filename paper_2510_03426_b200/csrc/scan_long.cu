@@ -1,5 +1,5 @@
-// Long-chain scan for small matrices (d <= 32; d = 64 complex64 folds on tcgen05,
-// scan_long64.cu): reduce-then-scan over LMME combines.
+// Long-chain scan for small matrices (d <= 32; complex64 d = 16 / 32 / 64 fold on tcgen05 at the
+// leaf level, scan_long_tc.cu): reduce-then-scan over LMME combines.
 //
 // The reference's two-level tree (_scan_affine_stack, scan.py:181-214) has a sequential
 // depth of s + T/s combines — ~2,000 dependent LMMEs at T = 2^20 however s is chosen —
@@ -27,6 +27,8 @@
 // core.py:252-255), sign * exp, one FMA per term in ascending k, (log|I| + a) + b), so
 // each step is bitwise the generic LMME of the same operands and a single chain is
 // bitwise the sequential fold (scan_chain with block >= T).
+#include <cstdlib>
+
 #include "goom_internal.cuh"
 
 namespace goom {
@@ -272,8 +274,16 @@ int launch_fold_d(const Cx<R>* A, int64_t T, int d, int64_t s, const Cx<R>* carr
 template <class R>
 int launch_fold(const Cx<R>* A, int64_t T, int d, int64_t s, const Cx<R>* carry0,
                 const Cx<R>* carries, Cx<R>* out, Cx<R>* tot, cudaStream_t st) {
-  if constexpr (sizeof(R) == 4) {  // d = 64: the tcgen05 fold (scan_long64.cu)
-    if (d == 64) return launch_fold64(A, T, s, carry0, carries, out, tot, st);
+  if constexpr (sizeof(R) == 4) {
+    // complex64 d = 64, and d = 16 / 32 at the leaf level (chains of kLongS0): the
+    // tile-resident tcgen05 fold (scan_long_tc.cu); the short upper levels (and every level
+    // with GOOM_LONG_TC=0) keep the lane-group fold below
+    static const bool tc_small = [] {
+      const char* e = getenv("GOOM_LONG_TC");
+      return !(e && atoi(e) == 0);
+    }();
+    if (fold_tc_eligible(d) && (d == 64 || (tc_small && s >= kLongS0)))
+      return launch_fold_tc(A, T, d, s, carry0, carries, out, tot, st);
   }
   if (d <= 8) return launch_fold_d<R, 8>(A, T, d, s, carry0, carries, out, tot, st);
   if (d <= 16) return launch_fold_d<R, 16>(A, T, d, s, carry0, carries, out, tot, st);

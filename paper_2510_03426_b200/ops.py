@@ -311,8 +311,8 @@ def scan_chain(a: torch.Tensor, block: int, carry: Optional[torch.Tensor]) -> to
 
 @torch.library.custom_op("goom::scan_chain_long", mutates_args=(), device_types="cuda")
 def scan_chain_long(a: torch.Tensor, carry: Optional[torch.Tensor]) -> torch.Tensor:
-    """The same inclusive product chain for d <= 32 (and d = 64 complex64, folded on tcgen05:
-    scan_long64.cu) on the long-chain engine (scan_long.cu: reduce-then-scan, a fixed tree of
+    """The same inclusive product chain for d <= 32 (and complex64 d = 16 / 32 / 64 folded on tcgen05 at the leaf level:
+    scan_long_tc.cu) on the long-chain engine (scan_long.cu: reduce-then-scan, a fixed tree of
     depth O(s log_s T) instead of the block tree's s + T/s)."""
     _need_cuda(a, carry)
     _need_goom(a, carry)

@@ -76,9 +76,44 @@ def test_long_chain_matches_oracle_complex64(g, d, T):
     want = G.chain_blocked(al, as_, T)           # float64 sequential fold (the oracle)
     l32, s32 = G.log_sign(x.astype(np.float32))
     refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 64)]
-    r = chain_parity(gl, gs, al, as_, want, refs)
+    # d = 16 / 32: the leaf level folds on tcgen05 (scan_long_tc.cu, 3xTF32: the truncating
+    # FP32 accumulation's scaled-real floor); other d on the lane-group FP32 fold
+    from goom_testlib import tc_chain_scaled_floor
+    floor = tc_chain_scaled_floor(d, T) if d in (16, 32) else 1e-4
+    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=floor)
     assert r["ok"], (r["bad"], r["e_gpu"][r["bad"]], r["e_ref"][r["bad"]], r["flips"],
                      r["scaled_bad"])
+
+
+@pytest.mark.parametrize("d,T,with_carry", [(16, 4500, True), (32, 4500, False), (16, 65, False),
+                                            (32, 130, True), (16, 200, False)])
+def test_long_chain_tc_small_d_matches_oracle(g, d, T, with_carry):
+    """d = 16 / 32 at the leaf level on tcgen05 (8 / 4 chains per block-diagonal MMA):
+    partial tiles (chain counts not a multiple of the chains per tile), ragged tails, carries,
+    against the float64 oracle by the §8c chain criterion."""
+    from goom_testlib import tc_chain_scaled_floor
+
+    rng = np.random.default_rng(d * 7 + T)
+    x = rng.standard_normal((T, d, d))
+    al, as_ = G.log_sign(x)
+    if with_carry:
+        c = rng.standard_normal((d, d))
+        cl, cs = G.log_sign(c)
+        out = torch.ops.goom.scan_chain_long(g.join(al, as_), g.join(cl, cs))
+        wl, ws = G.chain_blocked(np.concatenate([cl[None], al]), np.concatenate([cs[None], as_]),
+                                 T + 1)
+        want = (wl[1:], ws[1:])
+        l32, s32 = G.log_sign(np.concatenate([c[None], x]).astype(np.float32))
+        refs = [tuple(v[1:] for v in G.chain_blocked(l32, s32, T + 1))]
+    else:
+        out = torch.ops.goom.scan_chain_long(g.join(al, as_), None)
+        want = G.chain_blocked(al, as_, T)
+        l32, s32 = G.log_sign(x.astype(np.float32))
+        refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 64)]
+    gl, gs = to_np(out)
+    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=tc_chain_scaled_floor(d, T))
+    assert r["ok"], (r["bad"], r["e_gpu"][r["bad"]], r["e_ref"][r["bad"]], r["flips"],
+                     r["scaled_bad"], r["scaled_max"])
 
 
 @pytest.mark.parametrize("d,T", [(4, 70000), (8, 3000), (32, 700)])
@@ -125,7 +160,7 @@ def test_long_chain_underflow_and_zeros_follow_the_clamp(g):
 @pytest.mark.parametrize("T,with_carry", [(1, True), (2, False), (63, False), (64, True),
                                           (65, False), (130, True), (700, False), (4500, True)])
 def test_long_chain_d64_tcgen05_matches_oracle(g, T, with_carry):
-    """d = 64 complex64 folds on tcgen05 (scan_long64.cu: two chains per MMA, 3xTF32): one to
+    """d = 64 complex64 folds on tcgen05 (scan_long_tc.cu: two chains per MMA, 3xTF32): one to
     three levels of recursion (4,500 = 71 chains of 64 -> 5 of 16 -> one), an odd chain count
     (a pair with one chain missing), ragged tails, chains that start from their first leaf
     and from a carry, against the float64 oracle by the §8c chain criterion (scaled-real floor

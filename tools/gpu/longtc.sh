@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_scan_long.py -q -x > gpurun_out/longtc_pytest.log 2>&1; echo "rc $?" >> gpurun_out/longtc_pytest.log
+timeout 600 python tools/small_d_bench.py --ds 16,32,64 --engines long --reps 3 --cpu-sample 64 > gpurun_out/longtc_bench.jsonl 2> gpurun_out/longtc_bench.err

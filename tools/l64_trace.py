@@ -1,5 +1,5 @@
-"""Profiling aid (not product): step timeline of CTA 0 in the d = 64 long-chain fold
-(scan_long64.cu) from the trace build (tools/tc_trace.sh -> tools/bin/libgoom_trace.so).
+"""Profiling aid (not product): step timeline of CTA 0 in the tile-resident long-chain fold (d = 16 / 32 / 64)
+(scan_long_tc.cu) from the trace build (tools/tc_trace.sh -> tools/bin/libgoom_trace.so).
 Rows: 0 MMA has the leaf, 1 MMA has B (issue), 2 epilogue has the accumulator, 3 row
 maxima done, 4 chain maximum done, 5 B written; 6 transform has the leaf, 7 transform done."""
 import ctypes
@@ -16,7 +16,8 @@ from paper_2510_03426_b200 import harness  # noqa: E402
 
 lib = g._lib.load(os.path.join(ROOT, "tools", "bin", "libgoom_trace.so"))
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 18
-A = harness.random_chain(T, 64, seed=1)
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+A = harness.random_chain(T, d, seed=1)
 for _ in range(2):
     out = torch.ops.goom.scan_chain_long(A, None)
 torch.cuda.synchronize()

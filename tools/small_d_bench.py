@@ -78,9 +78,10 @@ def report(args, d, eng, A, run, hbm, G, np, torch):
         t0 = time.perf_counter()
         G.chain_blocked(al, as_, min(args.block, args.cpu_sample))
         cpu_s = time.perf_counter() - t0
-        if eng == "long" and d == 64:
-            engine = ("scan_long64 (reduce-then-scan; each fold step one tcgen05 3xTF32 MMA "
-                      "for two chains, state resident in shared memory / TMEM)")
+        if eng == "long" and d in (16, 32, 64):
+            engine = ("scan_long + scan_long_tc (reduce-then-scan; each leaf-level fold step one "
+                      f"tcgen05 3xTF32 MMA for {128 // d} chains, block-diagonal, state resident "
+                      "in shared memory)")
             moved = 24 * d * d
         elif eng == "long":
             engine = ("scan_long (reduce-then-scan, group of d lanes per chain; a fixed tree "
