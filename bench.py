@@ -331,8 +331,14 @@ def main():
 
     # sanity of the run itself: growth rate of log||P_t|| vs (ln 2 + psi(d/2)) / 2
     dg = run.digests
+    own = getattr(run, "windows", None)  # relay time-sharding: this rank's windows only
+    if own:
+        dg = torch.cat([dg[w0:w0 + m] for w0, m in own])
+        w0, m = max(own, key=lambda x: x[1])
+        growth = harness.growth_rate(run.digests[w0:w0 + m]) if m > 2 else float("nan")
+    else:
+        growth = harness.growth_rate(dg) if dg.shape[0] > 2 else float("nan")
     finite = bool((dg[:, 2] == 1).all().item())
-    growth = harness.growth_rate(dg) if run.digests.shape[0] > 2 else float("nan")
     reanchored = reanchor_checks(run, t0, anchors, W, d, args.seed, ops, world, dist)
 
     # ---- roofline of the dominant kernel: the phase-3 batched LMME of a window ----
@@ -552,7 +558,11 @@ def main():
             "data": "synthetic N(0,1) leaves generated on device (Philox, keyed by leaf index)",
             "config": {"workload": f"chain T={T} of {d}x{d} GOOM leaves, all prefixes digested",
                        "T": T, "d": d, "window": args.window, "block": args.block,
-                       "parallelism": f"time-sharded x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"time-sharded x{world} ({sharded.shard_mode()}: "
+                                       + ("windows round-robin, carry relayed rank to rank"
+                                          if sharded.shard_mode() == "relay" else
+                                          "contiguous shards, all-gather of the shard totals")
+                                       + ")") if world > 1 else "single GPU",
                        "l2": "no flush: every window (>= 16 GiB) exceeds the 126 MB L2"},
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak_3xtf32,
                          "unit": "TFLOP/s", "frac": tflops / peak_3xtf32, "traffic": traffic,

@@ -1,5 +1,11 @@
 """Time-sharded LMME chain scan over the GPUs of one node.
 
+Two schemes. The long-chain harness (bench.py, run_chain_sharded) deals windows round-robin
+and relays the carry rank to rank (relay_windows: the single-GPU work per leaf, one d x d
+product and one point-to-point message per window). The north star's scheme — contiguous
+chunks, one all-gather of the chunk totals, a second pass with the exclusive carry — is the
+C-ABI entry (goom_scan_chain_sharded_c64, scan_chain_nccl) and GOOM_SHARD_MODE=allgather:
+
 Rank g owns leaves [g*T/G, (g+1)*T/G). The only exchange is one all-gather of
 the G chunk totals (d x d GOOMs, 2 MiB each at d = 512):
 
@@ -143,16 +149,141 @@ def resident_fits(n: int, d: int, window: int) -> bool:
     return need < 0.92 * _free_bytes()
 
 
+def relay_windows(nwin: int, rank: int, world: int, local: Callable, combine: Callable,
+                  finish: Callable, send: Callable, recv: Callable):
+    """Window round-robin time-sharding with a carry relay: rank r scans windows
+    w = r, r + G, r + 2G, ... of the chain. Per window: `local(w)` runs the carry-independent
+    part (the engine's phases 1-2) and returns (state, window total); the carry into w (the
+    prefix P at the end of window w - 1) arrives from rank (w - 1) mod G (`recv`), the carry
+    out carry(w) = total(w) (x) carry(w - 1) (`combine`; products accumulate on the left) goes
+    to rank (w + 1) mod G (`send`), and `finish(w, state, carry_in)` applies the carry (phase
+    3). Every leaf costs the single-GPU work (two LMMEs) plus one d x d product and one
+    point-to-point message per window: no shard totals recomputed, nothing kept resident
+    beyond the window in flight. The relay is a pipeline: each rank runs its window's
+    phases 1-2 while the carry travels, so after the first round the ranks are staggered by
+    one hop. Returns [(w, finish(...))] for this rank's windows."""
+    out = []
+    for w in range(rank, nwin, world):
+        state, total = local(w)
+        cin = None if w == 0 else recv((w - 1) % world)
+        cout = total if cin is None else combine(total, cin)
+        if w + 1 < nwin:
+            send(cout, (w + 1) % world)
+        out.append((w, finish(w, state, cin)))
+    return out
+
+
+def _p2p(group=None):
+    """(send(tensors, dst), recv(like, src), drain()) over torch.distributed point-to-point:
+    NCCL sends device tensors directly; gloo (CPU tests, the shared-GPU bench aid) goes
+    through host copies. Sends are asynchronous; drain() waits for them."""
+    backend = dist.get_backend(group)
+    pending = []
+
+    def send(ts, dst):
+        for t in ts:
+            x = t.contiguous() if backend == "nccl" else t.detach().cpu().contiguous()
+            pending.append((dist.isend(x, dst, group=group), x))
+
+    def recv(likes, src):
+        got = []
+        for like in likes:
+            x = torch.empty_like(like) if backend == "nccl" else torch.empty(
+                like.shape, dtype=like.dtype)
+            dist.recv(x, src, group=group)
+            got.append(x.to(like.device, non_blocking=True))
+        return got
+
+    def drain():
+        for work, _ in pending:
+            work.wait()
+        pending.clear()
+
+    return send, recv, drain
+
+
+def run_chain_relay(T: int, d: int, seed: int = 0, window: int = 32768, block: int = 128,
+                    group=None, snapshots=(), anchors=()):
+    """Rank-local part of the window round-robin, carry-relay time-sharding (relay_windows) on
+    the tile-scaled engine (d % 256 == 0); returns (0, ChainRun) whose digests cover the whole
+    chain with this rank's windows filled (the others zero) and `windows` = [(w0, m)]."""
+    from . import ops
+    from .harness import ChainRun, _window_anchor_blocks
+
+    rank, world = _world(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if anchors and window % block:
+        raise ValueError("anchors need window to be a multiple of block")
+    nwin = (T + window - 1) // window
+    digests = torch.zeros((T, 4), dtype=torch.float32, device=dev)
+    snaps, snaps_ts, anch = {}, {}, {}
+    send_t, recv_t, drain = _p2p(group)
+    like = ops.ts_empty(1, d, dev)
+
+    def local(w):
+        w0 = w * window
+        m = min(window, T - w0)
+        leaves = ops.ts_random_normal(m, d, seed, w0, dev)
+        return ops.chain_ts_local(leaves, block)
+
+    def send(c, dst):
+        send_t((c.U, c.q, c.G), dst)
+
+    def recv(src):
+        return ops.TsMats(*recv_t((like.U, like.q, like.G), src))
+
+    def finish(w, win, cin):
+        w0 = w * window
+        m = min(window, T - w0)
+        local_snaps = [t - w0 for t in snapshots if w0 <= int(t) < w0 + m]
+        ks = _window_anchor_blocks(anchors, w0, m, block)
+        _, dg, c, S, K = ops.chain_ts_finish(win, cin, digests=True, carry_out=True,
+                                             snapshots=local_snaps, carries=ks)
+        digests[w0:w0 + m] = dg
+        for j, k in enumerate(ks):
+            anch[w0 + k * block] = K[j:j + 1]
+        if local_snaps:
+            S64 = ops.ts_to_goom(S)
+            for j, t in enumerate(local_snaps):
+                snaps[w0 + t] = S64[j]
+                snaps_ts[w0 + t] = S[j:j + 1]
+        return (w0, m, c)
+
+    done = relay_windows(nwin, rank, world, local, lambda tot, cin: ops.lmme_ts(tot, cin, 1),
+                         finish, send, recv)
+    drain()
+    last = ops.ts_to_goom(done[-1][1][2])[0] if done else None
+    run = ChainRun(digests, last, snaps, snaps_ts, anch)
+    run.windows = [(w0, m) for _, (w0, m, _) in done]
+    return 0, run
+
+
+def shard_mode() -> str:
+    """GOOM_SHARD_MODE: "relay" (default; relay_windows) or "allgather" (contiguous shards,
+    one all-gather of the shard totals, the local products kept resident where they fit)."""
+    import os
+
+    m = os.environ.get("GOOM_SHARD_MODE", "relay")
+    if m not in ("relay", "allgather"):
+        raise ValueError("GOOM_SHARD_MODE must be relay or allgather")
+    return m
+
+
 def run_chain_sharded(T: int, d: int, seed: int = 0, window: int = 4096, block: int = 64,
                       group=None, snapshot_every: int = 0, snapshots=(), anchors=()):
     """Rank-local part of a time-sharded chain run; returns (t0, ChainRun). `snapshots`:
-    absolute prefix indices to keep (those inside this rank's shard come back)."""
+    absolute prefix indices to keep (those inside this rank's part come back). d % 256 == 0
+    shards windows round-robin with a carry relay (run_chain_relay; GOOM_SHARD_MODE=allgather
+    for contiguous shards with one all-gather of the shard totals)."""
     from . import ops
     from .harness import run_chain
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     t0, n = shard_range(T, rank, world)
+    if world > 1 and ops.ts_eligible(d) and not snapshot_every and shard_mode() == "relay":
+        return run_chain_relay(T, d, seed, window, block, group, snapshots=snapshots,
+                               anchors=anchors)
     if world > 1 and ops.ts_eligible(d) and not snapshot_every:
         # a smaller window only pays when it lets the WHOLE shard stay resident (the engine's
         # launches lose efficiency below ~8k products); otherwise keep the window and let

@@ -139,17 +139,75 @@ def test_resident_shards_equal_the_single_gpu_chain(h):
     assert scaled_real_err(gl, gs, rl, rs).max() < 1e-2
 
 
-def test_bench_two_ranks_on_one_gpu():
-    """bench.py's N > 1 path end to end (torchrun, shard totals all-gathered, exclusive
-    carries, max-over-ranks timing, one JSON line from rank 0), with both ranks sharing the
-    box's GPU over gloo (GOOM_BENCH_SHARE_GPU=1)."""
+def _relay_gpu_worker(rank, world, port, T, d, window, block, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_03426_b200 as g
+        from paper_2510_03426_b200 import sharded
+
+        g._lib.load()
+        t0, run = sharded.run_chain_relay(T, d, seed=12, window=window, block=block)
+        q.put((rank, run.windows, run.digests.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_relay_shards_equal_the_single_gpu_chain(h, world):
+    """run_chain_relay (windows round-robin, the tile-scaled carry relayed rank to rank over
+    real gloo point-to-point messages, every rank on this GPU) gives the single-GPU chain's
+    digests: every window is covered exactly once, log-norms within 1e-4."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    T, d, window, block = 700, 256, 128, 16
+    full = h.run_chain(T, d, seed=12, window=window, block=block)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_relay_gpu_worker, args=(r, world, port, T, d, window, block, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dg = np.zeros((T, 4))
+    seen = []
+    for _, wins, dig in parts:
+        for w0, m in wins:
+            dg[w0:w0 + m] = dig[w0:w0 + m]
+            seen.append(w0)
+    assert sorted(seen) == list(range(0, T, window))
+    ref = full.digests.double().cpu().numpy()
+    assert (dg[:, 2] == 1).all()
+    assert np.max(np.abs(dg[:, 1] - ref[:, 1]) / np.maximum(1, np.abs(ref[:, 1]))) < 1e-4
+
+
+@pytest.mark.parametrize("mode", ["relay", "allgather"])
+def test_bench_two_ranks_on_one_gpu(mode):
+    """bench.py's N > 1 path end to end (torchrun; the carry relay, or the shard totals
+    all-gathered with exclusive carries; max-over-ranks timing, one JSON line from rank 0),
+    with both ranks sharing the box's GPU over gloo (GOOM_BENCH_SHARE_GPU=1)."""
     import json
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GOOM_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="1")
+    env = dict(os.environ, GOOM_BENCH_SHARE_GPU="1", OMP_NUM_THREADS="1", GOOM_SHARD_MODE=mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29547", "bench.py", "--gpus", "2",
            "--steps", "1", "--warmup", "1", "--T", "4096", "--window", "1024", "--block", "64",
@@ -159,7 +217,7 @@ def test_bench_two_ranks_on_one_gpu():
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     r = json.loads(lines[0])
-    assert r["n_gpus"] == 2 and r["config"]["parallelism"] == "time-sharded x2"
+    assert r["n_gpus"] == 2 and r["config"]["parallelism"].startswith(f"time-sharded x2 ({mode}")
     assert r["check"]["finite"]
     assert abs(r["check"]["growth_per_step"] - r["check"]["expected_growth"]) < 0.05
 

@@ -83,6 +83,71 @@ def test_sharded_chain_matches_sequential(world, T):
     np.testing.assert_array_equal(got_s, want.asign)
 
 
+def _relay_worker(rank, world, port, T, d, window, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_03426_b200 import sharded
+
+        al, as_ = leaves(T, d)
+        nwin = (T + window - 1) // window
+        send_t, recv_t, drain = sharded._p2p()
+        like = torch.view_as_real(torch.zeros((d, d), dtype=torch.complex128))
+
+        def local(w):  # the window's carry-independent prefixes and its total
+            a, b = w * window, min(T, (w + 1) * window)
+            L, S = G.chain_blocked(al[a:b], as_[a:b], b - a)
+            return (L, S), torch.from_numpy(G.join_complex(L[-1], S[-1], np.complex128))
+
+        def finish(w, state, cin):
+            L, S = state
+            if cin is not None:
+                cl, cs = G.split_complex(cin.numpy())
+                L, S = G.lmme(L, S, np.broadcast_to(cl, L.shape), np.broadcast_to(cs, S.shape))
+            return L, S
+
+        def send(c, dst):
+            send_t((torch.view_as_real(c),), dst)
+
+        def recv(src):
+            return torch.view_as_complex(recv_t((like,), src)[0].contiguous())
+
+        out = sharded.relay_windows(nwin, rank, world, local, oracle_lmme, finish, send, recv)
+        drain()
+        q.put((rank, [(w, L, S) for w, (L, S) in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T,window", [(2, 23, 4), (3, 31, 5), (2, 8, 8)])
+def test_relay_sharded_chain_matches_sequential(world, T, window):
+    """Window round-robin time-sharding with the carry relayed rank to rank (the bench's
+    default, sharded.relay_windows) over real gloo point-to-point messages: every prefix of
+    the global chain, ragged last window, and a run where one rank gets no window."""
+    d = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_relay_worker, args=(r, world, port, T, d, window, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    wins = sorted((w, L, S) for _, lst in parts for (w, L, S) in lst)
+    assert [w for w, _, _ in wins] == list(range((T + window - 1) // window))
+    got_l = np.concatenate([L for _, L, _ in wins])
+    got_s = np.concatenate([S for _, _, S in wins])
+    al, as_ = leaves(T, d)
+    st = G.Stack(al, as_, np.full_like(al, -np.inf), np.ones_like(as_), np.zeros(T, bool))
+    want = G.scan_sequential(st)
+    assert G.rel_log_diff(got_l, want.alog) < 1e-10
+    np.testing.assert_array_equal(got_s, want.asign)
+
+
 def test_shard_range_partitions():
     from paper_2510_03426_b200 import sharded
 
