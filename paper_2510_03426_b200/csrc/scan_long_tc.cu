@@ -244,56 +244,55 @@ __global__ void __launch_bounds__(kThreads, FoldCfg<D>::kMinBlocks)
         mbar_wait(smem_u32(&a_full[buf]), (uint32_t)((g >> 1) & 1));
         if (w == 0 && lane == 0) L64_TRACE(6, g, clock64());
         const bool valid = j < mysteps;
-        float sc[4] = {0.f, 0.f, 0.f, 0.f};  // rows (group 2w: r, r+4), (group 2w+1: r, r+4)
-        bool odd = false;
-        if (valid) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) sc[q] = kNegInf;
-#pragma unroll
-          for (int kb = 0; kb < kNKB; ++kb)
-#pragma unroll
-            for (int gg = 0; gg < 2; ++gg) {
-              const uint32_t ga = ab + kb * kKB + (2 * w + gg) * kGroupBytes;
-              const float4 a0 = ld_shared_v4(ga + lane * 16), a1 = ld_shared_v4(ga + 512 + lane * 16);
-              sc[2 * gg] = fmaxf(sc[2 * gg], fmaxf(a0.x, a0.z));
-              sc[2 * gg + 1] = fmaxf(sc[2 * gg + 1], fmaxf(a1.x, a1.z));
-              odd |= odd_phase(a0.y) | odd_phase(a0.w) | odd_phase(a1.y) | odd_phase(a1.w);
-            }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1) sc[q] = fmaxf(sc[q], __shfl_xor_sync(0xffffffffu, sc[q], o));
-            sc[q] = fmaxf(sc[q], 0.0f);  // Eq. 11 clamp
-          }
-        }
-        const bool canon = !__any_sync(0xffffffffu, odd);  // phases all 0 / pi: cheap sign
         // the epilogue of step g - 2 has read this buffer's row scales
         if (g >= 2) mbar_wait(smem_u32(&rs_free[buf]), (uint32_t)(((g >> 1) - 1) & 1));
-        if (kp == 0) {
-          float* rs = rS + buf * 128 + 16 * w;
-          rs[r] = sc[0];
-          rs[r + 4] = sc[1];
-          rs[8 + r] = sc[2];
-          rs[8 + r + 4] = sc[3];
-        }
 #pragma unroll
-        for (int kb = 0; kb < kNKB; ++kb)
+        for (int gg = 0; gg < 2; ++gg) {  // group 2w + gg: its 8 rows x D k held in registers
+          float4 raw[2 * kNKB];           // [kb][a0 | a1]: one shared-memory read per element
+          float s0 = 0.f, s1 = 0.f;       // rows r, r + 4
+          bool odd = false;
+          if (valid) {
+            s0 = s1 = kNegInf;
 #pragma unroll
-          for (int gg = 0; gg < 2; ++gg) {
+            for (int kb = 0; kb < kNKB; ++kb) {
+              const uint32_t ga = ab + kb * kKB + (2 * w + gg) * kGroupBytes;
+              raw[2 * kb] = ld_shared_v4(ga + lane * 16);
+              raw[2 * kb + 1] = ld_shared_v4(ga + 512 + lane * 16);
+              s0 = fmaxf(s0, fmaxf(raw[2 * kb].x, raw[2 * kb].z));
+              s1 = fmaxf(s1, fmaxf(raw[2 * kb + 1].x, raw[2 * kb + 1].z));
+              odd |= odd_phase(raw[2 * kb].y) | odd_phase(raw[2 * kb].w) |
+                     odd_phase(raw[2 * kb + 1].y) | odd_phase(raw[2 * kb + 1].w);
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+              s0 = fmaxf(s0, __shfl_xor_sync(0xffffffffu, s0, o));
+              s1 = fmaxf(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+            }
+            s0 = fmaxf(s0, 0.0f);  // Eq. 11 clamp
+            s1 = fmaxf(s1, 0.0f);
+          }
+          const bool canon = !__any_sync(0xffffffffu, odd);  // phases all 0 / pi: cheap sign
+          if (kp == 0) {
+            rS[buf * 128 + 16 * w + 8 * gg + r] = s0;
+            rS[buf * 128 + 16 * w + 8 * gg + r + 4] = s1;
+          }
+          __syncwarp();  // the group is in registers before it is overwritten
+#pragma unroll
+          for (int kb = 0; kb < kNKB; ++kb) {
             const uint32_t ga = ab + kb * kKB + (2 * w + gg) * kGroupBytes;
             uint32_t hb[4], lb[4];
             if (valid) {
-              const float4 a0 = ld_shared_v4(ga + lane * 16), a1 = ld_shared_v4(ga + 512 + lane * 16);
+              const float4 a0 = raw[2 * kb], a1 = raw[2 * kb + 1];
               if (canon) {
-                goom_split<true>(make_float2(a0.x, a0.y), sc[2 * gg], hb[0], lb[0]);
-                goom_split<true>(make_float2(a0.z, a0.w), sc[2 * gg], hb[1], lb[1]);
-                goom_split<true>(make_float2(a1.x, a1.y), sc[2 * gg + 1], hb[2], lb[2]);
-                goom_split<true>(make_float2(a1.z, a1.w), sc[2 * gg + 1], hb[3], lb[3]);
+                goom_split<true>(make_float2(a0.x, a0.y), s0, hb[0], lb[0]);
+                goom_split<true>(make_float2(a0.z, a0.w), s0, hb[1], lb[1]);
+                goom_split<true>(make_float2(a1.x, a1.y), s1, hb[2], lb[2]);
+                goom_split<true>(make_float2(a1.z, a1.w), s1, hb[3], lb[3]);
               } else {
-                goom_split<false>(make_float2(a0.x, a0.y), sc[2 * gg], hb[0], lb[0]);
-                goom_split<false>(make_float2(a0.z, a0.w), sc[2 * gg], hb[1], lb[1]);
-                goom_split<false>(make_float2(a1.x, a1.y), sc[2 * gg + 1], hb[2], lb[2]);
-                goom_split<false>(make_float2(a1.z, a1.w), sc[2 * gg + 1], hb[3], lb[3]);
+                goom_split<false>(make_float2(a0.x, a0.y), s0, hb[0], lb[0]);
+                goom_split<false>(make_float2(a0.z, a0.w), s0, hb[1], lb[1]);
+                goom_split<false>(make_float2(a1.x, a1.y), s1, hb[2], lb[2]);
+                goom_split<false>(make_float2(a1.z, a1.w), s1, hb[3], lb[3]);
               }
             } else {  // a finished chain multiplies by the identity (its output is dropped)
               const int row = (16 * w + 8 * gg + r) % D, k0 = kb * 16 + 2 * kp;
@@ -303,7 +302,6 @@ __global__ void __launch_bounds__(kThreads, FoldCfg<D>::kMinBlocks)
               hb[3] = row + 4 == k0 + 1 ? 0x3f800000u : 0u;
               lb[0] = lb[1] = lb[2] = lb[3] = 0u;
             }
-            __syncwarp();  // the group is in registers before it is overwritten
             const uint32_t o0 = sw64_off(r, kp >> 1) + (kp & 1) * 8;
             const uint32_t o1 = sw64_off(r + 4, kp >> 1) + (kp & 1) * 8;
             st_shared_v2(ga + o0, hb[0], hb[1]);
@@ -311,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, FoldCfg<D>::kMinBlocks)
             st_shared_v2(ga + o1, hb[2], hb[3]);
             st_shared_v2(ga + 512 + o1, lb[2], lb[3]);
           }
+        }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&a_ready[buf]));
