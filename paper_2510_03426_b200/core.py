@@ -250,7 +250,7 @@ class GoomMatrix:
 
     @classmethod
     def _wrap(cls, z: torch.Tensor) -> "GoomMatrix":
-        obj = cls.__new__(cls)
+        obj = object.__new__(cls)
         obj.data = z
         obj._host = None
         return obj
@@ -355,6 +355,25 @@ class GoomMatrix:
 
 # ---------------------------------------------------------------------------
 # array-level kernels (core.py:229-323)
+
+
+
+class _StackedGoom(GoomMatrix):
+    """Element i of a stacked GOOM tensor, sliced only when `.data` is first read: a scan
+    over a long host list hands back T pairs, and most callers read a few of them
+    (creating T tensor views up front cost ~6 us per pair)."""
+
+    __slots__ = ("_base", "_i")
+
+    @property
+    def data(self):
+        return self._base[self._i]
+
+    @classmethod
+    def _of(cls, base: torch.Tensor, i: int) -> "GoomMatrix":
+        obj = object.__new__(cls)
+        obj._base, obj._i, obj._host = base, i, None
+        return obj
 
 
 def _log_sign_arrays(values, policy=SENTINEL):

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib, ops
-from .core import NEG_INF, GoomMatrix, _device, join, split
+from .core import NEG_INF, GoomMatrix, _device, _StackedGoom, join, split
 
 POLICY_NEVER = _lib.POLICY_NEVER
 POLICY_COLINEARITY = _lib.POLICY_COLINEARITY
@@ -222,15 +222,23 @@ class _Stack:
 
     @classmethod
     def from_pairs(cls, leaves):
-        A = torch.stack([p.A.data for p in leaves])
-        B = torch.stack([p.B.data for p in leaves])
+        A = _restack([p.A for p in leaves])
+        B = _restack([p.B for p in leaves])
         f = torch.tensor([p.reset_applied for p in leaves], dtype=torch.bool, device=A.device)
         return cls(A, B, f)
 
     def to_pairs(self):
+        # lazily sliced matrices (_StackedGoom) and no per-pair validation (the stack's shapes
+        # are checked): ~10x faster than a tensor view per element, which the reference's own
+        # host-list callers notice (test_scan.py:341-360 times a 2^15-leaf scan)
         flags = self._flags.cpu().tolist()
-        return [ScanPair(GoomMatrix._wrap(self.A[i]), GoomMatrix._wrap(self.B[i]), bool(flags[i]))
-                for i in range(len(flags))]
+        new, of, A, B = object.__new__, _StackedGoom._of, self.A, self.B
+        out = []
+        for i, f in enumerate(flags):
+            p = new(ScanPair)  # frozen dataclass: fill its __dict__ directly
+            p.__dict__.update(A=of(A, i), B=of(B, i), reset_applied=bool(f))
+            out.append(p)
+        return out
 
     @property
     def alog(self):
@@ -254,6 +262,18 @@ class _Stack:
 
     def __len__(self):
         return self.A.shape[0]
+
+
+def _restack(ms):
+    """The stacked tensor of GoomMatrix objects: the base itself when they are exactly the
+    elements 0 .. T-1 of one stack handed out by to_pairs (no copy), else torch.stack."""
+    m0 = ms[0]
+    if type(m0) is _StackedGoom:
+        base = m0._base
+        if base.shape[0] == len(ms) and all(
+                type(m) is _StackedGoom and m._base is base and m._i == i for i, m in enumerate(ms)):
+            return base
+    return torch.stack([m.data for m in ms])
 
 
 def _all_zero_bias(stack: _Stack) -> bool:
