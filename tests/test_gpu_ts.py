@@ -12,7 +12,7 @@ import pytest
 import torch
 
 from goom_testlib import (chain_kappa, chain_parity, lmme_parity, scaled_real_err,
-                          tc_chain_scaled_floor, to_np)
+                          TC_CHAIN_FLOOR, tc_chain_scaled_floor, to_np)
 from oracle import gooms_port as G
 
 pytestmark = pytest.mark.gpu
@@ -259,7 +259,8 @@ def test_chain_ts_matches_float64_oracle(g, ops, d, T, block, engine):
     want = G.chain_blocked(al, as_, T)
     l32, s32 = G.log_sign(mats.astype(np.float32))
     refs = [G.chain_blocked(l32, s32, block), G.chain_blocked(l32, s32, T)]
-    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=tc_chain_scaled_floor(d, T))
+    r = chain_parity(gl, gs, al, as_, want, refs, scaled_floor=tc_chain_scaled_floor(d, T),
+                     floor=TC_CHAIN_FLOOR)
     assert r["ok"], (r["bad"], r["flips"], r["scaled_bad"])
 
 
