@@ -71,8 +71,13 @@ for seed in range(1, 31):
     t0 = time.perf_counter()
     G.chain_blocked(al, as_, 32)
     cpu["blocked32_f64_ms"].append((time.perf_counter() - t0) * 1e3)
-    l32, s32 = al.astype(np.float32), as_.astype(np.float32)
-    refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 32)]  # the reference's f32 runs
+    # the reference's own float32 runs: its float32 path converts the float32 matrices
+    # (log_sign of x.astype(float32), as tests/golden/make_golden.py records), sequential
+    # and block 32; the float64 logs rounded to float32 (the GPU's exact input) beside them
+    l32, s32 = G.log_sign(mats.astype(np.float32))
+    r32, q32 = al.astype(np.float32), as_.astype(np.float32)
+    refs = [G.chain_blocked(l32, s32, T), G.chain_blocked(l32, s32, 32),
+            G.chain_blocked(r32, q32, T), G.chain_blocked(r32, q32, 32)]
     r = chain_parity(gl, gs, al, as_, want, refs)
     ok += bool(r["ok"])
     if not r["ok"]:
