@@ -94,6 +94,15 @@ int goom_ssm_export_c128(const goom_c128* X, int64_t H, int64_t L, int d, int64_
 int goom_ssm_panels_c128(const double* h, const double* K, const double* c, int64_t H, int64_t L,
                          int d, int64_t S, int64_t nC, int64_t T, int reverse, goom_c128* out,
                          void* stream);
+/* The adjoint scan's source term of the SSM backward (ssm.ssm_backward_heads): per state
+ * (n states of d <= 64 float64 values; sl / ss / c the forward's log, sign and per-state
+ * scale, gz = C^T gy_t), z = ss * exp(sl - c + 2) and h = e^2 gz - [live] corr at i*, where
+ * i* is the first index of the largest sl, corr = ss[i*] * sum_j gz_j z_j and live means some
+ * sl is finite — the gradient through the shifted export's max (ssm.py:84-98). One warp per
+ * state; writes h and z (n x d). */
+int goom_ssm_adjoint_source_f64(const double* sl, const double* ss, const double* c,
+                                const double* gz, int64_t n, int d, double* h, double* z,
+                                void* stream);
 /* Elementwise signed log-sum-exp, bitwise commutative.  _gadd_arrays core.py:264-275. */
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream);
 int goom_gadd_c128(const goom_c128* a, const goom_c128* b, goom_c128* out, int64_t n,

@@ -100,6 +100,7 @@ SIGNATURES = {
     "goom_ssm_export_c128": (_I, [_P, _I64, _I64, _I, _I64, _I64, _I64, _P, _P, _P, _P, _I, _P,
                                   _P]),
     "goom_ssm_panels_c128": (_I, [_P, _P, _P, _I64, _I64, _I, _I64, _I64, _I64, _I, _P, _P]),
+    "goom_ssm_adjoint_source_f64": (_I, [_P, _P, _P, _P, _I64, _I, _P, _P, _P]),
     "goom_gadd_c128": (_I, [_P, _P, _P, _I64, _P]),
     "goom_col_log_norms_c128": (_I, [_P, _P, _I64, _I, _I, _P]),
     "goom_lmme_workspace_size_c128": (_SZ, [_I64, _I, _I, _I]),

@@ -114,6 +114,63 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// SSM backward source term, one warp per state (d <= 64: lane j holds elements j, j + 32)
+__global__ void ssm_adjoint_source_kernel(const double* __restrict__ sl,
+                                          const double* __restrict__ ss,
+                                          const double* __restrict__ cvec,
+                                          const double* __restrict__ gz, int64_t n, int d,
+                                          double* __restrict__ h, double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t st = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (st >= n) return;
+  const int64_t o = st * d;
+  const double c = cvec[st];
+  double zv[2], gv[2], lv[2], sv[2];
+  double m = -INFINITY, dot = 0.0;
+  int im = 1 << 30;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (j < d) {
+      lv[q] = sl[o + j];
+      sv[q] = ss[o + j];
+      gv[q] = gz[o + j];
+      zv[q] = sv[q] * exp(add_rn(sub_rn(lv[q], c), 2.0));
+      dot = fma(gv[q], zv[q], dot);
+      if (lv[q] > m) {  // first index of the maximum
+        m = lv[q];
+        im = j;
+      }
+    } else {
+      lv[q] = sv[q] = gv[q] = zv[q] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const int i2 = __shfl_xor_sync(0xffffffffu, im, off);
+    if (m2 > m || (m2 == m && i2 < im)) {
+      m = m2;
+      im = i2;
+    }
+    dot += __shfl_xor_sync(0xffffffffu, dot, off);
+  }
+  const bool live = m != -INFINITY;
+  const double sstar = __shfl_sync(0xffffffffu, im < 32 ? sv[0] : sv[1], im & 31);
+  const double corr = live ? sstar * dot : 0.0;
+  const double e2 = 7.38905609893065;  // e^2 (torch's math.exp(2.0))
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (j < d) {
+      double hv = e2 * gv[q];
+      if (j == im) hv = hv + (-corr);
+      h[o + j] = hv;
+      z[o + j] = zv[q];
+    }
+  }
+}
+
 // The adjoint scan's inputs in _chunked_scan's panel layout (inverse of the export): from
 // real h (H, S, T, d) float64, out[i][h][r][s nC + cc] = GOOM of h at time t_src, log part
 // + (K[h, s] - c[h, s, t_src]) when K is given, with scan time cc L + i and t_src = T - 1 -
@@ -445,6 +502,18 @@ int goom_ssm_panels_c128(const double* h, const double* K, const double* c, int6
                          int d, int64_t S, int64_t nC, int64_t T, int reverse, goom_c128* out,
                          void* stream) {
   return ssm_panels(h, K, c, H, L, d, S, nC, T, reverse, out, stream);
+}
+int goom_ssm_adjoint_source_f64(const double* sl, const double* ss, const double* c,
+                                const double* gz, int64_t n, int d, double* h, double* z,
+                                void* stream) {
+  if (n < 0 || d < 1 || d > 64) return fail(GOOM_ESHAPE, "ssm_adjoint_source: need 1 <= d <= 64");
+  if (n == 0) return GOOM_OK;
+  if (!sl || !ss || !c || !gz || !h || !z) return fail(GOOM_EINVAL, "null pointer");
+  const int64_t blocks = (n + 7) / 8;  // 8 warps (states) per block
+  ssm_adjoint_source_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(sl, ss, c, gz, n, d,
+                                                                            h, z);
+  GOOM_CHECK_LAUNCH("ssm_adjoint_source");
+  return GOOM_OK;
 }
 int goom_gadd_c64(const goom_c64* a, const goom_c64* b, goom_c64* out, int64_t n, void* stream) {
   return gadd<float>(a, b, out, n, stream);

@@ -271,6 +271,23 @@ def ssm_export(X: torch.Tensor, H: int, L: int, S: int, nC: int, T: int, full: b
     return (sl, ss, c, z) if full else (sl, ss)
 
 
+def ssm_adjoint_source(sl: torch.Tensor, ss: torch.Tensor, c: torch.Tensor,
+                       gz: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+    """(h, z) of the SSM backward (goom_ssm_adjoint_source_f64): z = ss e^{sl - c + 2} and
+    h = e^2 gz minus the export max's gradient at each state's first argmax. sl, ss, gz
+    (..., d) and c (...) float64 CUDA tensors, d <= 64."""
+    _need_cuda(sl, ss, c, gz)
+    d = sl.shape[-1]
+    if not (sl.shape == ss.shape == gz.shape and c.shape == sl.shape[:-1]):
+        raise ValueError("sl, ss, gz (..., d) and c (...) must match")
+    sl, ss, c, gz = (t.to(torch.float64).contiguous() for t in (sl, ss, c, gz))
+    h = torch.empty_like(sl)
+    z = torch.empty_like(sl)
+    _lib.call("goom_ssm_adjoint_source_f64", sl.data_ptr(), ss.data_ptr(), c.data_ptr(),
+              gz.data_ptr(), c.numel(), d, h.data_ptr(), z.data_ptr(), _stream())
+    return h, z
+
+
 def ssm_panels(h: torch.Tensor, L: int, K: Optional[torch.Tensor] = None,
                c: Optional[torch.Tensor] = None, reverse: bool = False) -> torch.Tensor:
     """Real h (H, S, T, d) float64 -> complex128 GOOM panels (L, H, d, S T / L) in the

@@ -393,6 +393,25 @@ def _scaled_outer(alog, asign, b, heads_shape):
     return torch.where(torch.isfinite(m)[:, None, None], out, torch.zeros_like(out))
 
 
+def _factored_outer(za, ea, b, heads_shape):
+    """sum over (S, T) of a_t b_t^T for a_t = za_t e^{ea_t} (za (H, S, T, d) bounded, ea
+    (H, S, T) one log factor per step), b (H, S, T, d') real -> (H, d, d'): the factors,
+    shifted by their per-head maximum, scale b; the maximum comes back once at the end."""
+    H = heads_shape
+    mh = ea.reshape(H, -1).max(dim=1).values                           # (H,)
+    w = torch.exp(ea - mh[:, None, None])
+    d, d2 = za.shape[-1], b.shape[-1]
+    out = _bmm_tn(za.reshape(H, -1, d), (b * w[..., None]).reshape(H, -1, d2))
+    return out * torch.exp(mh)[:, None, None]
+
+
+def _factored_rows(za, ea, M):
+    """a_t M per step for a_t = za_t e^{ea_t} (za (H, S, T, d), ea (H, S, T), M (H, d, d'))."""
+    H, S, T, d = za.shape
+    out = torch.bmm(za.reshape(H, S * T, d), M).reshape(H, S, T, M.shape[-1])
+    return out * torch.exp(ea)[..., None]
+
+
 def _rowwise(alog, asign, M):
     """a_t M per step (a = asign e^{alog} (H, S, T, d), M (H, d, d')) with a per-step shift,
     so a step whose adjoint is below float64 range rounds to zero instead of to garbage."""
@@ -428,14 +447,17 @@ def ssm_backward_heads(A, B, C, D, x0s, us, state_log, state_sign, scales, gy, c
     H, S, T, d = us.shape
     if gy.shape != (H, S, T, 2 * d) or sl.shape != (H, S, T, d) or c.shape != (H, S, T):
         raise ValueError("forward results / gy shapes do not match the inputs")
-    z = ss * torch.exp(sl - c[..., None] + 2.0)
     gz = torch.bmm(gy.reshape(H, S * T, 2 * d), C).reshape(H, S, T, d)
-    # direct gradient through z_t = x_t e^{2 - c(x_t)}
-    h = _E2 * gz
-    live = sl.max(dim=-1).values != NEG_INF
-    istar = sl.argmax(dim=-1, keepdim=True)
-    corr = torch.gather(ss, -1, istar) * (gz * z).sum(-1, keepdim=True)
-    h = h.scatter_add(-1, istar, -corr * live[..., None].to(h.dtype))
+    # direct gradient through z_t = x_t e^{2 - c(x_t)}: h = e^2 gz minus the max's share
+    if d <= 64:  # one fused pass (goom_ssm_adjoint_source_f64)
+        h, z = ops.ssm_adjoint_source(sl, ss, c, gz)
+    else:
+        z = ss * torch.exp(sl - c[..., None] + 2.0)
+        h = _E2 * gz
+        live = sl.max(dim=-1).values != NEG_INF
+        istar = sl.argmax(dim=-1, keepdim=True)
+        corr = torch.gather(ss, -1, istar) * (gz * z).sum(-1, keepdim=True)
+        h = h.scatter_add(-1, istar, -corr * live[..., None].to(h.dtype))
     # adjoint: reverse-time scan with A^T from a zero adjoint, run on lam e^{K} with K the
     # sequence's largest scale: the reference LMME clamps its scales at 0 (core.py:250-251),
     # so adjoints ~ e^{-c_t} below float64 range would vanish, while lam e^{K} >~ 1
@@ -445,13 +467,31 @@ def ssm_backward_heads(A, B, C, D, x0s, us, state_log, state_sign, scales, gy, c
     L = max(1, min(chunk, T))
     if T % L == 0 and d <= 64:
         # reversed, shifted GOOMs straight into the panel layout and the adjoints straight out
-        # of it (goom_ssm_panels_c128 / goom_ssm_export_c128): no flipped or permuted copies
+        # of it (goom_ssm_panels_c128 / goom_ssm_export_c128): no flipped or permuted copies.
+        # The export's per-step scale gives every adjoint as lam_t = zl_t e^{e_t} with
+        # zl = sign e^{log + K - cl + 2} (|zl| <= e^2) and e_t = cl_t - K - 2 one number per
+        # step, so the parameter gradients need no per-element max / exp over (S, T, d)
         bi = ops.ssm_panels(h, L, K, c, reverse=True)
         X, L, nC = _chunked_scan(At, h.new_empty(()).expand(H, S, T, d), zero, chunk, bi=bi,
                                  panels=True)
         del bi
-        ll, ls = ops.ssm_export(X, H, L, S, nC, T, full=False, reverse=True, kshift=K)
+        _, _, cl, zl = ops.ssm_export(X, H, L, S, nC, T, full=True, reverse=True, kshift=K)
         del X
+        e = cl - K[..., None] - 2.0                                      # (H, S, T)
+        x0g = _goom(x0s)
+        c0 = _scales(x0g.real)
+        x0n = _sign_of(x0g) * torch.exp(x0g.real - c0[..., None])
+        dA = _factored_outer(zl[:, :, :1], e[:, :, :1] + c0[..., None], x0n[:, :, None], H)
+        if T > 1:  # x_{t-1} = z_{t-1} e^{c_{t-1} - 2}
+            dA = dA + _factored_outer(zl[:, :, 1:], e[:, :, 1:] + c[:, :, :-1] - 2.0,
+                                      z[:, :, :-1], H)
+        dB = _factored_outer(zl, e, us, H)
+        dus = _factored_rows(zl, e, B) + torch.bmm(gy.reshape(H, S * T, 2 * d), D).reshape(
+            H, S, T, d)
+        dx0s = _factored_rows(zl[:, :, :1], e[:, :, :1], A)[:, :, 0]
+        dC = _bmm_tn(gy.reshape(H, S * T, 2 * d), z.reshape(H, S * T, d))
+        dD = _bmm_tn(gy.reshape(H, S * T, 2 * d), us.reshape(H, S * T, d))
+        return dA, dB, dC, dD, dx0s, dus
     else:
         g = _goom(h)
         g = torch.complex(g.real + (K[..., None] - c)[..., None], g.imag)

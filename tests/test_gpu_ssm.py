@@ -2,6 +2,8 @@
 reference produced (tests/golden/make_golden_ssm.py) and the reference's own test cases
 (pkg/tests/test_ssm.py)."""
 
+import math
+
 import numpy as np
 import pytest
 
@@ -365,3 +367,35 @@ def test_ssm_heads_past_grid_y_limit(s):
         for k, got in zip("ABCD", grads[:4]):
             assert _rel_max(got[h], getattr(g, k)) < 1e-9, (h, k)
         assert _rel_max(grads[5][h, 0], g.u) < 1e-9
+
+
+def test_ssm_adjoint_source_kernel_matches_torch_reference(s):
+    """goom_ssm_adjoint_source_f64 against the torch formulation it replaces (ssm.py:84-98's
+    export, differentiated): z = ss e^{sl - c + 2}, h = e^2 gz minus ss[i*] sum(gz z) at the
+    first argmax i*; with an all-zero state (sl = -inf: no correction), ties for the maximum
+    (the first index takes it) and d < 32 / d = 64."""
+    import torch
+
+    from paper_2510_03426_b200 import ops
+
+    for d in (7, 64):
+        torch.manual_seed(d)
+        n = 1000
+        sl = torch.randn(n, d, dtype=torch.float64, device="cuda") * 5
+        ss = torch.where(torch.rand(n, d, device="cuda") < 0.5, -1.0, 1.0).to(torch.float64)
+        gz = torch.randn(n, d, dtype=torch.float64, device="cuda")
+        sl[3] = float("-inf")
+        sl[5, 1] = sl[5, 4] = sl[5].max() + 1.0  # a tie: index 1 wins
+        c = sl.max(dim=-1).values
+        c = torch.where(c == float("-inf"), torch.zeros_like(c), c)
+        h, z = ops.ssm_adjoint_source(sl, ss, c, gz)
+        zr = ss * torch.exp(sl - c[:, None] + 2.0)
+        hr = math.exp(2.0) * gz
+        live = sl.max(dim=-1).values != float("-inf")
+        istar = sl.argmax(dim=-1, keepdim=True)
+        corr = torch.gather(ss, -1, istar) * (gz * zr).sum(-1, keepdim=True)
+        hr = hr.scatter_add(-1, istar, -corr * live[:, None].to(hr.dtype))
+        assert torch.equal(z, zr)
+        torch.testing.assert_close(h, hr, rtol=1e-13, atol=1e-13)
+        assert torch.equal(h[3], math.exp(2.0) * gz[3])
+        assert h[5, 1] != math.exp(2.0) * gz[5, 1] and h[5, 4] == math.exp(2.0) * gz[5, 4]
