@@ -36,8 +36,33 @@ namespace goom {
 namespace {
 
 constexpr int kLongS0 = 64;   // chain length at the leaf level
-constexpr int kLongS = 16;    // chain length at the upper levels
-constexpr int kLongTop = 32;  // a level this short runs as one chain
+constexpr int kLongTop = 32;  // an input this short runs as one chain (the sequential fold)
+
+// the upper levels (chains of totals) are latency-bound: each SIMT fold step is a ~1 us
+// dependent chain whatever the load, so their cost is the tree's sequential depth (2 s per
+// level plus the top chain) and ~2 us per launch. Chains of s = 4 up to a top chain of 4
+// measured best for the lane-group fold (d <= 32: 2-4% off the whole scan against 16 / 32);
+// the d = 64 tcgen05 fold keeps 16 / 32 (s = 4 / 8 measured 1.5% / 0% slower;
+// profiles/r2_long_upper_tree.txt). GOOM_LONG_S / GOOM_LONG_TOP override both for measurement.
+struct UpperTree {
+  int s, top;
+};
+inline UpperTree upper_tree(int d) {
+  static const UpperTree env = [] {
+    UpperTree v{0, 0};
+    if (const char* e = getenv("GOOM_LONG_S")) v.s = atoi(e) >= 2 ? atoi(e) : 0;
+    if (const char* e = getenv("GOOM_LONG_TOP")) v.top = atoi(e) >= 1 ? atoi(e) : 0;
+    return v;
+  }();
+  UpperTree u = d > 32 ? UpperTree{16, 32} : UpperTree{4, 4};
+  if (env.s) u.s = env.s;
+  if (env.top) u.top = env.top;
+  return u;
+}
+inline int64_t level_s(int level, int d) { return level == 0 ? kLongS0 : upper_tree(d).s; }
+inline int64_t level_top(int level, int d) {
+  return level == 0 ? kLongTop : upper_tree(d).top;
+}
 
 inline size_t rup(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -293,8 +318,9 @@ int launch_fold(const Cx<R>* A, int64_t T, int d, int64_t s, const Cx<R>* carry0
 template <class R>
 int long_scan(const Cx<R>* A, Cx<R>* out, int64_t T, int d, const Cx<R>* carry_in, char* ws,
               cudaStream_t st, int level) {
-  if (T <= kLongTop) return launch_fold<R>(A, T, d, T, carry_in, nullptr, out, nullptr, st);
-  const int64_t s = level == 0 ? kLongS0 : kLongS;
+  if (T <= level_top(level, d))
+    return launch_fold<R>(A, T, d, T, carry_in, nullptr, out, nullptr, st);
+  const int64_t s = level_s(level, d);
   const int64_t nb = (T + s - 1) / s;
   const size_t mats = rup(sizeof(Cx<R>) * (size_t)nb * d * d);
   Cx<R>* tot = reinterpret_cast<Cx<R>*>(ws);
@@ -313,8 +339,8 @@ template <class R>
 size_t chain_long_workspace_bytes(int64_t T, int d) {
   size_t total = 256;
   int64_t n = T;
-  for (int level = 0; n > kLongTop; ++level) {
-    const int64_t s = level == 0 ? kLongS0 : kLongS;
+  for (int level = 0; n > level_top(level, d); ++level) {
+    const int64_t s = level_s(level, d);
     const int64_t nb = (n + s - 1) / s;
     total += 2 * rup(sizeof(Cx<R>) * (size_t)nb * d * d);
     n = nb;
