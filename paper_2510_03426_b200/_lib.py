@@ -180,6 +180,8 @@ _lock = threading.Lock()
 def load(path: str = LIB_PATH):
     """Load libgoom.so and declare every ABI signature (no GPU needed)."""
     global _lib
+    if _lib is not None:  # loaded: no lock on the per-call path
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib
