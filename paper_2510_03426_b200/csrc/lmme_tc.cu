@@ -204,8 +204,10 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
   using G = Cfg<BN, kFuse>;
   constexpr int kEpiWarps = G::kEpiWarps;
   constexpr int STAGES = G::kStages;
-  const int pf = debug >> 8;  // kFuse: L2 prefetch distance (GOOM_TC_PREFETCH)
+  const int pf = (debug >> 8) & 15;  // kFuse: L2 prefetch distance (GOOM_TC_PREFETCH)
   const int fflags = debug & 0xF0;  // kFuse probes: 16 A row chunks, 32 no L2 hints, 64 late
+  // FuseSeq lateness: GOOM_TC1_LATE (default 1), or 2 with GOOM_TC_DEBUG bit 64
+  const int late = (fflags & 64) ? 2 : ((debug >> 12) & 15);
   debug &= 15;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB-align the ring while keeping the pointer's shared-space provenance
@@ -259,7 +261,6 @@ __global__ void __launch_bounds__(Cfg<BN, kFuse>::kThreads, 1)
   // re-reads them one tile later), main-pass loads evict_first, output stores evict_first
   const bool hints = kFuse && (fflags & 32) == 0;
   const uint64_t pol_keep = policy_evict_last(), pol_drop = policy_evict_first();
-  const bool late = (fflags & 64) != 0;  // FuseSeq late interleave (GOOM_TC_DEBUG bit 64)
   // a tile's load coordinates, computed once per tile (the loader is one thread: int64
   // divisions per stage measured ~1.5 k clocks per issue, slower than the ring drains)
   struct TileAt {
@@ -783,7 +784,8 @@ int tc_debug() {
   static int v = [] {
     const char* e = getenv("GOOM_TC_DEBUG");
     const char* p = getenv("GOOM_TC_PREFETCH");  // kFuse: L2 prefetch distance in tiles
-    return (e ? atoi(e) : 0) | ((p ? atoi(p) : 0) << 8);
+    return (e ? atoi(e) : 0) | (((p ? atoi(p) : 0) & 15) << 8) |
+           ((fuse_lateness("GOOM_TC1_LATE", 1) & 15) << 12);
   }();
   return v;
 }

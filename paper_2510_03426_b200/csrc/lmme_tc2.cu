@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // kFuse: the late interleave (FuseSeq) by default — scale-read lines wait ~3/4 of a tile for
   // their main-pass re-read instead of a whole one, which the L2 holds better (d = 256: DRAM
   // reads 2.02 -> 1.50 GB, 422 -> 397 us); GOOM_TC_DEBUG bit 64 restores one per main stage
-  const bool late = (debug & 64) == 0;
+  const int late = (debug & 64) ? 1 : ((debug >> 8) & 15);  // FuseSeq lateness (GOOM_TC_LATE)
   debug &= 63;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -614,6 +614,10 @@ int tc_debug() {
   }();
   return v;
 }
+int late_factor() {
+  static const int v = fuse_lateness("GOOM_TC_LATE", 2) & 15;
+  return v;
+}
 
 template <bool kFuse>
 int query_clusters() {
@@ -739,7 +743,7 @@ int lmme_tc2_run(const LmmeProblem& p, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, lmme_tc2_kernel<kFuse>, mapA, mapB, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C,
-                     p.strideC, pg, p.k, p.m, p.noncanon, emit, tc_debug());
+                     p.strideC, pg, p.k, p.m, p.noncanon, emit, tc_debug() | (late_factor() << 8));
   GOOM_CHECK_LAUNCH("lmme_tc2_kernel");
   return GOOM_OK;
 }

@@ -348,18 +348,21 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
 
 // Fused-scale kernels (lmme_tc.cu, lmme_tc2.cu kFuse): the ring positions of one CTA (pair)
 // in issue order. The first tile's scale stages, then per tile t the main K-blocks
-// main(t, kb) with the NEXT tile's scale stages interleaved. `late` (nk even): the scale
-// stages come two per main stage in the second half of the tile, so a scale-read line waits
-// ~3/4 of a tile (not a whole one) in L2 for its main-pass re-read; else one per main stage.
-// Every role walks the same sequence, so slot and phase bookkeeping agree.
+// main(t, kb) with the NEXT tile's scale stages interleaved. Lateness lf (nk % lf == 0): the
+// scale stages come lf per main stage in the last 1/lf of the tile (lf = 1: one per main
+// stage; 2: "late", two per main stage in the second half), so the later the scale pass, the
+// shorter a scale-read line waits in L2 for its main-pass re-read (and the denser the ring
+// traffic at the end of a tile). Every role walks the same sequence, so slot and phase
+// bookkeeping agree.
 struct FuseSeq {
   int64_t t, step, tiles;
-  int kb, nk, sub, skb;  // sub: 0 main, 1 / 2 scale stage skb of tile t + step
-  bool prologue, late;
+  int kb, nk, sub, skb;  // sub: 0 main, 1 .. lf scale stage skb of tile t + step
+  int lf;
+  bool prologue;
   __device__ __forceinline__ FuseSeq(int64_t t0, int64_t step_, int64_t tiles_, int nk_,
-                                     bool late_ = false)
-      : t(t0), step(step_), tiles(tiles_), kb(0), nk(nk_), sub(0), skb(0), prologue(true),
-        late(late_ && (nk_ % 2) == 0) {}
+                                     int lf_ = 1)
+      : t(t0), step(step_), tiles(tiles_), kb(0), nk(nk_), sub(0), skb(0),
+        lf(lf_ > 1 && nk_ % lf_ == 0 ? lf_ : 1), prologue(true) {}
   __device__ __forceinline__ bool valid() const { return t < tiles; }
   __device__ __forceinline__ bool scale() const { return prologue || sub != 0; }
   // tile whose data the stage holds, and its K-block
@@ -373,17 +376,10 @@ struct FuseSeq {
       }
       return;
     }
-    const bool more = t + step < tiles;
-    if (late) {
-      const int h = nk / 2;
-      if (more && kb >= h && sub < 2) {  // main(kb) -> scale(2 (kb - h)) -> scale(2 (kb - h) + 1)
-        ++sub;
-        skb = 2 * (kb - h) + sub - 1;
-        return;
-      }
-    } else if (more && sub == 0) {
-      sub = 1;
-      skb = kb;
+    const int h = nk - nk / lf;  // first main stage followed by scale stages
+    if (t + step < tiles && kb >= h && sub < lf) {  // main(kb) -> scale(lf (kb - h) + i)
+      ++sub;
+      skb = lf * (kb - h) + sub - 1;
       return;
     }
     sub = 0;
@@ -393,6 +389,14 @@ struct FuseSeq {
     }
   }
 };
+
+// FuseSeq lateness for the pair kernel (GOOM_TC_LATE, default 2) and the one-SM kernel
+// (GOOM_TC1_LATE, default 1), read once on the host
+inline int fuse_lateness(const char* var, int dflt) {
+  const char* e = getenv(var);
+  const int v = e ? atoi(e) : dflt;
+  return v >= 1 ? v : dflt;
+}
 
 // per-slot phase bits of the shared ring (kFuse: slots carry main and scale stages)
 template <int STAGES>
