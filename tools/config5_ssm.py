@@ -75,6 +75,8 @@ def main():
 
     f_s, (sl, ss, c, y) = timed(fwd)
     fb_s, (_, grads) = timed(fwd_bwd)
+    b_s, _ = timed(lambda: ssm.ssm_backward_heads(dA_, dB_, dC_, dD_, dx0_, du_, sl, ss, c, dgy_,
+                                                  chunk=args.chunk))
     finite = bool(torch.isfinite(sl).all() and torch.isfinite(y).all() and
                   all(bool(torch.isfinite(g).all()) for g in grads))
     # parity: head 0, sequence 0 vs the oracle
@@ -96,6 +98,7 @@ def main():
     print(json.dumps({
         "config": "ssm_forward_backward", "d": d, "heads": H, "batch": S, "T": T,
         "chunk": args.chunk, "gpu_forward_s": f_s, "gpu_forward_backward_s": fb_s,
+        "gpu_backward_s": b_s,
         "gpu_steps_per_s_fwd": steps / f_s, "gpu_steps_per_s_fwd_bwd": steps / fb_s,
         "upload_s": upload_s, "finite": finite, "max_scale": float(c.max()),
         "gpu_timing": "CUDA events, float64 inputs resident on the device; outputs and "
