@@ -88,6 +88,50 @@ def test_long_chain_matches_oracle_complex64(g, d, T):
                      r["scaled_bad"])
 
 
+@pytest.mark.parametrize("T", [64 * 4 + 1, 64 * 5, 64 * 17 - 1, 64 * 64 + 3])
+@pytest.mark.parametrize("with_carry", [False, True])
+def test_long_chain_upper_tree_boundaries(g, T, with_carry):
+    """The upper levels (chains of 4 totals up to a top chain of <= 4, d <= 32): leaf-level
+    chain counts just above / at the top size (5, 5), a ragged 17-chain level (two upper
+    levels with a 1-total tail) and 65 chains (three upper levels), with and without a
+    carry, against the float64 sequential oracle under the §8c criterion (d = 8, the
+    lane-group fold). The calibration runs include the reference's float32 blocked scan with
+    block 64: its carry products (A_127..A_64) (x) P_63 are this engine's leaf-level
+    association, which at some seeds (T = 257: 4.4e-4 at position 129) loses far more than
+    the sequential float32 fold does."""
+    from goom_testlib import scaled_real_err
+
+    d = 8
+    rng = np.random.default_rng(T)
+    x = rng.standard_normal((T + 1, d, d))
+    al, as_ = G.log_sign(x)
+    l32, s32 = G.log_sign(x.astype(np.float32))
+    if with_carry:  # leaf 0 plays the carry: the chain checked is [carry, P_0 .. P_{T-1}]
+        gl, gs = to_np(torch.ops.goom.scan_chain_long(g.join(al[1:], as_[1:]),
+                                                      g.join(al[0], as_[0])))
+        gl = np.concatenate([al[:1], gl])
+        gs = np.concatenate([as_[:1], gs])
+        # float32 block-64 run over the leaves, each prefix then (x) the carry
+        bl, bs = G.chain_blocked(l32[1:], s32[1:], 64)
+        cl, cs = G.lmme(bl, bs, np.broadcast_to(l32[0], bl.shape),
+                        np.broadcast_to(s32[0], bl.shape))
+        blk = [(np.concatenate([l32[:1], cl]), np.concatenate([s32[:1], cs]))]
+    else:
+        gl, gs = to_np(torch.ops.goom.scan_chain_long(g.join(al, as_), None))
+        blk = [G.chain_blocked(l32, s32, 64)]
+    want = G.chain_blocked(al, as_, T + 1)
+    from goom_testlib import TC_CHAIN_FLOOR
+    refs = [G.chain_blocked(l32, s32, T + 1)] + blk
+    # scaled-real error (relative to the largest entry): bounded chain-wide by 4x the worst the
+    # reference's float32 runs reach anywhere on this chain (~2e-4 at T = 257), since the
+    # positions where float32 rounding peaks differ between associations; the rel-log
+    # criterion stays per position
+    ref_scaled = max(float(scaled_real_err(r_[0], r_[1], *want).max()) for r_ in refs)
+    r = chain_parity(gl, gs, al, as_, want, refs, floor=TC_CHAIN_FLOOR,
+                     scaled_floor=max(1e-4, 4.0 * ref_scaled))
+    assert r["ok"], (r["bad"], r["flips"], r["scaled_bad"], r["scaled_max"], ref_scaled)
+
+
 @pytest.mark.parametrize("d,T,with_carry", [(16, 4500, True), (32, 4500, False), (16, 65, False),
                                             (32, 130, True), (16, 200, False)])
 def test_long_chain_tc_small_d_matches_oracle(g, d, T, with_carry):
