@@ -603,8 +603,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// GOOM_TC_DEBUG (profiling only; results invalid unless noted): +64 L2 prefetch of the next
-// tile in the fused-scale pair kernel (results valid); 1 no transform, 2 no MMA, 3 no loads
+// GOOM_TC_DEBUG (profiling only; results invalid unless noted): +64 one scale stage per main
+// stage in the fused-scale pair kernel instead of GOOM_TC_LATE's lateness (results valid);
+// 1 no transform, 2 no MMA, 3 no loads
 // and no transform, 4 no loads, 5 loads only (no transform / MMA), 7 as 5 without the
 // epilogue body, 8 MMA only (no loads / transform / epilogue body), 9 epilogue only
 int tc_debug() {
