@@ -61,13 +61,27 @@ __global__ void random_normal_kernel(float2* __restrict__ out, int64_t n, uint64
 }
 
 // the same leaves as tile-scaled fp32 (chain_ts.cu): U = the normals, q = 0, G = bits(0)
+template <int kU>
 __global__ void random_normal_ts_kernel(float* __restrict__ U, float* __restrict__ qv,
                                         uint32_t* __restrict__ G, int64_t n, int64_t nq,
                                         int64_t ng, uint64_t seed, uint64_t offset) {
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = tid; q * 4 < n; q += stride) {
+  const int64_t whole = n / 4;  // whole quads
+  int64_t q = tid;
+  // kU independent counters per iteration: the Philox rounds of one hide the multiply and
+  // MUFU latencies of the others (the generator is ALU-bound). Bitwise the one-counter loop;
+  // d = 512 window of 32,768 leaves: kU = 1 / 2 / 3 / 4 10.85 / 9.64 / 9.31 / 9.42 ms
+  // (profiles/r2_rng_interleave.txt)
+  for (; q + (kU - 1) * stride < whole; q += kU * stride) {
+    float4 z[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) z[u] = normals4((offset / 4) + (uint64_t)(q + u * stride), key);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) reinterpret_cast<float4*>(U)[q + u * stride] = z[u];
+  }
+  for (; q * 4 < n; q += stride) {
     const float4 z = normals4((offset / 4) + (uint64_t)q, key);
     if (q * 4 + 3 < n) {
       reinterpret_cast<float4*>(U)[q] = z;
@@ -152,7 +166,7 @@ int goom_random_normal_ts(float* U, float* q, uint32_t* G, int64_t T, int d, uin
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   PhaseTimer timer(as_stream(stream), 0, T);
-  random_normal_ts_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+  random_normal_ts_kernel<3><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
       U, q, G, n, T * d * (d / 256), T * (d / 256), seed, (uint64_t)offset);
   GOOM_CHECK_LAUNCH("random_normal_ts_kernel");
   timer.stop();

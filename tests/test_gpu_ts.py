@@ -305,6 +305,20 @@ def test_random_normal_ts_is_the_same_chain(g, ops):
     assert (t.q == 0).all()
 
 
+def test_random_normal_ts_is_counter_based(g, ops):
+    """Leaf t is a function of (seed, t) only: one call over 7 leaves equals two calls over
+    3 + 4 (different grid-stride partitions of the counters, the two-counter main loop and
+    its single-counter tail), bit for bit; and different seeds differ."""
+    d, dev = 256, torch.device("cuda")
+    whole = ops.ts_random_normal(7, d, 9, 5, dev).U
+    parts = torch.cat([ops.ts_random_normal(3, d, 9, 5, dev).U,
+                       ops.ts_random_normal(4, d, 9, 8, dev).U])
+    assert torch.equal(whole, parts)
+    assert not torch.equal(whole, ops.ts_random_normal(7, d, 10, 5, dev).U)
+    z = whole.double()
+    assert abs(float(z.mean())) < 0.01 and abs(float(z.std()) - 1.0) < 0.01
+
+
 def test_harness_ts_growth_and_digest_parity(g, ops):
     """Config 3 machinery at d = 512 on the tile-scaled engine: per-prefix digests equal
     the complex64 digests of the same chain, and log||P_t|| grows at (ln 2 + psi(d/2)) / 2."""
