@@ -357,12 +357,12 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
 struct FuseSeq {
   int64_t t, step, tiles;
   int kb, nk, sub, skb;  // sub: 0 main, 1 .. lf scale stage skb of tile t + step
-  int lf;
+  int lf, h;             // h: the first main stage followed by scale stages (no per-step division)
   bool prologue;
   __device__ __forceinline__ FuseSeq(int64_t t0, int64_t step_, int64_t tiles_, int nk_,
                                      int lf_ = 1)
       : t(t0), step(step_), tiles(tiles_), kb(0), nk(nk_), sub(0), skb(0),
-        lf(lf_ > 1 && nk_ % lf_ == 0 ? lf_ : 1), prologue(true) {}
+        lf(lf_ > 1 && nk_ % lf_ == 0 ? lf_ : 1), h(nk_ - nk_ / lf), prologue(true) {}
   __device__ __forceinline__ bool valid() const { return t < tiles; }
   __device__ __forceinline__ bool scale() const { return prologue || sub != 0; }
   // tile whose data the stage holds, and its K-block
@@ -376,7 +376,6 @@ struct FuseSeq {
       }
       return;
     }
-    const int h = nk - nk / lf;  // first main stage followed by scale stages
     if (t + step < tiles && kb >= h && sub < lf) {  // main(kb) -> scale(lf (kb - h) + i)
       ++sub;
       skb = lf * (kb - h) + sub - 1;
