@@ -785,7 +785,7 @@ int tc_debug() {
     const char* e = getenv("GOOM_TC_DEBUG");
     const char* p = getenv("GOOM_TC_PREFETCH");  // kFuse: L2 prefetch distance in tiles
     return (e ? atoi(e) : 0) | (((p ? atoi(p) : 0) & 15) << 8) |
-           ((fuse_lateness("GOOM_TC1_LATE", 1) & 15) << 12);
+           ((fuse_lateness("GOOM_TC1_LATE", 1) & 15) << 12);  // (fitted per launch)
   }();
   return v;
 }
@@ -843,7 +843,7 @@ int launch_tc(const LmmeProblem& p, cudaStream_t s) {
   Emit emit{p.emitRow, p.emitRowStride, p.emitCol, p.emitColStride};
   lmme_tc_kernel<BN, kFuse, kDuo><<<grid, G::kThreads, G::kSmem, s>>>(
       mapA, mapB, mapB3, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C, p.strideC, tg, p.n, p.k, p.m, p.noncanon,
-      emit, tc_debug());
+      emit, (tc_debug() & ~(15 << 12)) | (fit_lateness((tc_debug() >> 12) & 15, p.k / BK) << 12));
   GOOM_CHECK_LAUNCH("lmme_tc_kernel");
   return GOOM_OK;
 }

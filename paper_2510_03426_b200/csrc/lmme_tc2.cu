@@ -176,9 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = Tc2Cfg<kFuse>;
   constexpr int kStages = Cfg::S, kRing = Cfg::kRing;
   using Ring = RingPos<kStages>;
-  // kFuse: the late interleave (FuseSeq) by default — scale-read lines wait ~3/4 of a tile for
-  // their main-pass re-read instead of a whole one, which the L2 holds better (d = 256: DRAM
-  // reads 2.02 -> 1.50 GB, 422 -> 397 us); GOOM_TC_DEBUG bit 64 restores one per main stage
+  // kFuse: a late scale pass (FuseSeq lateness, GOOM_TC_LATE, default 8 per main stage in the
+  // tile's last 1/8) — scale-read lines wait less than a tile in L2 for their main-pass re-read
+  // (d = 256: one per main stage 422 us, DRAM reads 2.02 GB; lateness 2 397 us, 1.50 GB;
+  // lateness 8 390 us); GOOM_TC_DEBUG bit 64 restores one per main stage
   const int late = (debug & 64) ? 1 : ((debug >> 8) & 15);  // FuseSeq lateness (GOOM_TC_LATE)
   debug &= 63;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -616,7 +617,7 @@ int tc_debug() {
   return v;
 }
 int late_factor() {
-  static const int v = fuse_lateness("GOOM_TC_LATE", 2) & 15;
+  static const int v = fuse_lateness("GOOM_TC_LATE", 8) & 15;
   return v;
 }
 
@@ -744,7 +745,8 @@ int lmme_tc2_run(const LmmeProblem& p, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, lmme_tc2_kernel<kFuse>, mapA, mapB, mapC, p.A, p.B, p.D, p.rowA, p.colB, p.C,
-                     p.strideC, pg, p.k, p.m, p.noncanon, emit, tc_debug() | (late_factor() << 8));
+                     p.strideC, pg, p.k, p.m, p.noncanon, emit,
+      tc_debug() | (fit_lateness(late_factor(), p.k / BK) << 8));
   GOOM_CHECK_LAUNCH("lmme_tc2_kernel");
   return GOOM_OK;
 }

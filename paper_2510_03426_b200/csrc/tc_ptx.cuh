@@ -389,12 +389,20 @@ struct FuseSeq {
   }
 };
 
-// FuseSeq lateness for the pair kernel (GOOM_TC_LATE, default 2) and the one-SM kernel
-// (GOOM_TC1_LATE, default 1), read once on the host
+// FuseSeq lateness for the pair kernel (GOOM_TC_LATE, default 8: d = 256 399 -> 390 us against
+// 2, profiles/r2_fuse_lateness_ab.txt) and the one-SM kernel (GOOM_TC1_LATE, default 1), read
+// once on the host
 inline int fuse_lateness(const char* var, int dflt) {
   const char* e = getenv(var);
   const int v = e ? atoi(e) : dflt;
   return v >= 1 ? v : dflt;
+}
+// the lateness a launch with nk K-blocks per tile uses (host side, so the kernels' loops carry
+// no extra work): at most half the tile's main stages carry scale stages (lf = nk, every scale
+// stage after the last main stage, measured 8% slower at d = 256), and lf divides nk
+inline int fit_lateness(int lf, int nk) {
+  while (lf > 1 && (2 * lf > nk || nk % lf != 0)) lf >>= 1;
+  return lf < 1 ? 1 : lf;
 }
 
 // per-slot phase bits of the shared ring (kFuse: slots carry main and scale stages)
