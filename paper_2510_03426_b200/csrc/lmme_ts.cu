@@ -60,7 +60,10 @@ constexpr int kMaxK = 1024;
 // per-tile right-operand row factors (2 x kMaxK floats) | barriers
 template <int kOut, int S>
 struct Lay {
-  static constexpr int kOutBytes = kOut == kTsOutDigest ? 0 : kEpiWarps * 2 * kOutStage;
+  // staging buffers per epilogue warp: 2 (a TMA store in flight while the next is written),
+  // 1 when a 6-deep ring leaves no room for two
+  static constexpr int kOutBufs = kOut == kTsOutDigest ? 0 : (S >= 6 ? 1 : 2);
+  static constexpr int kOutBytes = kEpiWarps * kOutBufs * kOutStage;
   static constexpr int kOutOff = S * kStage;
   static constexpr int kFacOff = kOutOff + kOutBytes;
   static constexpr int kBarOff = kFacOff + 2 * kMaxK * 4;
@@ -392,7 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t acc_empty0 = smem_u32(&acc_empty[0]);
-    const uint32_t obuf = base + kOutOff + (uint32_t)(warp - 2 - kXformWarps) * 2 * kOutStage;
+    constexpr int kOB = Y::kOutBufs > 0 ? Y::kOutBufs : 1;
+    const uint32_t obuf = base + kOutOff + (uint32_t)(warp - 2 - kXformWarps) * kOB * kOutStage;
     int lt = 0;
     for (int64_t t = cluster; t < grid.tiles; t += nclusters, ++lt) {
       int64_t b;
@@ -423,8 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tacc + col, v);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const uint32_t sbuf = obuf + (uint32_t)h * kOutStage;
-            if (lane == 0) tma_store_wait_read<1>();
+            const uint32_t sbuf = obuf + (uint32_t)(h % kOB) * kOutStage;
+            if (lane == 0) tma_store_wait_read<kOB - 1>();
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
@@ -469,8 +473,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int col = 0; col < kPairN; col += 32) {
             uint32_t v[32];
             tmem_ld32(tacc + col, v);
-            const uint32_t sbuf = obuf + (uint32_t)((col >> 5) & 1) * kOutStage;
-            if (lane == 0) tma_store_wait_read<1>();
+            const uint32_t sbuf = obuf + (uint32_t)(((col >> 5) & 1) % kOB) * kOutStage;
+            if (lane == 0) tma_store_wait_read<kOB - 1>();
             __syncwarp();
             const uint32_t rb = sbuf + (uint32_t)lane * 128;
 #pragma unroll
@@ -651,6 +655,7 @@ int launch(const TsProblem& p, const CUtensorMap& mapA, const CUtensorMap& mapB,
     if constexpr (kOut == kTsOutTs)
       if (p.chain_s) return launch_cfg<kOut, 5, true>(p, mapA, mapB, mapOut, s);
     if (stage_cfg() == 1) return launch_cfg<kOut, 4>(p, mapA, mapB, mapOut, s);
+    if (stage_cfg() == 2) return launch_cfg<kOut, 6>(p, mapA, mapB, mapOut, s);
     return launch_cfg<kOut, 5>(p, mapA, mapB, mapOut, s);
   }
 }
