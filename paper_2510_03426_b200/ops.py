@@ -169,7 +169,7 @@ def _bcast_operands(a: torch.Tensor, b: torch.Tensor):
     if ab == bb and a.is_contiguous() and b.is_contiguous():  # the common case: no broadcast
         batch = math.prod(ab)
         mat_a, mat_b = a.shape[-1] * a.shape[-2], b.shape[-1] * b.shape[-2]
-        return a, b, ab, batch, (mat_a if batch > 1 else 0), (mat_b if batch > 1 else 0)
+        return a, b, ab, batch, (mat_a if batch != 1 else 0), (mat_b if batch != 1 else 0)
     batch_shape = torch.broadcast_shapes(ab, bb)
     batch = math.prod(batch_shape)
 

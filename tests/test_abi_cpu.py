@@ -144,3 +144,43 @@ def test_ops_refuse_cpu_tensors():
     x = torch.zeros(2, 2, dtype=torch.complex64)
     with pytest.raises(Exception):
         torch.ops.goom.lmme(x, x)
+
+
+def test_lmme_broadcast_fast_path_matches_general():
+    """ops._bcast_operands: the no-broadcast fast path (same leading dims, contiguous) returns
+    what np.matmul broadcasting gives (batch shape, batch, per-operand matrix strides) — the
+    general path is kept for broadcasts and non-contiguous operands. Shape logic only: CPU
+    tensors, no GPU."""
+    import math
+
+    import torch
+
+    from paper_2510_03426_b200 import ops
+
+    def general(a, b):
+        batch_shape = torch.broadcast_shapes(a.shape[:-2], b.shape[:-2])
+        batch = 1
+        for s in batch_shape:
+            batch *= s
+        # the reference's operand of one matrix is shared (stride 0), else one matrix per index
+        sa = 0 if math.prod(a.shape[:-2]) == 1 else a.shape[-1] * a.shape[-2]
+        sb = 0 if math.prod(b.shape[:-2]) == 1 else b.shape[-1] * b.shape[-2]
+        return tuple(batch_shape), batch, sa, sb
+
+    z = torch.complex64
+    cases = [((5, 3, 4), (5, 4, 2)), ((1, 3, 4), (1, 4, 2)), ((3, 4), (4, 2)),
+             ((2, 3, 3, 4), (2, 3, 4, 2)), ((0, 3, 4), (0, 4, 2)),
+             ((5, 3, 4), (1, 4, 2)), ((5, 3, 4), (4, 2)), ((2, 1, 3, 4), (1, 6, 4, 2))]
+    for sa_, sb_ in cases:
+        a, b = torch.zeros(sa_, dtype=z), torch.zeros(sb_, dtype=z)
+        a2, b2, batch_shape, batch, sa, sb = ops._bcast_operands(a, b)
+        want = general(a, b)
+        assert (tuple(batch_shape), batch, sa, sb) == want, (sa_, sb_)
+        assert a2.is_contiguous() and b2.is_contiguous()
+        mat = a.shape[-1] * a.shape[-2]
+        assert a2.numel() in (a.numel(), batch * mat, mat)
+    # a non-contiguous operand takes the general path and comes back contiguous
+    a = torch.zeros(4, 5, 3, dtype=z).transpose(1, 2)
+    b = torch.zeros(4, 5, 2, dtype=z)
+    a2, b2, batch_shape, batch, sa, sb = ops._bcast_operands(a, b)
+    assert a2.is_contiguous() and tuple(batch_shape) == (4,) and sa == 15 and sb == 10
