@@ -16,6 +16,7 @@ complex64, flags: (T,) bool). The engines run in libgoom:
 
 from __future__ import annotations
 
+import gc
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -231,13 +232,22 @@ class _Stack:
         # lazily sliced matrices (_StackedGoom) and no per-pair validation (the stack's shapes
         # are checked): ~10x faster than a tensor view per element, which the reference's own
         # host-list callers notice (test_scan.py:341-360 times a 2^15-leaf scan)
+        # The cyclic garbage collector is paused while the 3 T objects are made: every 700
+        # allocations it would traverse the growing list (and the caller's leaves), which
+        # cost ~4x the creation itself for 2^15 pairs
         flags = self._flags.cpu().tolist()
         new, of, A, B = object.__new__, _StackedGoom._of, self.A, self.B
         out = []
-        for i, f in enumerate(flags):
-            p = new(ScanPair)  # frozen dataclass: fill its __dict__ directly
-            p.__dict__.update(A=of(A, i), B=of(B, i), reset_applied=bool(f))
-            out.append(p)
+        paused = gc.isenabled()
+        gc.disable()
+        try:
+            for i, f in enumerate(flags):
+                p = new(ScanPair)  # frozen dataclass: fill its __dict__ directly
+                p.__dict__.update(A=of(A, i), B=of(B, i), reset_applied=bool(f))
+                out.append(p)
+        finally:
+            if paused:
+                gc.enable()
         return out
 
     @property

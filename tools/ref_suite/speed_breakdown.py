@@ -21,3 +21,7 @@ for rep in range(2):
 import cProfile, pstats
 cProfile.run("S.scan_parallel(leaves, S.combine_affine, block_size=256, workers=4)", "/tmp/pp.out")
 pstats.Stats("/tmp/pp.out").sort_stats("cumtime").print_stats(12)
+t0 = time.perf_counter(); S.scan_sequential(leaves, S.combine_affine); t1 = time.perf_counter()
+print(f"scan_sequential {t1 - t0:.3f} s")
+cProfile.run("S.scan_sequential(leaves, S.combine_affine)", "/tmp/ps.out")
+pstats.Stats("/tmp/ps.out").sort_stats("tottime").print_stats(10)
