@@ -1,7 +1,7 @@
 # round-2 final evidence: GPU suite, smoke, default bench (+ --impl reference), ncu launch list and
 # phase captures, config-2 sweep, small-d long chains
 mkdir -p gpurun_out
-TAG=r2z
+TAG=r2f2
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
