@@ -163,7 +163,9 @@ int goom_random_normal_ts(float* U, float* q, uint32_t* G, int64_t T, int d, uin
   const int64_t n = T * d * d, offset = (int64_t)t0 * d * d;
   if (offset % 4) return fail(GOOM_EINVAL, "offset must be a multiple of 4");
   int64_t blocks = (n / 4 + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 16;
+  // 64 blocks per SM of grid-stride work (16 / 32 / 64 / 128: 9.32 / 9.22 / 9.17 / 9.17 ms per
+  // 32,768-leaf window; bitwise the same leaves, profiles/r2_rng_interleave.txt)
+  const int64_t cap = (int64_t)num_sms() * 64;
   if (blocks > cap) blocks = cap;
   PhaseTimer timer(as_stream(stream), 0, T);
   random_normal_ts_kernel<3><<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
